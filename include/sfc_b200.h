@@ -1,0 +1,149 @@
+/* C-ABI of the B200 quantized SFC 3x3 convolution (libsfc_b200.so).
+ *
+ * This is the drop-in boundary a host binding (ctypes / cgo / JNI / the C++
+ * `sfconv::` shim in include/sfconv/) calls.  Plain pointers, sizes and opaque
+ * handles only.  Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).
+ *
+ * Conventions
+ *  - Return 0 on success, a negative SFC_ERR_* code otherwise; the message is
+ *    in a thread-local buffer read with sfc_last_error().  The C++ shim maps
+ *    the codes to the reference's exception types:
+ *      SFC_ERR_INVALID     -> std::invalid_argument   (quant.cpp:155-156, conv.cpp:353-355, quant.cpp:49)
+ *      SFC_ERR_DOMAIN      -> std::domain_error       (catalog.cpp:284-285)
+ *      SFC_ERR_UNSUPPORTED -> std::invalid_argument   (configuration the device path does not cover)
+ *      SFC_ERR_CUDA        -> std::runtime_error
+ *  - Pointers named d_* are device pointers; `stream` is a cudaStream_t
+ *    (NULL = legacy default stream).  Device calls are stream-ordered and
+ *    asynchronous unless documented as synchronous.
+ *  - Tensors are row-major NCHW like sfconv::DenseTensor (tensor.hpp:11-31);
+ *    activations and weights are int8 (the integer values the reference
+ *    receives as doubles); weights are [OC][IC][3][3].
+ *  - Plans and layers are immutable after creation and may be shared across
+ *    host threads; all per-call state lives in the caller's workspace, so
+ *    concurrent calls on distinct streams need distinct workspaces.
+ */
+#ifndef SFC_B200_H
+#define SFC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFC_OK 0
+#define SFC_ERR_INVALID -1
+#define SFC_ERR_DOMAIN -2
+#define SFC_ERR_UNSUPPORTED -3
+#define SFC_ERR_CUDA -4
+
+/* Scope / search codes, numerically equal to the reference enums (quant.hpp:16-18). */
+#define SFC_ACT_PER_TENSOR 0
+#define SFC_ACT_PER_FREQUENCY 1
+#define SFC_FIL_PER_CHANNEL 0
+#define SFC_FIL_PER_FREQUENCY 1
+#define SFC_FIL_PER_CHANNEL_FREQUENCY 2
+#define SFC_SEARCH_MINMAX 0
+#define SFC_SEARCH_MSE_GRID 1
+
+typedef struct sfc_plan* sfc_plan_t;
+typedef struct sfc_layer* sfc_layer_t;
+
+const char* sfc_last_error(void);
+int sfc_version(void);
+
+/* ---- catalog: replaces catalog_algorithm / catalog_export_json / catalog_hash
+ *      (include/sfconv/spec.hpp:76-79, src/catalog.cpp:275-287, 562-601) ----------- */
+
+/* JSON of the three 3x3 SFC algorithms in the reference export layout; hash = FNV-1a 64 of it. */
+int sfc_catalog_json(char* buf, size_t cap, uint64_t* hash);
+/* Derive + exactness-gate + bind the compiled kernels for `name`
+ * ("sfc4-4x4-3x3" | "sfc6-6x6-3x3" | "sfc6-7x7-3x3"). */
+int sfc_plan_create(const char* name, sfc_plan_t* out);
+int sfc_plan_destroy(sfc_plan_t plan);
+/* dims[10] = {K, n_in, M, R, N, offset, a_denom, n_corrections, mults_full, mults_reduced} */
+int sfc_plan_dims(sfc_plan_t plan, int64_t* dims);
+/* Row-major integer matrices BT[K][n_in], G[K][R], A[K][M] (any pointer may be NULL). */
+int sfc_plan_matrices(sfc_plan_t plan, int64_t* bt, int64_t* g, int64_t* a);
+
+/* ---- layer: offline filter stage of quantized_fast_conv2d
+ *      (transform_filters src/conv.cpp:352-382 + filter scales/quantize src/quant.cpp:183-229) */
+
+/* Runs U = G f G^T, the per-output-channel minmax scale and exact RNE
+ * quantization on `stream` and keeps the quantized transformed filters on the
+ * device.  Synchronous (returns once the layer is ready).  v1 scope: bits in
+ * [2, 8], filter_scope PerChannel, search MinMax. */
+int sfc_layer_create(sfc_plan_t plan, const int8_t* d_weights, int out_channels, int in_channels, int bits,
+                     int filter_scope, int search, void* stream, sfc_layer_t* out);
+int sfc_layer_destroy(sfc_layer_t layer);
+/* Host copies of the filter scales sf[OC] (double) and per-oc max|U| (int32); synchronous. */
+int sfc_layer_filter_scales(sfc_layer_t layer, double* sf, int32_t* umax);
+/* Filter-side saturation count (0 by construction for MinMax); synchronous. */
+int sfc_layer_saturations(sfc_layer_t layer, int64_t* count);
+/* Device view of the quantized transformed filters uq[f][oc][ic] with row pitch
+ * `*ic_pitch` and plane pitch `*oc_pitch` rows. */
+int sfc_layer_uq(sfc_layer_t layer, const int8_t** d_uq, int64_t* ic_pitch, int64_t* oc_pitch);
+
+/* ---- per call: the activation stage, contraction and output stage of
+ *      quantized_fast_conv2d (src/quant.cpp:163-181, 239-279) ------------------------- */
+
+/* Bytes of caller-owned device workspace one sfc_conv_int8 call needs. */
+int sfc_conv_workspace_size(sfc_layer_t layer, int n, int h, int w, int pad, size_t* bytes);
+
+/* Absmax pre-pass: atomically max-accumulates max|B^T x B| over every tile
+ * and channel of x into *d_vmax (caller zero-initialises it).  Multi-GPU
+ * callers run this on their batch shard and all-reduce(MAX) d_vmax before
+ * sfc_conv_int8, which makes the per-tensor scale global (quant.cpp:171-172). */
+int sfc_act_absmax(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, int32_t* d_vmax,
+                   void* stream);
+
+typedef struct {
+    int32_t* y_int32;      /* [N][OC][HO][WO] integer output accumulator sum_kl A A pacc, or NULL */
+    int64_t* y_int64;      /* same, 64-bit (required when the int32 bound does not hold), or NULL */
+    float* out_f32;        /* dequantised output y * sa * sf[oc] / N^2, or NULL */
+    int8_t* out_i8;        /* harness requant clamp(rint(out * requant_scale), 0, 127), or NULL */
+    double requant_scale;
+} sfc_outputs;
+
+/* Quantize the transformed activations with the global scale derived from
+ * *d_vmax, contract over channels on the tensor cores and apply the output
+ * transform.  Asynchronous on `stream`. */
+int sfc_conv_int8(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax,
+                  void* d_workspace, size_t workspace_bytes, const sfc_outputs* outs, void* stream);
+
+/* Convenience: zero the workspace's vmax slot, absmax pre-pass, then sfc_conv_int8 (single GPU). */
+int sfc_conv_forward(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, void* d_workspace,
+                     size_t workspace_bytes, const sfc_outputs* outs, void* stream);
+
+/* Inspection of the last call's workspace (synchronous on `stream`):
+ * stats[0..5] = {sa (as double bits), vmax, activation saturations, fast-quantizer-exact flag,
+ *                values_quantized, tiles}. */
+int sfc_conv_stats(sfc_layer_t layer, int n, int h, int w, int pad, const void* d_workspace, int64_t* stats,
+                   void* stream);
+/* Device views into the workspace after sfc_conv_int8:
+ *   vq   int8  [F][Tpad][Cpad]   quantized transformed activations
+ *   pacc int32 [F][Tpad][OCpad]  per-frequency channel contractions
+ * geom[6] = {T, Tpad, Cpad, OCpad, th, tw}. */
+int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_workspace, int8_t** d_vq,
+                   int32_t** d_pacc, int64_t* geom);
+
+/* Exact int8 direct correlation (int32 accumulate), the report baseline
+ * of quantized_fast_conv2d (quant.cpp:282) and direct_conv2d (conv.cpp:320-350). */
+int sfc_direct_conv_int8(const int8_t* d_x, int n, int c, int h, int w, const int8_t* d_weights, int oc, int r,
+                         int stride, int pad, int32_t* d_out, void* stream);
+
+/* Exact per-frequency energy sum_{tiles,channels} V^2 (frequency_energy, quant.cpp:136-150).
+ * d_sum[K*K] (uint64, caller zeroes) accumulates; divide by n*th*tw*c on the host. */
+int sfc_frequency_energy_int8(sfc_plan_t plan, const int8_t* d_x, int n, int c, int h, int w, int pad,
+                              unsigned long long* d_sum, void* stream);
+
+/* U = G f G^T for every (oc, ic) as exact int32 [OC][IC][K][K] (transform_filters, conv.cpp:352-382). */
+int sfc_transform_filters_int8(sfc_plan_t plan, const int8_t* d_weights, int oc, int ic, int32_t* d_u,
+                               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFC_B200_H */

@@ -1,0 +1,360 @@
+// C-ABI implementation (include/sfc_b200.h).  Host orchestration only: every
+// numerical stage runs in the CUDA kernels of kernels.cu; there is no CPU
+// fallback -- a missing / failing device path returns SFC_ERR_CUDA.
+#include "../../include/sfc_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "plan.hpp"
+#include "sfc_kernels.hpp"
+
+using namespace sfcb200;
+
+struct sfc_plan {
+    const SfcPlan* p;
+};
+
+struct sfc_layer {
+    const SfcPlan* plan;
+    int variant, OC, IC, bits, BK, Cpad, BN, OCpad, F;
+    int8_t* d_uq = nullptr;        // [F][OCpad][Cpad]
+    double* d_sf = nullptr;        // [OC]
+    int* d_umax = nullptr;         // [OC]
+    unsigned long long* d_sat = nullptr;
+    int64_t max_a_col_l1 = 0;      // for the int32 output bound
+};
+
+namespace {
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+struct CudaFail : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SFC_OK;
+    } catch (const CudaFail& e) {
+        return set_err(SFC_ERR_CUDA, e.what());
+    } catch (const std::invalid_argument& e) {
+        return set_err(SFC_ERR_INVALID, e.what());
+    } catch (const std::domain_error& e) {
+        return set_err(SFC_ERR_DOMAIN, e.what());
+    } catch (const std::length_error& e) {
+        return set_err(SFC_ERR_UNSUPPORTED, e.what());
+    } catch (const std::bad_alloc&) {
+        return set_err(SFC_ERR_CUDA, "out of host memory");
+    } catch (const std::exception& e) {
+        return set_err(SFC_ERR_CUDA, e.what());
+    }
+}
+
+struct Unsupported : std::length_error {
+    using std::length_error::length_error;
+};
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Workspace carve-up (kept in sync with workspace_bytes()).
+struct WsView {
+    int* vmax;
+    unsigned long long* sat;
+    QuantParams* qp;
+    int8_t* vq;
+    int32_t* P;
+};
+WsView carve(void* ws, const ConvGeom& g, int F) {
+    auto up = [](size_t v) { return (v + 255) / 256 * 256; };
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    WsView v;
+    v.vmax = reinterpret_cast<int*>(base);
+    v.sat = reinterpret_cast<unsigned long long*>(base + 8);
+    v.qp = reinterpret_cast<QuantParams*>(base + 64);
+    v.vq = reinterpret_cast<int8_t*>(base + up(256));
+    v.P = reinterpret_cast<int32_t*>(base + up(256) + up(size_t(F) * g.Tpad * g.Cpad));
+    return v;
+}
+
+void check_call(const sfc_layer* L, const void* x, int n, int h, int w, int pad) {
+    if (!L) throw std::invalid_argument("null layer");
+    if (!x) throw std::invalid_argument("null input");
+    if (n <= 0 || h <= 0 || w <= 0 || pad < 0) throw std::invalid_argument("bad input shape");
+    if (h + 2 * pad - L->plan->R + 1 <= 0 || w + 2 * pad - L->plan->R + 1 <= 0)
+        throw std::invalid_argument("filter larger than padded input");
+}
+
+ConvGeom geom_of(const sfc_layer* L, int n, int h, int w, int pad) {
+    ConvGeom g;
+    geom_init(g, L->variant, n, L->IC, h, w, pad, L->OC);
+    return g;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sfc_last_error(void) { return g_err.c_str(); }
+int sfc_version(void) { return 1; }
+
+int sfc_catalog_json(char* buf, size_t cap, uint64_t* hash) {
+    return guarded([&] {
+        const std::string s = plan_export_json(plan_names());
+        if (hash) *hash = fnv1a64(s);
+        if (buf && cap) {
+            const size_t n = std::min(cap - 1, s.size());
+            std::memcpy(buf, s.data(), n);
+            buf[n] = 0;
+            if (s.size() >= cap) throw std::invalid_argument("buffer too small for catalog json");
+        }
+    });
+}
+
+int sfc_plan_create(const char* name, sfc_plan_t* out) {
+    return guarded([&] {
+        if (!name || !out) throw std::invalid_argument("null argument");
+        *out = new sfc_plan{&plan_for(name)};
+    });
+}
+
+int sfc_plan_destroy(sfc_plan_t plan) {
+    delete plan;
+    return SFC_OK;
+}
+
+int sfc_plan_dims(sfc_plan_t plan, int64_t* d) {
+    return guarded([&] {
+        if (!plan || !d) throw std::invalid_argument("null argument");
+        const SfcPlan& p = *plan->p;
+        const int64_t v[10] = {p.K, p.n_in, p.M, p.R, p.N, p.offset, p.a_denom, int64_t(p.corrections.size()),
+                               p.mults_full(), p.mults_reduced()};
+        std::memcpy(d, v, sizeof v);
+    });
+}
+
+int sfc_plan_matrices(sfc_plan_t plan, int64_t* bt, int64_t* g, int64_t* a) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("null plan");
+        const SfcPlan& p = *plan->p;
+        if (bt) std::memcpy(bt, p.BT.data(), p.BT.size() * sizeof(int64_t));
+        if (g) std::memcpy(g, p.G.data(), p.G.size() * sizeof(int64_t));
+        if (a) std::memcpy(a, p.A.data(), p.A.size() * sizeof(int64_t));
+    });
+}
+
+int sfc_layer_create(sfc_plan_t plan, const int8_t* d_w, int oc, int ic, int bits, int filter_scope, int search,
+                     void* stream, sfc_layer_t* out) {
+    sfc_layer* L = nullptr;
+    int rc = guarded([&] {
+        if (!plan || !d_w || !out) throw std::invalid_argument("null argument");
+        if (bits < 2 || bits > 16) throw std::invalid_argument("quantization width must be between 2 and 16 bits");
+        if (oc <= 0 || ic <= 0) throw std::invalid_argument("bad filter shape");
+        if (bits > 8) throw Unsupported("bits > 8 is not on the int8 tensor-core path yet");
+        if (filter_scope != SFC_FIL_PER_CHANNEL) throw Unsupported("only PerChannel filter scales on the device path");
+        if (search != SFC_SEARCH_MINMAX) throw Unsupported("only MinMax scale search on the device path");
+        L = new sfc_layer();
+        L->plan = plan->p;
+        L->variant = plan->p->variant;
+        L->OC = oc;
+        L->IC = ic;
+        L->bits = bits;
+        L->F = plan->p->K * plan->p->K;
+        ConvGeom g;
+        geom_init(g, L->variant, 1, ic, 8, 8, 1, oc);
+        L->BK = g.BK, L->Cpad = g.Cpad, L->BN = g.BN, L->OCpad = g.OCpad;
+        for (int t = 0; t < plan->p->M; ++t) {
+            int64_t l1 = 0;
+            for (int k = 0; k < plan->p->K; ++k) l1 += std::abs(plan->p->a(k, t));
+            L->max_a_col_l1 = std::max(L->max_a_col_l1, l1);
+        }
+        const size_t uq_bytes = size_t(L->F) * L->OCpad * L->Cpad;
+        ck(cudaMalloc(&L->d_uq, uq_bytes), "cudaMalloc uq");
+        ck(cudaMalloc(&L->d_sf, sizeof(double) * oc), "cudaMalloc sf");
+        ck(cudaMalloc(&L->d_umax, sizeof(int) * oc), "cudaMalloc umax");
+        ck(cudaMalloc(&L->d_sat, sizeof(unsigned long long)), "cudaMalloc sat");
+        ck(cudaMemsetAsync(L->d_uq, 0, uq_bytes, S(stream)), "memset uq");
+        ck(cudaMemsetAsync(L->d_sat, 0, sizeof(unsigned long long), S(stream)), "memset sat");
+        ck(launch_filter_prepare(L->variant, d_w, oc, ic, L->Cpad, L->OCpad, bits, L->d_sf, L->d_umax, L->d_uq,
+                                 L->d_sat, S(stream)),
+           "filter prepare launch");
+        ck(cudaStreamSynchronize(S(stream)), "filter prepare");
+        *out = L;
+    });
+    if (rc != SFC_OK && L) sfc_layer_destroy(L);
+    return rc;
+}
+
+int sfc_layer_destroy(sfc_layer_t L) {
+    if (!L) return SFC_OK;
+    cudaFree(L->d_uq);
+    cudaFree(L->d_sf);
+    cudaFree(L->d_umax);
+    cudaFree(L->d_sat);
+    delete L;
+    return SFC_OK;
+}
+
+int sfc_layer_filter_scales(sfc_layer_t L, double* sf, int32_t* umax) {
+    return guarded([&] {
+        if (!L) throw std::invalid_argument("null layer");
+        if (sf) ck(cudaMemcpy(sf, L->d_sf, sizeof(double) * L->OC, cudaMemcpyDeviceToHost), "copy sf");
+        if (umax) ck(cudaMemcpy(umax, L->d_umax, sizeof(int) * L->OC, cudaMemcpyDeviceToHost), "copy umax");
+    });
+}
+
+int sfc_layer_saturations(sfc_layer_t L, int64_t* count) {
+    return guarded([&] {
+        if (!L || !count) throw std::invalid_argument("null argument");
+        unsigned long long c = 0;
+        ck(cudaMemcpy(&c, L->d_sat, sizeof c, cudaMemcpyDeviceToHost), "copy sat");
+        *count = int64_t(c);
+    });
+}
+
+int sfc_layer_uq(sfc_layer_t L, const int8_t** d_uq, int64_t* ic_pitch, int64_t* oc_pitch) {
+    return guarded([&] {
+        if (!L) throw std::invalid_argument("null layer");
+        if (d_uq) *d_uq = L->d_uq;
+        if (ic_pitch) *ic_pitch = L->Cpad;
+        if (oc_pitch) *oc_pitch = L->OCpad;
+    });
+}
+
+int sfc_conv_workspace_size(sfc_layer_t L, int n, int h, int w, int pad, size_t* bytes) {
+    return guarded([&] {
+        if (!L || !bytes) throw std::invalid_argument("null argument");
+        if (n <= 0 || h <= 0 || w <= 0 || pad < 0) throw std::invalid_argument("bad input shape");
+        *bytes = workspace_bytes(geom_of(L, n, h, w, pad), L->F);
+    });
+}
+
+int sfc_act_absmax(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad, int32_t* d_vmax, void* stream) {
+    return guarded([&] {
+        check_call(L, d_x, n, h, w, pad);
+        if (!d_vmax) throw std::invalid_argument("null vmax");
+        ck(launch_act_absmax(L->variant, d_x, geom_of(L, n, h, w, pad), d_vmax, S(stream)), "absmax launch");
+    });
+}
+
+int sfc_conv_int8(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax, void* ws,
+                  size_t ws_bytes, const sfc_outputs* o, void* stream) {
+    return guarded([&] {
+        check_call(L, d_x, n, h, w, pad);
+        if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
+        // |y| <= (max_t sum_k |A[k,t]|)^2 * IC * qmax^2 (MinMax never clips, so |vq|,|uq| <= qmax).
+        const double qmax = double((1 << (L->bits - 1)) - 1);
+        const double bound = double(L->max_a_col_l1) * double(L->max_a_col_l1) * L->IC * qmax * qmax;
+        const bool need64 = bound >= 2147483647.0;
+        if (need64 && o->y_int32)
+            throw Unsupported("y_int may exceed int32 for this layer; request y_int64 instead");
+        WsView v = carve(ws, g, L->F);
+        cudaStream_t st = S(stream);
+        ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
+        ck(launch_quant_params(d_vmax, L->bits, v.qp, st), "quant params launch");
+        ck(launch_act_quant(L->variant, d_x, g, v.qp, L->bits, v.vq, v.sat, st), "act quant launch");
+        ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st), "gemm launch");
+        ck(launch_output(L->variant, need64, v.P, g, v.qp, L->d_sf, o->requant_scale, o->y_int32, o->y_int64,
+                         o->out_f32, o->out_i8, st),
+           "output launch");
+    });
+}
+
+int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad, void* ws, size_t ws_bytes,
+                     const sfc_outputs* o, void* stream) {
+    int rc = guarded([&] {
+        check_call(L, d_x, n, h, w, pad);
+        if (!ws) throw std::invalid_argument("null workspace");
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
+        WsView v = carve(ws, g, L->F);
+        ck(cudaMemsetAsync(v.vmax, 0, sizeof(int), S(stream)), "memset vmax");
+        ck(launch_act_absmax(L->variant, d_x, g, v.vmax, S(stream)), "absmax launch");
+    });
+    if (rc != SFC_OK) return rc;
+    return sfc_conv_int8(L, d_x, n, h, w, pad, reinterpret_cast<const int32_t*>(ws), ws, ws_bytes, o, stream);
+}
+
+int sfc_conv_stats(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, int64_t* stats, void* stream) {
+    return guarded([&] {
+        if (!L || !ws || !stats) throw std::invalid_argument("null argument");
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        WsView v = carve(const_cast<void*>(ws), g, L->F);
+        QuantParams qp;
+        unsigned long long sat = 0;
+        ck(cudaMemcpyAsync(&qp, v.qp, sizeof qp, cudaMemcpyDeviceToHost, S(stream)), "copy qp");
+        ck(cudaMemcpyAsync(&sat, v.sat, sizeof sat, cudaMemcpyDeviceToHost, S(stream)), "copy sat");
+        ck(cudaStreamSynchronize(S(stream)), "stats sync");
+        std::memcpy(&stats[0], &qp.sa, sizeof(double));
+        stats[1] = qp.vmax;
+        stats[2] = int64_t(sat);
+        stats[3] = qp.exact;
+        stats[4] = int64_t(L->OC) * L->IC * L->F + int64_t(g.T) * L->IC * L->F;
+        stats[5] = g.T;
+    });
+}
+
+int sfc_conv_views(sfc_layer_t L, int n, int h, int w, int pad, void* ws, int8_t** d_vq, int32_t** d_pacc,
+                   int64_t* geom) {
+    return guarded([&] {
+        if (!L || !ws) throw std::invalid_argument("null argument");
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        WsView v = carve(ws, g, L->F);
+        if (d_vq) *d_vq = v.vq;
+        if (d_pacc) *d_pacc = v.P;
+        if (geom) {
+            geom[0] = g.T, geom[1] = g.Tpad, geom[2] = g.Cpad, geom[3] = g.OCpad, geom[4] = g.th, geom[5] = g.tw;
+        }
+    });
+}
+
+int sfc_direct_conv_int8(const int8_t* d_x, int n, int c, int h, int w, const int8_t* d_w, int oc, int r, int stride,
+                         int pad, int32_t* d_out, void* stream) {
+    return guarded([&] {
+        if (!d_x || !d_w || !d_out) throw std::invalid_argument("null argument");
+        if (stride < 1) throw std::invalid_argument("stride must be positive");
+        if ((h + 2 * pad - r) / stride + 1 <= 0 || (w + 2 * pad - r) / stride + 1 <= 0 || h + 2 * pad < r ||
+            w + 2 * pad < r)
+            throw std::invalid_argument("filter larger than padded input");
+        ck(launch_direct_conv(d_x, n, c, h, w, d_w, oc, r, stride, pad, d_out, S(stream)), "direct conv launch");
+    });
+}
+
+int sfc_frequency_energy_int8(sfc_plan_t plan, const int8_t* d_x, int n, int c, int h, int w, int pad,
+                              unsigned long long* d_sum, void* stream) {
+    return guarded([&] {
+        if (!plan || !d_x || !d_sum) throw std::invalid_argument("null argument");
+        if (h + 2 * pad - plan->p->R + 1 <= 0 || w + 2 * pad - plan->p->R + 1 <= 0)
+            throw std::invalid_argument("filter larger than padded input");
+        ConvGeom g;
+        geom_init(g, plan->p->variant, n, c, h, w, pad, 1);
+        ck(launch_freq_energy(plan->p->variant, d_x, g, d_sum, S(stream)), "energy launch");
+    });
+}
+
+int sfc_transform_filters_int8(sfc_plan_t plan, const int8_t* d_w, int oc, int ic, int32_t* d_u, void* stream) {
+    return guarded([&] {
+        if (!plan || !d_w || !d_u) throw std::invalid_argument("null argument");
+        ck(launch_transform_filters(plan->p->variant, d_w, oc, ic, d_u, S(stream)), "transform filters launch");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,60 @@
+// Host-side plan layer: the SFC bilinear algorithms for 3x3 kernels.
+//
+// Mirrors the reference's catalog for the three 3x3 SFC variants
+// (proj/src/catalog.cpp:246-248, derive_correction_spec at catalog.cpp:132-215)
+// but derives them differently: B^T and G are assembled from the symbolic DFT
+// component rows, and the output transform A is *solved* exactly from the
+// correlation identity  sum_k A[k,t] BT[k,i] G[k,j] = N * [i == t + j]
+// (the same constraint the reference's repair tool uses, catalog.cpp:477-542),
+// so it is not a transcription of the reference's A tables.  Every plan passes
+// an exhaustive exactness gate before use and is checked against the tables
+// compiled into the CUDA kernels.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace sfcb200 {
+
+struct Correction {
+    int out, desired, wrapped, tap;
+};
+
+struct SfcPlan {
+    std::string name;
+    int N = 0, M = 0, R = 0, offset = 0;
+    int K = 0, n_in = 0;
+    int64_t a_denom = 1;
+    std::vector<int64_t> BT;  // K x n_in
+    std::vector<int64_t> G;   // K x R
+    std::vector<int64_t> A;   // K x M
+    std::vector<Correction> corrections;
+    std::vector<int> triples;  // flattened (a, b, c) per axis triple
+    int variant = -1;          // index into the compiled device tables
+
+    long mults_full() const { return long(K) * K; }
+    long mults_reduced() const {
+        long t = long(triples.size() / 3);
+        return mults_full() - 3 * t * t;
+    }
+    double complexity_pct() const { return 100.0 * double(mults_reduced()) / (double(M) * M * R * R); }
+    int64_t bt(int k, int i) const { return BT[size_t(k) * n_in + i]; }
+    int64_t g(int k, int j) const { return G[size_t(k) * R + j]; }
+    int64_t a(int k, int t) const { return A[size_t(k) * M + t]; }
+};
+
+// Throws std::invalid_argument for unknown names and std::domain_error when the
+// exactness gate fails.  Returned references live for the process lifetime.
+const SfcPlan& plan_for(const std::string& name);
+const std::vector<std::string>& plan_names();
+
+// Number of (t, i, j) triples violating sum_k A BT G = a_denom [i == t + j].
+long plan_identity_violations(const SfcPlan& p);
+
+// JSON in the reference's catalog_export_json layout (catalog.cpp:562-591)
+// restricted to `names`; FNV-1a 64 over that text.
+std::string plan_export_json(const std::vector<std::string>& names);
+uint64_t fnv1a64(const std::string& s);
+
+}  // namespace sfcb200
