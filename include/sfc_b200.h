@@ -113,6 +113,17 @@ typedef struct {
 int sfc_conv_int8(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax,
                   void* d_workspace, size_t workspace_bytes, const sfc_outputs* outs, void* stream);
 
+/* Same as sfc_conv_int8 but launches only the kernels selected by `stage_mask`
+ * (profiling / per-kernel timing; stages must still run in order on one stream). */
+#define SFC_STAGE_QPARAMS 1u   /* scale + exact quantizer from *d_vmax      */
+#define SFC_STAGE_ACT 2u       /* input transform + quantize -> vq         */
+#define SFC_STAGE_GEMM 4u      /* per-frequency int8 contraction -> pacc   */
+#define SFC_STAGE_OUTPUT 8u    /* output transform + dequant / requant     */
+#define SFC_STAGE_ALL 15u
+int sfc_conv_int8_stages(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax,
+                         void* d_workspace, size_t workspace_bytes, const sfc_outputs* outs, unsigned stage_mask,
+                         void* stream);
+
 /* Convenience: zero the workspace's vmax slot, absmax pre-pass, then sfc_conv_int8 (single GPU). */
 int sfc_conv_forward(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, void* d_workspace,
                      size_t workspace_bytes, const sfc_outputs* outs, void* stream);

@@ -446,6 +446,7 @@ int sfo_quantized_conv(const int8_t* x, int B, int C, int H, int W, const int8_t
         double all = 0.0;
         for (int f = 0; f < F; ++f) all = fmaxv[f] > all ? fmaxv[f] : all;
         vmax = (int64_t)all;
+        if (cfg->vmax_override >= 0) all = (double)cfg->vmax_override;
         if (n_act == 1) {
             double sc = all / qmax;
             act_scale[0] = sc > kScaleFloor ? sc : kScaleFloor;

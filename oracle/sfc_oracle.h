@@ -39,6 +39,8 @@ typedef struct {
     int bits, act_scope, filter_scope, search;
     int threads;      /* worker threads for the tile loop (results are thread-count independent) */
     int want_report;  /* 1: run the fp64 direct conv for mse / signal_energy / snr_db */
+    int64_t vmax_override; /* >= 0: use this max|V| for the PerTensor MinMax scale instead of the
+                              local one (a batch shard quantized with the global batch scale) */
 } sfo_config;
 
 typedef struct {

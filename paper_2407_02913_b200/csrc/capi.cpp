@@ -255,6 +255,11 @@ int sfc_act_absmax(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pa
 
 int sfc_conv_int8(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax, void* ws,
                   size_t ws_bytes, const sfc_outputs* o, void* stream) {
+    return sfc_conv_int8_stages(L, d_x, n, h, w, pad, d_vmax, ws, ws_bytes, o, SFC_STAGE_ALL, stream);
+}
+
+int sfc_conv_int8_stages(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax,
+                         void* ws, size_t ws_bytes, const sfc_outputs* o, unsigned mask, void* stream) {
     return guarded([&] {
         check_call(L, d_x, n, h, w, pad);
         if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
@@ -268,13 +273,14 @@ int sfc_conv_int8(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad
             throw Unsupported("y_int may exceed int32 for this layer; request y_int64 instead");
         WsView v = carve(ws, g, L->F);
         cudaStream_t st = S(stream);
-        ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
-        ck(launch_quant_params(d_vmax, L->bits, v.qp, st), "quant params launch");
-        ck(launch_act_quant(L->variant, d_x, g, v.qp, L->bits, v.vq, v.sat, st), "act quant launch");
-        ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st), "gemm launch");
-        ck(launch_output(L->variant, need64, v.P, g, v.qp, L->d_sf, o->requant_scale, o->y_int32, o->y_int64,
-                         o->out_f32, o->out_i8, st),
-           "output launch");
+        if (mask & SFC_STAGE_QPARAMS) ck(launch_quant_params(d_vmax, L->bits, v.qp, v.sat, st), "quant params launch");
+        if (mask & SFC_STAGE_ACT)
+            ck(launch_act_quant(L->variant, d_x, g, v.qp, L->bits, v.vq, v.sat, st), "act quant launch");
+        if (mask & SFC_STAGE_GEMM) ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st), "gemm launch");
+        if (mask & SFC_STAGE_OUTPUT)
+            ck(launch_output(L->variant, need64, v.P, g, v.qp, L->d_sf, o->requant_scale, o->y_int32, o->y_int64,
+                             o->out_f32, o->out_i8, st),
+               "output launch");
     });
 }
 

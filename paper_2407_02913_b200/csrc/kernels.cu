@@ -185,8 +185,8 @@ __global__ void __launch_bounds__(256) k_act_transform(const int8_t* __restrict_
 // rint(double(v) / sa) for every integer |v| <= vmax, verified exhaustively
 // here (falls back to per-element fp64 division if no candidate is exact,
 // e.g. when exact ties alternate their rounding direction).
-__global__ void __launch_bounds__(256) k_quant_params(const int* __restrict__ vmax_p, int bits,
-                                                      QuantParams* __restrict__ qp) {
+__global__ void __launch_bounds__(1024) k_quant_params(const int* __restrict__ vmax_p, int bits,
+                                                       QuantParams* __restrict__ qp, unsigned long long* sat) {
     const int vmax = *vmax_p;
     const int qmax = (1 << (bits - 1)) - 1;
     const double sa = fmax(double(vmax) / double(qmax), 1e-8);
@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(256) k_quant_params(const int* __restrict__ vm
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        *sat = 0;  // activation saturation counter of this call
         QuantParams p;
         p.sa = sa;
         p.shift = shift;
@@ -504,8 +505,9 @@ cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, i
     }
 }
 
-cudaError_t launch_quant_params(const int* vmax, int bits, QuantParams* qp, cudaStream_t st) {
-    k_quant_params<<<1, 256, 0, st>>>(vmax, bits, qp);
+cudaError_t launch_quant_params(const int* vmax, int bits, QuantParams* qp, unsigned long long* sat,
+                                cudaStream_t st) {
+    k_quant_params<<<1, 1024, 0, st>>>(vmax, bits, qp, sat);
     return cudaGetLastError();
 }
 

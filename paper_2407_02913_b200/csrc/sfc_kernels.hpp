@@ -34,7 +34,8 @@ size_t workspace_bytes(const ConvGeom& g, int F);
 cudaError_t launch_filter_prepare(int variant, const int8_t* w, int OC, int IC, int Cpad, int OCpad, int bits,
                                   double* sf, int* umax, int8_t* uqB, unsigned long long* sat, cudaStream_t st);
 cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, cudaStream_t st);
-cudaError_t launch_quant_params(const int* vmax, int bits, QuantParams* qp, cudaStream_t st);
+cudaError_t launch_quant_params(const int* vmax, int bits, QuantParams* qp, unsigned long long* sat,
+                                cudaStream_t st);
 cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, const QuantParams* qp, int bits,
                              int8_t* vqA, unsigned long long* sat, cudaStream_t st);
 cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F,

@@ -1,0 +1,80 @@
+"""Batch-sharded multi-GPU execution of one quantized SFC layer (one process per GPU).
+
+SURVEY.md §8(e): tiles and images are independent, so the batch is split across ranks
+with no data-path collective.  The single exchange needed for bit-exactness is the
+per-tensor activation scale, which the reference takes over the *whole* batch
+(proj/src/quant.cpp:171-172): every rank runs the absmax pre-pass on its shard, then one
+all-reduce(MAX) of an int32 (order-free, exact) makes the scale global before
+quantization.  Outputs are gathered to rank 0 only for checking, outside timing.
+
+The engine is injected so the same host logic runs on the GPU (``CudaEngine`` over the
+C-ABI, NCCL) and in the CPU multi-process tests (gloo + a test engine).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def shard_bounds(batch: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced batch shard [lo, hi) of `rank` (sizes differ by at most one)."""
+    base, rem = divmod(batch, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+class CudaEngine:
+    """Adapter of sfconv.SfcLayer to the engine protocol used by ShardedConv."""
+
+    def __init__(self, layer, pad: int):
+        self.layer, self.pad = layer, pad
+        self._ws = {}
+
+    def new_vmax(self, device):
+        return torch.zeros(1, dtype=torch.int32, device=device)
+
+    def absmax(self, x, vmax):
+        self.layer.absmax(x, vmax, self.pad)
+
+    def conv(self, x, vmax, **outs):
+        key = tuple(x.shape)
+        if key not in self._ws:
+            n, _, h, w = x.shape
+            self._ws[key] = self.layer.workspace(n, h, w, self.pad)
+        self.layer.conv(x, vmax, self._ws[key], self.pad, **outs)
+
+
+@dataclass
+class ShardedConv:
+    engine: object
+    group: object = None
+
+    def forward(self, x_local, **outs):
+        """absmax on the local shard -> all-reduce(MAX) -> quantize/contract/transform locally."""
+        vmax = self.engine.new_vmax(x_local.device)
+        self.engine.absmax(x_local, vmax)
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(vmax, op=dist.ReduceOp.MAX, group=self.group)
+        self.engine.conv(x_local, vmax, **outs)
+        return vmax
+
+    @staticmethod
+    def gather_to_rank0(t_local, batch: int, group=None):
+        """Concatenate every rank's output shard on rank 0 (checking only; not timed)."""
+        if not dist.is_initialized() or dist.get_world_size(group) == 1:
+            return t_local
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        shapes = [shard_bounds(batch, r, world) for r in range(world)]
+        bufs = [t_local.new_empty((hi - lo,) + tuple(t_local.shape[1:])) for lo, hi in shapes]
+        if t_local.device.type == "cpu":  # gloo has no gather of unequal sizes; use all_gather of padded
+            maxn = max(hi - lo for lo, hi in shapes)
+            pad = t_local.new_zeros((maxn,) + tuple(t_local.shape[1:]))
+            pad[: t_local.shape[0]] = t_local
+            allp = [torch.empty_like(pad) for _ in range(world)]
+            dist.all_gather(allp, pad, group=group)
+            bufs = [p[: hi - lo] for p, (lo, hi) in zip(allp, shapes)]
+        else:
+            dist.all_gather(bufs, t_local.contiguous(), group=group)
+        return torch.cat(bufs, 0) if rank == 0 else None

@@ -1,0 +1,99 @@
+"""Generate the committed golden fixtures from the *reference itself* (oracle/_ref, built
+from /root/reference/proj/src by oracle/Makefile).  Run in the build container:
+
+    python tests/golden/make_golden.py
+
+Writes tests/golden/catalog_3x3.json (the reference's catalog export restricted to the
+three 3x3 SFC specs + the full-catalog FNV hash) and tests/golden/qconv_cases.npz (seeded
+int8 inputs, the reference's quantized_fast_conv2d output and report, its fp64
+direct_conv2d and transform_filters, and scalar known answers).  The fixtures pin the
+oracle and the GPU path on a box where /root/reference does not exist.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import bindings as ob  # noqa: E402
+
+VARIANTS = ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]
+
+# (tag, B, C, OC, H, W, pad, lo, bits, act_scope, filter_scope, search)
+CASES = [
+    ("small_p1", 1, 8, 8, 14, 14, 1, -128, 8, 0, 0, 0),
+    ("ragged_p1", 2, 5, 3, 13, 11, 1, -128, 8, 0, 0, 0),
+    ("relu_p0", 1, 16, 4, 12, 12, 0, 0, 8, 0, 0, 0),
+    ("pad2", 1, 4, 6, 9, 10, 2, -128, 8, 0, 0, 0),
+    ("bits4", 1, 6, 5, 11, 11, 1, -128, 4, 0, 0, 0),
+    ("bits6", 1, 6, 5, 11, 11, 1, -128, 6, 0, 0, 0),
+    ("bits2", 1, 3, 2, 8, 8, 1, -128, 2, 0, 0, 0),
+    ("bits12", 1, 3, 2, 8, 8, 1, -128, 12, 0, 0, 0),
+    ("actfreq", 1, 6, 4, 12, 12, 1, -128, 8, 1, 0, 0),
+    ("filfreq", 1, 6, 4, 12, 12, 1, -128, 8, 0, 1, 0),
+    ("filchfreq", 1, 6, 4, 12, 12, 1, -128, 8, 1, 2, 0),
+    ("msegrid", 1, 3, 3, 10, 10, 1, -128, 8, 0, 0, 1),
+    ("tiny_h", 1, 2, 2, 3, 3, 1, -128, 8, 0, 0, 0),
+]
+
+
+def main():
+    if not ob.ref_available():
+        raise SystemExit("oracle/_ref/libsfconv_ref.so missing: run `make -C oracle` with /root/reference present")
+    js, h = ob.ref_catalog_json()
+    full = json.loads(js)
+    sel = [a for a in full["algorithms"] if a["name"] in VARIANTS]
+    raw = {a["name"]: js[js.index('{"name":"' + a["name"]):] for a in sel}
+    exact = {}
+    for name, tail in raw.items():  # the exact substring of the reference export for each algorithm
+        depth = 0
+        for i, ch in enumerate(tail):
+            depth += ch == "{"
+            depth -= ch == "}"
+            if depth == 0:
+                exact[name] = tail[: i + 1]
+                break
+    with open(os.path.join(HERE, "catalog_3x3.json"), "w") as f:
+        json.dump({"full_catalog_fnv1a64": f"{h:016x}", "algorithms": sel, "exact_text": exact}, f, indent=1)
+
+    arrays = {}
+    rng = np.random.default_rng(0x5FC0)
+    for tag, B, C, OC, H, W, pad, lo, bits, asc, fsc, srch in CASES:
+        x = rng.integers(lo, 128, size=(B, C, H, W), dtype=np.int8)
+        w = rng.integers(-127, 128, size=(OC, C, 3, 3), dtype=np.int8)
+        arrays[f"{tag}/x"] = x
+        arrays[f"{tag}/w"] = w
+        arrays[f"{tag}/meta"] = np.array([pad, bits, asc, fsc, srch], np.int64)
+        arrays[f"{tag}/direct"] = ob.ref_direct_conv2d(x, w, pad)
+        for v in VARIANTS:
+            out, rep = ob.ref_quantized_fast_conv2d(x, w, v, pad, bits, asc, fsc, srch)
+            arrays[f"{tag}/{v}/out"] = out
+            arrays[f"{tag}/{v}/report"] = np.array([rep["mse"], rep["signal_energy"], rep["snr_db"],
+                                                    rep["saturations"], rep["values_quantized"]], np.float64)
+            if tag == "small_p1":
+                arrays[f"{tag}/{v}/u"] = ob.ref_transform_filters(w, v)
+                xe = rng.integers(-128, 128, size=(1, 3, 14, 14), dtype=np.int8)
+                arrays[f"{tag}/{v}/energy_x"] = xe
+                arrays[f"{tag}/{v}/energy"] = ob.ref_frequency_energy(xe, v, 1)
+    # scalar known answers (test_quant.cpp:34-72) evaluated by the reference
+    kat_in = [(2.5, 1.0, 8), (3.5, 1.0, 8), (-2.5, 1.0, 8), (2.4999, 1.0, 8), (0.26, 0.1, 8), (127.4, 1.0, 8),
+              (127.6, 1.0, 8), (-128.4, 1.0, 8), (-130.0, 1.0, 8), (9.0, 1.0, 4), (-9.0, 1.0, 4),
+              (1020.0, 2040.0 / 127.0, 8), (-1020.0, 2040.0 / 127.0, 8)]
+    arrays["kat/quantize_in"] = np.array(kat_in, np.float64)
+    arrays["kat/quantize_out"] = np.array([ob.ref_quantize_value(*k) for k in kat_in], np.int64)
+    grp = rng.normal(size=200)
+    grp[0] = 12.0
+    arrays["kat/scale_group"] = grp
+    arrays["kat/scale_out"] = np.array([ob.ref_scale([-3.0, 1.0, 2.0], 8), ob.ref_scale([-3.0, 1.0, 2.0], 4),
+                                        ob.ref_scale(np.zeros(10), 8), ob.ref_scale(grp, 8),
+                                        ob.ref_scale(grp, 8, True), ob.ref_scale(grp, 4, True)], np.float64)
+    np.savez_compressed(os.path.join(HERE, "qconv_cases.npz"), **arrays)
+    print("wrote", len(arrays), "arrays")
+
+
+if __name__ == "__main__":
+    main()
