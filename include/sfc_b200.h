@@ -154,6 +154,11 @@ int sfc_frequency_energy_int8(sfc_plan_t plan, const int8_t* d_x, int n, int c, 
 int sfc_transform_filters_int8(sfc_plan_t plan, const int8_t* d_weights, int oc, int ic, int32_t* d_u,
                                void* stream);
 
+/* Test hook: run the device activation quantizer for every integer v in [-vmax, vmax]
+ * (d_q has 2*vmax+1 int32 slots); info[4] = {fast path exact flag, shift, multiplier,
+ * sa as double bits}.  Synchronous. */
+int sfc_debug_quantizer(int vmax, int bits, int32_t* d_q, int64_t* info, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -543,7 +543,8 @@ int sfo_quantized_conv(const int8_t* x, int B, int C, int H, int W, const int8_t
         wk[i].pacc_out = pacc;
         wk[i].vq_out = vq;
     }
-    run_threads(pass_main, wk, nthreads);
+    /* Nothing requested from the tile loop: the call only wanted scales / vmax. */
+    if (out || y_int || pacc || vq) run_threads(pass_main, wk, nthreads);
     for (int i = 0; i < nthreads; ++i) saturations += wk[i].saturations;
     free(wk);
 

@@ -20,7 +20,7 @@ EXPORTED = (
     "sfc_plan_matrices", "sfc_layer_create", "sfc_layer_destroy", "sfc_layer_filter_scales",
     "sfc_layer_saturations", "sfc_layer_uq", "sfc_conv_workspace_size", "sfc_act_absmax", "sfc_conv_int8",
     "sfc_conv_int8_stages", "sfc_conv_forward", "sfc_conv_stats", "sfc_conv_views", "sfc_direct_conv_int8", "sfc_frequency_energy_int8",
-    "sfc_transform_filters_int8",
+    "sfc_transform_filters_int8", "sfc_debug_quantizer",
 )
 
 
@@ -79,6 +79,7 @@ _SIGS = {
     "sfc_direct_conv_int8": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp]),
     "sfc_frequency_energy_int8": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "sfc_transform_filters_int8": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
+    "sfc_debug_quantizer": (_i, [_i, _i, _vp, _i64p, _vp]),
 }
 
 

@@ -363,4 +363,28 @@ int sfc_transform_filters_int8(sfc_plan_t plan, const int8_t* d_w, int oc, int i
     });
 }
 
+int sfc_debug_quantizer(int vmax, int bits, int32_t* d_q, int64_t* info, void* stream) {
+    return guarded([&] {
+        if (!d_q || vmax < 0 || bits < 2 || bits > 8) throw std::invalid_argument("bad quantizer probe");
+        void* scratch = nullptr;
+        ck(cudaMallocAsync(&scratch, 256, S(stream)), "alloc");
+        int* d_vmax = static_cast<int*>(scratch);
+        unsigned long long* sat = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 8);
+        QuantParams* qp = reinterpret_cast<QuantParams*>(static_cast<uint8_t*>(scratch) + 64);
+        ck(cudaMemcpyAsync(d_vmax, &vmax, sizeof(int), cudaMemcpyHostToDevice, S(stream)), "copy vmax");
+        ck(launch_quant_params(d_vmax, bits, qp, sat, S(stream)), "qparams");
+        ck(launch_debug_quant(qp, vmax, d_q, sat, S(stream)), "debug quant");
+        QuantParams h;
+        ck(cudaMemcpyAsync(&h, qp, sizeof h, cudaMemcpyDeviceToHost, S(stream)), "copy qp");
+        ck(cudaStreamSynchronize(S(stream)), "sync");
+        ck(cudaFreeAsync(scratch, S(stream)), "free");
+        if (info) {
+            info[0] = h.exact;
+            info[1] = h.shift;
+            info[2] = h.mul;
+            std::memcpy(&info[3], &h.sa, sizeof(double));
+        }
+    });
+}
+
 }  // extern "C"

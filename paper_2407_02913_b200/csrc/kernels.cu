@@ -695,3 +695,19 @@ cudaError_t launch_transform_filters(int variant, const int8_t* w, int OC, int I
 }
 
 }  // namespace sfcb200
+
+namespace sfcb200 {
+// Debug / test hook: q(v) for every integer v in [-vmax, vmax] through the same device
+// quantizer the activation kernel uses (fast multiply-shift or the fp64 fallback).
+__global__ void k_debug_quant(const QuantParams* __restrict__ qpp, int vmax, int32_t* __restrict__ q,
+                              unsigned long long* sat) {
+    const QuantParams qp = *qpp;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= 2 * vmax; i += gridDim.x * blockDim.x)
+        q[i] = quant_act(i - vmax, qp, sat);
+}
+
+cudaError_t launch_debug_quant(const QuantParams* qp, int vmax, int32_t* q, unsigned long long* sat, cudaStream_t st) {
+    k_debug_quant<<<64, 256, 0, st>>>(qp, vmax, q, sat);
+    return cudaGetLastError();
+}
+}  // namespace sfcb200

@@ -48,6 +48,7 @@ cudaError_t launch_direct_conv(const int8_t* x, int B, int C, int H, int W, cons
                                int stride, int pad, int32_t* out, cudaStream_t st);
 cudaError_t launch_freq_energy(int variant, const int8_t* x, const ConvGeom& g, unsigned long long* sum,
                                cudaStream_t st);
+cudaError_t launch_debug_quant(const QuantParams* qp, int vmax, int32_t* q, unsigned long long* sat, cudaStream_t st);
 cudaError_t launch_transform_filters(int variant, const int8_t* w, int OC, int IC, int32_t* u, cudaStream_t st);
 
 }  // namespace sfcb200

@@ -1,0 +1,281 @@
+"""GPU parity of the B200 path (libsfc_b200.so via the C-ABI) against the oracle and the
+reference's golden fixtures.
+
+Bar (BASELINE.json north_star): integer transform-domain values (vq, uq), per-frequency
+contractions (pacc) and the output accumulator y_int bit-exact; the dequantised fp32
+output within max|got - want| / max|want| <= 1e-6 (the reference's own error metric,
+proj/tests/test_conv.cpp:47-55).
+"""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import bindings as ob  # noqa: E402
+from paper_2407_02913_b200 import _lib, sfconv as sc, workloads as wl  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = np.load(os.path.join(HERE, "golden", "qconv_cases.npz"))
+VARIANTS = ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]
+TOL = 1e-6
+
+
+def maxrel(got, want):
+    want = np.asarray(want, np.float64)
+    den = np.abs(want).max()
+    return np.abs(np.asarray(got, np.float64) - want).max() / (den if den > 0 else 1.0)
+
+
+def run_gpu(x, w, variant, pad=1, bits=8, outs=("y", "f32"), requant=0.0, vmax=None, views=True):
+    dev = torch.device("cuda", 0)
+    layer = sc.SfcLayer(variant, torch.from_numpy(w).to(dev), bits=bits)
+    xt = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    B, C, H, W = x.shape
+    HO, WO = H + 2 * pad - 2, W + 2 * pad - 2
+    ws = layer.workspace(B, H, W, pad)
+    res = {}
+    kw = {}
+    if "y" in outs:
+        kw["y_int32"] = res["y"] = torch.empty((B, w.shape[0], HO, WO), dtype=torch.int32, device=dev)
+    if "f32" in outs:
+        kw["out_f32"] = res["f32"] = torch.empty((B, w.shape[0], HO, WO), dtype=torch.float32, device=dev)
+    if "i8" in outs:
+        kw["out_i8"] = res["i8"] = torch.empty((B, w.shape[0], HO, WO), dtype=torch.int8, device=dev)
+    if vmax is None:
+        layer.forward(xt, ws, pad, requant_scale=requant, **kw)
+    else:
+        vm = torch.tensor([vmax], dtype=torch.int32, device=dev)
+        layer.conv(xt, vm, ws, pad, requant_scale=requant, **kw)
+    torch.cuda.synchronize()
+    out = {k: v.cpu().numpy() for k, v in res.items()}
+    out["stats"] = layer.stats(B, H, W, pad, ws)
+    out["sf"], out["umax"] = layer.filter_scales()
+    if views:
+        vq, pacc = layer.views(B, H, W, pad, ws)
+        out["vq"], out["pacc"] = vq.cpu().numpy(), pacc.cpu().numpy()
+        out["uq"] = layer.uq().cpu().numpy()
+    out["filter_sat"] = layer.filter_saturations()
+    return out
+
+
+def check_against_oracle(x, w, variant, pad=1, bits=8, intermediates=True):
+    want = ("out", "y_int", "pacc", "vq", "uq") if intermediates else ("out", "y_int")
+    r = ob.quantized_conv(x, w, variant, pad, bits, want=want)
+    g = run_gpu(x, w, variant, pad, bits, views=intermediates)
+    assert np.array_equal(g["sf"], r["fil_scale"]), "filter scales"
+    assert g["stats"]["act_scale"] == r["act_scale"][0], "activation scale"
+    if intermediates:
+        assert np.array_equal(g["uq"], r["uq"].transpose(2, 0, 1)), "uq"
+        assert np.array_equal(g["vq"], r["vq"].transpose(2, 0, 1)), "vq"
+        assert np.array_equal(g["pacc"].astype(np.int64), r["pacc"].transpose(2, 0, 1)), "pacc"
+    assert np.array_equal(g["y"].astype(np.int64), r["y_int"]), "y_int"
+    assert maxrel(g["f32"], r["out"]) <= TOL
+    assert g["stats"]["saturations"] + g["filter_sat"] == 0
+    return g, r
+
+
+# ------------------------------------------------------------------------------ small seeded cases
+CASES = [  # (B, C, OC, H, W, pad, lo)
+    (1, 8, 8, 14, 14, 1, -128),
+    (2, 5, 3, 13, 11, 1, -128),
+    (1, 3, 17, 9, 23, 0, 0),
+    (3, 64, 64, 12, 12, 1, 0),
+    (1, 65, 130, 10, 10, 2, -128),
+    (2, 130, 33, 7, 7, 1, -128),
+    (1, 17, 257, 6, 6, 1, -128),
+    (1, 1, 1, 1, 1, 1, -128),
+    (1, 2, 2, 3, 3, 0, -128),
+]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("case", CASES, ids=[f"b{c[0]}c{c[1]}o{c[2]}h{c[3]}w{c[4]}p{c[5]}" for c in CASES])
+def test_small_cases_bit_exact(cuda, variant, case):
+    B, C, OC, H, W, pad, lo = case
+    rng = np.random.default_rng(hash(case) & 0xFFFF)
+    x = rng.integers(lo, 128, size=(B, C, H, W), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(OC, C, 3, 3), dtype=np.int8)
+    check_against_oracle(x, w, variant, pad)
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_bit_widths(cuda, variant, bits):
+    rng = np.random.default_rng(bits)
+    x = rng.integers(-128, 128, size=(2, 9, 15, 13), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(6, 9, 3, 3), dtype=np.int8)
+    check_against_oracle(x, w, variant, 1, bits)
+
+
+# ------------------------------------------------------------------------------ golden fixtures
+GOLD_TAGS = sorted({k.split("/")[0] for k in GOLD.files if k.endswith("/meta")})
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("tag", GOLD_TAGS)
+def test_golden_reference_outputs(cuda, tag, variant):
+    pad, bits, asc, fsc, srch = (int(v) for v in GOLD[f"{tag}/meta"])
+    if bits > 8 or asc or fsc or srch:
+        pytest.skip("configuration outside the device path (bits > 8 / per-frequency scopes / MseGrid)")
+    x, w = GOLD[f"{tag}/x"], GOLD[f"{tag}/w"]
+    ref = GOLD[f"{tag}/{variant}/out"]
+    g = run_gpu(x, w, variant, pad, bits)
+    assert maxrel(g["f32"], ref) <= TOL
+    d2 = sc.catalog_algorithm(variant).a_denom ** 2
+    rec = np.rint(ref * d2 / (g["stats"]["act_scale"] * g["sf"][None, :, None, None])).astype(np.int64)
+    assert np.array_equal(rec, g["y"].astype(np.int64))
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_golden_report_via_public_api(cuda, variant):
+    tag = "small_p1"
+    x, w = GOLD[f"{tag}/x"], GOLD[f"{tag}/w"]
+    rep_ref = GOLD[f"{tag}/{variant}/report"]
+    rep = sc.quantized_fast_conv2d(torch.from_numpy(x), torch.from_numpy(w), sc.catalog_algorithm(variant), 1)
+    assert rep.mse == pytest.approx(rep_ref[0], rel=1e-9)
+    assert rep.signal_energy == pytest.approx(rep_ref[1], rel=1e-12)
+    assert rep.snr_db == pytest.approx(rep_ref[2], rel=1e-9)
+    assert rep.saturations == rep_ref[3] and rep.values_quantized == rep_ref[4]
+    assert maxrel(rep.output.cpu().numpy(), GOLD[f"{tag}/{variant}/out"]) <= TOL
+    # the rest of the reference API on the device
+    u = sc.transform_filters(torch.from_numpy(w), sc.catalog_algorithm(variant)).cpu().numpy()
+    assert np.array_equal(u, GOLD[f"{tag}/{variant}/u"])
+    e = sc.frequency_energy(torch.from_numpy(GOLD[f"{tag}/{variant}/energy_x"]), sc.catalog_algorithm(variant), 1)
+    assert np.array_equal(e, GOLD[f"{tag}/{variant}/energy"])
+
+
+def test_golden_direct_conv(cuda):
+    for tag in GOLD_TAGS:
+        x, w = GOLD[f"{tag}/x"], GOLD[f"{tag}/w"]
+        pad = int(GOLD[f"{tag}/meta"][0])
+        got = sc.direct_conv2d(torch.from_numpy(x), torch.from_numpy(w), 1, pad).cpu().numpy()
+        assert np.array_equal(got, GOLD[f"{tag}/direct"])
+
+
+def test_frequency_energy_dc(cuda):
+    # test_quant.cpp:97-107
+    e = sc.frequency_energy(torch.ones((1, 1, 14, 14), dtype=torch.int8), sc.catalog_algorithm("sfc6-6x6-3x3"), 0)
+    assert e[0] == 1296.0 and np.all(e[1:] == 0.0)
+
+
+# ------------------------------------------------------------------------------ BASELINE configs
+@pytest.mark.parametrize("variant", ["sfc6-6x6-3x3"])
+def test_config1_bit_exact(cuda, variant):
+    L = wl.WORKLOADS[1].layers[0]
+    check_against_oracle(wl.activations(1, 0, L), wl.weights(1, 0, L), variant)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_config2_bit_exact(cuda, variant):
+    L = wl.WORKLOADS[2].layers[0]
+    check_against_oracle(wl.activations(2, 0, L), wl.weights(2, 0, L), variant)
+
+
+@pytest.mark.slow
+def test_config5_bit_exact(cuda):
+    L = wl.WORKLOADS[5].layers[0]
+    x, w = wl.activations(5, 0, L), wl.weights(5, 0, L)
+    check_against_oracle(x, w, "sfc6-6x6-3x3", intermediates=False)
+
+
+@pytest.mark.parametrize("cfg,idx", [(3, 0), (3, 4), (3, 7), (3, 10), (4, 0), (4, 2), (4, 8), (4, 12)])
+def test_stack_layers_shard_properties(cuda, cfg, idx):
+    """Full-size ResNet-18 / VGG-16 layers: the GPU global absmax equals the oracle's, and a
+    2-image shard of the full-batch output (y_int and harness int8 requant) is bit-exact against
+    the oracle run on those images with the full-batch scale (size-independent check)."""
+    work = wl.WORKLOADS[cfg]
+    L = work.layers[idx]
+    x, w = wl.activations(cfg, idx, L), wl.weights(cfg, idx, L)
+    s_l = float(wl.requant_scales(cfg, len(work.layers))[idx])
+    g = run_gpu(x, w, "sfc6-6x6-3x3", L.pad, outs=("y", "i8"), requant=s_l, views=False)
+    full = ob.quantized_conv(x, w, "sfc6-6x6-3x3", L.pad, want=())
+    assert g["stats"]["vmax"] == full["report"]["vmax"]
+    pick = np.random.default_rng(idx).choice(L.batch, size=2, replace=False)
+    part = ob.quantized_conv(x[pick], w, "sfc6-6x6-3x3", L.pad, want=("y_int",), vmax_override=full["report"]["vmax"])
+    assert np.array_equal(g["y"][pick].astype(np.int64), part["y_int"])
+    # harness requant: clamp(rint(y * (sa * sf / 36) * s), 0, 127) in fp64
+    scale = (g["stats"]["act_scale"] * g["sf"]) / 36.0
+    want8 = np.clip(np.rint(g["y"].astype(np.float64) * scale[None, :, None, None] * s_l), 0, 127).astype(np.int8)
+    assert np.array_equal(g["i8"], want8)
+
+
+# ------------------------------------------------------------------------------ quantizer exactness
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_device_quantizer_exhaustive(cuda, bits):
+    """Every integer v in [-vmax, vmax] for many vmax (incl. tie-prone multiples of 127 and 254):
+    device q(v) == rint(v / sa) with sa = max(vmax / qmax, 1e-8) in fp64 (quant.cpp:102-120)."""
+    qmax = (1 << (bits - 1)) - 1
+    vmaxes = sorted(set(list(range(0, 300)) + list(range(300, 4609, 37)) + [127 * k for k in range(1, 37)] +
+                        [254 * k for k in range(1, 19)] + [1020, 2040, 2041, 3084, 3164, 4064, 4572, 4607, 4608]))
+    n_fast = 0
+    for vmax in vmaxes:
+        d = torch.empty(2 * vmax + 1, dtype=torch.int32, device="cuda")
+        info = np.zeros(4, np.int64)
+        _lib.check(_lib.lib().sfc_debug_quantizer(vmax, bits, ctypes.c_void_p(d.data_ptr()),
+                                                  info.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), None))
+        sa = max(vmax / qmax, 1e-8)
+        assert info[3:4].view(np.float64)[0] == sa
+        v = np.arange(-vmax, vmax + 1, dtype=np.float64)
+        want = np.clip(np.rint(v / sa), -qmax - 1, qmax).astype(np.int32)
+        assert np.array_equal(d.cpu().numpy(), want), f"vmax={vmax} bits={bits} fast={info[0]}"
+        n_fast += int(info[0])
+    assert n_fast >= 0.9 * len(vmaxes)   # the verified multiply-shift path is the common case
+
+
+# ------------------------------------------------------------------------------ edge cases / errors
+def test_zero_and_constant_inputs(cuda):
+    w = np.random.default_rng(5).integers(-127, 128, size=(4, 3, 3, 3), dtype=np.int8)
+    for x in (np.zeros((1, 3, 10, 10), np.int8), np.full((1, 3, 10, 10), 7, np.int8),
+              np.full((2, 3, 5, 9), -128, np.int8)):
+        for v in VARIANTS:
+            check_against_oracle(x, w, v)
+    g = run_gpu(np.zeros((1, 3, 10, 10), np.int8), w, "sfc6-6x6-3x3")
+    assert g["stats"]["act_scale"] == 1e-8 and g["stats"]["vmax"] == 0 and not g["y"].any()
+
+
+def test_zero_filters(cuda):
+    x = np.random.default_rng(6).integers(-128, 128, size=(1, 4, 8, 8), dtype=np.int8)
+    w = np.zeros((3, 4, 3, 3), np.int8)
+    g, r = check_against_oracle(x, w, "sfc6-7x7-3x3")
+    assert np.all(g["sf"] == 1e-8) and not g["y"].any()
+
+
+def test_errors_like_reference(cuda):
+    spec = sc.catalog_algorithm("sfc4-4x4-3x3")
+    x = torch.zeros((1, 1, 8, 8), dtype=torch.int8)
+    f = torch.zeros((1, 1, 3, 3), dtype=torch.int8)
+    for bits in (1, 17):   # test_quant.cpp:190-199
+        with pytest.raises(ValueError, match="between 2 and 16 bits"):
+            sc.quantized_fast_conv2d(x, f, spec, 1, sc.QuantConfig(bits=bits))
+    with pytest.raises(ValueError, match="filter shape does not match"):
+        sc.transform_filters(torch.zeros((1, 1, 5, 5)), spec)
+    with pytest.raises(ValueError, match="input channel count"):
+        sc.quantized_fast_conv2d(torch.zeros((1, 2, 8, 8), dtype=torch.int8), f, spec, 1)
+    with pytest.raises(ValueError, match="filter larger than padded input"):
+        sc.quantized_fast_conv2d(torch.zeros((1, 1, 2, 2), dtype=torch.int8), f, spec, 0)
+    with pytest.raises(ValueError, match="int8-valued"):
+        sc.quantized_fast_conv2d(torch.full((1, 1, 8, 8), 0.5), f, spec, 1)
+    with pytest.raises(_lib.SfcUnsupported):
+        sc.quantized_fast_conv2d(x, f, spec, 1, sc.QuantConfig(bits=12))
+
+
+def test_concurrent_streams_match(cuda):
+    """Layers are immutable; two calls on two streams with distinct workspaces agree."""
+    L = wl.WORKLOADS[2].layers[0]
+    x = torch.from_numpy(wl.activations(2, 0, L)).cuda()
+    w = torch.from_numpy(wl.weights(2, 0, L)).cuda()
+    layer = sc.SfcLayer("sfc6-6x6-3x3", w)
+    outs = []
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for s in streams:
+        with torch.cuda.stream(s):
+            ws = layer.workspace(8, 28, 28, 1)
+            y = torch.empty((8, 128, 28, 28), dtype=torch.int32, device="cuda")
+            layer.forward(x, ws, 1, y_int32=y, stream=s)
+            outs.append(y)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
