@@ -115,8 +115,8 @@ int sfc_conv_int8(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int
 
 /* Same as sfc_conv_int8 but launches only the kernels selected by `stage_mask`
  * (profiling / per-kernel timing; stages must still run in order on one stream). */
-#define SFC_STAGE_QPARAMS 1u   /* scale + exact quantizer from *d_vmax      */
-#define SFC_STAGE_ACT 2u       /* input transform + quantize -> vq         */
+#define SFC_STAGE_QPARAMS 1u   /* reset the activation saturation counter  */
+#define SFC_STAGE_ACT 2u       /* scale + exact quantizer from *d_vmax, input transform, quantize -> vq */
 #define SFC_STAGE_GEMM 4u      /* per-frequency int8 contraction -> pacc   */
 #define SFC_STAGE_OUTPUT 8u    /* output transform + dequant / requant     */
 #define SFC_STAGE_ALL 15u

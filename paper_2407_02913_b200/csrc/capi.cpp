@@ -107,6 +107,42 @@ ConvGeom geom_of(const sfc_layer* L, int n, int h, int w, int pad) {
     geom_init(g, L->variant, n, L->IC, h, w, pad, L->OC);
     return g;
 }
+
+// Launch the per-call kernels.  `chained`: the previous operation on the stream is
+// this call's absmax kernel, so the activation kernel may start under PDL.  Inside a
+// full call every kernel after the first overlaps its predecessor's tail (PDL); the
+// kernels themselves wait (griddepcontrol.wait) before consuming upstream results.
+void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax, void* ws,
+              size_t ws_bytes, const sfc_outputs* o, unsigned mask, bool chained, cudaStream_t st) {
+    check_call(L, d_x, n, h, w, pad);
+    if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
+    const ConvGeom g = geom_of(L, n, h, w, pad);
+    if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
+    // |y| <= (max_t sum_k |A[k,t]|)^2 * IC * qmax^2 (MinMax never clips, so |vq|,|uq| <= qmax).
+    const double qmax = double((1 << (L->bits - 1)) - 1);
+    const double bound = double(L->max_a_col_l1) * double(L->max_a_col_l1) * L->IC * qmax * qmax;
+    const bool need64 = bound >= 2147483647.0;
+    if (need64 && o->y_int32) throw Unsupported("y_int may exceed int32 for this layer; request y_int64 instead");
+    WsView v = carve(ws, g, L->F);
+    const bool full = (mask | SFC_STAGE_QPARAMS) == SFC_STAGE_ALL;
+    bool pdl = chained && full;
+    if (mask & SFC_STAGE_QPARAMS) {
+        ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
+        pdl = false;
+    }
+    if (mask & SFC_STAGE_ACT) {
+        ck(launch_act_quant(L->variant, d_x, g, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "act launch");
+        pdl = full;
+    }
+    if (mask & SFC_STAGE_GEMM) {
+        ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st, pdl), "gemm launch");
+        pdl = full;
+    }
+    if (mask & SFC_STAGE_OUTPUT)
+        ck(launch_output(L->variant, need64, v.P, g, v.qp, L->d_sf, o->requant_scale, o->y_int32, o->y_int64,
+                         o->out_f32, o->out_i8, st, pdl),
+           "output launch");
+}
 }  // namespace
 
 extern "C" {
@@ -260,43 +296,23 @@ int sfc_conv_int8(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad
 
 int sfc_conv_int8_stages(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax,
                          void* ws, size_t ws_bytes, const sfc_outputs* o, unsigned mask, void* stream) {
-    return guarded([&] {
-        check_call(L, d_x, n, h, w, pad);
-        if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
-        const ConvGeom g = geom_of(L, n, h, w, pad);
-        if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
-        // |y| <= (max_t sum_k |A[k,t]|)^2 * IC * qmax^2 (MinMax never clips, so |vq|,|uq| <= qmax).
-        const double qmax = double((1 << (L->bits - 1)) - 1);
-        const double bound = double(L->max_a_col_l1) * double(L->max_a_col_l1) * L->IC * qmax * qmax;
-        const bool need64 = bound >= 2147483647.0;
-        if (need64 && o->y_int32)
-            throw Unsupported("y_int may exceed int32 for this layer; request y_int64 instead");
-        WsView v = carve(ws, g, L->F);
-        cudaStream_t st = S(stream);
-        if (mask & SFC_STAGE_QPARAMS) ck(launch_quant_params(d_vmax, L->bits, v.qp, v.sat, st), "quant params launch");
-        if (mask & SFC_STAGE_ACT)
-            ck(launch_act_quant(L->variant, d_x, g, v.qp, L->bits, v.vq, v.sat, st), "act quant launch");
-        if (mask & SFC_STAGE_GEMM) ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st), "gemm launch");
-        if (mask & SFC_STAGE_OUTPUT)
-            ck(launch_output(L->variant, need64, v.P, g, v.qp, L->d_sf, o->requant_scale, o->y_int32, o->y_int64,
-                             o->out_f32, o->out_i8, st),
-               "output launch");
-    });
+    return guarded([&] { run_conv(L, d_x, n, h, w, pad, d_vmax, ws, ws_bytes, o, mask, false, S(stream)); });
 }
 
 int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad, void* ws, size_t ws_bytes,
                      const sfc_outputs* o, void* stream) {
-    int rc = guarded([&] {
+    return guarded([&] {
         check_call(L, d_x, n, h, w, pad);
         if (!ws) throw std::invalid_argument("null workspace");
         const ConvGeom g = geom_of(L, n, h, w, pad);
         if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
         WsView v = carve(ws, g, L->F);
-        ck(cudaMemsetAsync(v.vmax, 0, sizeof(int), S(stream)), "memset vmax");
+        // vmax and the saturation counter share the first 16 bytes of the workspace
+        ck(cudaMemsetAsync(v.vmax, 0, 16, S(stream)), "memset vmax/sat");
         ck(launch_act_absmax(L->variant, d_x, g, v.vmax, S(stream)), "absmax launch");
+        run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, SFC_STAGE_ALL & ~SFC_STAGE_QPARAMS, true,
+                 S(stream));
     });
-    if (rc != SFC_OK) return rc;
-    return sfc_conv_int8(L, d_x, n, h, w, pad, reinterpret_cast<const int32_t*>(ws), ws, ws_bytes, o, stream);
 }
 
 int sfc_conv_stats(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, int64_t* stats, void* stream) {

@@ -1,0 +1,130 @@
+// Device helpers shared by the SFC kernels: exact activation quantizer and
+// programmatic-dependent-launch (PDL) controls.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sfc_kernels.hpp"
+
+namespace sfcb200 {
+
+constexpr int kRowsPerTile = 128;  // GEMM M block (tiles per CTA)
+
+// ---------------------------------------------------------------- PDL
+// A kernel launched with programmatic stream serialization may start while its
+// predecessor is still running; everything before griddep_wait() overlaps the
+// predecessor's tail, everything after sees its results.  Both are no-ops for
+// kernels launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- quantization
+__device__ __forceinline__ int clamp_q(int q, int qmax, unsigned long long* sat) {
+    const int qmin = -qmax - 1;
+    if (q > qmax || q < qmin) {
+        atomicAdd(sat, 1ull);
+        q = q > qmax ? qmax : qmin;
+    }
+    return q;
+}
+
+// The reference quantizer: nearbyint(double(v) / scale) (quant.cpp:102-115).
+__device__ __forceinline__ int exact_q(long long v, double sa) { return int(rint(__ddiv_rn(double(v), sa))); }
+
+// Activation quantizer.  Fast path (qp.exact): one 32x32->64 multiply-add and a
+// shift, proven equal to exact_q for every |v| <= vmax by derive_qparams (so no
+// clamp can trigger).  Otherwise the per-element fp64 division with clamping.
+__device__ __forceinline__ int quant_act(int v, const QuantParams& qp, unsigned long long* sat) {
+    if (qp.exact) return int(((long long)v * qp.mul + (1ll << (qp.shift - 1))) >> qp.shift);
+    return clamp_q(exact_q(v, qp.sa), qp.qmax, sat);
+}
+
+__device__ __forceinline__ long long qcand(long long m0, int c) {
+    return m0 + (c == 0 ? 0 : ((c & 1) ? (c + 1) / 2 : -(c / 2)));
+}
+
+// sa = max(vmax / qmax, 1e-8) (scale_minmax, quant.cpp:117-120) and a verified
+// multiply-shift quantizer, computed by ONE warp.
+//
+// fast(v) = floor((v * mul + 2^(S-1)) / 2^S) and exact(v) = rint(fl(v / sa)) are
+// both monotone non-decreasing step functions of the integer v with value 0 at
+// v = 0, so they agree on [-vmax, vmax] iff their level crossings agree.  For each
+// level k = 0..qmax the fast crossing on the positive side is
+// v_k = ceil((2k+1) 2^(S-1) / mul) and on the negative side
+// w_k = floor((2k+1) 2^(S-1) / mul) + 1; checking exact() on both sides of each
+// crossing (or exact(vmax) <= k when the crossing lies beyond vmax) proves
+// equality over the whole range with ~4 (qmax+1) fp64 divisions instead of
+// 2 vmax + 1.  Including k = qmax proves |fast(v)| <= qmax, i.e. no clamping.
+__device__ __forceinline__ bool qlevel_bad(int k, int vmax, double sa, long long mul, int S) {
+    const long long num = (long long)(2 * k + 1) << (S - 1);
+    const long long vk = (num + mul - 1) / mul;
+    const long long wk = num / mul + 1;
+    bool bad = false;
+    if (vk <= vmax)
+        bad |= exact_q(vk, sa) < k + 1 || exact_q(vk - 1, sa) > k;
+    else
+        bad |= exact_q(vmax, sa) > k;
+    if (wk <= vmax)
+        bad |= exact_q(wk, sa) < k + 1 || exact_q(wk - 1, sa) > k;
+    else
+        bad |= exact_q(vmax, sa) > k;
+    return bad;
+}
+
+// Block-cooperative variant: every thread of the CTA must call it (uses
+// __syncthreads_or); one level per thread for 8-bit and 256+ threads.
+__device__ __forceinline__ QuantParams derive_qparams_block(int vmax, int bits) {
+    const int qmax = (1 << (bits - 1)) - 1;
+    const double sa = fmax(double(vmax) / double(qmax), 1e-8);
+    int e;
+    frexp(sa, &e);
+    const int S = 29 + e;
+    const long long m0 = (long long)floor(ldexp(1.0, S) / sa);
+    int found = -1;
+    for (int cand = 0; cand < 5; ++cand) {
+        const long long mul = qcand(m0, cand);
+        bool bad = mul <= 0;
+        for (int k = threadIdx.x; k <= qmax && !bad; k += blockDim.x) bad = qlevel_bad(k, vmax, sa, mul, S);
+        if (!__syncthreads_or(bad)) {
+            found = cand;
+            break;
+        }
+    }
+    QuantParams p;
+    p.sa = sa;
+    p.shift = S;
+    p.vmax = vmax;
+    p.qmax = qmax;
+    p.exact = found >= 0;
+    p.mul = qcand(m0, found >= 0 ? found : 0);
+    return p;
+}
+
+__device__ __forceinline__ QuantParams derive_qparams_warp(int vmax, int bits) {
+    const int lane = threadIdx.x & 31;
+    const int qmax = (1 << (bits - 1)) - 1;
+    const double sa = fmax(double(vmax) / double(qmax), 1e-8);
+    int e;
+    frexp(sa, &e);
+    const int S = 29 + e;  // mul lands in (2^29, 2^30]
+    const long long m0 = (long long)floor(ldexp(1.0, S) / sa);
+    int found = -1;
+    for (int cand = 0; cand < 5 && found < 0; ++cand) {
+        const long long mul = qcand(m0, cand);
+        bool bad = mul <= 0;
+        for (int k = lane; k <= qmax && !bad; k += 32) bad = qlevel_bad(k, vmax, sa, mul, S);
+        if (!__any_sync(0xffffffffu, bad)) found = cand;
+    }
+    QuantParams p;
+    p.sa = sa;
+    p.shift = S;
+    p.vmax = vmax;
+    p.qmax = qmax;
+    p.exact = found >= 0;
+    p.mul = qcand(m0, found >= 0 ? found : 0);
+    return p;
+}
+
+}  // namespace sfcb200

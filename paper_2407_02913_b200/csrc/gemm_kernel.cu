@@ -1,0 +1,259 @@
+// Stage 4 of the quantized SFC conv: the per-frequency channel contraction
+//   P[f][t][oc] = sum_ic vq[f][t][ic] * uq[f][oc][ic]            (quant.cpp:251-257)
+// as int8 x int8 -> int32 GEMMs on the 5th-gen tensor cores (tcgen05.mma kind::i8,
+// accumulators in TMEM), operands staged by TMA with 128B/64B swizzle.
+//
+// Persistent static schedule: CTA i processes work units u = i, i + grid, ...,
+// unit -> (f, t-block, oc-block) with the oc-block fastest so concurrently resident
+// CTAs share a frequency's A/B tiles in L2.  Warp roles: 0 = TMA producer,
+// 1 = MMA issuer (one elected lane) and TMEM owner, 2..5 = epilogue
+// (tcgen05.ld -> swizzle-free smem box -> TMA store).  TMEM accumulators are
+// double-buffered so unit u+1's MMAs overlap unit u's epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+#include "sfc_kernels.hpp"
+
+namespace sfcb200 {
+
+namespace {
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+}  // namespace
+
+template <int BN, int BK, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmP, int n_tb, int n_ob, int F, int nk) {
+    constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
+    constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
+    constexpr int kEpiBox = 16;                       // columns per TMA store box
+    constexpr int kEpiBoxBytes = 32 * kEpiBox * 4;    // 32 rows x 16 int32
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + STAGES * kRowsPerTile * BK;
+    uint8_t* sE = sB + STAGES * BN * BK;              // [4 warps][2 bufs][32 x 16 int32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(sE + 4 * 2 * kEpiBoxBytes);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int units = F * n_tb * n_ob;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&tmA);
+        ptx::tma_prefetch(&tmB);
+        ptx::tma_prefetch(&tmP);
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_holder, kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+    griddep_launch_dependents();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            griddep_wait();  // vq written by the activation kernel
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                const int ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
+                for (int kc = 0; kc < nk; ++kc) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_expect_tx(&full[stage], kStageBytes);
+                    ptx::tma_load_3d(sA + stage * kRowsPerTile * BK, &tmA, &full[stage], kc * BK, tb * kRowsPerTile, f);
+                    ptx::tma_load_3d(sB + stage * BN * BK, &tmB, &full[stage], kc * BK, ob * BN, f);
+                    if (++stage == STAGES) stage = 0, phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_i8(kRowsPerTile, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int i = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+                const int ab = i & 1;
+                ptx::mbar_wait(&tempty[ab], ((i >> 1) & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + uint32_t(ab * BN);
+                for (int kc = 0; kc < nk; ++kc) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + stage * kRowsPerTile * BK);
+                    const uint32_t b0 = ptx::smem_u32(sB + stage * BN * BK);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 32; ++kk)
+                        ptx::mma_i8(d, ptx::smem_desc_kmajor(a0 + kk * 32, BK), ptx::smem_desc_kmajor(b0 + kk * 32, BK),
+                                    idesc, (kc | kk) != 0);
+                    ptx::mma_commit(&empty[stage]);
+                    if (++stage == STAGES) stage = 0, phase ^= 1;
+                }
+                ptx::mma_commit(&tfull[ab]);
+            }
+        }
+    } else {
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        uint8_t* myE = sE + q * 2 * kEpiBoxBytes;
+        int buf = 0;
+        int i = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+            const int ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
+            const int ab = i & 1;
+            ptx::mbar_wait(&tfull[ab], (i >> 1) & 1);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN; c += kEpiBox) {
+                int32_t r[16];
+                ptx::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(ab * BN + c), r);
+                ptx::tmem_wait_ld();
+                // the previous store out of this buffer must have finished reading smem
+                if (lane == 0) bulk_wait_read<1>();
+                __syncwarp();
+                int4* row = reinterpret_cast<int4*>(myE + buf * kEpiBoxBytes + lane * kEpiBox * 4);
+                row[0] = make_int4(r[0], r[1], r[2], r[3]);
+                row[1] = make_int4(r[4], r[5], r[6], r[7]);
+                row[2] = make_int4(r[8], r[9], r[10], r[11]);
+                row[3] = make_int4(r[12], r[13], r[14], r[15]);
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&tmP, myE + buf * kEpiBoxBytes, ob * BN + c, tb * kRowsPerTile + q * 32, f);
+                    bulk_commit();
+                }
+                buf ^= 1;
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[ab]);
+        }
+        if (lane == 0) bulk_wait_all();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, kTmemCols);
+    }
+}
+
+// ============================================================================ host
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+bool make_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base, uint64_t d0, uint64_t d1,
+                  uint64_t d2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {d0 * esize, d0 * d1 * esize};
+    cuuint32_t box[3] = {b0, b1, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int BN, int BK, int STAGES>
+cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const ConvGeom& g, int F,
+                        cudaStream_t st, bool pdl) {
+    const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + 4 * 2 * 32 * 16 * 4 + 1024 + 256;
+    auto kern = k_gemm<BN, BK, STAGES>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    const int n_tb = g.Tpad / kRowsPerTile, n_ob = g.OCpad / BN;
+    const int units = F * n_tb * n_ob;
+    // CTAs per SM bounded by shared memory and by TMEM (2*BN columns each of 512).
+    constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
+    int per_sm = int((227 * 1024) / smem);
+    per_sm = per_sm < 1 ? 1 : per_sm;
+    per_sm = per_sm > 512 / kTmemCols ? 512 / kTmemCols : per_sm;
+    per_sm = per_sm > 2 ? 2 : per_sm;
+    const int resident = sm_count() * per_sm;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(units < resident ? units : resident);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a, b, p, n_tb, n_ob, F, g.Cpad / BK);
+}
+
+template <int BK, int STAGES>
+cudaError_t gemm_by_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const ConvGeom& g, int F,
+                       cudaStream_t st, bool pdl) {
+    if (g.BN == 64) return gemm_launch<64, BK, STAGES>(a, b, p, g, F, st, pdl);
+    if (g.BN == 128) return gemm_launch<128, BK, STAGES>(a, b, p, g, F, st, pdl);
+    return gemm_launch<256, BK, STAGES>(a, b, p, g, F, st, pdl);
+}
+}  // namespace
+
+cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
+                        bool pdl) {
+    CUtensorMap ta, tb, tp;
+    const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, vqA, g.Cpad, g.Tpad, F, g.BK, kRowsPerTile, sw) ||
+        !make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
+        !make_tmap_3d(&tp, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, g.Tpad, F, 16, 32,
+                      CU_TENSOR_MAP_SWIZZLE_NONE))
+        return cudaErrorInvalidValue;
+    const int nk = g.Cpad / g.BK;
+    if (g.BK == 128) return nk <= 2 ? gemm_by_bn<128, 2>(ta, tb, tp, g, F, st, pdl) : gemm_by_bn<128, 4>(ta, tb, tp, g, F, st, pdl);
+    return nk <= 2 ? gemm_by_bn<64, 2>(ta, tb, tp, g, F, st, pdl) : gemm_by_bn<64, 4>(ta, tb, tp, g, F, st, pdl);
+}
+
+}  // namespace sfcb200

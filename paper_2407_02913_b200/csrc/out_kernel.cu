@@ -1,0 +1,186 @@
+// Stage 5 of the quantized SFC conv: the output transform with correction rows
+// folded into A, in exact integers, then dequantisation / requantisation
+// (reference: proj/src/quant.cpp:258-278).
+//
+//   stage A  Q[t1][l]  = sum_k A[k][t1] P[k*K + l]     items (tj, l, oc)
+//   stage B  y[t1][t2] = sum_l Q[t1][l] A[l][t2]       items (tj, t1, oc) -> shared row tile
+//   stage C  whole output rows (oc, oh) of the tile row, coalesced:
+//            y_int, out = y * sa * sf[oc] / N^2 (fp32), out_i8 = clamp(rint(y * scale * s), 0, 127)
+//
+// One CTA per (image b, tile row ti, chunk of OCC output channels).  P reads are
+// coalesced over oc; shared strides are odd so lanes stepping oc hit distinct banks.
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "sfc_kernels.hpp"
+#include "sfc_tables.cuh"
+
+namespace sfcb200 {
+
+namespace {
+constexpr int kOutThreads = 256;
+
+struct OutSmem {
+    int qstride;   // elements per (tj, t1, l) row of Q  (>= OCC, odd)
+    int ystride;   // elements per (t1, oc) output row   (>= M*tw, odd)
+    size_t y_off, bytes;
+};
+
+template <int V, bool Y64, int OCC>
+__host__ __device__ inline OutSmem out_smem(int tw) {
+    using T = Tab<V>;
+    const size_t es = Y64 ? 8 : 4;
+    OutSmem s;
+    s.qstride = OCC | 1;
+    s.ystride = (T::M * tw) | 1;
+    const size_t q = size_t(tw) * T::M * T::K * s.qstride * es;
+    s.y_off = (q + 15) & ~size_t(15);
+    s.bytes = s.y_off + size_t(T::M) * OCC * s.ystride * es;
+    return s;
+}
+}  // namespace
+
+template <int V, bool Y64, int OCC>
+__global__ void __launch_bounds__(kOutThreads) k_output(const int32_t* __restrict__ P, ConvGeom g,
+                                                        const QuantParams* __restrict__ qpp,
+                                                        const double* __restrict__ sf, double requant,
+                                                        int32_t* __restrict__ y32, int64_t* __restrict__ y64,
+                                                        float* __restrict__ out, int8_t* __restrict__ out8) {
+    using T = Tab<V>;
+    constexpr int K = T::K, M = T::M;
+    using acc_t = typename std::conditional<Y64, long long, int>::type;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int tw = g.tw;
+    const OutSmem L = out_smem<V, Y64, OCC>(tw);
+    acc_t* s_q = reinterpret_cast<acc_t*>(smem);            // [tw][M][K] rows of qstride
+    acc_t* s_y = reinterpret_cast<acc_t*>(smem + L.y_off);  // [M][OCC] rows of ystride
+    const int ti = blockIdx.x, b = blockIdx.y, oc0 = blockIdx.z * OCC;
+    const int noc = min(OCC, g.OC - oc0);
+    const int t0 = (b * g.th + ti) * tw;
+    griddep_wait();  // P complete
+    griddep_launch_dependents();
+
+    // ---- stage A
+    for (int it = threadIdx.x; it < tw * K * OCC; it += kOutThreads) {
+        const int oc = it % OCC, l = (it / OCC) % K, tj = it / (OCC * K);
+        if (oc >= noc) continue;
+        const int32_t* src = P + (size_t(l) * g.Tpad + t0 + tj) * g.OCpad + oc0 + oc;
+        int p[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) p[k] = __ldg(src + size_t(k) * K * g.Tpad * g.OCpad);
+#pragma unroll
+        for (int t1 = 0; t1 < M; ++t1) {
+            acc_t qv = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (T::a(k, t1) != 0) qv += acc_t(T::a(k, t1)) * p[k];
+            s_q[((tj * M + t1) * K + l) * L.qstride + oc] = qv;
+        }
+    }
+    __syncthreads();
+
+    // ---- stage B
+    for (int it = threadIdx.x; it < tw * M * OCC; it += kOutThreads) {
+        const int oc = it % OCC, t1 = (it / OCC) % M, tj = it / (OCC * M);
+        if (oc >= noc) continue;
+        acc_t qv[K];
+#pragma unroll
+        for (int l = 0; l < K; ++l) qv[l] = s_q[((tj * M + t1) * K + l) * L.qstride + oc];
+        acc_t* dst = s_y + (t1 * OCC + oc) * L.ystride + tj * M;
+#pragma unroll
+        for (int t2 = 0; t2 < M; ++t2) {
+            acc_t y = 0;
+#pragma unroll
+            for (int l = 0; l < K; ++l)
+                if (T::a(l, t2) != 0) y += qv[l] * T::a(l, t2);
+            dst[t2] = y;
+        }
+    }
+    __syncthreads();
+
+    // ---- stage C: one warp per output row (t1, oc), lanes along ow
+    const QuantParams qp = *qpp;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int row = warp; row < M * noc; row += kOutThreads / 32) {
+        const int oc = row % noc, t1 = row / noc;
+        const int oh = ti * M + t1;
+        if (oh >= g.HO) continue;
+        const double scale = (qp.sa * sf[oc0 + oc]) / double(T::DEN * T::DEN);
+        const float scale_f = float(scale);
+        const acc_t* src = s_y + (t1 * OCC + oc) * L.ystride;
+        const size_t base = ((size_t(b) * g.OC + oc0 + oc) * g.HO + oh) * g.WO;
+        for (int ow = lane; ow < g.WO; ow += 32) {
+            const acc_t y = src[ow];
+            if (y32) y32[base + ow] = int(y);
+            if (y64) y64[base + ow] = (long long)y;
+            if (out) out[base + ow] = Y64 ? float(double(y) * scale) : __int2float_rn(int(y)) * scale_f;
+            if (out8) out8[base + ow] = int8_t(fmin(fmax(rint(double(y) * scale * requant), 0.0), 127.0));
+        }
+    }
+}
+
+namespace {
+template <int V, bool Y64, int OCC>
+cudaError_t out_launch_occ(const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
+                           double requant, int32_t* y32, int64_t* y64, float* out, int8_t* out8, cudaStream_t st,
+                           bool pdl) {
+    const size_t smem = out_smem<V, Y64, OCC>(g.tw).bytes;
+    auto kern = k_output<V, Y64, OCC>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.th, g.B, (g.OC + OCC - 1) / OCC);
+    cfg.blockDim = dim3(kOutThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, P, g, qp, sf, requant, y32, y64, out, out8);
+}
+
+template <int V, bool Y64>
+cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf, double requant,
+                       int32_t* y32, int64_t* y64, float* out, int8_t* out8, cudaStream_t st, bool pdl) {
+    auto ctas = [&](int o) { return long(g.th) * g.B * ((g.OC + o - 1) / o); };
+    auto smem = [&](int o) {
+        return o == 32 ? out_smem<V, Y64, 32>(g.tw).bytes
+             : o == 16 ? out_smem<V, Y64, 16>(g.tw).bytes
+             : o == 8  ? out_smem<V, Y64, 8>(g.tw).bytes
+                       : out_smem<V, Y64, 4>(g.tw).bytes;
+    };
+    int occ = 32;
+    while (occ > 4 && ctas(occ) < 2 * 148) occ /= 2;
+    while (occ > 4 && smem(occ) > 96 * 1024) occ /= 2;
+    switch (occ) {
+        case 32: return out_launch_occ<V, Y64, 32>(P, g, qp, sf, requant, y32, y64, out, out8, st, pdl);
+        case 16: return out_launch_occ<V, Y64, 16>(P, g, qp, sf, requant, y32, y64, out, out8, st, pdl);
+        case 8: return out_launch_occ<V, Y64, 8>(P, g, qp, sf, requant, y32, y64, out, out8, st, pdl);
+        default: return out_launch_occ<V, Y64, 4>(P, g, qp, sf, requant, y32, y64, out, out8, st, pdl);
+    }
+}
+
+template <int V>
+cudaError_t out_by_width(bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
+                         double requant, int32_t* y32, int64_t* y64p, float* out, int8_t* out8, cudaStream_t st,
+                         bool pdl) {
+    return y64 ? out_launch<V, true>(P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl)
+               : out_launch<V, false>(P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl);
+}
+}  // namespace
+
+cudaError_t launch_output(int variant, bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
+                          const double* sf, double requant, int32_t* y32, int64_t* y64p, float* out, int8_t* out8,
+                          cudaStream_t st, bool pdl) {
+    switch (variant) {
+        case 0: return out_by_width<0>(y64, P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl);
+        case 1: return out_by_width<1>(y64, P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl);
+        default: return out_by_width<2>(y64, P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl);
+    }
+}
+
+}  // namespace sfcb200

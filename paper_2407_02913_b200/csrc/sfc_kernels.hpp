@@ -17,13 +17,13 @@ struct ConvGeom {
     int OC, OCpad, BN;
 };
 
-// Device-resident activation quantizer, derived on device from the global
-// absmax so multi-GPU callers can all-reduce the absmax first.
+// Activation quantizer derived on device from the global absmax (so multi-GPU
+// callers can all-reduce the absmax first).
 struct QuantParams {
     double sa;        // activation scale  max(vmax / qmax, 1e-8)     (quant.cpp:117-120)
     long long mul;    // exact fast path: q = (v * mul + 2^(shift-1)) >> shift
     int shift;
-    int exact;        // 1 when the fast path was verified for every |v| <= vmax
+    int exact;        // 1 when the fast path was proven equal to rint(v / sa) on [-vmax, vmax]
     int vmax;
     int qmax;
 };
@@ -31,24 +31,24 @@ struct QuantParams {
 void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, int OC);
 size_t workspace_bytes(const ConvGeom& g, int F);
 
+// `pdl`: launch with programmatic stream serialization (overlap the predecessor's tail).
 cudaError_t launch_filter_prepare(int variant, const int8_t* w, int OC, int IC, int Cpad, int OCpad, int bits,
                                   double* sf, int* umax, int8_t* uqB, unsigned long long* sat, cudaStream_t st);
 cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, cudaStream_t st);
-cudaError_t launch_quant_params(const int* vmax, int bits, QuantParams* qp, unsigned long long* sat,
-                                cudaStream_t st);
-cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, const QuantParams* qp, int bits,
-                             int8_t* vqA, unsigned long long* sat, cudaStream_t st);
-cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F,
-                        cudaStream_t st);
+cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, const int* vmax, int bits,
+                             QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl);
+cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
+                        bool pdl);
 cudaError_t launch_output(int variant, bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, double requant, int32_t* y32, int64_t* y64out, float* out, int8_t* out8,
-                          cudaStream_t st);
-
+                          cudaStream_t st, bool pdl);
+cudaError_t launch_quant_params(const int* vmax, int bits, QuantParams* qp, unsigned long long* sat,
+                                cudaStream_t st);
+cudaError_t launch_debug_quant(const QuantParams* qp, int vmax, int32_t* q, unsigned long long* sat, cudaStream_t st);
 cudaError_t launch_direct_conv(const int8_t* x, int B, int C, int H, int W, const int8_t* w, int OC, int R,
                                int stride, int pad, int32_t* out, cudaStream_t st);
 cudaError_t launch_freq_energy(int variant, const int8_t* x, const ConvGeom& g, unsigned long long* sum,
                                cudaStream_t st);
-cudaError_t launch_debug_quant(const QuantParams* qp, int vmax, int32_t* q, unsigned long long* sat, cudaStream_t st);
 cudaError_t launch_transform_filters(int variant, const int8_t* w, int OC, int IC, int32_t* u, cudaStream_t st);
 
 }  // namespace sfcb200
