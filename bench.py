@@ -358,7 +358,7 @@ def run_b200(args, rank, world, local_rank):
             e = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
             x, ws, pad = c["x"], c["ws"], c["L"].pad
             n, _, h, w_ = x.shape
-            o = sc.Outputs(*(sc._ptr(c["outs"].get(k)) for k in ("y_int32", "y_int64", "out_f32", "out_i8")),
+            o = sc.Outputs(*(sc._ptr(c["outs"].get(k)) for k in ("y_int32", "y_int64", "out_f32", "out_f64", "out_i8")),
                            c["rq"])
             c["vmax"].zero_()
             e[0].record(stream)

@@ -103,6 +103,7 @@ typedef struct {
     int32_t* y_int32;      /* [N][OC][HO][WO] integer output accumulator sum_kl A A pacc, or NULL */
     int64_t* y_int64;      /* same, 64-bit (required when the int32 bound does not hold), or NULL */
     float* out_f32;        /* dequantised output y * sa * sf[oc] / N^2, or NULL */
+    double* out_f64;       /* the same in fp64 (what the sfconv:: DenseTensor shim returns), or NULL */
     int8_t* out_i8;        /* harness requant clamp(rint(out * requant_scale), 0, 127), or NULL */
     double requant_scale;
 } sfc_outputs;
@@ -153,6 +154,11 @@ int sfc_frequency_energy_int8(sfc_plan_t plan, const int8_t* d_x, int n, int c, 
 /* U = G f G^T for every (oc, ic) as exact int32 [OC][IC][K][K] (transform_filters, conv.cpp:352-382). */
 int sfc_transform_filters_int8(sfc_plan_t plan, const int8_t* d_weights, int oc, int ic, int32_t* d_u,
                                void* stream);
+
+/* Report sums of quantized_fast_conv2d (quant.cpp:283-291) on the device: host_sums[0] =
+ * sum (out - ref)^2, host_sums[1] = sum ref^2 over n elements (ref = sfc_direct_conv_int8 output).
+ * Synchronous. */
+int sfc_report_sq_err(const double* d_out, const int32_t* d_ref, int64_t n, double* host_sums, void* stream);
 
 /* Test hook: run the device activation quantizer for every integer v in [-vmax, vmax]
  * (d_q has 2*vmax+1 int32 slots); info[4] = {fast path exact flag, shift, multiplier,

@@ -20,7 +20,7 @@ EXPORTED = (
     "sfc_plan_matrices", "sfc_layer_create", "sfc_layer_destroy", "sfc_layer_filter_scales",
     "sfc_layer_saturations", "sfc_layer_uq", "sfc_conv_workspace_size", "sfc_act_absmax", "sfc_conv_int8",
     "sfc_conv_int8_stages", "sfc_conv_forward", "sfc_conv_stats", "sfc_conv_views", "sfc_direct_conv_int8", "sfc_frequency_energy_int8",
-    "sfc_transform_filters_int8", "sfc_debug_quantizer",
+    "sfc_transform_filters_int8", "sfc_debug_quantizer", "sfc_report_sq_err",
 )
 
 
@@ -46,7 +46,7 @@ class SfcCudaError(RuntimeError):
 
 class Outputs(ctypes.Structure):
     _fields_ = [("y_int32", ctypes.c_void_p), ("y_int64", ctypes.c_void_p), ("out_f32", ctypes.c_void_p),
-                ("out_i8", ctypes.c_void_p), ("requant_scale", ctypes.c_double)]
+                ("out_f64", ctypes.c_void_p), ("out_i8", ctypes.c_void_p), ("requant_scale", ctypes.c_double)]
 
 
 _lib = None
@@ -80,6 +80,7 @@ _SIGS = {
     "sfc_frequency_energy_int8": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "sfc_transform_filters_int8": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "sfc_debug_quantizer": (_i, [_i, _i, _vp, _i64p, _vp]),
+    "sfc_report_sq_err": (_i, [_vp, _vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _vp]),
 }
 
 

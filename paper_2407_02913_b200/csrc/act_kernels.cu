@@ -125,21 +125,32 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
 
     // ---- stage 2: column transform (+ quantize), items (tj, l)
     int local = 0;
-    for (int idx = j; idx < tw * K; idx += TPC) {
-        const int l = idx % K, tj = idx / K;
-        int zr[n];
+    auto column = [&](auto quantize) {
+        for (int idx = j; idx < tw * K; idx += TPC) {
+            const int l = idx % K, tj = idx / K;
+            int zr[n];
 #pragma unroll
-        for (int r = 0; r < n; ++r) zr[r] = s_z[((tj * n + r) * K + l) * CC + c];
+            for (int r = 0; r < n; ++r) zr[r] = s_z[((tj * n + r) * K + l) * CC + c];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            int v = 0;
+            for (int k = 0; k < K; ++k) {
+                int v = 0;
 #pragma unroll
-            for (int r = 0; r < n; ++r) v += T::bt(k, r) * zr[r];
-            if (MODE == 1)
-                s_q[(tj * F + k * K + l) * CC + c] = int8_t(quant_act(v, qp, sat));
-            else
-                local = max(local, abs(v));
+                for (int r = 0; r < n; ++r) v += T::bt(k, r) * zr[r];
+                if (MODE == 1)
+                    s_q[(tj * F + k * K + l) * CC + c] = int8_t(quantize(v));
+                else
+                    local = max(local, abs(v));
+            }
         }
+    };
+    if (MODE == 0) {
+        column([](int v) { return v; });
+    } else if (qp.exact) {  // uniform over the CTA: no per-value branch
+        const long long mul = qp.mul, half = 1ll << (qp.shift - 1);
+        const int shift = qp.shift;
+        column([=](int v) { return int(((long long)v * mul + half) >> shift); });
+    } else {
+        column([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, sat); });
     }
 
     if (MODE == 0) {

@@ -224,3 +224,38 @@ size_t workspace_bytes(const ConvGeom& g, int F) {
 }
 
 }  // namespace sfcb200
+
+namespace sfcb200 {
+// Report sums for quantized_fast_conv2d (quant.cpp:283-291): sums[0] += sum (out - ref)^2,
+// sums[1] += sum ref^2 in fp64 (ref is the exact int8 direct conv).
+__global__ void __launch_bounds__(256) k_sq_err(const double* __restrict__ out, const int32_t* __restrict__ ref,
+                                                long long n, double* __restrict__ sums) {
+    double e = 0.0, s = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double r = double(ref[i]), d = out[i] - r;
+        e += d * d;
+        s += r * r;
+    }
+    __shared__ double se[8], ss[8];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    if ((threadIdx.x & 31) == 0) se[threadIdx.x >> 5] = e, ss[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < 8; ++w) a += se[w], b += ss[w];
+        atomicAdd(&sums[0], a);
+        atomicAdd(&sums[1], b);
+    }
+}
+
+cudaError_t launch_sq_err(const double* out, const int32_t* ref, long long n, double* sums, cudaStream_t st) {
+    long long blocks = (n + 255) / 256;
+    blocks = blocks > 4 * 148 ? 4 * 148 : (blocks < 1 ? 1 : blocks);
+    k_sq_err<<<int(blocks), 256, 0, st>>>(out, ref, n, sums);
+    return cudaGetLastError();
+}
+}  // namespace sfcb200

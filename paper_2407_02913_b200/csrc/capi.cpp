@@ -138,10 +138,10 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
         ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st, pdl), "gemm launch");
         pdl = full;
     }
-    if (mask & SFC_STAGE_OUTPUT)
-        ck(launch_output(L->variant, need64, v.P, g, v.qp, L->d_sf, o->requant_scale, o->y_int32, o->y_int64,
-                         o->out_f32, o->out_i8, st, pdl),
-           "output launch");
+    if (mask & SFC_STAGE_OUTPUT) {
+        const OutPtrs op{o->y_int32, o->y_int64, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
+        ck(launch_output(L->variant, need64, v.P, g, v.qp, L->d_sf, op, st, pdl), "output launch");
+    }
 }
 }  // namespace
 
@@ -376,6 +376,19 @@ int sfc_transform_filters_int8(sfc_plan_t plan, const int8_t* d_w, int oc, int i
     return guarded([&] {
         if (!plan || !d_w || !d_u) throw std::invalid_argument("null argument");
         ck(launch_transform_filters(plan->p->variant, d_w, oc, ic, d_u, S(stream)), "transform filters launch");
+    });
+}
+
+int sfc_report_sq_err(const double* d_out, const int32_t* d_ref, int64_t n, double* host_sums, void* stream) {
+    return guarded([&] {
+        if (!d_out || !d_ref || !host_sums || n < 0) throw std::invalid_argument("bad report arguments");
+        void* d_sums = nullptr;
+        ck(cudaMallocAsync(&d_sums, 2 * sizeof(double), S(stream)), "alloc");
+        ck(cudaMemsetAsync(d_sums, 0, 2 * sizeof(double), S(stream)), "memset");
+        ck(launch_sq_err(d_out, d_ref, n, static_cast<double*>(d_sums), S(stream)), "sq_err launch");
+        ck(cudaMemcpyAsync(host_sums, d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, S(stream)), "copy");
+        ck(cudaFreeAsync(d_sums, S(stream)), "free");
+        ck(cudaStreamSynchronize(S(stream)), "sync");
     });
 }
 

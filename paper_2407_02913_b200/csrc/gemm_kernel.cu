@@ -44,12 +44,13 @@ __global__ void __launch_bounds__(192, 1)
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
     constexpr int kEpiBox = 16;                       // columns per TMA store box
     constexpr int kEpiBoxBytes = 32 * kEpiBox * 4;    // 32 rows x 16 int32
+    constexpr int kEpiBufs = 4;                       // TMA-store staging buffers per epilogue warp
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = sA + STAGES * kRowsPerTile * BK;
-    uint8_t* sE = sB + STAGES * BN * BK;              // [4 warps][2 bufs][32 x 16 int32]
-    uint64_t* full = reinterpret_cast<uint64_t*>(sE + 4 * 2 * kEpiBoxBytes);
+    uint8_t* sE = sB + STAGES * BN * BK;              // [4 warps][kEpiBufs][32 x 16 int32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(sE + 4 * kEpiBufs * kEpiBoxBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else {
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        uint8_t* myE = sE + q * 2 * kEpiBoxBytes;
+        uint8_t* myE = sE + q * kEpiBufs * kEpiBoxBytes;
         int buf = 0;
         int i = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
@@ -138,8 +139,8 @@ __global__ void __launch_bounds__(192, 1)
                 int32_t r[16];
                 ptx::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(ab * BN + c), r);
                 ptx::tmem_wait_ld();
-                // the previous store out of this buffer must have finished reading smem
-                if (lane == 0) bulk_wait_read<1>();
+                // the store issued kEpiBufs boxes ago from this buffer must have read smem
+                if (lane == 0) bulk_wait_read<kEpiBufs - 1>();
                 __syncwarp();
                 int4* row = reinterpret_cast<int4*>(myE + buf * kEpiBoxBytes + lane * kEpiBox * 4);
                 row[0] = make_int4(r[0], r[1], r[2], r[3]);
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(192, 1)
                     tma_store_3d(&tmP, myE + buf * kEpiBoxBytes, ob * BN + c, tb * kRowsPerTile + q * 32, f);
                     bulk_commit();
                 }
-                buf ^= 1;
+                buf = (buf + 1) % kEpiBufs;
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -207,7 +208,7 @@ int sm_count() {
 template <int BN, int BK, int STAGES>
 cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const ConvGeom& g, int F,
                         cudaStream_t st, bool pdl) {
-    const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + 4 * 2 * 32 * 16 * 4 + 1024 + 256;
+    const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + 4 * 4 * 32 * 16 * 4 + 1024 + 256;
     auto kern = k_gemm<BN, BK, STAGES>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;

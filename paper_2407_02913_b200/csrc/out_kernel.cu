@@ -45,9 +45,7 @@ __host__ __device__ inline OutSmem out_smem(int tw) {
 template <int V, bool Y64, int OCC>
 __global__ void __launch_bounds__(kOutThreads) k_output(const int32_t* __restrict__ P, ConvGeom g,
                                                         const QuantParams* __restrict__ qpp,
-                                                        const double* __restrict__ sf, double requant,
-                                                        int32_t* __restrict__ y32, int64_t* __restrict__ y64,
-                                                        float* __restrict__ out, int8_t* __restrict__ out8) {
+                                                        const double* __restrict__ sf, OutPtrs o) {
     using T = Tab<V>;
     constexpr int K = T::K, M = T::M;
     using acc_t = typename std::conditional<Y64, long long, int>::type;
@@ -101,30 +99,33 @@ __global__ void __launch_bounds__(kOutThreads) k_output(const int32_t* __restric
     __syncthreads();
 
     // ---- stage C: one warp per output row (t1, oc), lanes along ow
-    const QuantParams qp = *qpp;
+    __shared__ double s_scale[OCC];
+    if (threadIdx.x < OCC && int(threadIdx.x) < noc)
+        s_scale[threadIdx.x] = (qpp->sa * sf[oc0 + threadIdx.x]) / double(T::DEN * T::DEN);
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int row = warp; row < M * noc; row += kOutThreads / 32) {
-        const int oc = row % noc, t1 = row / noc;
+    for (int row = warp; row < M * OCC; row += kOutThreads / 32) {
+        const int oc = row % OCC, t1 = row / OCC;
         const int oh = ti * M + t1;
-        if (oh >= g.HO) continue;
-        const double scale = (qp.sa * sf[oc0 + oc]) / double(T::DEN * T::DEN);
+        if (oc >= noc || oh >= g.HO) continue;
+        const double scale = s_scale[oc];
         const float scale_f = float(scale);
         const acc_t* src = s_y + (t1 * OCC + oc) * L.ystride;
         const size_t base = ((size_t(b) * g.OC + oc0 + oc) * g.HO + oh) * g.WO;
         for (int ow = lane; ow < g.WO; ow += 32) {
             const acc_t y = src[ow];
-            if (y32) y32[base + ow] = int(y);
-            if (y64) y64[base + ow] = (long long)y;
-            if (out) out[base + ow] = Y64 ? float(double(y) * scale) : __int2float_rn(int(y)) * scale_f;
-            if (out8) out8[base + ow] = int8_t(fmin(fmax(rint(double(y) * scale * requant), 0.0), 127.0));
+            if (o.y32) o.y32[base + ow] = int(y);
+            if (o.y64) o.y64[base + ow] = (long long)y;
+            if (o.f32) o.f32[base + ow] = Y64 ? float(double(y) * scale) : __int2float_rn(int(y)) * scale_f;
+            if (o.f64) o.f64[base + ow] = double(y) * scale;
+            if (o.i8) o.i8[base + ow] = int8_t(fmin(fmax(rint(double(y) * scale * o.requant), 0.0), 127.0));
         }
     }
 }
 
 namespace {
 template <int V, bool Y64, int OCC>
-cudaError_t out_launch_occ(const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
-                           double requant, int32_t* y32, int64_t* y64, float* out, int8_t* out8, cudaStream_t st,
+cudaError_t out_launch_occ(const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf, const OutPtrs& o, cudaStream_t st,
                            bool pdl) {
     const size_t smem = out_smem<V, Y64, OCC>(g.tw).bytes;
     auto kern = k_output<V, Y64, OCC>;
@@ -140,12 +141,11 @@ cudaError_t out_launch_occ(const int32_t* P, const ConvGeom& g, const QuantParam
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, P, g, qp, sf, requant, y32, y64, out, out8);
+    return cudaLaunchKernelEx(&cfg, kern, P, g, qp, sf, o);
 }
 
 template <int V, bool Y64>
-cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf, double requant,
-                       int32_t* y32, int64_t* y64, float* out, int8_t* out8, cudaStream_t st, bool pdl) {
+cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl) {
     auto ctas = [&](int o) { return long(g.th) * g.B * ((g.OC + o - 1) / o); };
     auto smem = [&](int o) {
         return o == 32 ? out_smem<V, Y64, 32>(g.tw).bytes
@@ -157,29 +157,27 @@ cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* q
     while (occ > 4 && ctas(occ) < 2 * 148) occ /= 2;
     while (occ > 4 && smem(occ) > 96 * 1024) occ /= 2;
     switch (occ) {
-        case 32: return out_launch_occ<V, Y64, 32>(P, g, qp, sf, requant, y32, y64, out, out8, st, pdl);
-        case 16: return out_launch_occ<V, Y64, 16>(P, g, qp, sf, requant, y32, y64, out, out8, st, pdl);
-        case 8: return out_launch_occ<V, Y64, 8>(P, g, qp, sf, requant, y32, y64, out, out8, st, pdl);
-        default: return out_launch_occ<V, Y64, 4>(P, g, qp, sf, requant, y32, y64, out, out8, st, pdl);
+        case 32: return out_launch_occ<V, Y64, 32>(P, g, qp, sf, o, st, pdl);
+        case 16: return out_launch_occ<V, Y64, 16>(P, g, qp, sf, o, st, pdl);
+        case 8: return out_launch_occ<V, Y64, 8>(P, g, qp, sf, o, st, pdl);
+        default: return out_launch_occ<V, Y64, 4>(P, g, qp, sf, o, st, pdl);
     }
 }
 
 template <int V>
-cudaError_t out_by_width(bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
-                         double requant, int32_t* y32, int64_t* y64p, float* out, int8_t* out8, cudaStream_t st,
+cudaError_t out_by_width(bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf, const OutPtrs& o, cudaStream_t st,
                          bool pdl) {
-    return y64 ? out_launch<V, true>(P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl)
-               : out_launch<V, false>(P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl);
+    return y64 ? out_launch<V, true>(P, g, qp, sf, o, st, pdl)
+               : out_launch<V, false>(P, g, qp, sf, o, st, pdl);
 }
 }  // namespace
 
 cudaError_t launch_output(int variant, bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
-                          const double* sf, double requant, int32_t* y32, int64_t* y64p, float* out, int8_t* out8,
-                          cudaStream_t st, bool pdl) {
+                          const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl) {
     switch (variant) {
-        case 0: return out_by_width<0>(y64, P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl);
-        case 1: return out_by_width<1>(y64, P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl);
-        default: return out_by_width<2>(y64, P, g, qp, sf, requant, y32, y64p, out, out8, st, pdl);
+        case 0: return out_by_width<0>(y64, P, g, qp, sf, o, st, pdl);
+        case 1: return out_by_width<1>(y64, P, g, qp, sf, o, st, pdl);
+        default: return out_by_width<2>(y64, P, g, qp, sf, o, st, pdl);
     }
 }
 

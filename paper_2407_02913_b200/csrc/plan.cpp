@@ -189,6 +189,22 @@ SfcPlan derive(int N, int M, int R) {
             p.A[size_t(k) * M + t] = col[k].n;
         }
     }
+    // Square overlapped form (used only for conditioning analysis by the reference,
+    // catalog.cpp:197-209): the SFT at the window offset plus one difference row per
+    // distinct out-of-window alias.
+    std::vector<std::pair<int, int>> diffs;
+    for (const Correction& ct : p.corrections) {
+        const std::pair<int, int> d{ct.desired, ct.wrapped};
+        if (std::find(diffs.begin(), diffs.end(), d) == diffs.end()) diffs.push_back(d);
+    }
+    p.n_overlap = N + int(diffs.size());
+    p.overlap.assign(size_t(p.n_overlap) * p.n_overlap, 0);
+    for (int r = 0; r < N; ++r)
+        for (int t = 0; t < N; ++t) p.overlap[size_t(r) * p.n_overlap + o + t] = F[r][t];
+    for (size_t d = 0; d < diffs.size(); ++d) {
+        p.overlap[(N + d) * p.n_overlap + diffs[d].first] = 1;
+        p.overlap[(N + d) * p.n_overlap + diffs[d].second] = -1;
+    }
     std::ostringstream nm;
     nm << "sfc" << N << "-" << M << "x" << M << "-" << R << "x" << R;
     p.name = nm.str();
@@ -217,6 +233,13 @@ std::map<std::string, SfcPlan>& cache() {
 }
 
 }  // namespace
+
+SfcPlan derive_sfc_plan(int N, int M, int R) {
+    SfcPlan p = derive(N, M, R);
+    if (long bad = plan_identity_violations(p))
+        throw std::domain_error(p.name + ": " + std::to_string(bad) + " identity violations");
+    return p;
+}
 
 long plan_identity_violations(const SfcPlan& p) {
     long bad = 0;

@@ -31,6 +31,8 @@ struct SfcPlan {
     std::vector<int64_t> A;   // K x M
     std::vector<Correction> corrections;
     std::vector<int> triples;  // flattened (a, b, c) per axis triple
+    int n_overlap = 0;
+    std::vector<int64_t> overlap;  // n_overlap x n_overlap: SFT rows + one difference row per alias
     int variant = -1;          // index into the compiled device tables
 
     long mults_full() const { return long(K) * K; }
@@ -47,6 +49,10 @@ struct SfcPlan {
 // Throws std::invalid_argument for unknown names and std::domain_error when the
 // exactness gate fails.  Returned references live for the process lifetime.
 const SfcPlan& plan_for(const std::string& name);
+
+// Host-only derivation of SFC-N(M, R) for N in {4, 6} (any M, R with M + R - 1 >= N);
+// not bound to device tables (variant = -1).  derive_correction_spec, catalog.cpp:132-215.
+SfcPlan derive_sfc_plan(int N, int M, int R);
 const std::vector<std::string>& plan_names();
 
 // Number of (t, i, j) triples violating sum_k A BT G = a_denom [i == t + j].

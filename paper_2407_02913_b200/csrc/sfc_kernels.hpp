@@ -39,9 +39,18 @@ cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, co
                              QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl);
 cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
                         bool pdl);
+// Output pointers of the output-transform kernel (any may be null).
+struct OutPtrs {
+    int32_t* y32;
+    int64_t* y64;
+    float* f32;
+    double* f64;
+    int8_t* i8;
+    double requant;
+};
 cudaError_t launch_output(int variant, bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
-                          const double* sf, double requant, int32_t* y32, int64_t* y64out, float* out, int8_t* out8,
-                          cudaStream_t st, bool pdl);
+                          const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
+cudaError_t launch_sq_err(const double* out, const int32_t* ref, long long n, double* sums, cudaStream_t st);
 cudaError_t launch_quant_params(const int* vmax, int bits, QuantParams* qp, unsigned long long* sat,
                                 cudaStream_t st);
 cudaError_t launch_debug_quant(const QuantParams* qp, int vmax, int32_t* q, unsigned long long* sat, cudaStream_t st);

@@ -261,20 +261,20 @@ class SfcLayer:
         check(lib().sfc_act_absmax(self._h, _ptr(x), n, h, w, pad, _ptr(vmax), ctypes.c_void_p(_stream_ptr(stream))))
 
     def conv(self, x: torch.Tensor, vmax: torch.Tensor, ws: torch.Tensor, pad: int, y_int32=None, y_int64=None,
-             out_f32=None, out_i8=None, requant_scale: float = 0.0, stream=None):
+             out_f32=None, out_i8=None, requant_scale: float = 0.0, stream=None, out_f64=None):
         n, c, h, w = x.shape
         if c != self.IC:
             raise ValueError("input channel count does not match filters")
-        o = Outputs(_ptr(y_int32), _ptr(y_int64), _ptr(out_f32), _ptr(out_i8), float(requant_scale))
+        o = Outputs(_ptr(y_int32), _ptr(y_int64), _ptr(out_f32), _ptr(out_f64), _ptr(out_i8), float(requant_scale))
         check(lib().sfc_conv_int8(self._h, _ptr(x), n, h, w, pad, _ptr(vmax), _ptr(ws), ws.numel(), ctypes.byref(o),
                                   ctypes.c_void_p(_stream_ptr(stream))))
 
     def forward(self, x: torch.Tensor, ws: torch.Tensor, pad: int, y_int32=None, y_int64=None, out_f32=None,
-                out_i8=None, requant_scale: float = 0.0, stream=None):
+                out_i8=None, requant_scale: float = 0.0, stream=None, out_f64=None):
         n, c, h, w = x.shape
         if c != self.IC:
             raise ValueError("input channel count does not match filters")
-        o = Outputs(_ptr(y_int32), _ptr(y_int64), _ptr(out_f32), _ptr(out_i8), float(requant_scale))
+        o = Outputs(_ptr(y_int32), _ptr(y_int64), _ptr(out_f32), _ptr(out_f64), _ptr(out_i8), float(requant_scale))
         check(lib().sfc_conv_forward(self._h, _ptr(x), n, h, w, pad, _ptr(ws), ws.numel(), ctypes.byref(o),
                                      ctypes.c_void_p(_stream_ptr(stream))))
 
@@ -389,15 +389,18 @@ def quantized_fast_conv2d(input, filters, spec: AlgorithmSpec, padding: int, con
                       saturations=st["saturations"] + layer.filter_saturations(),
                       values_quantized=st["values_quantized"])
     if report:
-        # quant.cpp:282-291, against the exact int8 direct conv; the output is
-        # evaluated in fp64 from the exact integer accumulator.
-        ref = direct_conv2d(x, filters, 1, padding)
-        scale = torch.as_tensor(st["act_scale"] * sf / float(spec.a_denom ** 2), device=x.device).view(1, -1, 1, 1)
-        out64 = y.to(torch.float64) * scale
-        d = out64 - ref
-        err = float((d * d).sum())
-        sig = float((ref * ref).sum())
-        n = ref.numel()
+        # quant.cpp:282-291 on the device: fp64 output from the exact integer accumulator
+        # against the exact int8 direct conv.
+        out64 = torch.empty((B, layer.OC, HO, WO), dtype=torch.float64, device=x.device)
+        layer.forward(x, ws, padding, out_f64=out64)
+        w8 = as_int8_device(filters, "filters", x.device)
+        ref = torch.empty((B, layer.OC, HO, WO), dtype=torch.int32, device=x.device)
+        check(lib().sfc_direct_conv_int8(_ptr(x), B, C, H, W, _ptr(w8), layer.OC, spec.R, 1, padding, _ptr(ref),
+                                         ctypes.c_void_p(_stream_ptr())))
+        sums = (ctypes.c_double * 2)()
+        check(lib().sfc_report_sq_err(_ptr(out64), _ptr(ref), out64.numel(), sums, ctypes.c_void_p(_stream_ptr())))
+        err, sig = sums[0], sums[1]
+        n = out64.numel()
         rep.mse = err / n
         rep.signal_energy = sig / n
         rep.snr_db = 10.0 * math.log10(sig / max(err, 1e-300))

@@ -1,0 +1,63 @@
+"""The C++ sfconv:: drop-in (include/sfconv/*.hpp over libsfc_b200.so), exercised by a C++
+program written against the reference's own API (tests/cpp/test_dropin.cpp)."""
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle import bindings as ob
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIN = os.path.join(HERE, "cpp", "test_dropin")
+
+
+def _build():
+    subprocess.run(["make", "-s", "-C", os.path.join(HERE, "cpp")], check=True)
+
+
+def test_dropin_host_side():
+    """Catalog, exact tile execution, validation gate and scalar quantizer KATs (no GPU needed)."""
+    _build()
+    r = subprocess.run([BIN, "--host-only"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "[FAIL]" not in r.stdout
+
+
+@pytest.mark.gpu
+def test_dropin_full_suite(cuda):
+    _build()
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "[SKIP]" not in r.stdout and "[FAIL]" not in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"])
+@pytest.mark.parametrize("shape", [(2, 5, 13, 11, 7, 1, 8), (1, 64, 28, 28, 32, 1, 8), (1, 9, 10, 12, 4, 0, 5)])
+def test_dropin_quantized_fast_conv2d_matches_oracle(cuda, variant, shape):
+    """quantized_fast_conv2d through the C++ API vs the oracle: fp64 output within 1e-6 (the
+    dequantisation runs in fp64 on the device from the bit-exact integer accumulator), the
+    report and the counters."""
+    _build()
+    B, C, H, W, OC, pad, bits = shape
+    rng = np.random.default_rng(sum(shape))
+    x = rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(OC, C, 3, 3), dtype=np.int8)
+    with tempfile.TemporaryDirectory() as d:
+        xp, wp, op = (os.path.join(d, n) for n in ("x.bin", "w.bin", "o.bin"))
+        x.tofile(xp)
+        w.tofile(wp)
+        r = subprocess.run([BIN, "run", variant, str(pad), str(bits), str(B), str(C), str(H), str(W), str(OC), xp, wp,
+                            op], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        raw = np.fromfile(op, np.float64)
+    HO, WO = H + 2 * pad - 2, W + 2 * pad - 2
+    out, tail = raw[:-5].reshape(B, OC, HO, WO), raw[-5:]
+    ref = ob.quantized_conv(x, w, variant, pad, bits, want=("out",), report=True)
+    err = np.abs(out - ref["out"]).max() / np.abs(ref["out"]).max()
+    assert err <= 1e-12   # fp64 from the exact y_int: only the last-bit rounding differs
+    assert tail[0] == pytest.approx(ref["report"]["mse"], rel=1e-9)
+    assert tail[2] == pytest.approx(ref["report"]["snr_db"], rel=1e-9)
+    assert tail[3] == ref["report"]["saturations"] and tail[4] == ref["report"]["values_quantized"]
