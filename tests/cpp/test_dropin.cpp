@@ -105,7 +105,7 @@ double max_rel(const DenseTensor& got, const DenseTensor& want) {
 }
 
 int run_mode(int argc, char** argv) {
-    if (argc != 14) {
+    if (argc != 13) {
         std::fprintf(stderr, "usage: test_dropin run SPEC PAD BITS B C H W OC x.bin w.bin out.bin\n");
         return 2;
     }
