@@ -18,6 +18,7 @@
 #include "ptx.cuh"
 #include "sfc_kernels.hpp"
 #include "sfc_tables.cuh"
+#include "transforms.cuh"
 
 namespace sfcb200 {
 
@@ -25,7 +26,8 @@ namespace {
 constexpr int kActThreads = 256;
 
 struct ActSmem {
-    int wcp;      // staged window columns, padded to 4
+    int wcp;      // staged window columns per row, padded to 4
+    int chs;      // bytes per staged channel (n * wcp, padded so chs / 4 is odd: conflict-free)
     size_t x_off, z_off, q_off, bytes;
 };
 
@@ -34,8 +36,10 @@ __host__ __device__ inline ActSmem act_smem(int tw) {
     using T = Tab<V>;
     ActSmem s;
     s.wcp = ((tw - 1) * T::M + T::n + 3) & ~3;
+    s.chs = T::n * s.wcp;
+    if (((s.chs / 4) & 1) == 0) s.chs += 4;
     s.x_off = 0;
-    s.z_off = (size_t(T::n) * s.wcp * CC + 15) & ~size_t(15);
+    s.z_off = (size_t(s.chs) * CC + 15) & ~size_t(15);
     s.q_off = s.z_off + ((size_t(tw) * T::n * T::K * CC * 2 + 15) & ~size_t(15));
     s.bytes = s.q_off + size_t(tw) * T::F * CC;
     return s;
@@ -52,8 +56,6 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     using T = Tab<V>;
     constexpr int n = T::n, K = T::K, M = T::M, F = T::F;
     constexpr int TPC = kActThreads / CC;   // work-groups per channel
-    constexpr int ROWS = CC * n;            // staged (channel, row) pairs
-    constexpr int RPW = (ROWS + 7) / 8;     // ... per warp
     extern __shared__ __align__(16) uint8_t smem[];
     if (MODE == 0) griddep_launch_dependents();
 
@@ -61,37 +63,31 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     const int ti = blockIdx.x, b = blockIdx.y, c0 = blockIdx.z * CC;
     const int nch = min(CC, g.C - c0);
     const ActSmem L = act_smem<V, CC>(tw);
-    int8_t* s_x = reinterpret_cast<int8_t*>(smem + L.x_off);     // [n][wcp][CC]
+    int8_t* s_x = reinterpret_cast<int8_t*>(smem + L.x_off);     // [CC][n][wcp], channel stride chs
     int16_t* s_z = reinterpret_cast<int16_t*>(smem + L.z_off);   // [tw][n][K][CC]
     int8_t* s_q = reinterpret_cast<int8_t*>(smem + L.q_off);     // [tw][F][CC]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = threadIdx.x % CC, j = threadIdx.x / CC;
-    const int wc = (tw - 1) * M + n;
 
-    // ---- stage 0: every warp loads its (channel, row) rows in batches of 8 with all
-    // loads of a batch in flight before the shared stores
+    // ---- stage 0: zero the staging area, then each warp copies whole channel segments:
+    // the window rows [ih0, ih0 + n) of one channel are contiguous in NCHW, so lanes walk
+    // that byte range coalesced and scatter into [c][r][pad + col] (32-bit index math).
     {
-        constexpr int BATCH = RPW < 8 ? RPW : 8;
+        uint4* z4 = reinterpret_cast<uint4*>(s_x);
+        for (int i = threadIdx.x; i < (L.chs * CC) / 16; i += kActThreads) z4[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
         const int ih0 = ti * M - g.pad;
-        for (int col = lane; col < wc; col += 32) {
-            const int iw = col - g.pad;
-            const bool col_ok = iw >= 0 && iw < g.W;
-#pragma unroll 1
-            for (int i0 = 0; i0 < RPW; i0 += BATCH) {
-                int v[BATCH];
-#pragma unroll
-                for (int i = 0; i < BATCH; ++i) {
-                    const int rr = warp + 8 * (i0 + i);
-                    const int ch = rr / n, r = rr % n, ih = ih0 + r;
-                    v[i] = 0;
-                    if (rr < ROWS && ch < nch && col_ok && ih >= 0 && ih < g.H)
-                        v[i] = x[((size_t(b) * g.C + c0 + ch) * g.H + ih) * g.W + iw];
-                }
-#pragma unroll
-                for (int i = 0; i < BATCH; ++i) {
-                    const int rr = warp + 8 * (i0 + i);
-                    if (rr < ROWS) s_x[((rr % n) * L.wcp + col) * CC + rr / n] = int8_t(v[i]);
-                }
+        const int r_lo = max(ih0, 0), r_hi = min(ih0 + n, g.H);
+        const int seg = (r_hi - r_lo) * g.W;                      // bytes per channel
+        const unsigned wmagic = 0xffffffffu / unsigned(g.W) + 1;  // i / W == umulhi(i, wmagic) for i < 2^16
+        const int8_t* src0 = x + (size_t(b) * g.C + c0) * size_t(g.H) * g.W + size_t(r_lo) * g.W;
+        const int dst_row0 = (r_lo - ih0) * L.wcp + g.pad;
+        for (int ch = warp; ch < nch; ch += kActThreads / 32) {
+            const int8_t* src = src0 + size_t(ch) * g.H * g.W;
+            int8_t* dst = s_x + ch * L.chs + dst_row0;
+            for (int i = lane; i < seg; i += 32) {
+                const int r = int(__umulhi(unsigned(i), wmagic));
+                dst[r * L.wcp + (i - r * g.W)] = src[i];
             }
         }
     }
@@ -100,18 +96,15 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     // ---- stage 1: row transform, items (tj, r)
     for (int idx = j; idx < tw * n; idx += TPC) {
         const int r = idx % n, tj = idx / n;
-        const int8_t* src = s_x + (r * L.wcp + tj * M) * CC + c;
+        const int8_t* src = s_x + c * L.chs + r * L.wcp + tj * M;
         int xs[n];
 #pragma unroll
-        for (int s = 0; s < n; ++s) xs[s] = src[s * CC];
+        for (int s = 0; s < n; ++s) xs[s] = src[s];
         int16_t* dst = s_z + ((tj * n + r) * K) * CC + c;
+        int z[K];
+        fwd1d<V>(xs, z);
 #pragma unroll
-        for (int l = 0; l < K; ++l) {
-            int z = 0;
-#pragma unroll
-            for (int s = 0; s < n; ++s) z += T::bt(l, s) * xs[s];
-            dst[l * CC] = int16_t(z);
-        }
+        for (int l = 0; l < K; ++l) dst[l * CC] = int16_t(z[l]);
     }
 
     QuantParams qp{};
@@ -131,15 +124,14 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
             int zr[n];
 #pragma unroll
             for (int r = 0; r < n; ++r) zr[r] = s_z[((tj * n + r) * K + l) * CC + c];
+            int v[K];
+            fwd1d<V>(zr, v);
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                int v = 0;
-#pragma unroll
-                for (int r = 0; r < n; ++r) v += T::bt(k, r) * zr[r];
                 if (MODE == 1)
-                    s_q[(tj * F + k * K + l) * CC + c] = int8_t(quantize(v));
+                    s_q[(tj * F + k * K + l) * CC + c] = int8_t(quantize(v[k]));
                 else
-                    local = max(local, abs(v));
+                    local = max(local, abs(v[k]));
             }
         }
     };

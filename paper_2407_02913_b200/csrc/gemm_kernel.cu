@@ -7,7 +7,7 @@
 // unit -> (f, t-block, oc-block) with the oc-block fastest so concurrently resident
 // CTAs share a frequency's A/B tiles in L2.  Warp roles: 0 = TMA producer,
 // 1 = MMA issuer (one elected lane) and TMEM owner, 2..5 = epilogue
-// (tcgen05.ld -> swizzle-free smem box -> TMA store).  TMEM accumulators are
+// (tcgen05.ld -> 128B-swizzled smem box -> TMA store), two epilogue warps per lane quarter.  TMEM accumulators are
 // double-buffered so unit u+1's MMAs overlap unit u's epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -34,23 +34,26 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+constexpr int kEpiWarps = 8;                 // two epilogue warps per TMEM lane quarter
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiBufs = 2;                  // TMA-store staging boxes per epilogue warp
+constexpr int kEpiBoxBytes = 32 * 32 * 4;    // 32 rows x 32 int32 (one 128B-swizzle box)
 }  // namespace
 
 template <int BN, int BK, int STAGES>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmP, int n_tb, int n_ob, int F, int nk) {
     constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
-    constexpr int kEpiBox = 16;                       // columns per TMA store box
-    constexpr int kEpiBoxBytes = 32 * kEpiBox * 4;    // 32 rows x 16 int32
-    constexpr int kEpiBufs = 4;                       // TMA-store staging buffers per epilogue warp
+    constexpr int kHalf = BN / 2;                     // columns per epilogue warp (two warps per lane quarter)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = sA + STAGES * kRowsPerTile * BK;
-    uint8_t* sE = sB + STAGES * BN * BK;              // [4 warps][kEpiBufs][32 x 16 int32]
-    uint64_t* full = reinterpret_cast<uint64_t*>(sE + 4 * kEpiBufs * kEpiBoxBytes);
+    uint8_t* sE = sB + STAGES * BN * BK;              // [8 warps][kEpiBufs][32 rows x 128 B], 128B-swizzled
+    uint64_t* full = reinterpret_cast<uint64_t*>(sE + kEpiWarps * kEpiBufs * kEpiBoxBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
@@ -66,7 +69,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], 4);
+            ptx::mbar_init(&tempty[i], kEpiWarps);
         }
         ptx::fence_mbar_init();
     }
@@ -125,8 +128,9 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
     } else {
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        uint8_t* myE = sE + q * kEpiBufs * kEpiBoxBytes;
+        // Epilogue: warp e = warp - 2 owns TMEM lane quarter (warp & 3) and column half e / 4.
+        const int q = warp & 3, half = (warp - 2) >> 2;
+        uint8_t* myE = sE + (warp - 2) * kEpiBufs * kEpiBoxBytes;
         int buf = 0;
         int i = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
@@ -135,18 +139,18 @@ __global__ void __launch_bounds__(192, 1)
             ptx::mbar_wait(&tfull[ab], (i >> 1) & 1);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < BN; c += kEpiBox) {
-                int32_t r[16];
-                ptx::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(ab * BN + c), r);
+            for (int c = half * kHalf; c < (half + 1) * kHalf; c += 32) {
+                int32_t r[32];
+                ptx::tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(ab * BN + c), r);
                 ptx::tmem_wait_ld();
-                // the store issued kEpiBufs boxes ago from this buffer must have read smem
-                if (lane == 0) bulk_wait_read<kEpiBufs - 1>();
+                if (lane == 0) bulk_wait_read<kEpiBufs - 1>();  // this buffer's previous store has read smem
                 __syncwarp();
-                int4* row = reinterpret_cast<int4*>(myE + buf * kEpiBoxBytes + lane * kEpiBox * 4);
-                row[0] = make_int4(r[0], r[1], r[2], r[3]);
-                row[1] = make_int4(r[4], r[5], r[6], r[7]);
-                row[2] = make_int4(r[8], r[9], r[10], r[11]);
-                row[3] = make_int4(r[12], r[13], r[14], r[15]);
+                // row `lane` of a 32 x 32 int32 box, 16-byte chunk j stored at j ^ (lane & 7) (128B swizzle)
+                uint8_t* row = myE + buf * kEpiBoxBytes + lane * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    *reinterpret_cast<int4*>(row + ((j ^ (lane & 7)) << 4)) =
+                        make_int4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -208,7 +212,7 @@ int sm_count() {
 template <int BN, int BK, int STAGES>
 cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const ConvGeom& g, int F,
                         cudaStream_t st, bool pdl) {
-    const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + 4 * 4 * 32 * 16 * 4 + 1024 + 256;
+    const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256;
     auto kern = k_gemm<BN, BK, STAGES>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
@@ -223,7 +227,7 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     const int resident = sm_count() * per_sm;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units < resident ? units : resident);
-    cfg.blockDim = dim3(192);
+    cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -249,11 +253,11 @@ cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const 
     const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, vqA, g.Cpad, g.Tpad, F, g.BK, kRowsPerTile, sw) ||
         !make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
-        !make_tmap_3d(&tp, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, g.Tpad, F, 16, 32,
-                      CU_TENSOR_MAP_SWIZZLE_NONE))
+        !make_tmap_3d(&tp, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, g.Tpad, F, 32, 32,
+                      CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
     const int nk = g.Cpad / g.BK;
-    if (g.BK == 128) return nk <= 2 ? gemm_by_bn<128, 2>(ta, tb, tp, g, F, st, pdl) : gemm_by_bn<128, 4>(ta, tb, tp, g, F, st, pdl);
+    if (g.BK == 128) return nk <= 2 ? gemm_by_bn<128, 2>(ta, tb, tp, g, F, st, pdl) : gemm_by_bn<128, 3>(ta, tb, tp, g, F, st, pdl);
     return nk <= 2 ? gemm_by_bn<64, 2>(ta, tb, tp, g, F, st, pdl) : gemm_by_bn<64, 4>(ta, tb, tp, g, F, st, pdl);
 }
 

@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "sfc_kernels.hpp"
 #include "sfc_tables.cuh"
+#include "transforms.cuh"
 
 namespace sfcb200 {
 
@@ -68,14 +69,12 @@ __global__ void __launch_bounds__(kOutThreads) k_output(const int32_t* __restric
         int p[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) p[k] = __ldg(src + size_t(k) * K * g.Tpad * g.OCpad);
+        acc_t pk[K], qt[M];
 #pragma unroll
-        for (int t1 = 0; t1 < M; ++t1) {
-            acc_t qv = 0;
+        for (int k = 0; k < K; ++k) pk[k] = p[k];
+        inv1d<V>(pk, qt);
 #pragma unroll
-            for (int k = 0; k < K; ++k)
-                if (T::a(k, t1) != 0) qv += acc_t(T::a(k, t1)) * p[k];
-            s_q[((tj * M + t1) * K + l) * L.qstride + oc] = qv;
-        }
+        for (int t1 = 0; t1 < M; ++t1) s_q[((tj * M + t1) * K + l) * L.qstride + oc] = qt[t1];
     }
     __syncthreads();
 
@@ -87,14 +86,10 @@ __global__ void __launch_bounds__(kOutThreads) k_output(const int32_t* __restric
 #pragma unroll
         for (int l = 0; l < K; ++l) qv[l] = s_q[((tj * M + t1) * K + l) * L.qstride + oc];
         acc_t* dst = s_y + (t1 * OCC + oc) * L.ystride + tj * M;
+        acc_t yt[M];
+        inv1d<V>(qv, yt);
 #pragma unroll
-        for (int t2 = 0; t2 < M; ++t2) {
-            acc_t y = 0;
-#pragma unroll
-            for (int l = 0; l < K; ++l)
-                if (T::a(l, t2) != 0) y += qv[l] * T::a(l, t2);
-            dst[t2] = y;
-        }
+        for (int t2 = 0; t2 < M; ++t2) dst[t2] = yt[t2];
     }
     __syncthreads();
 
@@ -103,24 +98,40 @@ __global__ void __launch_bounds__(kOutThreads) k_output(const int32_t* __restric
     if (threadIdx.x < OCC && int(threadIdx.x) < noc)
         s_scale[threadIdx.x] = (qpp->sa * sf[oc0 + threadIdx.x]) / double(T::DEN * T::DEN);
     __syncthreads();
+    // Rows of at most 32 columns are packed several per warp (lane -> (sub-row, ow)); one
+    // tight loop per requested output so no per-element pointer tests remain.
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int row = warp; row < M * OCC; row += kOutThreads / 32) {
-        const int oc = row % OCC, t1 = row / OCC;
-        const int oh = ti * M + t1;
-        if (oc >= noc || oh >= g.HO) continue;
-        const double scale = s_scale[oc];
-        const float scale_f = float(scale);
-        const acc_t* src = s_y + (t1 * OCC + oc) * L.ystride;
-        const size_t base = ((size_t(b) * g.OC + oc0 + oc) * g.HO + oh) * g.WO;
-        for (int ow = lane; ow < g.WO; ow += 32) {
-            const acc_t y = src[ow];
-            if (o.y32) o.y32[base + ow] = int(y);
-            if (o.y64) o.y64[base + ow] = (long long)y;
-            if (o.f32) o.f32[base + ow] = Y64 ? float(double(y) * scale) : __int2float_rn(int(y)) * scale_f;
-            if (o.f64) o.f64[base + ow] = double(y) * scale;
-            if (o.i8) o.i8[base + ow] = int8_t(fmin(fmax(rint(double(y) * scale * o.requant), 0.0), 127.0));
+    const int WO = g.WO;
+    const int rpw = WO <= 32 ? 32 / WO : 1;       // rows per warp pass
+    const int sub = WO <= 32 ? lane / WO : 0;
+    const int col0 = WO <= 32 ? lane % WO : lane;
+    const int cstep = WO <= 32 ? 32 : 32;          // only used when WO > 32
+    const bool lane_ok = sub < rpw;
+    const int hrows = min(M, g.HO - ti * M);       // output rows of this tile row inside the image
+    const size_t plane = size_t(g.HO) * WO;
+    const size_t base0 = (size_t(b) * g.OC + oc0) * plane + size_t(ti) * M * WO;
+    auto emit = [&](auto store) {
+        for (int r0 = warp * rpw; r0 < M * OCC; r0 += (kOutThreads / 32) * rpw) {
+            const int row = r0 + sub;
+            const int oc = row % OCC, t1 = row / OCC;
+            if (!lane_ok || row >= M * OCC || oc >= noc || t1 >= hrows) continue;
+            const acc_t* src = s_y + (t1 * OCC + oc) * L.ystride;
+            const size_t base = base0 + oc * plane + t1 * WO;
+            const double scale = s_scale[oc];
+            for (int c = col0; c < WO; c += (WO <= 32 ? 1 << 30 : cstep)) store(base + c, src[c], scale);
         }
-    }
+    };
+    if (o.y32) emit([&](size_t i, acc_t y, double) { o.y32[i] = int(y); });
+    if (o.y64) emit([&](size_t i, acc_t y, double) { o.y64[i] = (long long)y; });
+    if (o.f32)
+        emit([&](size_t i, acc_t y, double s) {
+            o.f32[i] = Y64 ? float(double(y) * s) : __int2float_rn(int(y)) * float(s);
+        });
+    if (o.f64) emit([&](size_t i, acc_t y, double s) { o.f64[i] = double(y) * s; });
+    if (o.i8)
+        emit([&](size_t i, acc_t y, double s) {
+            o.i8[i] = int8_t(fmin(fmax(rint(double(y) * s * o.requant), 0.0), 127.0));
+        });
 }
 
 namespace {
