@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
             const int8_t* src = src0 + size_t(ch) * g.H * g.W;
             int8_t* dst = s_x + ch * L.chs + dst_row0;
             for (int i = lane; i < seg; i += 32) {
-                const int r = int(__umulhi(unsigned(i), wmagic));
+                const int r = g.W == 1 ? i : int(__umulhi(unsigned(i), wmagic));
                 dst[r * L.wcp + (i - r * g.W)] = src[i];
             }
         }
