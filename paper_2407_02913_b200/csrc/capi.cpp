@@ -124,7 +124,7 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     const bool need64 = bound >= 2147483647.0;
     if (need64 && o->y_int32) throw Unsupported("y_int may exceed int32 for this layer; request y_int64 instead");
     WsView v = carve(ws, g, L->F);
-    const bool full = (mask | SFC_STAGE_QPARAMS) == SFC_STAGE_ALL;
+    const bool full = chained || (mask | SFC_STAGE_QPARAMS) == SFC_STAGE_ALL;
     bool pdl = chained && full;
     if (mask & SFC_STAGE_QPARAMS) {
         ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
@@ -310,8 +310,9 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
         // vmax and the saturation counter share the first 16 bytes of the workspace
         ck(cudaMemsetAsync(v.vmax, 0, 16, S(stream)), "memset vmax/sat");
         ck(launch_act_absmax(L->variant, d_x, g, v.vmax, S(stream)), "absmax launch");
-        run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, SFC_STAGE_ALL & ~SFC_STAGE_QPARAMS, true,
-                 S(stream));
+        unsigned mask = SFC_STAGE_ALL & ~SFC_STAGE_QPARAMS;
+        if (const char* dbg = std::getenv("SFC_DEBUG_FORWARD_MASK")) mask = unsigned(std::atoi(dbg));  // profiling only
+        run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask, true, S(stream));
     });
 }
 
