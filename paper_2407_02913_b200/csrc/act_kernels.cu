@@ -31,8 +31,9 @@ struct ActSmem {
     size_t x_off, z_off, q_off, bytes;
 };
 
+// `fused`: the staging area holds int16 V (kept across the grid barrier) instead of int8 vq.
 template <int V, int CC>
-__host__ __device__ inline ActSmem act_smem(int tw) {
+__host__ __device__ inline ActSmem act_smem(int tw, bool fused) {
     using T = Tab<V>;
     ActSmem s;
     s.wcp = ((tw - 1) * T::M + T::n + 3) & ~3;
@@ -41,18 +42,44 @@ __host__ __device__ inline ActSmem act_smem(int tw) {
     s.x_off = 0;
     s.z_off = (size_t(s.chs) * CC + 15) & ~size_t(15);
     s.q_off = s.z_off + ((size_t(tw) * T::n * T::K * CC * 2 + 15) & ~size_t(15));
-    s.bytes = s.q_off + size_t(tw) * T::F * CC;
+    s.bytes = s.q_off + size_t(tw) * T::F * CC * (fused ? 2 : 1);
     return s;
 }
 }  // namespace
 
+// Grid-wide barrier for a co-resident (cooperatively launched) grid; called by ONE
+// thread per CTA.  `bar[0]` counts arrivals and is reset by the last arriver, which
+// then bumps the generation `bar[1]` the others spin on, so the pair is reusable
+// without re-initialisation as long as bar[0] starts at 0.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+    const unsigned gen = ld_acquire(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+        atomicExch(bar, 0u);
+        __threadfence();
+        atomicAdd(bar + 1, 1u);
+    } else {
+        while (ld_acquire(bar + 1) == gen) __nanosleep(64);
+    }
+    __threadfence();
+}
+
 // MODE 0: max|V| -> atomicMax(*vmax).  MODE 1: quantize with the scale derived
 // from *vmax_in and write vq[f][t][c] (row pitch Cpad) for f = k*K + l.
+// MODE 2 (fused, co-resident grid only): V is computed once and kept in shared memory
+// as int16 (|V| <= 4608), the block max goes to *vmax, a grid barrier publishes the
+// global max, and the quantized rows are written from the kept V -- one launch and
+// one transform instead of two of each.
 template <int V, int MODE, int CC>
 __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ x, ConvGeom g,
                                                      int* __restrict__ vmax, const int* __restrict__ vmax_in, int bits,
                                                      QuantParams* __restrict__ qp_out, int8_t* __restrict__ vqA,
-                                                     unsigned long long* __restrict__ sat) {
+                                                     unsigned long long* __restrict__ sat, unsigned* __restrict__ gbar) {
     using T = Tab<V>;
     constexpr int n = T::n, K = T::K, M = T::M, F = T::F;
     constexpr int TPC = kActThreads / CC;   // work-groups per channel
@@ -62,32 +89,65 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     const int tw = g.tw;
     const int ti = blockIdx.x, b = blockIdx.y, c0 = blockIdx.z * CC;
     const int nch = min(CC, g.C - c0);
-    const ActSmem L = act_smem<V, CC>(tw);
+    const ActSmem L = act_smem<V, CC>(tw, MODE == 2);
     int8_t* s_x = reinterpret_cast<int8_t*>(smem + L.x_off);     // [CC][n][wcp], channel stride chs
     int16_t* s_z = reinterpret_cast<int16_t*>(smem + L.z_off);   // [tw][n][K][CC]
     int8_t* s_q = reinterpret_cast<int8_t*>(smem + L.q_off);     // [tw][F][CC]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = threadIdx.x % CC, j = threadIdx.x / CC;
 
-    // ---- stage 0: zero the staging area, then each warp copies whole channel segments:
-    // the window rows [ih0, ih0 + n) of one channel are contiguous in NCHW, so lanes walk
-    // that byte range coalesced and scatter into [c][r][pad + col] (32-bit index math).
+    // ---- stage 0: stage rows [ih0, ih0 + n) of the CTA's channels as [c][r][pad + col].
+    // The padding bytes (rows outside the image, columns outside [pad, pad + W)) are
+    // zeroed separately from the copied bytes -- disjoint, so no barrier between the two.
+    // Each warp copies two channels at a time with lanes walking the columns (coalesced
+    // in NCHW); all 2n row loads of a lane are issued before any is consumed, so a CTA
+    // pays about one global round trip instead of one per row.
     {
-        uint4* z4 = reinterpret_cast<uint4*>(s_x);
-        for (int i = threadIdx.x; i < (L.chs * CC) / 16; i += kActThreads) z4[i] = make_uint4(0, 0, 0, 0);
-        __syncthreads();
         const int ih0 = ti * M - g.pad;
-        const int r_lo = max(ih0, 0), r_hi = min(ih0 + n, g.H);
-        const int seg = (r_hi - r_lo) * g.W;                      // bytes per channel
-        const unsigned wmagic = 0xffffffffu / unsigned(g.W) + 1;  // i / W == umulhi(i, wmagic) for i < 2^16
-        const int8_t* src0 = x + (size_t(b) * g.C + c0) * size_t(g.H) * g.W + size_t(r_lo) * g.W;
-        const int dst_row0 = (r_lo - ih0) * L.wcp + g.pad;
-        for (int ch = warp; ch < nch; ch += kActThreads / 32) {
-            const int8_t* src = src0 + size_t(ch) * g.H * g.W;
-            int8_t* dst = s_x + ch * L.chs + dst_row0;
-            for (int i = lane; i < seg; i += 32) {
-                const int r = g.W == 1 ? i : int(__umulhi(unsigned(i), wmagic));
-                dst[r * L.wcp + (i - r * g.W)] = src[i];
+        const int r_lo = max(ih0, 0), nrows = min(ih0 + n, g.H) - r_lo;
+        const int rimg0 = r_lo - ih0;  // first staged row that holds image data
+        for (int i = threadIdx.x; i < CC * n; i += kActThreads) {
+            const int ch = i / n, r = i % n;
+            int8_t* row = s_x + ch * L.chs + r * L.wcp;
+            if (ch >= nch || r < rimg0 || r >= rimg0 + nrows) {
+                for (int q = 0; q < L.wcp / 4; ++q) reinterpret_cast<uint32_t*>(row)[q] = 0u;
+            } else {
+                for (int q = 0; q < g.pad; ++q) row[q] = 0;
+                for (int q = g.pad + g.W; q < L.wcp; ++q) row[q] = 0;
+            }
+        }
+        // The window rows of one channel are one contiguous byte range of NCHW: lane loads
+        // at seg_base + 32u (immediate offsets from one pointer), then scatter with
+        // r = i / W by multiply-high (exact for i < 2^32 / W; i < n * W here).
+        const size_t cstride = size_t(g.H) * g.W;
+        const int seg = nrows * g.W;
+        const unsigned wmagic = 0xffffffffu / unsigned(g.W) + 1u;
+        const int8_t* src0 = x + (size_t(b) * g.C + c0) * cstride + size_t(r_lo) * g.W;
+        int8_t* dst0 = s_x + rimg0 * L.wcp + g.pad;
+        constexpr int kWarps = kActThreads / 32, kU = 8;
+        auto scatter = [&](int8_t* d, int i, int8_t v) {
+            const int r = g.W == 1 ? i : int(__umulhi(unsigned(i), wmagic));
+            d[r * L.wcp + (i - r * g.W)] = v;
+        };
+        for (int ch0 = 2 * warp; ch0 < nch; ch0 += 2 * kWarps) {
+            const bool two = ch0 + 1 < nch;
+            const int8_t* s0 = src0 + size_t(ch0) * cstride;
+            const int8_t* s1 = two ? s0 + cstride : s0;
+            int8_t* d0 = dst0 + ch0 * L.chs;
+            for (int i0 = lane; i0 < seg; i0 += 32 * kU) {
+                int8_t v0[kU], v1[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const bool ok = i0 + 32 * u < seg;
+                    v0[u] = ok ? __ldg(s0 + i0 + 32 * u) : int8_t(0);
+                    v1[u] = ok ? __ldg(s1 + i0 + 32 * u) : int8_t(0);
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                    if (i0 + 32 * u < seg) {
+                        scatter(d0, i0 + 32 * u, v0[u]);
+                        if (two) scatter(d0 + L.chs, i0 + 32 * u, v1[u]);
+                    }
             }
         }
     }
@@ -105,6 +165,65 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
         fwd1d<V>(xs, z);
 #pragma unroll
         for (int l = 0; l < K; ++l) dst[l * CC] = int16_t(z[l]);
+    }
+
+    if (MODE == 2) {
+        int16_t* s_v = reinterpret_cast<int16_t*>(smem + L.q_off);  // [tw][F][CC]
+        __shared__ int s_max;
+        if (threadIdx.x == 0) s_max = 0;
+        __syncthreads();
+        int local = 0;
+        for (int idx = j; idx < tw * K; idx += TPC) {
+            const int l = idx % K, tj = idx / K;
+            int zr[n];
+#pragma unroll
+            for (int r = 0; r < n; ++r) zr[r] = s_z[((tj * n + r) * K + l) * CC + c];
+            int v[K];
+            fwd1d<V>(zr, v);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                s_v[(tj * F + k * K + l) * CC + c] = int16_t(v[k]);
+                local = max(local, abs(v[k]));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+        if (lane == 0 && local > 0) atomicMax(&s_max, local);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (s_max > 0) atomicMax(vmax, s_max);
+            grid_barrier(gbar, gridDim.x * gridDim.y * gridDim.z);
+            s_max = int(ld_acquire(reinterpret_cast<const unsigned*>(vmax)));
+        }
+        __syncthreads();
+        const QuantParams qp = derive_qparams_block(s_max, bits);  // contains __syncthreads
+        if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *qp_out = qp;
+        griddep_launch_dependents();  // every CTA is resident: the GEMM may start its prologue
+
+        // quantize 4 channels per 32-bit word straight from the kept V
+        constexpr int WPR = CC / 4;
+        const int t0 = (b * g.th + ti) * tw;
+        auto store = [&](auto quantize) {
+            for (int i = threadIdx.x; i < tw * F * WPR; i += kActThreads) {
+                const int wd = i % WPR, row = i / WPR;
+                const int f = row % F, tj = row / F;
+                const uint2 v4 = *reinterpret_cast<const uint2*>(s_v + size_t(row) * CC + wd * 4);
+                const uint32_t q0 = uint32_t(quantize(int(int16_t(v4.x & 0xffff)))) & 0xff;
+                const uint32_t q1 = uint32_t(quantize(int(v4.x) >> 16)) & 0xff;
+                const uint32_t q2 = uint32_t(quantize(int(int16_t(v4.y & 0xffff)))) & 0xff;
+                const uint32_t q3 = uint32_t(quantize(int(v4.y) >> 16)) & 0xff;
+                reinterpret_cast<uint32_t*>(vqA + (size_t(f) * g.Tpad + t0 + tj) * g.Cpad + c0)[wd] =
+                    q0 | (q1 << 8) | (q2 << 16) | (q3 << 24);
+            }
+        };
+        if (qp.exact) {
+            const long long mul = qp.mul, half = 1ll << (qp.shift - 1);
+            const int shift = qp.shift;
+            store([=](int v) { return int(((long long)v * mul + half) >> shift); });
+        } else {
+            store([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, sat); });
+        }
+        return;
     }
 
     QuantParams qp{};
@@ -148,6 +267,7 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     if (MODE == 0) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+        griddep_wait();  // under PDL: *vmax has been zeroed by the predecessor
         if (lane == 0 && local > 0) atomicMax(vmax, local);
         return;
     }
@@ -185,24 +305,56 @@ __global__ void k_debug_quant(const QuantParams* __restrict__ qpp, int vmax, int
 // ============================================================================ host
 namespace {
 
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// MODE 2 returns cudaErrorCooperativeLaunchTooLarge (nothing launched) when the grid
+// cannot be co-resident; the caller then runs the two-kernel form.
 template <int V, int MODE, int CC>
 cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits,
-                          QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl) {
-    const size_t smem = act_smem<V, CC>(g.tw).bytes;
+                          QuantParams* qp, int8_t* vqA, unsigned long long* sat, unsigned* gbar, cudaStream_t st,
+                          bool pdl) {
+    const size_t smem = act_smem<V, CC>(g.tw, MODE == 2).bytes;
     auto kern = k_act<V, MODE, CC>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
+    static size_t attr_bytes = 0;  // per instantiation: raise the opt-in only when a layer needs more
+    int per_sm = 0;
+    if (smem > attr_bytes) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        attr_bytes = smem;
+    }
+    const long grid = long(g.th) * g.B * ((g.C + CC - 1) / CC);
+    if (MODE == 2) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kActThreads, smem) != cudaSuccess)
+            return cudaErrorCooperativeLaunchTooLarge;
+        if (long(per_sm) * sm_count() < grid) return cudaErrorCooperativeLaunchTooLarge;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.th, g.B, (g.C + CC - 1) / CC);
     cfg.blockDim = dim3(kActThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (MODE == 2) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na++].val.cooperative = 1;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, x, g, vmax, vmax_in, bits, qp, vqA, sat);
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, x, g, vmax, vmax_in, bits, qp, vqA, sat, gbar);
 }
 
 // Channels per CTA: 32 gives full 32-byte vq row segments; shrink for two waves
@@ -211,10 +363,10 @@ template <int V>
 int pick_cc(const ConvGeom& g) {
     auto ctas = [&](int c) { return long(g.th) * g.B * ((g.C + c - 1) / c); };
     auto smem = [&](int c) {
-        return c == 32 ? act_smem<V, 32>(g.tw).bytes
-             : c == 16 ? act_smem<V, 16>(g.tw).bytes
-             : c == 8  ? act_smem<V, 8>(g.tw).bytes
-                       : act_smem<V, 4>(g.tw).bytes;
+        return c == 32 ? act_smem<V, 32>(g.tw, true).bytes
+             : c == 16 ? act_smem<V, 16>(g.tw, true).bytes
+             : c == 8  ? act_smem<V, 8>(g.tw, true).bytes
+                       : act_smem<V, 4>(g.tw, true).bytes;
     };
     int cc = 32;
     while (cc > 4 && ctas(cc) < 2 * 148) cc /= 2;
@@ -224,31 +376,40 @@ int pick_cc(const ConvGeom& g) {
 
 template <int V, int MODE>
 cudaError_t act_launch(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits, QuantParams* qp,
-                       int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl) {
+                       int8_t* vqA, unsigned long long* sat, unsigned* gbar, cudaStream_t st, bool pdl) {
     switch (pick_cc<V>(g)) {
-        case 32: return act_launch_cc<V, MODE, 32>(x, g, vmax, vmax_in, bits, qp, vqA, sat, st, pdl);
-        case 16: return act_launch_cc<V, MODE, 16>(x, g, vmax, vmax_in, bits, qp, vqA, sat, st, pdl);
-        case 8: return act_launch_cc<V, MODE, 8>(x, g, vmax, vmax_in, bits, qp, vqA, sat, st, pdl);
-        default: return act_launch_cc<V, MODE, 4>(x, g, vmax, vmax_in, bits, qp, vqA, sat, st, pdl);
+        case 32: return act_launch_cc<V, MODE, 32>(x, g, vmax, vmax_in, bits, qp, vqA, sat, gbar, st, pdl);
+        case 16: return act_launch_cc<V, MODE, 16>(x, g, vmax, vmax_in, bits, qp, vqA, sat, gbar, st, pdl);
+        case 8: return act_launch_cc<V, MODE, 8>(x, g, vmax, vmax_in, bits, qp, vqA, sat, gbar, st, pdl);
+        default: return act_launch_cc<V, MODE, 4>(x, g, vmax, vmax_in, bits, qp, vqA, sat, gbar, st, pdl);
     }
 }
 
 }  // namespace
 
-cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, cudaStream_t st) {
+cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, cudaStream_t st, bool pdl) {
     switch (variant) {
-        case 0: return act_launch<0, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, st, false);
-        case 1: return act_launch<1, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, st, false);
-        default: return act_launch<2, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, st, false);
+        case 0: return act_launch<0, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, nullptr, st, pdl);
+        case 1: return act_launch<1, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, nullptr, st, pdl);
+        default: return act_launch<2, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, nullptr, st, pdl);
     }
 }
 
 cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, const int* vmax, int bits,
                              QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl) {
     switch (variant) {
-        case 0: return act_launch<0, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, st, pdl);
-        case 1: return act_launch<1, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, st, pdl);
-        default: return act_launch<2, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, st, pdl);
+        case 0: return act_launch<0, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
+        case 1: return act_launch<1, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
+        default: return act_launch<2, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
+    }
+}
+
+cudaError_t launch_act_fused(int variant, const int8_t* x, const ConvGeom& g, int* vmax, int bits, QuantParams* qp,
+                             int8_t* vqA, unsigned long long* sat, unsigned* gbar, cudaStream_t st) {
+    switch (variant) {
+        case 0: return act_launch<0, 2>(x, g, vmax, nullptr, bits, qp, vqA, sat, gbar, st, false);
+        case 1: return act_launch<1, 2>(x, g, vmax, nullptr, bits, qp, vqA, sat, gbar, st, false);
+        default: return act_launch<2, 2>(x, g, vmax, nullptr, bits, qp, vqA, sat, gbar, st, false);
     }
 }
 

@@ -252,6 +252,25 @@ __global__ void __launch_bounds__(256) k_sq_err(const double* __restrict__ out, 
     }
 }
 
+__global__ void k_zero_words(uint32_t* __restrict__ p, int words) {
+    griddep_wait();
+    griddep_launch_dependents();
+    if (int(threadIdx.x) < words) p[threadIdx.x] = 0u;
+}
+
+cudaError_t launch_zero_words(uint32_t* p, int words, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_zero_words, p, words);
+}
+
 cudaError_t launch_sq_err(const double* out, const int32_t* ref, long long n, double* sums, cudaStream_t st) {
     long long blocks = (n + 255) / 256;
     blocks = blocks > 4 * 148 ? 4 * 148 : (blocks < 1 ? 1 : blocks);

@@ -78,6 +78,7 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 struct WsView {
     int* vmax;
     unsigned long long* sat;
+    unsigned* gbar;
     QuantParams* qp;
     int8_t* vq;
     int32_t* P;
@@ -88,6 +89,7 @@ WsView carve(void* ws, const ConvGeom& g, int F) {
     WsView v;
     v.vmax = reinterpret_cast<int*>(base);
     v.sat = reinterpret_cast<unsigned long long*>(base + 8);
+    v.gbar = reinterpret_cast<unsigned*>(base + 16);
     v.qp = reinterpret_cast<QuantParams*>(base + 64);
     v.vq = reinterpret_cast<int8_t*>(base + up(256));
     v.P = reinterpret_cast<int32_t*>(base + up(256) + up(size_t(F) * g.Tpad * g.Cpad));
@@ -98,6 +100,7 @@ void check_call(const sfc_layer* L, const void* x, int n, int h, int w, int pad)
     if (!L) throw std::invalid_argument("null layer");
     if (!x) throw std::invalid_argument("null input");
     if (n <= 0 || h <= 0 || w <= 0 || pad < 0) throw std::invalid_argument("bad input shape");
+    if (w > 16384 || h > 16384 || pad > 64) throw Unsupported("image sides above 16384 or padding above 64");
     if (h + 2 * pad - L->plan->R + 1 <= 0 || w + 2 * pad - L->plan->R + 1 <= 0)
         throw std::invalid_argument("filter larger than padded input");
 }
@@ -106,6 +109,16 @@ ConvGeom geom_of(const sfc_layer* L, int n, int h, int w, int pad) {
     ConvGeom g;
     geom_init(g, L->variant, n, L->IC, h, w, pad, L->OC);
     return g;
+}
+
+// |y| <= (max_t sum_k |A[k,t]|)^2 * IC * qmax^2 (MinMax never clips, so |vq|,|uq| <= qmax):
+// whether the exact y needs 64-bit accumulation; int32 y is then refused up front.
+bool needs_y64(const sfc_layer* L, const sfc_outputs* o) {
+    const double qmax = double((1 << (L->bits - 1)) - 1);
+    const double bound = double(L->max_a_col_l1) * double(L->max_a_col_l1) * L->IC * qmax * qmax;
+    const bool need64 = bound >= 2147483647.0;
+    if (need64 && o && o->y_int32) throw Unsupported("y_int may exceed int32 for this layer; request y_int64 instead");
+    return need64;
 }
 
 // Launch the per-call kernels.  `chained`: the previous operation on the stream is
@@ -118,14 +131,10 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
     const ConvGeom g = geom_of(L, n, h, w, pad);
     if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
-    // |y| <= (max_t sum_k |A[k,t]|)^2 * IC * qmax^2 (MinMax never clips, so |vq|,|uq| <= qmax).
-    const double qmax = double((1 << (L->bits - 1)) - 1);
-    const double bound = double(L->max_a_col_l1) * double(L->max_a_col_l1) * L->IC * qmax * qmax;
-    const bool need64 = bound >= 2147483647.0;
-    if (need64 && o->y_int32) throw Unsupported("y_int may exceed int32 for this layer; request y_int64 instead");
+    const bool need64 = needs_y64(L, o);
     WsView v = carve(ws, g, L->F);
     const bool full = chained || (mask | SFC_STAGE_QPARAMS) == SFC_STAGE_ALL;
-    bool pdl = chained && full;
+    bool pdl = chained && full;  // (the fused activation kernel, when it ran, is the predecessor)
     if (mask & SFC_STAGE_QPARAMS) {
         ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
         pdl = false;
@@ -277,6 +286,7 @@ int sfc_conv_workspace_size(sfc_layer_t L, int n, int h, int w, int pad, size_t*
     return guarded([&] {
         if (!L || !bytes) throw std::invalid_argument("null argument");
         if (n <= 0 || h <= 0 || w <= 0 || pad < 0) throw std::invalid_argument("bad input shape");
+    if (w > 16384 || h > 16384 || pad > 64) throw Unsupported("image sides above 16384 or padding above 64");
         *bytes = workspace_bytes(geom_of(L, n, h, w, pad), L->F);
     });
 }
@@ -307,12 +317,24 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
         const ConvGeom g = geom_of(L, n, h, w, pad);
         if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
         WsView v = carve(ws, g, L->F);
-        // vmax and the saturation counter share the first 16 bytes of the workspace
-        ck(cudaMemsetAsync(v.vmax, 0, 16, S(stream)), "memset vmax/sat");
-        ck(launch_act_absmax(L->variant, d_x, g, v.vmax, S(stream)), "absmax launch");
+        // vmax, the saturation counter and the grid-barrier words share the first 24 bytes
+        ck(launch_zero_words(reinterpret_cast<uint32_t*>(v.vmax), 6, S(stream)), "workspace reset launch");
         unsigned mask = SFC_STAGE_ALL & ~SFC_STAGE_QPARAMS;
         if (const char* dbg = std::getenv("SFC_DEBUG_FORWARD_MASK")) mask = unsigned(std::atoi(dbg));  // profiling only
-        run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask, true, S(stream));
+        const bool try_fused = (mask & SFC_STAGE_ACT) && std::getenv("SFC_FUSED_ACT");
+        cudaError_t fe = cudaErrorCooperativeLaunchTooLarge;
+        if (!o) throw std::invalid_argument("null outputs");
+        needs_y64(L, o);  // refuse before anything is launched
+        if (try_fused) {
+            fe = launch_act_fused(L->variant, d_x, g, v.vmax, L->bits, v.qp, v.vq, v.sat, v.gbar, S(stream));
+            if (fe != cudaErrorCooperativeLaunchTooLarge) ck(fe, "fused activation launch");
+        }
+        if (fe == cudaSuccess) {
+            run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask & ~SFC_STAGE_ACT, true, S(stream));
+        } else {
+            ck(launch_act_absmax(L->variant, d_x, g, v.vmax, S(stream), true), "absmax launch");
+            run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask, true, S(stream));
+        }
     });
 }
 

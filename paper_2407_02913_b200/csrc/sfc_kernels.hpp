@@ -34,7 +34,18 @@ size_t workspace_bytes(const ConvGeom& g, int F);
 // `pdl`: launch with programmatic stream serialization (overlap the predecessor's tail).
 cudaError_t launch_filter_prepare(int variant, const int8_t* w, int OC, int IC, int Cpad, int OCpad, int bits,
                                   double* sf, int* umax, int8_t* uqB, unsigned long long* sat, cudaStream_t st);
-cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, cudaStream_t st);
+// pdl: launched under programmatic stream serialization; the CTAs stage and transform
+// their tiles before waiting on the predecessor (which zeroes *vmax).
+cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, cudaStream_t st,
+                              bool pdl = false);
+// Zero `words` 32-bit words (<= 32) at p once the predecessor kernel has finished --
+// a PDL kernel instead of a memset node, which costs ~3 us in a graph / stream chain.
+cudaError_t launch_zero_words(uint32_t* p, int words, cudaStream_t st);
+// Fused absmax + quantize for grids that fit co-resident (grid barrier on gbar[0..1],
+// gbar[0] zero on entry).  Returns cudaErrorCooperativeLaunchTooLarge without launching
+// anything when the grid does not fit; *vmax must be zero on entry.
+cudaError_t launch_act_fused(int variant, const int8_t* x, const ConvGeom& g, int* vmax, int bits, QuantParams* qp,
+                             int8_t* vqA, unsigned long long* sat, unsigned* gbar, cudaStream_t st);
 cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, const int* vmax, int bits,
                              QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl);
 cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
