@@ -10,7 +10,8 @@ from __future__ import annotations
 import ctypes
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsfc_b200.so")
+# SFC_B200_LIB selects another in-tree build (the timeline build libsfc_b200_tl.so).
+LIB_PATH = os.environ.get("SFC_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsfc_b200.so")
 
 SFC_OK, SFC_ERR_INVALID, SFC_ERR_DOMAIN, SFC_ERR_UNSUPPORTED, SFC_ERR_CUDA = 0, -1, -2, -3, -4
 
@@ -20,7 +21,7 @@ EXPORTED = (
     "sfc_plan_matrices", "sfc_layer_create", "sfc_layer_destroy", "sfc_layer_filter_scales",
     "sfc_layer_saturations", "sfc_layer_uq", "sfc_conv_workspace_size", "sfc_act_absmax", "sfc_conv_int8",
     "sfc_conv_int8_stages", "sfc_conv_forward", "sfc_conv_stats", "sfc_conv_views", "sfc_direct_conv_int8", "sfc_frequency_energy_int8",
-    "sfc_transform_filters_int8", "sfc_debug_quantizer", "sfc_report_sq_err",
+    "sfc_transform_filters_int8", "sfc_debug_quantizer", "sfc_report_sq_err", "sfc_debug_timeline",
 )
 
 
@@ -80,6 +81,7 @@ _SIGS = {
     "sfc_frequency_energy_int8": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "sfc_transform_filters_int8": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "sfc_debug_quantizer": (_i, [_i, _i, _vp, _i64p, _vp]),
+    "sfc_debug_timeline": (_i, [_vp, _i]),
     "sfc_report_sq_err": (_i, [_vp, _vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _vp]),
 }
 

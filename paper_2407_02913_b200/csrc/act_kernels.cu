@@ -14,6 +14,8 @@
 // and all item decompositions divide by compile-time constants.
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "ptx.cuh"
 #include "sfc_kernels.hpp"
@@ -79,11 +81,14 @@ template <int V, int MODE, int CC>
 __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ x, ConvGeom g,
                                                      int* __restrict__ vmax, const int* __restrict__ vmax_in, int bits,
                                                      QuantParams* __restrict__ qp_out, int8_t* __restrict__ vqA,
-                                                     unsigned long long* __restrict__ sat, unsigned* __restrict__ gbar) {
+                                                     unsigned long long* __restrict__ sat, unsigned* __restrict__ gbar,
+                                                     const QuantParams* __restrict__ qtab) {
     using T = Tab<V>;
     constexpr int n = T::n, K = T::K, M = T::M, F = T::F;
     constexpr int TPC = kActThreads / CC;   // work-groups per channel
     extern __shared__ __align__(16) uint8_t smem[];
+    constexpr int kTl = MODE == 0 ? kTlAbsmax : (MODE == 1 ? kTlQuant : kTlFused);
+    tl_mark(kTl, 0);
     if (MODE == 0) griddep_launch_dependents();
 
     const int tw = g.tw;
@@ -96,59 +101,78 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = threadIdx.x % CC, j = threadIdx.x / CC;
 
-    // ---- stage 0: stage rows [ih0, ih0 + n) of the CTA's channels as [c][r][pad + col].
-    // The padding bytes (rows outside the image, columns outside [pad, pad + W)) are
-    // zeroed separately from the copied bytes -- disjoint, so no barrier between the two.
-    // Each warp copies two channels at a time with lanes walking the columns (coalesced
-    // in NCHW); all 2n row loads of a lane are issued before any is consumed, so a CTA
-    // pays about one global round trip instead of one per row.
+    // ---- stage 0: stage rows [ih0, ih0 + n) of the CTA's channels as [c][r][pad + col],
+    // zero outside the image.  A channel's window rows are one contiguous byte range of
+    // NCHW (seg bytes), so the CTA moves 32-bit words: word w of channel ch covers bytes
+    // [4w - mis, 4w - mis + 4) of the segment (mis = its start's misalignment); words fully
+    // inside the segment are one LDG.32, the partial head / tail words byte loads.  A
+    // thread derives (row, col) of its word's first byte once (multiply-high, exact for
+    // i < 2^32 / W) and steps it.  The first batch of loads is in flight while the whole
+    // staging area is zeroed with 16-byte stores.
     {
         const int ih0 = ti * M - g.pad;
         const int r_lo = max(ih0, 0), nrows = min(ih0 + n, g.H) - r_lo;
         const int rimg0 = r_lo - ih0;  // first staged row that holds image data
-        for (int i = threadIdx.x; i < CC * n; i += kActThreads) {
-            const int ch = i / n, r = i % n;
-            int8_t* row = s_x + ch * L.chs + r * L.wcp;
-            if (ch >= nch || r < rimg0 || r >= rimg0 + nrows) {
-                for (int q = 0; q < L.wcp / 4; ++q) reinterpret_cast<uint32_t*>(row)[q] = 0u;
-            } else {
-                for (int q = 0; q < g.pad; ++q) row[q] = 0;
-                for (int q = g.pad + g.W; q < L.wcp; ++q) row[q] = 0;
-            }
-        }
-        // The window rows of one channel are one contiguous byte range of NCHW: lane loads
-        // at seg_base + 32u (immediate offsets from one pointer), then scatter with
-        // r = i / W by multiply-high (exact for i < 2^32 / W; i < n * W here).
         const size_t cstride = size_t(g.H) * g.W;
         const int seg = nrows * g.W;
         const unsigned wmagic = 0xffffffffu / unsigned(g.W) + 1u;
         const int8_t* src0 = x + (size_t(b) * g.C + c0) * cstride + size_t(r_lo) * g.W;
         int8_t* dst0 = s_x + rimg0 * L.wcp + g.pad;
-        constexpr int kWarps = kActThreads / 32, kU = 8;
-        auto scatter = [&](int8_t* d, int i, int8_t v) {
-            const int r = g.W == 1 ? i : int(__umulhi(unsigned(i), wmagic));
-            d[r * L.wcp + (i - r * g.W)] = v;
-        };
-        for (int ch0 = 2 * warp; ch0 < nch; ch0 += 2 * kWarps) {
-            const bool two = ch0 + 1 < nch;
-            const int8_t* s0 = src0 + size_t(ch0) * cstride;
-            const int8_t* s1 = two ? s0 + cstride : s0;
-            int8_t* d0 = dst0 + ch0 * L.chs;
-            for (int i0 = lane; i0 < seg; i0 += 32 * kU) {
-                int8_t v0[kU], v1[kU];
+        const int nw = (seg + 6) >> 2;  // words covering seg bytes at any misalignment
+        const unsigned nwmagic = 0xffffffffu / unsigned(nw) + 1u;
+        const int total = nch * nw;
+        constexpr int kJ = 4;
+        uint32_t wv[kJ];
+        int wch[kJ], wlo[kJ];
+        auto load = [&](int k0) {
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const bool ok = i0 + 32 * u < seg;
-                    v0[u] = ok ? __ldg(s0 + i0 + 32 * u) : int8_t(0);
-                    v1[u] = ok ? __ldg(s1 + i0 + 32 * u) : int8_t(0);
-                }
+            for (int jj = 0; jj < kJ; ++jj) {
+                const int k = k0 + jj * kActThreads + int(threadIdx.x);
+                wlo[jj] = 1 << 30;  // nothing to store
+                if (k < total) {
+                    const int ch = nw == 1 ? k : int(__umulhi(unsigned(k), nwmagic));
+                    const int w = k - ch * nw;
+                    const int8_t* cs = src0 + size_t(ch) * cstride;
+                    const int mis = int(reinterpret_cast<uintptr_t>(cs) & 3);
+                    const int lo = 4 * w - mis;  // segment index of the word's first byte
+                    uint32_t v = 0;
+                    if (lo >= 0 && lo + 4 <= seg) {
+                        v = __ldg(reinterpret_cast<const unsigned int*>(cs + lo));
+                    } else {
 #pragma unroll
-                for (int u = 0; u < kU; ++u)
-                    if (i0 + 32 * u < seg) {
-                        scatter(d0, i0 + 32 * u, v0[u]);
-                        if (two) scatter(d0 + L.chs, i0 + 32 * u, v1[u]);
+                        for (int q = 0; q < 4; ++q)
+                            if (lo + q >= 0 && lo + q < seg) v |= uint32_t(uint8_t(__ldg(cs + lo + q))) << (8 * q);
                     }
+                    wv[jj] = v, wch[jj] = ch, wlo[jj] = lo;
+                }
             }
+        };
+        auto store = [&]() {
+#pragma unroll
+            for (int jj = 0; jj < kJ; ++jj) {
+                const int lo = wlo[jj];
+                if (lo >= seg) continue;
+                const int i0 = lo < 0 ? 0 : lo;  // first in-segment byte
+                int r = g.W == 1 ? i0 : int(__umulhi(unsigned(i0), wmagic));
+                int col = i0 - r * g.W;
+                int8_t* d = dst0 + wch[jj] * L.chs;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int i = lo + q;
+                    if (i < i0 || i >= seg) continue;
+                    d[r * L.wcp + col] = int8_t(wv[jj] >> (8 * q));
+                    if (++col == g.W) col = 0, ++r;
+                }
+            }
+        };
+        load(0);
+        uint4* z4 = reinterpret_cast<uint4*>(s_x);
+        for (int i = threadIdx.x; i < (L.chs * CC) / 16; i += kActThreads) z4[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        store();
+        for (int k0 = kJ * kActThreads; k0 < total; k0 += kJ * kActThreads) {
+            load(k0);
+            store();
         }
     }
     __syncthreads();
@@ -196,7 +220,7 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
             s_max = int(ld_acquire(reinterpret_cast<const unsigned*>(vmax)));
         }
         __syncthreads();
-        const QuantParams qp = derive_qparams_block(s_max, bits);  // contains __syncthreads
+        const QuantParams qp = qparams_for(s_max, bits, qtab);
         if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *qp_out = qp;
         griddep_launch_dependents();  // every CTA is resident: the GEMM may start its prologue
 
@@ -223,17 +247,18 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
         } else {
             store([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, sat); });
         }
+        tl_mark(kTl, 2);
         return;
     }
 
     QuantParams qp{};
     if (MODE == 1) {
         griddep_wait();  // the absmax pre-pass (and any multi-GPU MAX exchange) is complete
-        qp = derive_qparams_block(*vmax_in, bits);  // contains __syncthreads
+        tl_mark(kTl, 1);
+        qp = qparams_for(*vmax_in, bits, qtab);
         if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *qp_out = qp;
-    } else {
-        __syncthreads();
     }
+    __syncthreads();  // stage 1's s_z is complete (the table lookup does not synchronise)
 
     // ---- stage 2: column transform (+ quantize), items (tj, l)
     int local = 0;
@@ -268,7 +293,9 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
 #pragma unroll
         for (int o = 16; o; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
         griddep_wait();  // under PDL: *vmax has been zeroed by the predecessor
+        tl_mark(kTl, 1);
         if (lane == 0 && local > 0) atomicMax(vmax, local);
+        tl_mark(kTl, 2);
         return;
     }
     __syncthreads();
@@ -283,16 +310,25 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
         const uint32_t v = reinterpret_cast<const uint32_t*>(s_q + size_t(row) * CC)[wd];
         reinterpret_cast<uint32_t*>(vqA + (size_t(f) * g.Tpad + t0 + tj) * g.Cpad + c0)[wd] = v;
     }
+    tl_mark(kTl, 2);
 }
 
 // Stand-alone quantizer derivation (stats / the exhaustive test hook).
 __global__ void k_quant_params(const int* __restrict__ vmax_p, int bits, QuantParams* __restrict__ qp,
-                               unsigned long long* sat) {
-    const QuantParams p = derive_qparams_block(*vmax_p, bits);
+                               unsigned long long* sat, const QuantParams* __restrict__ qtab) {
+    const QuantParams p = qparams_for(*vmax_p, bits, qtab);
     if (threadIdx.x == 0) {
         *qp = p;
         *sat = 0;
     }
+}
+
+// One warp per table entry: bits = 2 + e / (kQpTableMax + 1), vmax = e % (kQpTableMax + 1).
+__global__ void k_build_qtable(QuantParams* __restrict__ tab) {
+    const int e = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (e >= kQpTableEntries) return;
+    const QuantParams p = derive_qparams_warp(e % (kQpTableMax + 1), 2 + e / (kQpTableMax + 1));
+    if ((threadIdx.x & 31) == 0) tab[e] = p;
 }
 
 __global__ void k_debug_quant(const QuantParams* __restrict__ qpp, int vmax, int32_t* __restrict__ q,
@@ -303,6 +339,26 @@ __global__ void k_debug_quant(const QuantParams* __restrict__ qpp, int vmax, int
 }
 
 // ============================================================================ host
+const QuantParams* qparams_table(bool build) {
+    static std::mutex mu;
+    static QuantParams* tabs[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (tabs[dev] || !build) return tabs[dev];
+    std::lock_guard<std::mutex> lock(mu);
+    if (tabs[dev]) return tabs[dev];
+    QuantParams* t = nullptr;
+    if (cudaMalloc(&t, sizeof(QuantParams) * kQpTableEntries) != cudaSuccess) return nullptr;
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return cudaFree(t), nullptr;
+    k_build_qtable<<<(kQpTableEntries * 32 + 255) / 256, 256, 0, s>>>(t);
+    const bool ok = cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess;
+    cudaStreamDestroy(s);
+    if (!ok) return cudaFree(t), nullptr;
+    tabs[dev] = t;
+    return t;
+}
+
 namespace {
 
 int sm_count() {
@@ -354,7 +410,8 @@ cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int* vmax, const i
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, kern, x, g, vmax, vmax_in, bits, qp, vqA, sat, gbar);
+    return cudaLaunchKernelEx(&cfg, kern, x, g, vmax, vmax_in, bits, qp, vqA, sat, gbar,
+                              MODE == 0 ? nullptr : qparams_table(false));
 }
 
 // Channels per CTA: 32 gives full 32-byte vq row segments; shrink for two waves
@@ -413,9 +470,11 @@ cudaError_t launch_act_fused(int variant, const int8_t* x, const ConvGeom& g, in
     }
 }
 
+SFC_TL_UNIT_READER(tl_read_act)
+
 cudaError_t launch_quant_params(const int* vmax, int bits, QuantParams* qp, unsigned long long* sat,
                                 cudaStream_t st) {
-    k_quant_params<<<1, 256, 0, st>>>(vmax, bits, qp, sat);
+    k_quant_params<<<1, 256, 0, st>>>(vmax, bits, qp, sat, qparams_table(false));
     return cudaGetLastError();
 }
 

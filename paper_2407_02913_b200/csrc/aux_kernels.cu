@@ -253,10 +253,15 @@ __global__ void __launch_bounds__(256) k_sq_err(const double* __restrict__ out, 
 }
 
 __global__ void k_zero_words(uint32_t* __restrict__ p, int words) {
+    tl_mark(kTlZero, 0);
     griddep_wait();
+    tl_mark(kTlZero, 1);
     griddep_launch_dependents();
     if (int(threadIdx.x) < words) p[threadIdx.x] = 0u;
+    tl_mark(kTlZero, 2);
 }
+
+SFC_TL_UNIT_READER(tl_read_aux)
 
 cudaError_t launch_zero_words(uint32_t* p, int words, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};

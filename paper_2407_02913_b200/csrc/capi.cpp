@@ -134,18 +134,20 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     const bool need64 = needs_y64(L, o);
     WsView v = carve(ws, g, L->F);
     const bool full = chained || (mask | SFC_STAGE_QPARAMS) == SFC_STAGE_ALL;
-    bool pdl = chained && full;  // (the fused activation kernel, when it ran, is the predecessor)
+    static const bool no_pdl = std::getenv("SFC_DEBUG_NO_PDL") != nullptr;  // debugging knob
+    const bool full_pdl = full && !no_pdl;
+    bool pdl = chained && full_pdl;  // (the fused activation kernel, when it ran, is the predecessor)
     if (mask & SFC_STAGE_QPARAMS) {
         ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
         pdl = false;
     }
     if (mask & SFC_STAGE_ACT) {
         ck(launch_act_quant(L->variant, d_x, g, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "act launch");
-        pdl = full;
+        pdl = full_pdl;
     }
     if (mask & SFC_STAGE_GEMM) {
         ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st, pdl), "gemm launch");
-        pdl = full;
+        pdl = full_pdl;
     }
     if (mask & SFC_STAGE_OUTPUT) {
         const OutPtrs op{o->y_int32, o->y_int64, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
@@ -216,6 +218,7 @@ int sfc_layer_create(sfc_plan_t plan, const int8_t* d_w, int oc, int ic, int bit
         if (search != SFC_SEARCH_MINMAX) throw Unsupported("only MinMax scale search on the device path");
         L = new sfc_layer();
         L->plan = plan->p;
+        qparams_table(true);  // once per device; the kernels derive per CTA if this failed
         L->variant = plan->p->variant;
         L->OC = oc;
         L->IC = ic;
@@ -415,6 +418,29 @@ int sfc_report_sq_err(const double* d_out, const int32_t* d_ref, int64_t n, doub
     });
 }
 
+int sfc_debug_timeline(uint64_t* out, int reset) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("null argument");
+        ck(cudaDeviceSynchronize(), "sync");
+        unsigned long long part[4][kTlCount][3];
+        cudaError_t (*readers[4])(unsigned long long*, bool) = {tl_read_aux, tl_read_act, tl_read_gemm, tl_read_out};
+        for (int u = 0; u < 4; ++u) {
+            const cudaError_t e = readers[u](&part[u][0][0], reset != 0);
+            if (e == cudaErrorNotSupported) throw Unsupported("not the timeline build (make TIMELINE=1)");
+            ck(e, "timeline read");
+        }
+        for (int k = 0; k < kTlCount; ++k) {
+            unsigned long long a = ~0ull, b = ~0ull, c = 0;
+            for (int u = 0; u < 4; ++u) {
+                a = std::min(a, part[u][k][0]);
+                b = std::min(b, part[u][k][1]);
+                c = std::max(c, part[u][k][2]);
+            }
+            out[3 * k] = a, out[3 * k + 1] = b, out[3 * k + 2] = c;
+        }
+    });
+}
+
 int sfc_debug_quantizer(int vmax, int bits, int32_t* d_q, int64_t* info, void* stream) {
     return guarded([&] {
         if (!d_q || vmax < 0 || bits < 2 || bits > 8) throw std::invalid_argument("bad quantizer probe");
@@ -424,6 +450,7 @@ int sfc_debug_quantizer(int vmax, int bits, int32_t* d_q, int64_t* info, void* s
         unsigned long long* sat = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 8);
         QuantParams* qp = reinterpret_cast<QuantParams*>(static_cast<uint8_t*>(scratch) + 64);
         ck(cudaMemcpyAsync(d_vmax, &vmax, sizeof(int), cudaMemcpyHostToDevice, S(stream)), "copy vmax");
+        qparams_table(true);
         ck(launch_quant_params(d_vmax, bits, qp, sat, S(stream)), "qparams");
         ck(launch_debug_quant(qp, vmax, d_q, sat, S(stream)), "debug quant");
         QuantParams h;

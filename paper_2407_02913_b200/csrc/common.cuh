@@ -20,6 +20,36 @@ __device__ __forceinline__ void griddep_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- timeline (debug build)
+// Built with -DSFC_TIMELINE (make TIMELINE=1 -> libsfc_b200_tl.so): thread 0 of every CTA
+// stamps %globaltimer at kernel entry (slot 0, min over CTAs), after its dependency wait
+// (slot 1, min) and at exit (slot 2, max), per kernel id; sfc_debug_timeline() reads them.
+#ifdef SFC_TIMELINE
+static __device__ unsigned long long g_tl[kTlCount][3];
+__device__ __forceinline__ void tl_mark(int id, int which) {
+    if (threadIdx.x != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (which == 2)
+        atomicMax(&g_tl[id][2], t);
+    else
+        atomicMin(&g_tl[id][which], t);
+}
+// Per translation unit: copy out (and re-arm) this unit's stamps, merged by the caller.
+#define SFC_TL_UNIT_READER(fn)                                                                  \
+    cudaError_t fn(unsigned long long* out, bool reset) {                                     \
+        cudaError_t e = cudaMemcpyFromSymbol(out, g_tl, sizeof(g_tl));                         \
+        if (e != cudaSuccess || !reset) return e;                                              \
+        unsigned long long init[kTlCount][3];                                                  \
+        for (int i = 0; i < kTlCount; ++i) init[i][0] = init[i][1] = ~0ull, init[i][2] = 0ull; \
+        return cudaMemcpyToSymbol(g_tl, init, sizeof(init));                                   \
+    }
+#else
+__device__ __forceinline__ void tl_mark(int, int) {}
+#define SFC_TL_UNIT_READER(fn) \
+    cudaError_t fn(unsigned long long*, bool) { return cudaErrorNotSupported; }
+#endif
+
 // ---------------------------------------------------------------- quantization
 __device__ __forceinline__ int clamp_q(int q, int qmax, unsigned long long* sat) {
     const int qmin = -qmax - 1;
@@ -100,6 +130,20 @@ __device__ __forceinline__ QuantParams derive_qparams_block(int vmax, int bits) 
     p.exact = found >= 0;
     p.mul = qcand(m0, found >= 0 ? found : 0);
     return p;
+}
+
+// Quantizer parameters for every (bits, vmax) with bits in [2, 8] and vmax <= 4608 (the
+// largest |V| any catalogued algorithm produces from int8 inputs: (max row L1 of B^T)^2 * 128
+// = 6^2 * 128), derived once per device (build_qparams_table) so a CTA pays one dependent
+// load instead of the derivation; other vmax fall back to derive_qparams_block.
+constexpr int kQpTableMax = 4608;
+constexpr int kQpTableEntries = 7 * (kQpTableMax + 1);
+// Block-uniform; every thread of the CTA must call it (the fallback synchronises).
+__device__ __forceinline__ QuantParams derive_qparams_block(int vmax, int bits);
+__device__ __forceinline__ QuantParams qparams_for(int vmax, int bits, const QuantParams* __restrict__ tab) {
+    if (tab && vmax >= 0 && vmax <= kQpTableMax && bits >= 2 && bits <= 8)
+        return tab[(bits - 2) * (kQpTableMax + 1) + vmax];
+    return derive_qparams_block(vmax, bits);
 }
 
 __device__ __forceinline__ QuantParams derive_qparams_warp(int vmax, int bits) {

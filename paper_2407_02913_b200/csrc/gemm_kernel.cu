@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int units = F * n_tb * n_ob;
+    tl_mark(kTlGemm, 0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             griddep_wait();  // vq written by the activation kernel
+            tl_mark(kTlGemm, 1);
             int stage = 0;
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) bulk_wait_all();
     }
     __syncthreads();
+    tl_mark(kTlGemm, 2);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, kTmemCols);
@@ -260,5 +263,7 @@ cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const 
     if (g.BK == 128) return nk <= 2 ? gemm_by_bn<128, 2>(ta, tb, tp, g, F, st, pdl) : gemm_by_bn<128, 3>(ta, tb, tp, g, F, st, pdl);
     return nk <= 2 ? gemm_by_bn<64, 2>(ta, tb, tp, g, F, st, pdl) : gemm_by_bn<64, 4>(ta, tb, tp, g, F, st, pdl);
 }
+
+SFC_TL_UNIT_READER(tl_read_gemm)
 
 }  // namespace sfcb200

@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
 
     const int tcols = (g.tw + TB - 1) / TB, ocb = (g.OC + kOcc - 1) / kOcc;
     const int blk = blockIdx.x;
+    tl_mark(kTlOutput, 0);
     const int oc0 = (blk % ocb) * kOcc, rest = blk / ocb;
     const int tc = rest % tcols, row = rest / tcols;  // row = b * th + ti
     if (threadIdx.x == 0) {
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     }
     __syncthreads();
     griddep_wait();  // P complete
+    tl_mark(kTlOutput, 1);
     griddep_launch_dependents();
     if (threadIdx.x == 0) {
         ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 4));
@@ -157,6 +159,8 @@ __global__ void __launch_bounds__(kOutThreads, 2)
             if (i8) i8[x] = int8_t(fmin(fmax(rint(double(y) * s * rq), 0.0), 127.0));
         }
     }
+    __syncthreads();
+    tl_mark(kTlOutput, 2);
 }
 
 namespace {
@@ -211,6 +215,8 @@ cudaError_t out_by_width(bool y64, const int32_t* P, const ConvGeom& g, const Qu
     return y64 ? out_launch<V, true>(P, g, qp, sf, o, st, pdl) : out_launch<V, false>(P, g, qp, sf, o, st, pdl);
 }
 }  // namespace
+
+SFC_TL_UNIT_READER(tl_read_out)
 
 cudaError_t launch_output(int variant, bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl) {

@@ -306,3 +306,26 @@ def test_fused_activation_matches_two_kernel_path(cuda, variant, monkeypatch):
     assert torch.equal(res[0][0], res[1][0])
     assert torch.equal(res[0][1], res[1][1])
     assert res[0][2] == res[1][2]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_repeated_forwards_are_deterministic(cuda, variant):
+    """Races show up as run-to-run differences long before they hit a fixed oracle case:
+    ten forwards of the config-2 layer (fresh workspaces) must agree bit for bit."""
+    L = wl.WORKLOADS[2].layers[0]
+    x = torch.from_numpy(wl.activations(2, 0, L)).cuda()
+    w = torch.from_numpy(wl.weights(2, 0, L)).cuda()
+    ho = L.hw + 2 * L.pad - 2
+    first = None
+    for _ in range(10):
+        layer = sc.SfcLayer(variant, w)
+        ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
+        y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int32, device="cuda")
+        layer.forward(x, ws, L.pad, y_int32=y)
+        vq, p = layer.views(L.batch, L.hw, L.hw, L.pad, ws)
+        cur = (y.clone(), vq.clone(), p.clone())
+        if first is None:
+            first = cur
+        else:
+            for a, b in zip(first, cur):
+                assert torch.equal(a, b)

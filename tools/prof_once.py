@@ -18,9 +18,13 @@ w = torch.from_numpy(wl.weights(a.workload, a.layer, L)).cuda()
 layer = sc.SfcLayer(a.variant, w)
 ho = L.hw + 2 * L.pad - 2
 ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
-y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int32, device="cuda")
 out = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.float32, device="cuda")
+kw = dict(y_int32=torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int32, device="cuda"), out_f32=out)
+try:
+    layer.forward(x, ws, L.pad, **kw)
+except sc.SfcUnsupported if hasattr(sc, "SfcUnsupported") else Exception:
+    kw = dict(y_int64=torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int64, device="cuda"), out_f32=out)
 for _ in range(a.iters):
-    layer.forward(x, ws, L.pad, y_int32=y, out_f32=out)
+    layer.forward(x, ws, L.pad, **kw)
 torch.cuda.synchronize()
 print("ok")
