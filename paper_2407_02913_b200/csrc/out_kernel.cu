@@ -9,6 +9,7 @@
 //   stage B  y[t1][t2] = sum_l Q[t1][l] A[l][t2]         (y overwrites the consumed P slice)
 //   stage C  output row segments (oc, oh, TB*M columns), all requested outputs in one pass:
 //            y_int, fp32 / fp64 y * sa * sf[oc] / N^2, int8 clamp(rint(y * scale * s), 0, 127)
+// Grid (oc blocks, tile-column blocks, image rows): no runtime division to decode a block.
 // Not persistent: a CTA needs ~62 KB, so two or three are resident per SM and hide each
 // other's TMA / barrier latency (the persistent double-buffered form needed 115 KB and ran
 // one CTA per SM at 25% warp occupancy on the 28x28 layers).  Shared strides are odd so
@@ -73,12 +74,11 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     acc_t* s_q = reinterpret_cast<acc_t*>(smem + L.q_off);       // [TB][M][K] rows of qstride
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
     __shared__ double s_scale[kOcc];
+    __shared__ float s_scalef[kOcc];
 
-    const int tcols = (g.tw + TB - 1) / TB, ocb = (g.OC + kOcc - 1) / kOcc;
-    const int blk = blockIdx.x;
+    // grid = (oc blocks, tile-column blocks, image rows b * th + ti)
+    const int oc0 = blockIdx.x * kOcc, tc = blockIdx.y, row = blockIdx.z;
     tl_mark(kTlOutput, 0);
-    const int oc0 = (blk % ocb) * kOcc, rest = blk / ocb;
-    const int tc = rest % tcols, row = rest / tcols;  // row = b * th + ti
     if (threadIdx.x == 0) {
         ptx::tma_prefetch(&tmP);
         ptx::mbar_init(full, 1);
@@ -92,11 +92,14 @@ __global__ void __launch_bounds__(kOutThreads, 2)
         ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 4));
         ptx::tma_load_3d(smem, &tmP, full, oc0, row * g.tw + tc * TB, 0);
     }
-    const int b = row / g.th, ti = row % g.th;
+    const int b = row / g.th, ti = row - b * g.th;
     const int noc = min(kOcc, g.OC - oc0);
     const int ntb = min(TB, g.tw - tc * TB);
-    if (threadIdx.x < kOcc && int(threadIdx.x) < noc)
-        s_scale[threadIdx.x] = (qpp->sa * sf[oc0 + threadIdx.x]) / double(T::DEN * T::DEN);
+    if (threadIdx.x < kOcc && int(threadIdx.x) < noc) {
+        const double sc = (qpp->sa * sf[oc0 + threadIdx.x]) / double(T::DEN * T::DEN);
+        s_scale[threadIdx.x] = sc;
+        s_scalef[threadIdx.x] = float(sc);
+    }
     ptx::mbar_wait(full, 0);
 
     // stage A: items (tj, l, oc)
@@ -126,38 +129,50 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     }
     __syncthreads();
 
-    // stage C: the block's output row segments (t1, oc) x ncol columns, one element per
-    // thread per pass (consecutive threads -> consecutive columns of a row); e / ncol by
-    // multiply-high with a per-block magic, all offsets 32-bit relative to the block base.
+    // stage C: the block's output row segments r = (t1, oc), ncol columns each.  Thread t
+    // keeps column c = t % ncol and walks rows r = t / ncol, + kOutThreads / ncol, ...
+    // (consecutive threads -> consecutive columns: coalesced row segments).  The set of
+    // requested outputs is a compile-time mask (one specialisation per combination), so
+    // the per-element work is the stores and conversions only.
     const int WO = g.WO;
     const int col0 = tc * TB * M;
     const int ncol = min(ntb * M, WO - col0);
     const int hrows = min(M, g.HO - ti * M);
-    const unsigned magic = 0xffffffffu / unsigned(ncol) + 1u;
-    const int total = M * kOcc * ncol;
     const int plane = g.HO * WO;
     const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
-    int* const y32 = o.y32 ? o.y32 + base0 : nullptr;
-    int64_t* const y64 = o.y64 ? o.y64 + base0 : nullptr;
-    float* const f32 = o.f32 ? o.f32 + base0 : nullptr;
-    double* const f64 = o.f64 ? o.f64 + base0 : nullptr;
-    int8_t* const i8 = o.i8 ? o.i8 + base0 : nullptr;
+    const int rstep = kOutThreads / ncol;
+    const int c = int(threadIdx.x) % ncol, r0 = int(threadIdx.x) / ncol;
+    const bool active = r0 < rstep;
     const double rq = o.requant;
-    for (int e = threadIdx.x; e < total; e += kOutThreads) {
-        const int r = ncol == 1 ? e : int(__umulhi(unsigned(e), magic));
-        const int c = e - r * ncol;
-        const int oc = r % kOcc, t1 = r / kOcc;
-        if (oc >= noc || t1 >= hrows) continue;
-        const unsigned x = unsigned(oc * plane + t1 * WO + c);
-        const acc_t y = s_y[r * L.ystride + c];
-        if (y32) y32[x] = int(y);
-        if (y64) y64[x] = int64_t(y);
-        if (f32 || f64 || i8) {
-            const double s = s_scale[oc];
-            if (f32) f32[x] = Y64 ? float(double(y) * s) : __int2float_rn(int(y)) * float(s);
-            if (f64) f64[x] = double(y) * s;
-            if (i8) i8[x] = int8_t(fmin(fmax(rint(double(y) * s * rq), 0.0), 127.0));
+    auto emit = [&](auto mask_c) {
+        constexpr int MK = decltype(mask_c)::value;
+        if (!active) return;
+        for (int r = r0; r < M * kOcc; r += rstep) {
+            const int oc = r % kOcc, t1 = r / kOcc;
+            if (oc >= noc || t1 >= hrows) continue;
+            const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
+            const acc_t y = s_y[r * L.ystride + c];
+            if constexpr ((MK & 1) != 0) o.y32[x] = int(y);
+            if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y);
+            if constexpr ((MK & 4) != 0)
+                o.f32[x] = Y64 ? float(double(y) * s_scale[oc]) : __int2float_rn(int(y)) * s_scalef[oc];
+            if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * s_scale[oc];
+            if constexpr ((MK & 16) != 0)
+                o.i8[x] = int8_t(fmin(fmax(rint(double(y) * s_scale[oc] * rq), 0.0), 127.0));
         }
+    };
+    const int mask = (o.y32 ? 1 : 0) | (o.y64 ? 2 : 0) | (o.f32 ? 4 : 0) | (o.f64 ? 8 : 0) | (o.i8 ? 16 : 0);
+    switch (mask) {
+#define SFC_EMIT_CASE(m) \
+    case m: emit(std::integral_constant<int, m>{}); break;
+        SFC_EMIT_CASE(1) SFC_EMIT_CASE(2) SFC_EMIT_CASE(3) SFC_EMIT_CASE(4) SFC_EMIT_CASE(5) SFC_EMIT_CASE(6)
+        SFC_EMIT_CASE(7) SFC_EMIT_CASE(8) SFC_EMIT_CASE(9) SFC_EMIT_CASE(10) SFC_EMIT_CASE(11) SFC_EMIT_CASE(12)
+        SFC_EMIT_CASE(13) SFC_EMIT_CASE(14) SFC_EMIT_CASE(15) SFC_EMIT_CASE(16) SFC_EMIT_CASE(17) SFC_EMIT_CASE(18)
+        SFC_EMIT_CASE(19) SFC_EMIT_CASE(20) SFC_EMIT_CASE(21) SFC_EMIT_CASE(22) SFC_EMIT_CASE(23) SFC_EMIT_CASE(24)
+        SFC_EMIT_CASE(25) SFC_EMIT_CASE(26) SFC_EMIT_CASE(27) SFC_EMIT_CASE(28) SFC_EMIT_CASE(29) SFC_EMIT_CASE(30)
+        SFC_EMIT_CASE(31)
+#undef SFC_EMIT_CASE
+        default: break;
     }
     __syncthreads();
     tl_mark(kTlOutput, 2);
@@ -195,9 +210,10 @@ cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* q
     auto kern = k_output<V, Y64>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    const long blocks = long(g.B) * g.th * ((g.tw + TB - 1) / TB) * ((g.OC + kOcc - 1) / kOcc);
+    const long rows = long(g.B) * g.th;
+    if (rows > 65535 || (g.tw + TB - 1) / TB > 65535) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(blocks));
+    cfg.gridDim = dim3(unsigned((g.OC + kOcc - 1) / kOcc), unsigned((g.tw + TB - 1) / TB), unsigned(rows));
     cfg.blockDim = dim3(kOutThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
