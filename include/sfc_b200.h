@@ -168,7 +168,7 @@ int sfc_debug_quantizer(int vmax, int bits, int32_t* d_q, int64_t* info, void* s
 /* Profiling hook of the timeline build (libsfc_b200_tl.so, `make TIMELINE=1`): out[8][3] =
  * per kernel {first CTA entry, first CTA past its dependency wait, last CTA exit} in
  * %globaltimer ns (0 / UINT64_MAX when the kernel did not run); reset re-arms the stamps.
- * Kernel ids: 0 workspace reset, 1 absmax, 2 quantize, 3 GEMM, 4 output, 5 fused act.
+ * Kernel ids: 0 workspace reset, 1 absmax, 2 quantize, 3 GEMM, 4 output.
  * Synchronous.  Returns SFC_ERR_UNSUPPORTED in the normal build. */
 int sfc_debug_timeline(uint64_t* out, int reset);
 

@@ -78,7 +78,6 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 struct WsView {
     int* vmax;
     unsigned long long* sat;
-    unsigned* gbar;
     QuantParams* qp;
     int8_t* vq;
     int32_t* P;
@@ -89,7 +88,6 @@ WsView carve(void* ws, const ConvGeom& g, int F) {
     WsView v;
     v.vmax = reinterpret_cast<int*>(base);
     v.sat = reinterpret_cast<unsigned long long*>(base + 8);
-    v.gbar = reinterpret_cast<unsigned*>(base + 16);
     v.qp = reinterpret_cast<QuantParams*>(base + 64);
     v.vq = reinterpret_cast<int8_t*>(base + up(256));
     v.P = reinterpret_cast<int32_t*>(base + up(256) + up(size_t(F) * g.Tpad * g.Cpad));
@@ -136,7 +134,7 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     const bool full = chained || (mask | SFC_STAGE_QPARAMS) == SFC_STAGE_ALL;
     static const bool no_pdl = std::getenv("SFC_DEBUG_NO_PDL") != nullptr;  // debugging knob
     const bool full_pdl = full && !no_pdl;
-    bool pdl = chained && full_pdl;  // (the fused activation kernel, when it ran, is the predecessor)
+    bool pdl = chained && full_pdl;
     if (mask & SFC_STAGE_QPARAMS) {
         ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
         pdl = false;
@@ -320,24 +318,14 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
         const ConvGeom g = geom_of(L, n, h, w, pad);
         if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
         WsView v = carve(ws, g, L->F);
-        // vmax, the saturation counter and the grid-barrier words share the first 24 bytes
-        ck(launch_zero_words(reinterpret_cast<uint32_t*>(v.vmax), 6, S(stream)), "workspace reset launch");
-        unsigned mask = SFC_STAGE_ALL & ~SFC_STAGE_QPARAMS;
-        if (const char* dbg = std::getenv("SFC_DEBUG_FORWARD_MASK")) mask = unsigned(std::atoi(dbg));  // profiling only
-        const bool try_fused = (mask & SFC_STAGE_ACT) && std::getenv("SFC_FUSED_ACT");
-        cudaError_t fe = cudaErrorCooperativeLaunchTooLarge;
         if (!o) throw std::invalid_argument("null outputs");
         needs_y64(L, o);  // refuse before anything is launched
-        if (try_fused) {
-            fe = launch_act_fused(L->variant, d_x, g, v.vmax, L->bits, v.qp, v.vq, v.sat, v.gbar, S(stream));
-            if (fe != cudaErrorCooperativeLaunchTooLarge) ck(fe, "fused activation launch");
-        }
-        if (fe == cudaSuccess) {
-            run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask & ~SFC_STAGE_ACT, true, S(stream));
-        } else {
-            ck(launch_act_absmax(L->variant, d_x, g, v.vmax, S(stream), true), "absmax launch");
-            run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask, true, S(stream));
-        }
+        unsigned mask = SFC_STAGE_ALL & ~SFC_STAGE_QPARAMS;
+        if (const char* dbg = std::getenv("SFC_DEBUG_FORWARD_MASK")) mask = unsigned(std::atoi(dbg));  // profiling only
+        // vmax and the saturation counter share the first 16 bytes of the workspace
+        ck(launch_zero_words(reinterpret_cast<uint32_t*>(v.vmax), 4, S(stream)), "workspace reset launch");
+        ck(launch_act_absmax(L->variant, d_x, g, v.vmax, S(stream), true), "absmax launch");
+        run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask, true, S(stream));
     });
 }
 

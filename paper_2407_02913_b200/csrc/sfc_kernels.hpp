@@ -41,17 +41,12 @@ cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, i
 // Zero `words` 32-bit words (<= 32) at p once the predecessor kernel has finished --
 // a PDL kernel instead of a memset node, which costs ~3 us in a graph / stream chain.
 cudaError_t launch_zero_words(uint32_t* p, int words, cudaStream_t st);
-enum TlKernel { kTlZero = 0, kTlAbsmax = 1, kTlQuant = 2, kTlGemm = 3, kTlOutput = 4, kTlFused = 5, kTlCount = 8 };
+enum TlKernel { kTlZero = 0, kTlAbsmax = 1, kTlQuant = 2, kTlGemm = 3, kTlOutput = 4, kTlCount = 8 };
 // Timeline stamps of the debug build ([8][3] per unit; cudaErrorNotSupported otherwise).
 cudaError_t tl_read_act(unsigned long long* out, bool reset);
 cudaError_t tl_read_gemm(unsigned long long* out, bool reset);
 cudaError_t tl_read_out(unsigned long long* out, bool reset);
 cudaError_t tl_read_aux(unsigned long long* out, bool reset);
-// Fused absmax + quantize for grids that fit co-resident (grid barrier on gbar[0..1],
-// gbar[0] zero on entry).  Returns cudaErrorCooperativeLaunchTooLarge without launching
-// anything when the grid does not fit; *vmax must be zero on entry.
-cudaError_t launch_act_fused(int variant, const int8_t* x, const ConvGeom& g, int* vmax, int bits, QuantParams* qp,
-                             int8_t* vqA, unsigned long long* sat, unsigned* gbar, cudaStream_t st);
 cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, const int* vmax, int bits,
                              QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl);
 cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,

@@ -282,33 +282,6 @@ def test_concurrent_streams_match(cuda):
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_fused_activation_matches_two_kernel_path(cuda, variant, monkeypatch):
-    """sfc_conv_forward runs the fused absmax+quantize kernel when its grid is co-resident;
-    the two-kernel form (absmax, then quantize) must give identical bits."""
-    L = wl.WORKLOADS[2].layers[0]
-    x = torch.from_numpy(wl.activations(2, 0, L)).cuda()
-    w = torch.from_numpy(wl.weights(2, 0, L)).cuda()
-    layer = sc.SfcLayer(variant, w)
-    res = []
-    for fused in (True, False):
-        if fused:
-            monkeypatch.setenv("SFC_FUSED_ACT", "1")
-        else:
-            monkeypatch.delenv("SFC_FUSED_ACT", raising=False)
-        ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
-        ho = L.hw + 2 * L.pad - 2
-        y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int32, device="cuda")
-        for _ in range(2):  # the barrier words are reused by the second call
-            layer.forward(x, ws, L.pad, y_int32=y)
-        torch.cuda.synchronize()
-        vq, _ = layer.views(L.batch, L.hw, L.hw, L.pad, ws)
-        res.append((y.clone(), vq.clone(), layer.stats(L.batch, L.hw, L.hw, L.pad, ws)))
-    assert torch.equal(res[0][0], res[1][0])
-    assert torch.equal(res[0][1], res[1][1])
-    assert res[0][2] == res[1][2]
-
-
-@pytest.mark.parametrize("variant", VARIANTS)
 def test_repeated_forwards_are_deterministic(cuda, variant):
     """Races show up as run-to-run differences long before they hit a fixed oracle case:
     ten forwards of the config-2 layer (fresh workspaces) must agree bit for bit."""

@@ -30,4 +30,4 @@ for v in ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]:
         env = dict(os.environ, SFC_DEBUG_FORWARD_MASK=str(mask))
         r = subprocess.run([sys.executable, "-c", code, v], env=env, capture_output=True, text=True)
         res[name] = float(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-300:]
-    print(v, os.environ.get("SFC_FUSED_ACT", "-"), {k: (round(x, 1) if isinstance(x, float) else x) for k, x in res.items()})
+    print(v, {k: (round(x, 1) if isinstance(x, float) else x) for k, x in res.items()})

@@ -11,7 +11,7 @@ os.environ.setdefault("SFC_B200_LIB", os.path.join(ROOT, "paper_2407_02913_b200"
 import torch
 from paper_2407_02913_b200 import _lib, sfconv as sc, workloads as wl
 
-NAMES = ["reset", "absmax", "quantize", "gemm", "output", "fused-act"]
+NAMES = ["reset", "absmax", "quantize", "gemm", "output", "-"]
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", type=int, default=2)
 ap.add_argument("--layer", type=int, default=0)
