@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     // straight to its vq row (lanes = consecutive channels: CC contiguous bytes per store).
     const int t0 = (b * g.th + ti) * tw;
     int8_t* vrow = vqA + size_t(t0) * g.Cpad + c0 + c;
-    const size_t fstride = size_t(g.Tpad) * g.Cpad;
+    const size_t fstride = size_t(g.Tpad) * g.Cpad, kstride = size_t(K) * fstride;
     int local = 0;
     auto column = [&](auto quantize) {
         for (int idx = j; idx < tw * K; idx += TPC) {
@@ -175,19 +175,24 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
             for (int r = 0; r < n; ++r) zr[r] = s_z[((tj * n + r) * K + l) * CC + c];
             int v[K];
             fwd1d<V>(zr, v);
+            int8_t* p = vrow + size_t(l) * fstride + size_t(tj) * g.Cpad;  // f = l, then += K rows
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                if (MODE == 1)
-                    vrow[size_t(k * K + l) * fstride + size_t(tj) * g.Cpad] = int8_t(quantize(v[k]));
-                else
+                if (MODE == 1) {
+                    *p = int8_t(quantize(v[k]));
+                    p += kstride;
+                } else {
                     local = max(local, abs(v[k]));
+                }
             }
         }
     };
     if (MODE == 0) {
         column([](int v) { return v; });
     } else if (qp.exact) {  // uniform over the CTA: no per-value branch
-        const long long mul = qp.mul, half = 1ll << (qp.shift - 1);
+        // mul < 2^31 (derive_qparams): one 32x32+64 -> 64 multiply-add and a funnel shift
+        const int mul = int(qp.mul);
+        const long long half = 1ll << (qp.shift - 1);
         const int shift = qp.shift;
         column([=](int v) { return int(((long long)v * mul + half) >> shift); });
     } else {
