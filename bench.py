@@ -277,9 +277,10 @@ def run_b200(args, rank, world, local_rank):
             c["layer"].forward(c["x"], c["ws"], c["L"].pad, requant_scale=c["rq"], **c["outs"])
             return
         c["vmax"].zero_()
-        c["layer"].absmax(c["x"], c["vmax"], c["L"].pad)
+        c["layer"].transform(c["x"], c["vmax"], c["ws"], c["L"].pad)  # absmax, V kept in ws
         dist.all_reduce(c["vmax"], op=dist.ReduceOp.MAX, group=group)
-        c["layer"].conv(c["x"], c["vmax"], c["ws"], c["L"].pad, requant_scale=c["rq"], **c["outs"])
+        c["layer"].conv_kept(tuple(c["x"].shape), c["vmax"], c["ws"], c["L"].pad, requant_scale=c["rq"],
+                             **c["outs"])
 
     def step():
         for c in calls:
@@ -314,7 +315,9 @@ def run_b200(args, rank, world, local_rank):
     ms = float(t.item())
     step_ops = sum(wl.direct_equivalent_ops(c["L"]) for c in calls) * world
     value = step_ops / (ms / 1e3) / 1e12
-    launches_per_step = 4 * len(calls)  # absmax, act (scale+transform+quantize), gemm, output
+    # N=1: workspace reset, absmax (+V kept), quantize, gemm, output; N>1: the reset is a torch
+    # zero_() of vmax, not one of ours
+    launches_per_step = (5 if world == 1 else 4) * len(calls)
 
     # ---- end to end through the public API: pinned host input -> device -> outputs -> pinned host
     def e2e_step():
@@ -345,7 +348,7 @@ def run_b200(args, rank, world, local_rank):
     e2e_value = step_ops / (float(t.item()) / 1e3) / 1e12
 
     # ---- per-kernel live timing (same stream, CUDA events between the stage launches)
-    stage_names = ["absmax", "sat_reset", "act_transform", "gemm", "output"]
+    stage_names = ["absmax", "sat_reset", "quantize", "gemm", "output"]
     stage_ms = {n: 0.0 for n in stage_names}
     per_call_stage = []
     L_ = lib()
@@ -362,9 +365,9 @@ def run_b200(args, rank, world, local_rank):
                            c["rq"])
             c["vmax"].zero_()
             e[0].record(stream)
-            c["layer"].absmax(x, c["vmax"], pad)
+            c["layer"].transform(x, c["vmax"], ws, pad)  # absmax + V kept (as in forward)
             e[1].record(stream)
-            for si, mask in enumerate((1, 2, 4, 8)):
+            for si, mask in enumerate((1, 2 | 16, 4, 8)):  # 16: quantize the kept V
                 sc.check(L_.sfc_conv_int8_stages(c["layer"]._h, sc._ptr(x), n, h, w_, pad, sc._ptr(c["vmax"]),
                                                  sc._ptr(ws), ws.numel(), ctypes.byref(o), mask,
                                                  ctypes.c_void_p(stream.cuda_stream)))
@@ -389,9 +392,9 @@ def run_b200(args, rank, world, local_rank):
             xb = L.batch * L.cin * L.hw * L.hw
             outb = sum(t.numel() * t.element_size() for t in c["outs"].values())
             if dom == "absmax":
-                alg_bytes += xb
-            elif dom == "act_transform":
-                alg_bytes += xb + F * T * L.cin
+                alg_bytes += xb + 2 * F * T * L.cin  # read x, keep int16 V
+            elif dom == "quantize":
+                alg_bytes += 3 * F * T * L.cin  # read int16 V, write int8 vq
             elif dom == "gemm":
                 alg_ops += 2 * F * T * L.cin * L.cout
                 alg_bytes += F * T * L.cin + F * L.cin * L.cout + 4 * F * T * L.cout

@@ -99,6 +99,12 @@ int sfc_conv_workspace_size(sfc_layer_t layer, int n, int h, int w, int pad, siz
 int sfc_act_absmax(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, int32_t* d_vmax,
                    void* stream);
 
+/* sfc_act_absmax that also keeps the transformed activations V (int16) in the workspace,
+ * so sfc_conv_kept quantizes them with one streaming pass instead of recomputing the
+ * transform.  Multi-GPU: sfc_act_transform -> all-reduce(MAX) d_vmax -> sfc_conv_kept. */
+int sfc_act_transform(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, int32_t* d_vmax,
+                      void* d_workspace, size_t workspace_bytes, void* stream);
+
 typedef struct {
     int32_t* y_int32;      /* [N][OC][HO][WO] integer output accumulator sum_kl A A pacc, or NULL */
     int64_t* y_int64;      /* same, 64-bit (required when the int32 bound does not hold), or NULL */
@@ -121,11 +127,17 @@ int sfc_conv_int8(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int
 #define SFC_STAGE_GEMM 4u      /* per-frequency int8 contraction -> pacc   */
 #define SFC_STAGE_OUTPUT 8u    /* output transform + dequant / requant     */
 #define SFC_STAGE_ALL 15u
+#define SFC_STAGE_KEPT 16u     /* with SFC_STAGE_ACT: quantize the V kept by sfc_act_transform */
 int sfc_conv_int8_stages(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax,
                          void* d_workspace, size_t workspace_bytes, const sfc_outputs* outs, unsigned stage_mask,
                          void* stream);
 
-/* Convenience: zero the workspace's vmax slot, absmax pre-pass, then sfc_conv_int8 (single GPU). */
+/* sfc_conv_int8 after sfc_act_transform on the same workspace and input shape: quantizes
+ * the kept V (no input pointer needed), contracts and applies the output transform. */
+int sfc_conv_kept(sfc_layer_t layer, int n, int h, int w, int pad, const int32_t* d_vmax, void* d_workspace,
+                  size_t workspace_bytes, const sfc_outputs* outs, void* stream);
+
+/* Convenience (single GPU): zero the workspace's vmax slot, sfc_act_transform, sfc_conv_kept. */
 int sfc_conv_forward(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, void* d_workspace,
                      size_t workspace_bytes, const sfc_outputs* outs, void* stream);
 

@@ -52,14 +52,16 @@ __host__ __device__ inline size_t act_smem_bytes(int W, int tw) {
 }
 }  // namespace
 
-// MODE 0: max|V| -> atomicMax(*vmax).  MODE 1: quantize with the scale derived from
-// *vmax_in and write vq[f][t][c] (row pitch Cpad) for f = k*K + l.
+// MODE 0: max|V| -> atomicMax(*vmax); with vkeep != nullptr V itself is kept as int16
+// vkeep[f][t][c] (row pitch Cpad) for the streaming quantizer k_quant_kept.
+// MODE 1: quantize with the scale derived from *vmax_in and write vq[f][t][c] (row pitch
+// Cpad) for f = k*K + l.
 template <int V, int MODE, int CC>
 __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ x, ConvGeom g,
                                                      int* __restrict__ vmax, const int* __restrict__ vmax_in, int bits,
                                                      QuantParams* __restrict__ qp_out, int8_t* __restrict__ vqA,
                                                      unsigned long long* __restrict__ sat,
-                                                     const QuantParams* __restrict__ qtab) {
+                                                     const QuantParams* __restrict__ qtab, int16_t* __restrict__ vkeep) {
     using T = Tab<V>;
     constexpr int n = T::n, K = T::K, M = T::M;
     constexpr int TPC = kActThreads / CC;   // work-groups per channel
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     // straight to its vq row (lanes = consecutive channels: CC contiguous bytes per store).
     const int t0 = (b * g.th + ti) * tw;
     int8_t* vrow = vqA + size_t(t0) * g.Cpad + c0 + c;
+    int16_t* krow = vkeep + size_t(t0) * g.Cpad + c0 + c;  // (only dereferenced when vkeep != nullptr)
     const size_t fstride = size_t(g.Tpad) * g.Cpad, kstride = size_t(K) * fstride;
     int local = 0;
     auto column = [&](auto quantize) {
@@ -176,6 +179,7 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
             int v[K];
             fwd1d<V>(zr, v);
             int8_t* p = vrow + size_t(l) * fstride + size_t(tj) * g.Cpad;  // f = l, then += K rows
+            int16_t* pk = krow + size_t(l) * fstride + size_t(tj) * g.Cpad;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 if (MODE == 1) {
@@ -183,6 +187,10 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
                     p += kstride;
                 } else {
                     local = max(local, abs(v[k]));
+                    if (vkeep) {
+                        *pk = int16_t(v[k]);
+                        pk += kstride;
+                    }
                 }
             }
         }
@@ -208,6 +216,60 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
         if (lane == 0 && local > 0) atomicMax(vmax, local);
     }
     tl_mark(kTl, 2);
+}
+
+// Streaming quantizer over the V kept by the absmax pass: vq[f][t][c] = q(V[f][t][c]) for
+// t < T, 16 channels per item (two 16-byte loads, one 16-byte store); channels >= C are
+// written as 0.  HBM-bound: 3 bytes per value.
+__global__ void __launch_bounds__(kActThreads) k_quant_kept(const int16_t* __restrict__ vkeep, ConvGeom g, int F,
+                                                            const int* __restrict__ vmax_in, int bits,
+                                                            QuantParams* __restrict__ qp_out,
+                                                            int8_t* __restrict__ vqA,
+                                                            unsigned long long* __restrict__ sat,
+                                                            const QuantParams* __restrict__ qtab) {
+    tl_mark(kTlQuant, 0);
+    griddep_wait();  // V and the (all-reduced) vmax are complete
+    tl_mark(kTlQuant, 1);
+    const QuantParams qp = qparams_for(*vmax_in, bits, qtab);
+    if (threadIdx.x == 0 && blockIdx.x == 0) *qp_out = qp;
+    griddep_launch_dependents();
+    // grid = (x blocks striding over the (t, chunk) items of one frequency, F)
+    const int chunks = g.Cpad / 16;
+    const unsigned items = unsigned(g.T) * unsigned(chunks);  // < 2^32 / chunks (host check)
+    const unsigned cmagic = 0xffffffffu / unsigned(chunks) + 1u;
+    const size_t fbase = size_t(blockIdx.y) * g.Tpad * g.Cpad;
+    auto run = [&](auto quantize) {
+        for (unsigned it = blockIdx.x * blockDim.x + threadIdx.x; it < items; it += gridDim.x * blockDim.x) {
+            const unsigned t = chunks == 1 ? it : __umulhi(it, cmagic);
+            const int q = int(it - t * unsigned(chunks));
+            const size_t off = fbase + size_t(t) * g.Cpad + size_t(q) * 16;
+            uint4 out = make_uint4(0, 0, 0, 0);
+            const int cbase = q * 16;
+            if (cbase < g.C) {
+                const uint4* src = reinterpret_cast<const uint4*>(vkeep + off);
+                const uint4 a = __ldcs(src), b = __ldcs(src + 1);  // streamed once
+                const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
+                    const uint32_t qv = cbase + e < g.C ? uint32_t(uint8_t(int8_t(quantize(v)))) : 0u;
+                    o[e >> 2] |= qv << (8 * (e & 3));
+                }
+                out = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            *reinterpret_cast<uint4*>(vqA + off) = out;
+        }
+    };
+    if (qp.exact) {
+        const int mul = int(qp.mul);
+        const long long half = 1ll << (qp.shift - 1);
+        const int shift = qp.shift;
+        run([=](int v) { return int(((long long)v * mul + half) >> shift); });
+    } else {
+        run([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, sat); });
+    }
+    tl_mark(kTlQuant, 2);
 }
 
 // Stand-alone quantizer derivation (stats / the exhaustive test hook).
@@ -260,7 +322,8 @@ namespace {
 
 template <int V, int MODE, int CC>
 cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits,
-                          QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl) {
+                          QuantParams* qp, int8_t* vqA, unsigned long long* sat, int16_t* vkeep, cudaStream_t st,
+                          bool pdl) {
     const size_t smem = act_smem_bytes<V, CC>(g.W, g.tw);
     auto kern = k_act<V, MODE, CC>;
     static size_t attr_bytes = 0;  // per instantiation: raise the opt-in only when a layer needs more
@@ -280,7 +343,7 @@ cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int* vmax, const i
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, x, g, vmax, vmax_in, bits, qp, vqA, sat,
-                              MODE == 0 ? nullptr : qparams_table(false));
+                              MODE == 0 ? nullptr : qparams_table(false), vkeep);
 }
 
 // Channels per CTA: 32 gives full 32-byte vq row segments; shrink for two waves
@@ -302,32 +365,50 @@ int pick_cc(const ConvGeom& g) {
 
 template <int V, int MODE>
 cudaError_t act_launch(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits, QuantParams* qp,
-                       int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl) {
+                       int8_t* vqA, unsigned long long* sat, int16_t* vkeep, cudaStream_t st, bool pdl) {
     switch (pick_cc<V>(g)) {
-        case 32: return act_launch_cc<V, MODE, 32>(x, g, vmax, vmax_in, bits, qp, vqA, sat, st, pdl);
-        case 16: return act_launch_cc<V, MODE, 16>(x, g, vmax, vmax_in, bits, qp, vqA, sat, st, pdl);
-        case 8: return act_launch_cc<V, MODE, 8>(x, g, vmax, vmax_in, bits, qp, vqA, sat, st, pdl);
-        default: return act_launch_cc<V, MODE, 4>(x, g, vmax, vmax_in, bits, qp, vqA, sat, st, pdl);
+        case 32: return act_launch_cc<V, MODE, 32>(x, g, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
+        case 16: return act_launch_cc<V, MODE, 16>(x, g, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
+        case 8: return act_launch_cc<V, MODE, 8>(x, g, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
+        default: return act_launch_cc<V, MODE, 4>(x, g, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
     }
 }
 
 }  // namespace
 
-cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, cudaStream_t st, bool pdl) {
+cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep,
+                              cudaStream_t st, bool pdl) {
     switch (variant) {
-        case 0: return act_launch<0, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, st, pdl);
-        case 1: return act_launch<1, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, st, pdl);
-        default: return act_launch<2, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, st, pdl);
+        case 0: return act_launch<0, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, vkeep, st, pdl);
+        case 1: return act_launch<1, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, vkeep, st, pdl);
+        default: return act_launch<2, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, vkeep, st, pdl);
     }
 }
 
 cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, const int* vmax, int bits,
                              QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl) {
     switch (variant) {
-        case 0: return act_launch<0, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, st, pdl);
-        case 1: return act_launch<1, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, st, pdl);
-        default: return act_launch<2, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, st, pdl);
+        case 0: return act_launch<0, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
+        case 1: return act_launch<1, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
+        default: return act_launch<2, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
     }
+}
+
+cudaError_t launch_quant_kept(const int16_t* vkeep, const ConvGeom& g, int F, const int* vmax, int bits,
+                              QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl) {
+    const long items = long(g.T) * (g.Cpad / 16);
+    if (items * (g.Cpad / 16) >= (1l << 32)) return cudaErrorInvalidValue;
+    const long want = (items + kActThreads - 1) / kActThreads, cap = (148L * 8 + F - 1) / F;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(want < cap ? want : cap), unsigned(F));
+    cfg.blockDim = dim3(kActThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_quant_kept, vkeep, g, F, vmax, bits, qp, vqA, sat, qparams_table(false));
 }
 
 SFC_TL_UNIT_READER(tl_read_act)

@@ -81,6 +81,7 @@ struct WsView {
     QuantParams* qp;
     int8_t* vq;
     int32_t* P;
+    int16_t* vkeep;  // V kept by sfc_act_transform for the streaming quantizer
 };
 WsView carve(void* ws, const ConvGeom& g, int F) {
     auto up = [](size_t v) { return (v + 255) / 256 * 256; };
@@ -91,12 +92,13 @@ WsView carve(void* ws, const ConvGeom& g, int F) {
     v.qp = reinterpret_cast<QuantParams*>(base + 64);
     v.vq = reinterpret_cast<int8_t*>(base + up(256));
     v.P = reinterpret_cast<int32_t*>(base + up(256) + up(size_t(F) * g.Tpad * g.Cpad));
+    v.vkeep = reinterpret_cast<int16_t*>(reinterpret_cast<uint8_t*>(v.P) + up(size_t(F) * g.Tpad * g.OCpad * 4));
     return v;
 }
 
 void check_call(const sfc_layer* L, const void* x, int n, int h, int w, int pad) {
     if (!L) throw std::invalid_argument("null layer");
-    if (!x) throw std::invalid_argument("null input");
+    if (!x) throw std::invalid_argument("null input");  // (the kept-V entry points pass the workspace)
     if (n <= 0 || h <= 0 || w <= 0 || pad < 0) throw std::invalid_argument("bad input shape");
     if (w > 16384 || h > 16384 || pad > 64) throw Unsupported("image sides above 16384 or padding above 64");
     if (h + 2 * pad - L->plan->R + 1 <= 0 || w + 2 * pad - L->plan->R + 1 <= 0)
@@ -123,9 +125,13 @@ bool needs_y64(const sfc_layer* L, const sfc_outputs* o) {
 // this call's absmax kernel, so the activation kernel may start under PDL.  Inside a
 // full call every kernel after the first overlaps its predecessor's tail (PDL); the
 // kernels themselves wait (griddepcontrol.wait) before consuming upstream results.
+// mask & SFC_STAGE_KEPT: the activation stage quantizes the V kept in the workspace by
+// sfc_act_transform (streaming) instead of recomputing the transform from x.
 void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pad, const int32_t* d_vmax, void* ws,
               size_t ws_bytes, const sfc_outputs* o, unsigned mask, bool chained, cudaStream_t st) {
-    check_call(L, d_x, n, h, w, pad);
+    const bool kept = (mask & SFC_STAGE_KEPT) != 0;
+    mask &= SFC_STAGE_ALL;
+    check_call(L, kept ? ws : static_cast<const void*>(d_x), n, h, w, pad);
     if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
     const ConvGeom g = geom_of(L, n, h, w, pad);
     if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
@@ -140,7 +146,10 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
         pdl = false;
     }
     if (mask & SFC_STAGE_ACT) {
-        ck(launch_act_quant(L->variant, d_x, g, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "act launch");
+        if (kept)
+            ck(launch_quant_kept(v.vkeep, g, L->F, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "quantize launch");
+        else
+            ck(launch_act_quant(L->variant, d_x, g, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "act launch");
         pdl = full_pdl;
     }
     if (mask & SFC_STAGE_GEMM) {
@@ -296,7 +305,25 @@ int sfc_act_absmax(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pa
     return guarded([&] {
         check_call(L, d_x, n, h, w, pad);
         if (!d_vmax) throw std::invalid_argument("null vmax");
-        ck(launch_act_absmax(L->variant, d_x, geom_of(L, n, h, w, pad), d_vmax, S(stream)), "absmax launch");
+        ck(launch_act_absmax(L->variant, d_x, geom_of(L, n, h, w, pad), d_vmax, nullptr, S(stream)), "absmax launch");
+    });
+}
+
+int sfc_act_transform(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad, int32_t* d_vmax, void* ws,
+                      size_t ws_bytes, void* stream) {
+    return guarded([&] {
+        check_call(L, d_x, n, h, w, pad);
+        if (!d_vmax || !ws) throw std::invalid_argument("null argument");
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
+        ck(launch_act_absmax(L->variant, d_x, g, d_vmax, carve(ws, g, L->F).vkeep, S(stream)), "absmax launch");
+    });
+}
+
+int sfc_conv_kept(sfc_layer_t L, int n, int h, int w, int pad, const int32_t* d_vmax, void* ws, size_t ws_bytes,
+                  const sfc_outputs* o, void* stream) {
+    return guarded([&] {
+        run_conv(L, nullptr, n, h, w, pad, d_vmax, ws, ws_bytes, o, SFC_STAGE_ALL | SFC_STAGE_KEPT, false, S(stream));
     });
 }
 
@@ -324,8 +351,8 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
         if (const char* dbg = std::getenv("SFC_DEBUG_FORWARD_MASK")) mask = unsigned(std::atoi(dbg));  // profiling only
         // vmax and the saturation counter share the first 16 bytes of the workspace
         ck(launch_zero_words(reinterpret_cast<uint32_t*>(v.vmax), 4, S(stream)), "workspace reset launch");
-        ck(launch_act_absmax(L->variant, d_x, g, v.vmax, S(stream), true), "absmax launch");
-        run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask, true, S(stream));
+        ck(launch_act_absmax(L->variant, d_x, g, v.vmax, v.vkeep, S(stream), true), "absmax launch");
+        run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask | SFC_STAGE_KEPT, true, S(stream));
     });
 }
 

@@ -36,8 +36,13 @@ cudaError_t launch_filter_prepare(int variant, const int8_t* w, int OC, int IC, 
                                   double* sf, int* umax, int8_t* uqB, unsigned long long* sat, cudaStream_t st);
 // pdl: launched under programmatic stream serialization; the CTAs stage and transform
 // their tiles before waiting on the predecessor (which zeroes *vmax).
-cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, cudaStream_t st,
-                              bool pdl = false);
+// vkeep != nullptr: also keep V as int16 [F][Tpad][Cpad] for launch_quant_kept.
+cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep,
+                              cudaStream_t st, bool pdl = false);
+// vq = q(kept V) for t < T, channels >= C zeroed (streaming; replaces launch_act_quant's
+// recomputation of the transform).
+cudaError_t launch_quant_kept(const int16_t* vkeep, const ConvGeom& g, int F, const int* vmax, int bits,
+                              QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl);
 // Zero `words` 32-bit words (<= 32) at p once the predecessor kernel has finished --
 // a PDL kernel instead of a memset node, which costs ~3 us in a graph / stream chain.
 cudaError_t launch_zero_words(uint32_t* p, int words, cudaStream_t st);

@@ -35,15 +35,19 @@ class CudaEngine:
     def new_vmax(self, device):
         return torch.zeros(1, dtype=torch.int32, device=device)
 
-    def absmax(self, x, vmax):
-        self.layer.absmax(x, vmax, self.pad)
-
-    def conv(self, x, vmax, **outs):
+    def _workspace(self, x):
         key = tuple(x.shape)
         if key not in self._ws:
             n, _, h, w = x.shape
             self._ws[key] = self.layer.workspace(n, h, w, self.pad)
-        self.layer.conv(x, vmax, self._ws[key], self.pad, **outs)
+        return self._ws[key]
+
+    def absmax(self, x, vmax):
+        """Local absmax; V is kept in the shard's workspace for conv()."""
+        self.layer.transform(x, vmax, self._workspace(x), self.pad)
+
+    def conv(self, x, vmax, **outs):
+        self.layer.conv_kept(tuple(x.shape), vmax, self._workspace(x), self.pad, **outs)
 
 
 @dataclass

@@ -260,6 +260,22 @@ class SfcLayer:
             raise ValueError("input channel count does not match filters")
         check(lib().sfc_act_absmax(self._h, _ptr(x), n, h, w, pad, _ptr(vmax), ctypes.c_void_p(_stream_ptr(stream))))
 
+    def transform(self, x: torch.Tensor, vmax: torch.Tensor, ws: torch.Tensor, pad: int, stream=None):
+        """absmax pre-pass that keeps V in `ws` for conv_kept (sfc_act_transform)."""
+        n, c, h, w = x.shape
+        if c != self.IC:
+            raise ValueError("input channel count does not match filters")
+        check(lib().sfc_act_transform(self._h, _ptr(x), n, h, w, pad, _ptr(vmax), _ptr(ws), ws.numel(),
+                                      ctypes.c_void_p(_stream_ptr(stream))))
+
+    def conv_kept(self, shape, vmax: torch.Tensor, ws: torch.Tensor, pad: int, y_int32=None, y_int64=None,
+                  out_f32=None, out_i8=None, requant_scale: float = 0.0, stream=None, out_f64=None):
+        """Quantize the V kept by transform() with the (all-reduced) vmax, contract, output transform."""
+        n, c, h, w = shape
+        o = Outputs(_ptr(y_int32), _ptr(y_int64), _ptr(out_f32), _ptr(out_f64), _ptr(out_i8), float(requant_scale))
+        check(lib().sfc_conv_kept(self._h, n, h, w, pad, _ptr(vmax), _ptr(ws), ws.numel(), ctypes.byref(o),
+                                  ctypes.c_void_p(_stream_ptr(stream))))
+
     def conv(self, x: torch.Tensor, vmax: torch.Tensor, ws: torch.Tensor, pad: int, y_int32=None, y_int64=None,
              out_f32=None, out_i8=None, requant_scale: float = 0.0, stream=None, out_f64=None):
         n, c, h, w = x.shape

@@ -302,3 +302,33 @@ def test_repeated_forwards_are_deterministic(cuda, variant):
         else:
             for a, b in zip(first, cur):
                 assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_kept_and_recompute_paths_agree(cuda, variant):
+    """forward (absmax keeps V, streaming quantize) == transform + conv_kept (the multi-GPU
+    entry points) == absmax + conv (quantize recomputes the transform from x), bit for bit."""
+    for cfg, li, C in ((2, 0, None), (1, 0, None)):
+        L = wl.WORKLOADS[cfg].layers[li]
+        x = torch.from_numpy(wl.activations(cfg, li, L)).cuda()
+        w = torch.from_numpy(wl.weights(cfg, li, L)).cuda()
+        layer = sc.SfcLayer(variant, w)
+        ho = L.hw + 2 * L.pad - 2
+        res = []
+        for mode in ("forward", "kept", "recompute"):
+            ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
+            y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int32, device="cuda")
+            if mode == "forward":
+                layer.forward(x, ws, L.pad, y_int32=y)
+            else:
+                vmax = torch.zeros(1, dtype=torch.int32, device="cuda")
+                if mode == "kept":
+                    layer.transform(x, vmax, ws, L.pad)
+                    layer.conv_kept(tuple(x.shape), vmax, ws, L.pad, y_int32=y)
+                else:
+                    layer.absmax(x, vmax, L.pad)
+                    layer.conv(x, vmax, ws, L.pad, y_int32=y)
+            vq, _ = layer.views(L.batch, L.hw, L.hw, L.pad, ws)
+            res.append((y.clone(), vq.clone(), layer.stats(L.batch, L.hw, L.hw, L.pad, ws)))
+        for r in res[1:]:
+            assert torch.equal(res[0][0], r[0]) and torch.equal(res[0][1], r[1]) and res[0][2] == r[2]
