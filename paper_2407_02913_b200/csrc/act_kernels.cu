@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
         const int mul = int(qp.mul);
         const long long half = 1ll << (qp.shift - 1);
         const int shift = qp.shift;
-        column([=](int v) { return int(((long long)v * mul + half) >> shift); });
+        column([=](int v) { return quant_fast(v, mul, half, shift); });
     } else {
         column([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, sat); });
     }
@@ -238,34 +238,57 @@ __global__ void __launch_bounds__(kActThreads) k_quant_kept(const int16_t* __res
     const unsigned items = unsigned(g.T) * unsigned(chunks);  // < 2^32 / chunks (host check)
     const unsigned cmagic = 0xffffffffu / unsigned(chunks) + 1u;
     const size_t fbase = size_t(blockIdx.y) * g.Tpad * g.Cpad;
+    // kU items per thread per round: all their loads are in flight before the first is used.
+    constexpr int kU = 4;
+    const unsigned stride = gridDim.x * blockDim.x;
     auto run = [&](auto quantize) {
-        for (unsigned it = blockIdx.x * blockDim.x + threadIdx.x; it < items; it += gridDim.x * blockDim.x) {
-            const unsigned t = chunks == 1 ? it : __umulhi(it, cmagic);
-            const int q = int(it - t * unsigned(chunks));
-            const size_t off = fbase + size_t(t) * g.Cpad + size_t(q) * 16;
+        for (unsigned it0 = blockIdx.x * blockDim.x + threadIdx.x; it0 < items; it0 += kU * stride) {
+            uint4 a[kU], b[kU];
+            size_t off[kU];
+            int cb[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const unsigned it = it0 + u * stride;
+                const unsigned t = chunks == 1 ? it : __umulhi(it, cmagic);
+                const int q = int(it - t * unsigned(chunks));
+                off[u] = fbase + size_t(t) * g.Cpad + size_t(q) * 16;
+                cb[u] = it < items ? q * 16 : 1 << 30;  // (out of range: no load, no store)
+                a[u] = b[u] = make_uint4(0, 0, 0, 0);
+                if (cb[u] < g.C) {
+                    const uint4* src = reinterpret_cast<const uint4*>(vkeep + off[u]);
+                    a[u] = __ldcs(src);  // streamed once
+                    b[u] = __ldcs(src + 1);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+            if (cb[u] == (1 << 30)) continue;
             uint4 out = make_uint4(0, 0, 0, 0);
-            const int cbase = q * 16;
+            const int cbase = cb[u];
             if (cbase < g.C) {
-                const uint4* src = reinterpret_cast<const uint4*>(vkeep + off);
-                const uint4 a = __ldcs(src), b = __ldcs(src + 1);  // streamed once
-                const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                const uint32_t w[8] = {a[u].x, a[u].y, a[u].z, a[u].w, b[u].x, b[u].y, b[u].z, b[u].w};
                 uint32_t o[4] = {0, 0, 0, 0};
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
-                    const uint32_t qv = cbase + e < g.C ? uint32_t(uint8_t(int8_t(quantize(v)))) : 0u;
-                    o[e >> 2] |= qv << (8 * (e & 3));
+                    o[e >> 2] |= uint32_t(uint8_t(int8_t(quantize(v)))) << (8 * (e & 3));
+                }
+                if (cbase + 16 > g.C) {  // channels >= C within the chunk are 0 (V holds 0 there too)
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (cbase + e >= g.C) o[e >> 2] &= ~(0xffu << (8 * (e & 3)));
                 }
                 out = make_uint4(o[0], o[1], o[2], o[3]);
             }
-            *reinterpret_cast<uint4*>(vqA + off) = out;
+            *reinterpret_cast<uint4*>(vqA + off[u]) = out;
+            }
         }
     };
     if (qp.exact) {
         const int mul = int(qp.mul);
         const long long half = 1ll << (qp.shift - 1);
         const int shift = qp.shift;
-        run([=](int v) { return int(((long long)v * mul + half) >> shift); });
+        run([=](int v) { return quant_fast(v, mul, half, shift); });
     } else {
         run([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, sat); });
     }

@@ -145,15 +145,26 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
         ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
         pdl = false;
     }
+    // Kept V is quantized by the streaming quantizer (vq through HBM); SFC_QFUSE=1 selects the
+    // GEMM with converter warps instead (no vq round trip, but its V reads are latency-bound
+    // at BN = 256: slower on the large layers for now).
+    const bool qfuse = kept && std::getenv("SFC_QFUSE") != nullptr;
     if (mask & SFC_STAGE_ACT) {
-        if (kept)
-            ck(launch_quant_kept(v.vkeep, g, L->F, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "quantize launch");
-        else
+        if (!kept) {
             ck(launch_act_quant(L->variant, d_x, g, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "act launch");
-        pdl = full_pdl;
+            pdl = full_pdl;
+        } else if (!qfuse) {
+            ck(launch_quant_kept(v.vkeep, g, L->F, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "quantize launch");
+            pdl = full_pdl;
+        }
     }
     if (mask & SFC_STAGE_GEMM) {
-        ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st, pdl), "gemm launch");
+        if (qfuse)
+            ck(launch_gemm_qfused(QFuse{v.vkeep, d_vmax, qparams_table(false), v.qp, v.sat, L->bits}, L->d_uq, v.P, g,
+                                  L->F, st, pdl),
+               "fused quantize + gemm launch");
+        else
+            ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st, pdl), "gemm launch");
         pdl = full_pdl;
     }
     if (mask & SFC_STAGE_OUTPUT) {

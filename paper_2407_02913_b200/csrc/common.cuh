@@ -63,11 +63,19 @@ __device__ __forceinline__ int clamp_q(int q, int qmax, unsigned long long* sat)
 // The reference quantizer: nearbyint(double(v) / scale) (quant.cpp:102-115).
 __device__ __forceinline__ int exact_q(long long v, double sa) { return int(rint(__ddiv_rn(double(v), sa))); }
 
+// The verified multiply-shift quantizer: (v * mul + half) >> shift with mul < 2^31, as one
+// mad.wide.s32 (IMAD.WIDE with the 64-bit rounding addend) and one funnel shift.
+__device__ __forceinline__ int quant_fast(int v, int mul, long long half, int shift) {
+    long long r;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(v), "r"(mul), "l"(half));
+    return int(r >> shift);
+}
+
 // Activation quantizer.  Fast path (qp.exact): one 32x32->64 multiply-add and a
 // shift, proven equal to exact_q for every |v| <= vmax by derive_qparams (so no
 // clamp can trigger).  Otherwise the per-element fp64 division with clamping.
 __device__ __forceinline__ int quant_act(int v, const QuantParams& qp, unsigned long long* sat) {
-    if (qp.exact) return int(((long long)v * qp.mul + (1ll << (qp.shift - 1))) >> qp.shift);
+    if (qp.exact) return quant_fast(v, int(qp.mul), 1ll << (qp.shift - 1), qp.shift);
     return clamp_q(exact_q(v, qp.sa), qp.qmax, sat);
 }
 

@@ -6,9 +6,11 @@
 // Persistent static schedule: CTA i processes work units u = i, i + grid, ...,
 // unit -> (f, t-block, oc-block) with the oc-block fastest so concurrently resident
 // CTAs share a frequency's A/B tiles in L2.  Warp roles: 0 = TMA producer,
-// 1 = MMA issuer (one elected lane) and TMEM owner, 2..5 = epilogue
-// (tcgen05.ld -> 128B-swizzled smem box -> TMA store), two epilogue warps per lane quarter.  TMEM accumulators are
-// double-buffered so unit u+1's MMAs overlap unit u's epilogue.
+// 1 = MMA issuer (one elected lane) and TMEM owner, 2..9 = epilogue
+// (tcgen05.ld -> 128B-swizzled smem box -> TMA store), two epilogue warps per lane
+// quarter; with QF, 10..17 = converters that quantize the kept int16 V straight into the
+// A stage buffers.  TMEM accumulators are double-buffered so unit u+1's MMAs overlap
+// unit u's epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -36,15 +38,29 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 constexpr int kEpiWarps = 8;                 // two epilogue warps per TMEM lane quarter
-constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
+constexpr int kConvWarps = 8;                // QF: activation-quantizing A producers
 constexpr int kEpiBufs = 2;                  // TMA-store staging boxes per epilogue warp
 constexpr int kEpiBoxBytes = 32 * 32 * 4;    // 32 rows x 32 int32 (one 128B-swizzle box)
+template <bool QF>
+constexpr int gemm_threads() { return 64 + 32 * kEpiWarps + (QF ? 32 * kConvWarps : 0); }
+
+// Quantizer parameters for a subset of warps (no CTA-wide barrier): table or warp derivation.
+__device__ __forceinline__ QuantParams qparams_warp(int vmax, int bits, const QuantParams* __restrict__ tab) {
+    if (tab && vmax >= 0 && vmax <= kQpTableMax && bits >= 2 && bits <= 8)
+        return tab[(bits - 2) * (kQpTableMax + 1) + vmax];
+    return derive_qparams_warp(vmax, bits);
+}
 }  // namespace
 
-template <int BN, int BK, int STAGES>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+// QF = false: A = vq [F][Tpad][Cpad] int8 via TMA.  QF = true: A is produced by kConvWarps
+// converter warps from the kept int16 V: each thread owns 16-channel chunks of A rows,
+// loads them (2 x 16 B) before waiting for the stage to be free, quantizes, and stores the
+// 16 bytes at the chunk's swizzled position (128B swizzle: chunk j of row r at j ^ (r & 7);
+// 64B swizzle: j ^ ((r >> 1) & 3)), i.e. exactly the layout the TMA load would produce.
+template <int BN, int BK, int STAGES, bool QF>
+__global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmP, int n_tb, int n_ob, int F, int nk) {
+           const __grid_constant__ CUtensorMap tmP, int n_tb, int n_ob, int F, int nk, ConvGeom g, QFuse qf) {
     constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
     constexpr int kHalf = BN / 2;                     // columns per epilogue warp (two warps per lane quarter)
@@ -65,7 +81,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&full[s], QF ? 1 + kConvWarps : 1);
             ptx::mbar_init(&empty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -75,7 +91,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        ptx::tma_prefetch(&tmA);
+        if (!QF) ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB);
         ptx::tma_prefetch(&tmP);
     }
@@ -88,7 +104,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            griddep_wait();  // vq written by the activation kernel
+            // QF: B (the layer's filters) does not depend on the predecessor; the converters wait.
+            if (!QF) griddep_wait();  // vq written by the activation kernel
             tl_mark(kTlGemm, 1);
             int stage = 0;
             uint32_t phase = 0;
@@ -96,8 +113,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const int ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
                 for (int kc = 0; kc < nk; ++kc) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_expect_tx(&full[stage], kStageBytes);
-                    ptx::tma_load_3d(sA + stage * kRowsPerTile * BK, &tmA, &full[stage], kc * BK, tb * kRowsPerTile, f);
+                    if (QF) {
+                        ptx::mbar_expect_tx(&full[stage], uint32_t(BN * BK));
+                    } else {
+                        ptx::mbar_expect_tx(&full[stage], kStageBytes);
+                        ptx::tma_load_3d(sA + stage * kRowsPerTile * BK, &tmA, &full[stage], kc * BK, tb * kRowsPerTile, f);
+                    }
                     ptx::tma_load_3d(sB + stage * BN * BK, &tmB, &full[stage], kc * BK, ob * BN, f);
                     if (++stage == STAGES) stage = 0, phase ^= 1;
                 }
@@ -129,7 +150,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 ptx::mma_commit(&tfull[ab]);
             }
         }
-    } else {
+    } else if (warp < 2 + kEpiWarps) {
         // Epilogue: warp e = warp - 2 owns TMEM lane quarter (warp & 3) and column half e / 4.
         const int q = warp & 3, half = (warp - 2) >> 2;
         uint8_t* myE = sE + (warp - 2) * kEpiBufs * kEpiBoxBytes;
@@ -166,6 +187,79 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (lane == 0) ptx::mbar_arrive(&tempty[ab]);
         }
         if (lane == 0) bulk_wait_all();
+    } else if (QF) {
+        // Converters: thread ct owns items i = ct + j * (32 * kConvWarps) of a stage's
+        // kRowsPerTile x (BK / 16) chunk grid (row r = i / (BK / 16), chunk q = i % (BK / 16)).
+        constexpr int kCh = BK / 16, kItems = kRowsPerTile * kCh / (32 * kConvWarps);
+        const int ct = threadIdx.x - 32 * (2 + kEpiWarps);
+        griddep_wait();  // V and vmax come from the activation pass
+        const QuantParams qp = qparams_warp(*qf.vmax, qf.bits, qf.qtab);
+        if (blockIdx.x == 0 && ct == 0) *qf.qp_out = qp;
+        // (u, kc) pairs in issue order; the loads of pair s + 1 are in flight while pair s
+        // is converted (register double buffer).
+        const int npairs = ((units - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x)) * nk;
+        auto load = [&](int s, uint4 (&va)[kItems], uint4 (&vb)[kItems]) {
+            const int u = int(blockIdx.x) + (s / nk) * int(gridDim.x), kc = s % nk;
+            const int tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
+#pragma unroll
+            for (int j = 0; j < kItems; ++j) {
+                const int i = ct + j * (32 * kConvWarps);
+                const int r = i / kCh, qc = i % kCh;
+                const int t = tb * kRowsPerTile + r, c = kc * BK + qc * 16;
+                va[j] = vb[j] = make_uint4(0, 0, 0, 0);
+                if (s < npairs && t < g.T && c < g.C) {
+                    const uint4* src = reinterpret_cast<const uint4*>(qf.v + (size_t(f) * g.Tpad + t) * g.Cpad + c);
+                    va[j] = __ldg(src);
+                    vb[j] = __ldg(src + 1);
+                }
+            }
+        };
+        auto run = [&](auto quant) {
+            uint4 ca[kItems], cb[kItems], na[kItems], nb[kItems];
+            load(0, ca, cb);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int s = 0; s < npairs; ++s) {
+                load(s + 1, na, nb);
+                const int kc = s % nk;
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* a_st = sA + stage * kRowsPerTile * BK;
+#pragma unroll
+                for (int j = 0; j < kItems; ++j) {
+                    const int i = ct + j * (32 * kConvWarps);
+                    const int r = i / kCh, qc = i % kCh;
+                    const int valid = g.C - (kc * BK + qc * 16);  // channels >= C (and rows >= T, loaded as 0) give 0
+                    const uint32_t w[8] = {ca[j].x, ca[j].y, ca[j].z, ca[j].w, cb[j].x, cb[j].y, cb[j].z, cb[j].w};
+                    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
+                        o[e >> 2] |= uint32_t(uint8_t(int8_t(quant(v)))) << (8 * (e & 3));
+                    }
+                    if (valid < 16) {  // the channel tail of the last chunk (V was loaded as 0 there)
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if (e >= valid) o[e >> 2] &= ~(0xffu << (8 * (e & 3)));
+                    }
+                    const int sw = BK == 128 ? (qc ^ (r & 7)) : (qc ^ ((r >> 1) & 3));
+                    *reinterpret_cast<uint4*>(a_st + r * BK + (sw << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+                }
+                fence_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full[stage]);
+                if (++stage == STAGES) stage = 0, phase ^= 1;
+#pragma unroll
+                for (int j = 0; j < kItems; ++j) ca[j] = na[j], cb[j] = nb[j];
+            }
+        };
+        if (qp.exact) {  // CTA-uniform: one specialised loop per quantizer path
+            const int mul = int(qp.mul);
+            const long long half = 1ll << (qp.shift - 1);
+            const int shift = qp.shift;
+            run([=](int v) { return quant_fast(v, mul, half, shift); });
+        } else {
+            run([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, qf.sat); });
+        }
     }
     __syncthreads();
     tl_mark(kTlGemm, 2);
@@ -212,13 +306,17 @@ int sm_count() {
     return n;
 }
 
-template <int BN, int BK, int STAGES>
+template <int BN, int BK, int STAGES, bool QF>
 cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const ConvGeom& g, int F,
-                        cudaStream_t st, bool pdl) {
+                        const QFuse& qf, cudaStream_t st, bool pdl) {
     const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256;
-    auto kern = k_gemm<BN, BK, STAGES>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
+    auto kern = k_gemm<BN, BK, STAGES, QF>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
     const int n_tb = g.Tpad / kRowsPerTile, n_ob = g.OCpad / BN;
     const int units = F * n_tb * n_ob;
     // CTAs per SM bounded by shared memory and by TMEM (2*BN columns each of 512).
@@ -230,38 +328,53 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     const int resident = sm_count() * per_sm;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units < resident ? units : resident);
-    cfg.blockDim = dim3(kGemmThreads);
+    cfg.blockDim = dim3(gemm_threads<QF>());
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, a, b, p, n_tb, n_ob, F, g.Cpad / BK);
+    return cudaLaunchKernelEx(&cfg, kern, a, b, p, n_tb, n_ob, F, g.Cpad / BK, g, qf);
 }
 
-template <int BK, int STAGES>
+template <int BK, int STAGES, bool QF>
 cudaError_t gemm_by_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const ConvGeom& g, int F,
-                       cudaStream_t st, bool pdl) {
-    if (g.BN == 64) return gemm_launch<64, BK, STAGES>(a, b, p, g, F, st, pdl);
-    if (g.BN == 128) return gemm_launch<128, BK, STAGES>(a, b, p, g, F, st, pdl);
-    return gemm_launch<256, BK, STAGES>(a, b, p, g, F, st, pdl);
+                       const QFuse& qf, cudaStream_t st, bool pdl) {
+    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, g, F, qf, st, pdl);
+    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, g, F, qf, st, pdl);
+    return gemm_launch<256, BK, STAGES, QF>(a, b, p, g, F, qf, st, pdl);
 }
-}  // namespace
 
-cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
-                        bool pdl) {
+template <bool QF>
+cudaError_t gemm_dispatch(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, const QFuse& qf,
+                          cudaStream_t st, bool pdl) {
     CUtensorMap ta, tb, tp;
     const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-    if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, vqA, g.Cpad, g.Tpad, F, g.BK, kRowsPerTile, sw) ||
+    // (QF: the A map is unused; it is built over the filters only to keep one kernel signature)
+    if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, QF ? static_cast<const void*>(uqB) : vqA, g.Cpad,
+                      QF ? g.OCpad : g.Tpad, F, g.BK, QF ? g.BN : kRowsPerTile, sw) ||
         !make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
         !make_tmap_3d(&tp, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, g.Tpad, F, 32, 32,
                       CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
     const int nk = g.Cpad / g.BK;
-    if (g.BK == 128) return nk <= 2 ? gemm_by_bn<128, 2>(ta, tb, tp, g, F, st, pdl) : gemm_by_bn<128, 3>(ta, tb, tp, g, F, st, pdl);
-    return nk <= 2 ? gemm_by_bn<64, 2>(ta, tb, tp, g, F, st, pdl) : gemm_by_bn<64, 4>(ta, tb, tp, g, F, st, pdl);
+    if (g.BK == 128)
+        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, g, F, qf, st, pdl)
+                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, g, F, qf, st, pdl);
+    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, g, F, qf, st, pdl) : gemm_by_bn<64, 4, QF>(ta, tb, tp, g, F, qf, st, pdl);
+}
+}  // namespace
+
+cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
+                        bool pdl) {
+    return gemm_dispatch<false>(vqA, uqB, P, g, F, QFuse{}, st, pdl);
+}
+
+cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
+                               bool pdl) {
+    return gemm_dispatch<true>(nullptr, uqB, P, g, F, q, st, pdl);
 }
 
 SFC_TL_UNIT_READER(tl_read_gemm)

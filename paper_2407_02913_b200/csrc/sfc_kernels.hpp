@@ -47,6 +47,20 @@ cudaError_t launch_quant_kept(const int16_t* vkeep, const ConvGeom& g, int F, co
 // a PDL kernel instead of a memset node, which costs ~3 us in a graph / stream chain.
 cudaError_t launch_zero_words(uint32_t* p, int words, cudaStream_t st);
 enum TlKernel { kTlZero = 0, kTlAbsmax = 1, kTlQuant = 2, kTlGemm = 3, kTlOutput = 4, kTlCount = 8 };
+// Activation quantization fused into the GEMM (k_gemm<..., QF = true>): converter warps
+// read the int16 V kept by the absmax pass and write the quantized A tiles in shared
+// memory; the vq round trip through HBM and the quantize launch disappear.
+struct QFuse {
+    const int16_t* v;           // kept V [F][Tpad][Cpad]
+    const int* vmax;            // global max|V| (after any multi-GPU all-reduce)
+    const QuantParams* qtab;    // qparams_table(false) or nullptr
+    QuantParams* qp_out;        // written by CTA 0 for the output transform / stats
+    unsigned long long* sat;    // saturation counter of the non-verified quantizer path
+    int bits;
+};
+cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
+                               bool pdl);
+
 // Timeline stamps of the debug build ([8][3] per unit; cudaErrorNotSupported otherwise).
 cudaError_t tl_read_act(unsigned long long* out, bool reset);
 cudaError_t tl_read_gemm(unsigned long long* out, bool reset);

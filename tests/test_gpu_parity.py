@@ -45,7 +45,7 @@ def run_gpu(x, w, variant, pad=1, bits=8, outs=("y", "f32"), requant=0.0, vmax=N
         kw["out_f32"] = res["f32"] = torch.empty((B, w.shape[0], HO, WO), dtype=torch.float32, device=dev)
     if "i8" in outs:
         kw["out_i8"] = res["i8"] = torch.empty((B, w.shape[0], HO, WO), dtype=torch.int8, device=dev)
-    if vmax is None:
+    if vmax is None:  # the product path: absmax keeps V, quantization fused into the GEMM
         layer.forward(xt, ws, pad, requant_scale=requant, **kw)
     else:
         vm = torch.tensor([vmax], dtype=torch.int32, device=dev)
@@ -55,8 +55,23 @@ def run_gpu(x, w, variant, pad=1, bits=8, outs=("y", "f32"), requant=0.0, vmax=N
     out["stats"] = layer.stats(B, H, W, pad, ws)
     out["sf"], out["umax"] = layer.filter_scales()
     if views:
-        vq, pacc = layer.views(B, H, W, pad, ws)
-        out["vq"], out["pacc"] = vq.cpu().numpy(), pacc.cpu().numpy()
+        # forward never materialises vq: take it from the recompute path (absmax, then a
+        # quantize pass that re-derives V from x) on its own workspace, whose y must match.
+        _, pacc = layer.views(B, H, W, pad, ws)
+        out["pacc"] = pacc.cpu().numpy()
+        ws2 = layer.workspace(B, H, W, pad)
+        y2 = torch.empty_like(res["y"]) if "y" in res else None
+        vm = torch.zeros(1, dtype=torch.int32, device=dev)
+        if vmax is None:
+            layer.absmax(xt, vm, pad)
+        else:
+            vm.fill_(vmax)
+        layer.conv(xt, vm, ws2, pad, y_int32=y2)
+        vq, pacc2 = layer.views(B, H, W, pad, ws2)
+        out["vq"] = vq.cpu().numpy()
+        assert np.array_equal(pacc2.cpu().numpy(), out["pacc"]), "pacc: recompute path vs product path"
+        if y2 is not None:
+            assert torch.equal(y2, res["y"]), "y: recompute path vs product path"
         out["uq"] = layer.uq().cpu().numpy()
     out["filter_sat"] = layer.filter_saturations()
     return out
@@ -295,8 +310,8 @@ def test_repeated_forwards_are_deterministic(cuda, variant):
         ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
         y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int32, device="cuda")
         layer.forward(x, ws, L.pad, y_int32=y)
-        vq, p = layer.views(L.batch, L.hw, L.hw, L.pad, ws)
-        cur = (y.clone(), vq.clone(), p.clone())
+        _, p = layer.views(L.batch, L.hw, L.hw, L.pad, ws)
+        cur = (y.clone(), p.clone())
         if first is None:
             first = cur
         else:
@@ -305,30 +320,41 @@ def test_repeated_forwards_are_deterministic(cuda, variant):
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_kept_and_recompute_paths_agree(cuda, variant):
-    """forward (absmax keeps V, streaming quantize) == transform + conv_kept (the multi-GPU
-    entry points) == absmax + conv (quantize recomputes the transform from x), bit for bit."""
-    for cfg, li, C in ((2, 0, None), (1, 0, None)):
+def test_kept_and_recompute_paths_agree(cuda, variant, monkeypatch):
+    """forward (absmax keeps V, streaming quantizer) == transform + conv_kept (the multi-GPU
+    entry points) == the same with quantization fused into the GEMM (SFC_QFUSE=1) ==
+    absmax + conv (quantize recomputes the transform from x): y, P and stats bit for bit,
+    and vq where it is materialised."""
+    for cfg, li in ((2, 0), (1, 0), (3, 0)):
         L = wl.WORKLOADS[cfg].layers[li]
         x = torch.from_numpy(wl.activations(cfg, li, L)).cuda()
         w = torch.from_numpy(wl.weights(cfg, li, L)).cuda()
         layer = sc.SfcLayer(variant, w)
         ho = L.hw + 2 * L.pad - 2
-        res = []
-        for mode in ("forward", "kept", "recompute"):
+        res = {}
+        for mode in ("forward", "kept", "kept-qfused", "recompute"):
             ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
-            y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int32, device="cuda")
+            y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int64, device="cuda")
+            if mode == "kept-qfused":
+                monkeypatch.setenv("SFC_QFUSE", "1")
+            else:
+                monkeypatch.delenv("SFC_QFUSE", raising=False)
             if mode == "forward":
-                layer.forward(x, ws, L.pad, y_int32=y)
+                layer.forward(x, ws, L.pad, y_int64=y)
             else:
                 vmax = torch.zeros(1, dtype=torch.int32, device="cuda")
-                if mode == "kept":
+                if mode.startswith("kept"):
                     layer.transform(x, vmax, ws, L.pad)
-                    layer.conv_kept(tuple(x.shape), vmax, ws, L.pad, y_int32=y)
+                    layer.conv_kept(tuple(x.shape), vmax, ws, L.pad, y_int64=y)
                 else:
                     layer.absmax(x, vmax, L.pad)
-                    layer.conv(x, vmax, ws, L.pad, y_int32=y)
-            vq, _ = layer.views(L.batch, L.hw, L.hw, L.pad, ws)
-            res.append((y.clone(), vq.clone(), layer.stats(L.batch, L.hw, L.hw, L.pad, ws)))
-        for r in res[1:]:
-            assert torch.equal(res[0][0], r[0]) and torch.equal(res[0][1], r[1]) and res[0][2] == r[2]
+                    layer.conv(x, vmax, ws, L.pad, y_int64=y)
+            vq, p = layer.views(L.batch, L.hw, L.hw, L.pad, ws)
+            res[mode] = (y.clone(), p.clone(), vq.clone(), layer.stats(L.batch, L.hw, L.hw, L.pad, ws))
+        monkeypatch.delenv("SFC_QFUSE", raising=False)
+        ref = res["recompute"]
+        for mode, r in res.items():
+            assert torch.equal(ref[0], r[0]), (cfg, mode, "y")
+            assert torch.equal(ref[1], r[1]), (cfg, mode, "P")
+            assert ref[3] == r[3], (cfg, mode, "stats")
+        assert torch.equal(ref[2], res["kept"][2]) and torch.equal(ref[2], res["forward"][2]), (cfg, "vq")
