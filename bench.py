@@ -412,13 +412,16 @@ def run_b200(args, rank, world, local_rank):
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["kernel"] = dom
         roof["kernel_share_of_step"] = kms / sum(stage_ms.values())
-        roof["traffic"] = None
+        roof["alg_bytes_per_launch"] = alg_bytes / len(calls)
+        roof["traffic"] = None  # dram bytes per launch of this kernel (ncu --set full, profiles/)
         tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tr_path):
             try:
                 with open(tr_path) as f:
                     tr = json.load(f)
                 roof["traffic"] = tr.get(f"{work.name}:{dom}")
+                if roof["traffic"]:
+                    roof["traffic_src"] = tr.get("_note", "")
             except Exception:
                 pass
         # whole-step roofline: sum over calls of max(ops/P, bytes/BW), algorithmic
