@@ -32,23 +32,24 @@ struct ActSmem {
     int chs;      // bytes per staged channel: the channel's window rows as they lie in NCHW,
                   // from its 4-byte-aligned start; chs / 4 odd so lanes stepping channels
                   // hit distinct banks
-    size_t x_off, z_off, bytes;
+    size_t z_off, x_off, bytes;  // s_z first; s_x, then (once s_x is dead) the kept-V rows
 };
 
 template <int V, int CC>
-__host__ __device__ inline ActSmem act_smem(int W) {
+__host__ __device__ inline ActSmem act_smem(int W, int tw) {
     using T = Tab<V>;
     ActSmem s;
     s.chs = ((T::n * W + 6) >> 2) * 4;
     if (((s.chs / 4) & 1) == 0) s.chs += 4;
-    s.x_off = 0;
-    s.z_off = (size_t(s.chs) * CC + 15) & ~size_t(15);
+    s.z_off = 0;
+    s.x_off = (size_t(tw) * T::n * T::K * CC * 2 + 15) & ~size_t(15);
+    const size_t xb = size_t(s.chs) * CC, vb = size_t(tw) * T::F * CC * 2;
+    s.bytes = s.x_off + (xb > vb ? xb : vb);
     return s;
 }
 template <int V, int CC>
 __host__ __device__ inline size_t act_smem_bytes(int W, int tw) {
-    using T = Tab<V>;
-    return act_smem<V, CC>(W).z_off + size_t(tw) * T::n * T::K * CC * 2;
+    return act_smem<V, CC>(W, tw).bytes;
 }
 }  // namespace
 
@@ -66,16 +67,17 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     constexpr int n = T::n, K = T::K, M = T::M;
     constexpr int TPC = kActThreads / CC;   // work-groups per channel
     extern __shared__ __align__(16) uint8_t smem[];
-    constexpr int kTl = MODE == 0 ? kTlAbsmax : kTlQuant;
+    constexpr int kTl = MODE == 1 ? kTlQuant : kTlAbsmax;
     tl_mark(kTl, 0);
     if (MODE == 0) griddep_launch_dependents();
 
     const int tw = g.tw, W = g.W;
     const int ti = blockIdx.x, b = blockIdx.y, c0 = blockIdx.z * CC;
     const int nch = min(CC, g.C - c0);
-    const ActSmem L = act_smem<V, CC>(W);
+    const ActSmem L = act_smem<V, CC>(W, tw);
     int8_t* s_x = reinterpret_cast<int8_t*>(smem + L.x_off);     // [CC][chs]
     int16_t* s_z = reinterpret_cast<int16_t*>(smem + L.z_off);   // [tw][n][K][CC]
+    int16_t* s_v = reinterpret_cast<int16_t*>(smem + L.x_off);   // [tw][F][CC] kept V (after stage 1)
     const int c = threadIdx.x % CC, j = threadIdx.x / CC;
 
     // ---- stage 0: copy each channel's window rows [r_lo, r_lo + nrows) -- one contiguous
@@ -87,37 +89,39 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     const size_t cstride = size_t(g.H) * W;
     const int8_t* src0 = x + (size_t(b) * g.C + c0) * cstride + size_t(r_lo) * W;
     {
-        const int8_t* x_end = x + size_t(g.B) * g.C * cstride;
+        // 32-bit offsets from src0 (a CTA's channels span < 2^31 bytes); `avail` bounds the
+        // last word of the tensor.
+        const long long avail64 = (long long)(size_t(g.B) * g.C * cstride) - (long long)(src0 - x);
+        const int avail = avail64 > 0x7fffffffll ? 0x7fffffff : int(avail64);
+        const int cs32 = int(cstride);
+        const int mis0 = int(reinterpret_cast<uintptr_t>(src0) & 3);
         const int seg = nrows * W;
         const int nwc = L.chs >> 2;
         const unsigned magic = 0xffffffffu / unsigned(nwc) + 1u;
         constexpr int kJ = 4;
         for (int k0 = 0; k0 < nch * nwc; k0 += kJ * kActThreads) {
             uint32_t v[kJ];
-            int dst[kJ];
+            bool st[kJ];
 #pragma unroll
             for (int jj = 0; jj < kJ; ++jj) {
                 const int k = k0 + jj * kActThreads + int(threadIdx.x);
-                dst[jj] = -1;
-                if (k < nch * nwc) {
-                    const int ch = int(__umulhi(unsigned(k), magic)), w = k - ch * nwc;
-                    const int8_t* cs = src0 + size_t(ch) * cstride;
-                    const int8_t* a = cs - (reinterpret_cast<uintptr_t>(cs) & 3) + 4 * w;
-                    if (a < cs + seg) {
-                        if (a + 4 <= x_end) {
-                            v[jj] = __ldg(reinterpret_cast<const unsigned int*>(a));
-                        } else {
-                            uint32_t t = 0;
-                            for (int q = 0; q < 4 && a + q < x_end; ++q) t |= uint32_t(uint8_t(__ldg(a + q))) << (8 * q);
-                            v[jj] = t;
-                        }
-                        dst[jj] = ch * nwc + w;
+                const int ch = int(__umulhi(unsigned(k), magic)), w = k - ch * nwc;
+                const int coff = ch * cs32;
+                const int lo = 4 * w - ((mis0 + coff) & 3);  // segment index of the word's first byte
+                const int a = coff + lo;                     // its offset from src0 (4-aligned address)
+                st[jj] = k < nch * nwc && lo < seg;
+                v[jj] = 0;
+                if (st[jj]) {
+                    if (a + 4 <= avail) {
+                        v[jj] = __ldg(reinterpret_cast<const unsigned int*>(src0 + a));
+                    } else {
+                        for (int q = 0; q < 4 && a + q < avail; ++q) v[jj] |= uint32_t(uint8_t(__ldg(src0 + a + q))) << (8 * q);
                     }
                 }
             }
 #pragma unroll
             for (int jj = 0; jj < kJ; ++jj)
-                if (dst[jj] >= 0) reinterpret_cast<uint32_t*>(s_x)[dst[jj]] = v[jj];
+                if (st[jj]) reinterpret_cast<uint32_t*>(s_x)[k0 + jj * kActThreads + int(threadIdx.x)] = v[jj];
         }
     }
     __syncthreads();
@@ -167,9 +171,8 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     // straight to its vq row (lanes = consecutive channels: CC contiguous bytes per store).
     const int t0 = (b * g.th + ti) * tw;
     int8_t* vrow = vqA + size_t(t0) * g.Cpad + c0 + c;
-    int16_t* krow = vkeep + size_t(t0) * g.Cpad + c0 + c;  // (only dereferenced when vkeep != nullptr)
     const size_t fstride = size_t(g.Tpad) * g.Cpad, kstride = size_t(K) * fstride;
-    int local = 0;
+    int vhi = 0, vlo = 0;
     auto column = [&](auto quantize) {
         for (int idx = j; idx < tw * K; idx += TPC) {
             const int l = idx % K, tj = idx / K;
@@ -179,23 +182,20 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
             int v[K];
             fwd1d<V>(zr, v);
             int8_t* p = vrow + size_t(l) * fstride + size_t(tj) * g.Cpad;  // f = l, then += K rows
-            int16_t* pk = krow + size_t(l) * fstride + size_t(tj) * g.Cpad;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 if (MODE == 1) {
                     *p = int8_t(quantize(v[k]));
                     p += kstride;
                 } else {
-                    local = max(local, abs(v[k]));
-                    if (vkeep) {
-                        *pk = int16_t(v[k]);
-                        pk += kstride;
-                    }
+                    vhi = max(vhi, v[k]);
+                    vlo = min(vlo, v[k]);
+                    if (vkeep) s_v[(tj * T::F + k * K + l) * CC + c] = int16_t(v[k]);
                 }
             }
         }
     };
-    if (MODE == 0) {
+    if (MODE != 1) {
         column([](int v) { return v; });
     } else if (qp.exact) {  // uniform over the CTA: no per-value branch
         // mul < 2^31 (derive_qparams): one 32x32+64 -> 64 multiply-add and a funnel shift
@@ -207,8 +207,25 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
         column([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, sat); });
     }
 
+    if (MODE == 0 && vkeep) {
+        // kept V rows (tj, f): CC int16 channels contiguous in shared memory and in
+        // V[f][t][c0 .. c0+CC), moved in 16-byte (CC >= 8) or 8-byte (CC = 4) pieces
+        __syncthreads();
+        constexpr int kPB = CC >= 8 ? 16 : 8, kPR = CC * 2 / kPB;  // piece bytes, pieces per row
+        for (int i = threadIdx.x; i < tw * T::F * kPR; i += kActThreads) {
+            const int pc = i % kPR, row = i / kPR;
+            const int f = row % T::F, tj = row / T::F;
+            const uint8_t* s = reinterpret_cast<const uint8_t*>(s_v + row * CC) + pc * kPB;
+            uint8_t* d = reinterpret_cast<uint8_t*>(vkeep + (size_t(f) * g.Tpad + t0 + tj) * g.Cpad + c0) + pc * kPB;
+            if (kPB == 16)
+                *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(s);
+            else
+                *reinterpret_cast<uint2*>(d) = *reinterpret_cast<const uint2*>(s);
+        }
+    }
     if (MODE == 0) {
         const int lane = threadIdx.x & 31;
+        int local = max(vhi, -vlo);
 #pragma unroll
         for (int o = 16; o; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
         griddep_wait();  // under PDL: *vmax has been zeroed by the predecessor
@@ -345,8 +362,8 @@ namespace {
 
 template <int V, int MODE, int CC>
 cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits,
-                          QuantParams* qp, int8_t* vqA, unsigned long long* sat, int16_t* vkeep, cudaStream_t st,
-                          bool pdl) {
+                          QuantParams* qp, int8_t* vqA, unsigned long long* sat, int16_t* vkeep,
+                          cudaStream_t st, bool pdl) {
     const size_t smem = act_smem_bytes<V, CC>(g.W, g.tw);
     auto kern = k_act<V, MODE, CC>;
     static size_t attr_bytes = 0;  // per instantiation: raise the opt-in only when a layer needs more
