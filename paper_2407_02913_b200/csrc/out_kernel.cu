@@ -36,6 +36,8 @@ template <int V>
 __host__ __device__ constexpr int out_tb() {  // tile columns per block: ~40 KB of P per block
     return (40 * 1024) / (Tab<V>::F * kOcc * 4) < 1 ? 1 : (40 * 1024) / (Tab<V>::F * kOcc * 4);
 }
+static_assert(out_tb<0>() * Tab<0>::M <= 32 && out_tb<1>() * Tab<1>::M <= 32 && out_tb<2>() * Tab<2>::M <= 32,
+              "a block's output row segment must fit the 32-entry magic table");
 
 struct OutSmem {
     int qstride, ystride;
@@ -59,6 +61,14 @@ __host__ __device__ inline OutSmem out_smem() {
     return s;
 }
 }  // namespace
+
+// umulhi magics for the divisors 1..32 (ncol): t / d == umulhi(t, c_magic32[d]) for t < 2^16
+__constant__ unsigned c_magic32[33] = {  // 0xffffffff / d + 1 (exact for t < 2^16; generated)
+    0x00000000u, 0x00000000u, 0x80000000u, 0x55555556u, 0x40000000u, 0x33333334u, 0x2aaaaaabu, 0x24924925u,
+    0x20000000u, 0x1c71c71du, 0x1999999au, 0x1745d175u, 0x15555556u, 0x13b13b14u, 0x12492493u, 0x11111112u,
+    0x10000000u, 0x0f0f0f10u, 0x0e38e38fu, 0x0d79435fu, 0x0ccccccdu, 0x0c30c30du, 0x0ba2e8bbu, 0x0b21642du,
+    0x0aaaaaabu, 0x0a3d70a4u, 0x09d89d8au, 0x097b425fu, 0x0924924au, 0x08d3dcb1u, 0x08888889u, 0x08421085u,
+    0x08000000u};
 
 template <int V, bool Y64>
 __global__ void __launch_bounds__(kOutThreads, 2)
@@ -92,7 +102,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
         ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 4));
         ptx::tma_load_3d(smem, &tmP, full, oc0, row * g.tw + tc * TB, 0);
     }
-    const int b = row / g.th, ti = row - b * g.th;
+    const int b = g.th == 1 ? row : int(__umulhi(unsigned(row), g.th_magic)), ti = row - b * g.th;
     const int noc = min(kOcc, g.OC - oc0);
     const int ntb = min(TB, g.tw - tc * TB);
     if (threadIdx.x < kOcc && int(threadIdx.x) < noc) {
@@ -131,22 +141,23 @@ __global__ void __launch_bounds__(kOutThreads, 2)
 
     // stage C: the block's output row segments r = (t1, oc), ncol columns each.  Thread t
     // keeps column c = t % ncol and walks rows r = t / ncol, + kOutThreads / ncol, ...
-    // (consecutive threads -> consecutive columns: coalesced row segments).  The set of
-    // requested outputs is a compile-time mask (one specialisation per combination), so
-    // the per-element work is the stores and conversions only.
+    // (consecutive threads -> consecutive columns of a row: coalesced row segments); the
+    // divisions by ncol <= 32 are multiply-highs from a constant table.  The set of
+    // requested outputs is a compile-time mask (one specialisation per combination).
     const int WO = g.WO;
     const int col0 = tc * TB * M;
-    const int ncol = min(ntb * M, WO - col0);
+    const int ncol = min(ntb * M, WO - col0);           // <= TB * M <= 32
     const int hrows = min(M, g.HO - ti * M);
     const int plane = g.HO * WO;
     const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
-    const int rstep = kOutThreads / ncol;
-    const int c = int(threadIdx.x) % ncol, r0 = int(threadIdx.x) / ncol;
-    const bool active = r0 < rstep;
+    const unsigned nmag = c_magic32[ncol];
+    const int r0 = ncol == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
+    const int c = int(threadIdx.x) - r0 * ncol;
+    const int rstep = ncol == 1 ? kOutThreads : int(__umulhi(unsigned(kOutThreads), nmag));
     const double rq = o.requant;
     auto emit = [&](auto mask_c) {
         constexpr int MK = decltype(mask_c)::value;
-        if (!active) return;
+        if (r0 >= rstep) return;
         for (int r = r0; r < M * kOcc; r += rstep) {
             const int oc = r % kOcc, t1 = r / kOcc;
             if (oc >= noc || t1 >= hrows) continue;

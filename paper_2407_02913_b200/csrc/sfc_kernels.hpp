@@ -15,6 +15,7 @@ struct ConvGeom {
     int Cpad;   // input channels rounded up to the GEMM K chunk (BK)
     int BK;     // 64 or 128 bytes of K per pipeline stage
     int OC, OCpad, BN;
+    unsigned th_magic;  // r / th == umulhi(r, th_magic) for r < 2^16 (th == 1: 0, divide by identity)
 };
 
 // Activation quantizer derived on device from the global absmax (so multi-GPU
