@@ -145,10 +145,14 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
         ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
         pdl = false;
     }
-    // Kept V is quantized by the streaming quantizer (vq through HBM); SFC_QFUSE=1 selects the
-    // GEMM with converter warps instead (no vq round trip, but its V reads are latency-bound
-    // at BN = 256: slower on the large layers for now).
-    const bool qfuse = kept && std::getenv("SFC_QFUSE") != nullptr;
+    // Kept V is quantized inside the GEMM by converter warps (one launch and the vq round trip
+    // disappear) unless V is large and every A tile would be converted for several oc blocks:
+    // then the converters' DRAM-latency-bound V reads lose to the streaming quantizer (vq
+    // through HBM).  Measured: configs 1-4 faster fused, config 5 (V 236 MB, 2 oc blocks) not.
+    // SFC_QFUSE=0/1 forces either.
+    // (one oc block: every A tile is converted once; several: only if V is L2-sized)
+    bool qfuse = kept && (g.OCpad == g.BN || size_t(L->F) * g.Tpad * g.Cpad * 2 <= (size_t(64) << 20));
+    if (const char* q = std::getenv("SFC_QFUSE")) qfuse = kept && q[0] == '1';
     if (mask & SFC_STAGE_ACT) {
         if (!kept) {
             ck(launch_act_quant(L->variant, d_x, g, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "act launch");

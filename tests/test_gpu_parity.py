@@ -321,10 +321,11 @@ def test_repeated_forwards_are_deterministic(cuda, variant):
 
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_kept_and_recompute_paths_agree(cuda, variant, monkeypatch):
-    """forward (absmax keeps V, streaming quantizer) == transform + conv_kept (the multi-GPU
-    entry points) == the same with quantization fused into the GEMM (SFC_QFUSE=1) ==
-    absmax + conv (quantize recomputes the transform from x): y, P and stats bit for bit,
-    and vq where it is materialised."""
+    """forward (absmax keeps V; quantization in the GEMM when V is L2-sized, else streaming)
+    == transform + conv_kept (the multi-GPU entry points) with the streaming quantizer
+    (SFC_QFUSE=0) and with quantization fused into the GEMM (SFC_QFUSE=1) == absmax + conv
+    (quantize recomputes the transform from x): y, P and stats bit for bit, and vq where it
+    is materialised."""
     for cfg, li in ((2, 0), (1, 0), (3, 0)):
         L = wl.WORKLOADS[cfg].layers[li]
         x = torch.from_numpy(wl.activations(cfg, li, L)).cuda()
@@ -337,6 +338,8 @@ def test_kept_and_recompute_paths_agree(cuda, variant, monkeypatch):
             y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int64, device="cuda")
             if mode == "kept-qfused":
                 monkeypatch.setenv("SFC_QFUSE", "1")
+            elif mode == "kept":
+                monkeypatch.setenv("SFC_QFUSE", "0")  # streaming quantizer materialises vq
             else:
                 monkeypatch.delenv("SFC_QFUSE", raising=False)
             if mode.startswith("forward"):
@@ -357,5 +360,4 @@ def test_kept_and_recompute_paths_agree(cuda, variant, monkeypatch):
             assert torch.equal(ref[0], r[0]), (cfg, mode, "y")
             assert torch.equal(ref[1], r[1]), (cfg, mode, "P")
             assert ref[3] == r[3], (cfg, mode, "stats")
-        for mode in ("forward", "kept"):
-            assert torch.equal(ref[2], res[mode][2]), (cfg, mode, "vq")
+        assert torch.equal(ref[2], res["kept"][2]), (cfg, "vq")
