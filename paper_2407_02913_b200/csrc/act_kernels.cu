@@ -29,36 +29,38 @@ namespace {
 constexpr int kActThreads = 256;
 
 struct ActSmem {
-    int chs;      // bytes per staged channel: the channel's window rows as they lie in NCHW,
-                  // from its 4-byte-aligned start; chs / 4 odd so lanes stepping channels
-                  // hit distinct banks
+    int nwp;      // 32-bit words per staged row piece (the piece's bytes from its 4-aligned start)
+    int chw;      // words per staged channel: n * nwp, made odd so lanes stepping channels hit
+                  // distinct banks
     size_t z_off, x_off, bytes;  // s_z first; s_x, then (once s_x is dead) the kept-V rows
 };
 
+// Shared-memory layout of one CTA covering `twc` tile columns of one tile row.
 template <int V, int CC>
-__host__ __device__ inline ActSmem act_smem(int W, int tw) {
+__host__ __device__ inline ActSmem act_smem(int W, int twc) {
     using T = Tab<V>;
     ActSmem s;
-    s.chs = ((T::n * W + 6) >> 2) * 4;
-    if (((s.chs / 4) & 1) == 0) s.chs += 4;
+    const int pw = min((twc - 1) * T::M + T::n, W);  // widest row piece (window clipped to the image)
+    s.nwp = (pw + 6) >> 2;
+    s.chw = T::n * s.nwp;
+    if ((s.chw & 1) == 0) s.chw += 1;
     s.z_off = 0;
-    s.x_off = (size_t(tw) * T::n * T::K * CC * 2 + 15) & ~size_t(15);
-    const size_t xb = size_t(s.chs) * CC, vb = size_t(tw) * T::F * CC * 2;
+    s.x_off = (size_t(twc) * T::n * T::K * CC * 2 + 15) & ~size_t(15);
+    const size_t xb = size_t(s.chw) * 4 * CC, vb = size_t(twc) * T::F * CC * 2;
     s.bytes = s.x_off + (xb > vb ? xb : vb);
     return s;
-}
-template <int V, int CC>
-__host__ __device__ inline size_t act_smem_bytes(int W, int tw) {
-    return act_smem<V, CC>(W, tw).bytes;
 }
 }  // namespace
 
 // MODE 0: max|V| -> atomicMax(*vmax); with vkeep != nullptr V itself is kept as int16
-// vkeep[f][t][c] (row pitch Cpad) for the streaming quantizer k_quant_kept.
+// vkeep[f][t][c] (row pitch Cpad) for the quantizer (streaming or inside the GEMM).
 // MODE 1: quantize with the scale derived from *vmax_in and write vq[f][t][c] (row pitch
 // Cpad) for f = k*K + l.
+// Grid: x = tile row * column chunks + chunk (twc tile columns each), y = image, z =
+// channel chunk of CC.  Shared memory is bounded by twc, so wide images keep CC = 32
+// (64-byte kept-V rows) instead of narrowing the channel chunk.
 template <int V, int MODE, int CC>
-__global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ x, ConvGeom g,
+__global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ x, ConvGeom g, int twc,
                                                      int* __restrict__ vmax, const int* __restrict__ vmax_in, int bits,
                                                      QuantParams* __restrict__ qp_out, int8_t* __restrict__ vqA,
                                                      unsigned long long* __restrict__ sat,
@@ -71,57 +73,62 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     tl_mark(kTl, 0);
     if (MODE == 0) griddep_launch_dependents();
 
-    const int tw = g.tw, W = g.W;
-    const int ti = blockIdx.x, b = blockIdx.y, c0 = blockIdx.z * CC;
+    const int W = g.W;
+    const int nchunk = (g.tw + twc - 1) / twc;
+    const int ti = blockIdx.x / nchunk, tj0 = (blockIdx.x - ti * nchunk) * twc;
+    const int ntj = min(twc, g.tw - tj0);
+    const int b = blockIdx.y, c0 = blockIdx.z * CC;
     const int nch = min(CC, g.C - c0);
-    const ActSmem L = act_smem<V, CC>(W, tw);
-    int8_t* s_x = reinterpret_cast<int8_t*>(smem + L.x_off);     // [CC][chs]
-    int16_t* s_z = reinterpret_cast<int16_t*>(smem + L.z_off);   // [tw][n][K][CC]
-    int16_t* s_v = reinterpret_cast<int16_t*>(smem + L.x_off);   // [tw][F][CC] kept V (after stage 1)
+    const ActSmem L = act_smem<V, CC>(W, twc);
+    int8_t* s_x = reinterpret_cast<int8_t*>(smem + L.x_off);     // [CC][n][nwp words], channel stride chw
+    int16_t* s_z = reinterpret_cast<int16_t*>(smem + L.z_off);   // [twc][n][K][CC]
+    int16_t* s_v = reinterpret_cast<int16_t*>(smem + L.x_off);   // [twc][F][CC] kept V (after stage 1)
     const int c = threadIdx.x % CC, j = threadIdx.x / CC;
 
-    // ---- stage 0: copy each channel's window rows [r_lo, r_lo + nrows) -- one contiguous
-    // NCHW byte range -- word for word into shared memory, starting at the range's
-    // 4-byte-aligned address (so a word lands where it lies: no byte scatter).  Zero
-    // padding is left to stage 1.  Words past the end of x are assembled from bytes.
+    // ---- stage 0: the window rows [r_lo, r_lo + nrows) x columns [cb_lo, cb_lo + pw) of each
+    // channel, one row piece at a time, copied word for word from the piece's 4-byte-aligned
+    // start (so a word lands where it lies: no byte scatter).  Zero padding is left to
+    // stage 1.  Words past the end of x are assembled from bytes.  Offsets are 32-bit from
+    // the CTA's first channel plane (CC planes span < 2^31 bytes).
     const int ih0 = ti * M - g.pad;
     const int r_lo = max(ih0, 0), nrows = min(ih0 + n, g.H) - r_lo;
-    const size_t cstride = size_t(g.H) * W;
-    const int8_t* src0 = x + (size_t(b) * g.C + c0) * cstride + size_t(r_lo) * W;
+    const int cb_lo = max(tj0 * M - g.pad, 0);
+    const int pw = min((tj0 + ntj - 1) * M - g.pad + n, W) - cb_lo;
+    const int HW = g.H * W;
+    const int8_t* base = x + (size_t(b) * g.C + c0) * size_t(HW);
+    const int bmis = int(reinterpret_cast<uintptr_t>(base) & 3);
+    auto piece_off = [&](int ch, int r) { return ch * HW + (r_lo + r) * W + cb_lo; };  // from base
     {
-        // 32-bit offsets from src0 (a CTA's channels span < 2^31 bytes); `avail` bounds the
-        // last word of the tensor.
-        const long long avail64 = (long long)(size_t(g.B) * g.C * cstride) - (long long)(src0 - x);
+        const long long avail64 = (long long)(size_t(g.B) * g.C * HW) - (long long)(base - x);
         const int avail = avail64 > 0x7fffffffll ? 0x7fffffff : int(avail64);
-        const int cs32 = int(cstride);
-        const int mis0 = int(reinterpret_cast<uintptr_t>(src0) & 3);
-        const int seg = nrows * W;
-        const int nwc = L.chs >> 2;
-        const unsigned magic = 0xffffffffu / unsigned(nwc) + 1u;
+        const int nwp = L.nwp;
+        const unsigned wmag = 0xffffffffu / unsigned(nwp) + 1u, rmag = 0xffffffffu / unsigned(nrows) + 1u;
+        const int total = nch * nrows * nwp;
         constexpr int kJ = 4;
-        for (int k0 = 0; k0 < nch * nwc; k0 += kJ * kActThreads) {
+        for (int k0 = 0; k0 < total; k0 += kJ * kActThreads) {
             uint32_t v[kJ];
-            bool st[kJ];
+            int dst[kJ];
 #pragma unroll
             for (int jj = 0; jj < kJ; ++jj) {
                 const int k = k0 + jj * kActThreads + int(threadIdx.x);
-                const int ch = int(__umulhi(unsigned(k), magic)), w = k - ch * nwc;
-                const int coff = ch * cs32;
-                const int lo = 4 * w - ((mis0 + coff) & 3);  // segment index of the word's first byte
-                const int a = coff + lo;                     // its offset from src0 (4-aligned address)
-                st[jj] = k < nch * nwc && lo < seg;
+                const int cr = nwp == 1 ? k : int(__umulhi(unsigned(k), wmag)), w = k - cr * nwp;
+                const int ch = nrows == 1 ? cr : int(__umulhi(unsigned(cr), rmag)), r = cr - ch * nrows;
+                const int po = piece_off(ch, r);
+                const int lo = 4 * w - ((bmis + po) & 3);  // piece index of the word's first byte
+                const int a = po + lo;                     // its offset from base (4-aligned address)
+                dst[jj] = (k < total && lo < pw) ? ch * L.chw + r * nwp + w : -1;
                 v[jj] = 0;
-                if (st[jj]) {
+                if (dst[jj] >= 0) {
                     if (a + 4 <= avail) {
-                        v[jj] = __ldg(reinterpret_cast<const unsigned int*>(src0 + a));
+                        v[jj] = __ldg(reinterpret_cast<const unsigned int*>(base + a));
                     } else {
-                        for (int q = 0; q < 4 && a + q < avail; ++q) v[jj] |= uint32_t(uint8_t(__ldg(src0 + a + q))) << (8 * q);
+                        for (int q = 0; q < 4 && a + q < avail; ++q) v[jj] |= uint32_t(uint8_t(__ldg(base + a + q))) << (8 * q);
                     }
                 }
             }
 #pragma unroll
             for (int jj = 0; jj < kJ; ++jj)
-                if (st[jj]) reinterpret_cast<uint32_t*>(s_x)[k0 + jj * kActThreads + int(threadIdx.x)] = v[jj];
+                if (dst[jj] >= 0) reinterpret_cast<uint32_t*>(s_x)[dst[jj]] = v[jj];
         }
     }
     __syncthreads();
@@ -129,18 +136,18 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     // ---- stage 1: row transform, items (tj, r).  Rows outside the image and channels
     // beyond C are zero; columns outside [0, W) are zero (only border tiles test them).
     {
-        const int mis = int(reinterpret_cast<uintptr_t>(src0 + size_t(c) * cstride) & 3);
-        const int8_t* cbase = s_x + c * L.chs + mis;
-        for (int idx = j; idx < tw * n; idx += TPC) {
-            const int r = idx % n, tj = idx / n;
+        const int8_t* cx = s_x + c * L.chw * 4;
+        for (int idx = j; idx < ntj * n; idx += TPC) {
+            const int r = idx % n, tjl = idx / n;
             const int ir = ih0 + r - r_lo;  // row within the staged window
-            const int col0 = tj * M - g.pad;
+            const int col0 = (tj0 + tjl) * M - g.pad;
             int xs[n];
             if (c >= nch || ir < 0 || ir >= nrows) {
 #pragma unroll
                 for (int s = 0; s < n; ++s) xs[s] = 0;
             } else {
-                const int8_t* src = cbase + ir * W + col0;
+                const int mis = (bmis + piece_off(c, ir)) & 3;
+                const int8_t* src = cx + ir * L.nwp * 4 + mis + (col0 - cb_lo);
                 if (col0 >= 0 && col0 + n <= W) {
 #pragma unroll
                     for (int s = 0; s < n; ++s) xs[s] = src[s];
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
                     for (int s = 0; s < n; ++s) xs[s] = unsigned(col0 + s) < unsigned(W) ? int(src[s]) : 0;
                 }
             }
-            int16_t* dst = s_z + ((tj * n + r) * K) * CC + c;
+            int16_t* dst = s_z + ((tjl * n + r) * K) * CC + c;
             int z[K];
             fwd1d<V>(xs, z);
 #pragma unroll
@@ -169,12 +176,12 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
 
     // ---- stage 2: column transform, items (tj, l); MODE 1 quantizes and stores each value
     // straight to its vq row (lanes = consecutive channels: CC contiguous bytes per store).
-    const int t0 = (b * g.th + ti) * tw;
+    const int t0 = (b * g.th + ti) * g.tw + tj0;  // the CTA's first tile
     int8_t* vrow = vqA + size_t(t0) * g.Cpad + c0 + c;
     const size_t fstride = size_t(g.Tpad) * g.Cpad, kstride = size_t(K) * fstride;
     int vhi = 0, vlo = 0;
     auto column = [&](auto quantize) {
-        for (int idx = j; idx < tw * K; idx += TPC) {
+        for (int idx = j; idx < ntj * K; idx += TPC) {
             const int l = idx % K, tj = idx / K;
             int zr[n];
 #pragma unroll
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
         // V[f][t][c0 .. c0+CC), moved in 16-byte (CC >= 8) or 8-byte (CC = 4) pieces
         __syncthreads();
         constexpr int kPB = CC >= 8 ? 16 : 8, kPR = CC * 2 / kPB;  // piece bytes, pieces per row
-        for (int i = threadIdx.x; i < tw * T::F * kPR; i += kActThreads) {
+        for (int i = threadIdx.x; i < ntj * T::F * kPR; i += kActThreads) {
             const int pc = i % kPR, row = i / kPR;
             const int f = row % T::F, tj = row / T::F;
             const uint8_t* s = reinterpret_cast<const uint8_t*>(s_v + row * CC) + pc * kPB;
@@ -361,10 +368,10 @@ const QuantParams* qparams_table(bool build) {
 namespace {
 
 template <int V, int MODE, int CC>
-cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits,
-                          QuantParams* qp, int8_t* vqA, unsigned long long* sat, int16_t* vkeep,
-                          cudaStream_t st, bool pdl) {
-    const size_t smem = act_smem_bytes<V, CC>(g.W, g.tw);
+cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int twc, int* vmax, const int* vmax_in, int bits,
+                          QuantParams* qp, int8_t* vqA, unsigned long long* sat, int16_t* vkeep, cudaStream_t st,
+                          bool pdl) {
+    const size_t smem = act_smem<V, CC>(g.W, twc).bytes;
     auto kern = k_act<V, MODE, CC>;
     static size_t attr_bytes = 0;  // per instantiation: raise the opt-in only when a layer needs more
     if (smem > attr_bytes) {
@@ -372,8 +379,10 @@ cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int* vmax, const i
         if (e != cudaSuccess) return e;
         attr_bytes = smem;
     }
+    const long gx = long(g.th) * ((g.tw + twc - 1) / twc);
+    if (gx > 0x7fffffffL || g.B > 65535 || (g.C + CC - 1) / CC > 65535) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g.th, g.B, (g.C + CC - 1) / CC);
+    cfg.gridDim = dim3(unsigned(gx), g.B, (g.C + CC - 1) / CC);
     cfg.blockDim = dim3(kActThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -382,35 +391,41 @@ cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int* vmax, const i
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, x, g, vmax, vmax_in, bits, qp, vqA, sat,
+    return cudaLaunchKernelEx(&cfg, kern, x, g, twc, vmax, vmax_in, bits, qp, vqA, sat,
                               MODE == 0 ? nullptr : qparams_table(false), vkeep);
 }
 
-// Channels per CTA: 32 gives full 32-byte vq row segments; shrink for two waves
-// over the 148 SMs and a <= 96 KB shared-memory footprint.
+// CTA shape: CC = 32 channels (64-byte kept-V rows, 32-byte vq rows) unless the layer has
+// fewer channels; tile columns per CTA (twc) halved until shared memory is <= 64 KB and the
+// grid has two waves over the 148 SMs; only then narrower channel chunks.
 template <int V>
-int pick_cc(const ConvGeom& g) {
-    auto ctas = [&](int c) { return long(g.th) * g.B * ((g.C + c - 1) / c); };
-    auto smem = [&](int c) {
-        return c == 32 ? act_smem_bytes<V, 32>(g.W, g.tw)
-             : c == 16 ? act_smem_bytes<V, 16>(g.W, g.tw)
-             : c == 8  ? act_smem_bytes<V, 8>(g.W, g.tw)
-                       : act_smem_bytes<V, 4>(g.W, g.tw);
+void pick_shape(const ConvGeom& g, int& cc, int& twc) {
+    cc = 32;
+    while (cc > 4 && cc / 2 >= g.C) cc /= 2;
+    twc = g.tw;
+    auto bytes = [&](int c, int t) {
+        return c == 32 ? act_smem<V, 32>(g.W, t).bytes
+             : c == 16 ? act_smem<V, 16>(g.W, t).bytes
+             : c == 8  ? act_smem<V, 8>(g.W, t).bytes
+                       : act_smem<V, 4>(g.W, t).bytes;
     };
-    int cc = 32;
-    while (cc > 4 && ctas(cc) < 2 * 148) cc /= 2;
-    while (cc > 4 && smem(cc) > 96 * 1024) cc /= 2;
-    return cc;
+    auto ctas = [&](int c, int t) { return long(g.th) * ((g.tw + t - 1) / t) * g.B * ((g.C + c - 1) / c); };
+    while (twc > 1 && bytes(cc, twc) > 64 * 1024) twc = (twc + 1) / 2;
+    while (twc > 1 && ctas(cc, twc) < 2 * 148) twc = (twc + 1) / 2;
+    while (cc > 4 && ctas(cc, twc) < 2 * 148) cc /= 2;
+    while (cc > 4 && bytes(cc, twc) > 96 * 1024) cc /= 2;
 }
 
 template <int V, int MODE>
 cudaError_t act_launch(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits, QuantParams* qp,
                        int8_t* vqA, unsigned long long* sat, int16_t* vkeep, cudaStream_t st, bool pdl) {
-    switch (pick_cc<V>(g)) {
-        case 32: return act_launch_cc<V, MODE, 32>(x, g, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
-        case 16: return act_launch_cc<V, MODE, 16>(x, g, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
-        case 8: return act_launch_cc<V, MODE, 8>(x, g, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
-        default: return act_launch_cc<V, MODE, 4>(x, g, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
+    int cc, twc;
+    pick_shape<V>(g, cc, twc);
+    switch (cc) {
+        case 32: return act_launch_cc<V, MODE, 32>(x, g, twc, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
+        case 16: return act_launch_cc<V, MODE, 16>(x, g, twc, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
+        case 8: return act_launch_cc<V, MODE, 8>(x, g, twc, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
+        default: return act_launch_cc<V, MODE, 4>(x, g, twc, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
     }
 }
 
