@@ -93,9 +93,9 @@ def _check(lib, rc, which):
 # ----------------------------------------------------------------------------- specs
 def spec(name: str, source: str = "oracle") -> dict:
     dims = np.zeros(10, np.int64)
-    bt = np.zeros(12 * 9, np.int64)
-    g = np.zeros(12 * 3, np.int64)
-    a = np.zeros(12 * 7, np.int64)
+    bt = np.zeros(16 * 16, np.int64)  # room for every catalogued SFC size (K <= 14, n <= 10, R <= 7)
+    g = np.zeros(16 * 8, np.int64)
+    a = np.zeros(16 * 8, np.int64)
     if source == "oracle":
         lib = oracle_lib()
         _check(lib, lib.sfo_spec(name.encode(), _ptr(dims, _i64p), _ptr(bt, _i64p), _ptr(g, _i64p),
@@ -131,16 +131,18 @@ def scale_mse_grid(vals, bits):
 def quantized_conv(x: np.ndarray, w: np.ndarray, spec_name: str, pad: int = 1, bits: int = 8,
                    act_scope: int = 0, filter_scope: int = 0, search: int = 0, threads: int | None = None,
                    want=("out", "y_int"), report: bool = False, vmax_override: int = -1) -> dict:
-    """Run the C restatement.  x: int8 [B,C,H,W], w: int8 [OC,C,3,3]."""
+    """Run the C restatement.  x: int8 [B,C,H,W], w: int8 [OC,C,R,R]."""
     lib = oracle_lib()
     x = np.ascontiguousarray(x, np.int8)
     w = np.ascontiguousarray(w, np.int8)
     B, C, H, W = x.shape
     OC = w.shape[0]
     sp = spec(spec_name)
-    K, M = sp["K"], sp["M"]
+    K, M, R = sp["K"], sp["M"], sp["R"]
     F = K * K
-    HO, WO = H + 2 * pad - 2, W + 2 * pad - 2
+    if w.shape[1:] != (C, R, R):
+        raise ValueError("filter shape does not match algorithm")
+    HO, WO = H + 2 * pad - R + 1, W + 2 * pad - R + 1
     th, tw = -(-HO // M), -(-WO // M)
     T = B * th * tw
     res = {}

@@ -24,6 +24,13 @@ const char* sfo_last_error(void) { return g_err; }
 /* integer numerators; every denominator is 1.  Pinned against the reference */
 /* export in tests/golden/catalog_3x3.json.                                  */
 /* ------------------------------------------------------------------------ */
+/* buffer bounds over every catalogued SFC size */
+#define SFO_KMAX 14
+#define SFO_NMAX 10
+#define SFO_MMAX 7
+#define SFO_RMAX 7
+#define SFO_FMAX (SFO_KMAX * SFO_KMAX)
+
 typedef struct {
     const char* name;
     int K, n, M, R, N, offset, a_denom, ncorr, triples;
@@ -66,14 +73,110 @@ static const signed char G4x4[7 * 3] = {1, 1, 1, 1, -1, 1, 1, -1, -1, 1, 0, -1,
 static const signed char A4x4[7 * 4] = {1, 1, 1, 1,   1, -1, 1, -1, 0, 2, 0, -2, 2, -2, -2, 2,
                                         -2, -2, 2, 2, 4, 0, 0, 0,   0, 0, 0, 4};
 
-static const spec_t SPECS[3] = {
+/* The 5x5 / 7x7 SFC specs (catalog.cpp:249-250), dumped from the compiled reference
+ * (oracle/_ref: derive_correction_spec(6, 6, 5) and (6, 4, 7)) and pinned against it in
+ * tests/test_oracle.py. */
+static const signed char BT6x6r5[140] = {
+    0, 0, 1, 1, 1, 1, 1, 1, 0, 0,
+    0, 0, 1, 1, 0, -1, -1, 0, 0, 0,
+    0, 0, 0, -1, -1, 0, 1, 1, 0, 0,
+    0, 0, 1, 0, -1, -1, 0, 1, 0, 0,
+    0, 0, 1, 0, -1, 1, 0, -1, 0, 0,
+    0, 0, 0, -1, 1, 0, -1, 1, 0, 0,
+    0, 0, 1, -1, 0, 1, -1, 0, 0, 0,
+    0, 0, 1, -1, 1, -1, 1, -1, 0, 0,
+    1, 0, 0, 0, 0, 0, -1, 0, 0, 0,
+    0, 1, 0, 0, 0, 0, 0, -1, 0, 0,
+    0, 1, 0, 0, 0, 0, 0, -1, 0, 0,
+    0, 0, -1, 0, 0, 0, 0, 0, 1, 0,
+    0, 0, -1, 0, 0, 0, 0, 0, 1, 0,
+    0, 0, 0, -1, 0, 0, 0, 0, 0, 1};
+static const signed char G6x6r5[70] = {
+    1, 1, 1, 1, 1,
+    0, 1, 1, 0, -1,
+    -1, -1, 0, 1, 1,
+    -1, 0, 1, 1, 0,
+    -1, 0, 1, -1, 0,
+    1, -1, 0, 1, -1,
+    0, -1, 1, 0, -1,
+    1, -1, 1, -1, 1,
+    1, 0, 0, 0, 0,
+    1, 0, 0, 0, 0,
+    0, 1, 0, 0, 0,
+    0, 0, 0, 1, 0,
+    0, 0, 0, 0, 1,
+    0, 0, 0, 0, 1};
+static const signed char A6x6r5[84] = {
+    1, 1, 1, 1, 1, 1,
+    1, 2, 1, -1, -2, -1,
+    -2, -1, 1, 2, 1, -1,
+    1, -1, -2, -1, 1, 2,
+    1, 1, -2, 1, 1, -2,
+    -2, 1, 1, -2, 1, 1,
+    1, -2, 1, 1, -2, 1,
+    1, -1, 1, -1, 1, -1,
+    6, 0, 0, 0, 0, 0,
+    0, 6, 0, 0, 0, 0,
+    6, 0, 0, 0, 0, 0,
+    0, 0, 0, 0, 0, 6,
+    0, 0, 0, 0, 6, 0,
+    0, 0, 0, 0, 0, 6};
+static const signed char BT4x4r7[140] = {
+    0, 0, 1, 1, 1, 1, 1, 1, 0, 0,
+    0, 0, 1, 1, 0, -1, -1, 0, 0, 0,
+    0, 0, 0, -1, -1, 0, 1, 1, 0, 0,
+    0, 0, 1, 0, -1, -1, 0, 1, 0, 0,
+    0, 0, 1, 0, -1, 1, 0, -1, 0, 0,
+    0, 0, 0, -1, 1, 0, -1, 1, 0, 0,
+    0, 0, 1, -1, 0, 1, -1, 0, 0, 0,
+    0, 0, 1, -1, 1, -1, 1, -1, 0, 0,
+    1, 0, 0, 0, 0, 0, -1, 0, 0, 0,
+    0, 1, 0, 0, 0, 0, 0, -1, 0, 0,
+    0, 1, 0, 0, 0, 0, 0, -1, 0, 0,
+    0, 0, -1, 0, 0, 0, 0, 0, 1, 0,
+    0, 0, -1, 0, 0, 0, 0, 0, 1, 0,
+    0, 0, 0, -1, 0, 0, 0, 0, 0, 1};
+static const signed char G4x4r7[98] = {
+    1, 1, 1, 1, 1, 1, 1,
+    0, 1, 1, 0, -1, -1, 0,
+    -1, -1, 0, 1, 1, 0, -1,
+    -1, 0, 1, 1, 0, -1, -1,
+    -1, 0, 1, -1, 0, 1, -1,
+    1, -1, 0, 1, -1, 0, 1,
+    0, -1, 1, 0, -1, 1, 0,
+    1, -1, 1, -1, 1, -1, 1,
+    1, 0, 0, 0, 0, 0, 0,
+    1, 0, 0, 0, 0, 0, 0,
+    0, 1, 0, 0, 0, 0, 0,
+    0, 0, 0, 0, 0, 1, 0,
+    0, 0, 0, 0, 0, 0, 1,
+    0, 0, 0, 0, 0, 0, 1};
+static const signed char A4x4r7[56] = {
+    1, 1, 1, 1,
+    1, 2, 1, -1,
+    -2, -1, 1, 2,
+    1, -1, -2, -1,
+    1, 1, -2, 1,
+    -2, 1, 1, -2,
+    1, -2, 1, 1,
+    1, -1, 1, -1,
+    6, 0, 0, 0,
+    0, 6, 0, 0,
+    6, 0, 0, 0,
+    0, 0, 0, 6,
+    0, 0, 6, 0,
+    0, 0, 0, 6};
+
+static const spec_t SPECS[5] = {
     {"sfc4-4x4-3x3", 7, 6, 4, 3, 4, 1, 4, 2, 1, BT4x4, G4x4, A4x4},
     {"sfc6-6x6-3x3", 10, 8, 6, 3, 6, 1, 6, 2, 2, BT6x6, G6x6, A6x6},
     {"sfc6-7x7-3x3", 12, 9, 7, 3, 6, 1, 6, 4, 2, BT7x7, G6, A7x7},
+    {"sfc6-6x6-5x5", 14, 10, 6, 5, 6, 2, 6, 6, 2, BT6x6r5, G6x6r5, A6x6r5},
+    {"sfc6-4x4-7x7", 14, 10, 4, 7, 6, 2, 6, 6, 2, BT4x4r7, G4x4r7, A4x4r7},
 };
 
 static const spec_t* find_spec(const char* name) {
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 5; ++i)
         if (strcmp(SPECS[i].name, name) == 0) return &SPECS[i];
     snprintf(g_err, sizeof g_err, "unknown algorithm: %s", name);
     return NULL;
@@ -165,7 +268,7 @@ static double pick_scale(const double* v, int64_t n, int bits, int search) {
 /* ------------------------------------------------------------------------ */
 typedef struct {
     const spec_t* s;
-    double bt[12 * 9], gm[12 * 3], a[12 * 7]; /* a already divided by a_denom */
+    double bt[SFO_KMAX * SFO_NMAX], gm[SFO_KMAX * SFO_RMAX], a[SFO_KMAX * SFO_MMAX]; /* a already divided by a_denom */
     int B, C, H, W, OC, pad, HO, WO, th, tw, K, F;
     const int8_t* x;
     const int8_t* w;
@@ -173,7 +276,7 @@ typedef struct {
 
 static void tile_transform(const plan_t* p, int b, int ti, int tj, int c, double* V) {
     const int n = p->s->n, K = p->K, M = p->s->M;
-    double window[81], tmp[12 * 9];
+    double window[SFO_NMAX * SFO_NMAX], tmp[SFO_KMAX * SFO_NMAX];
     const int ih0 = ti * M - p->pad, iw0 = tj * M - p->pad;
     for (int r = 0; r < n; ++r) {
         const int ih = ih0 + r;
@@ -201,7 +304,7 @@ static void tile_transform(const plan_t* p, int b, int ti, int tj, int c, double
 /* transform_filters (conv.cpp:352-382) for one (oc, ic). */
 static void filter_transform(const plan_t* p, int oc, int ic, double* U) {
     const int R = p->s->R, K = p->K;
-    double tmp[12 * 3];
+    double tmp[SFO_KMAX * SFO_RMAX];
     const int8_t* f = p->w + ((size_t)oc * p->C + ic) * R * R;
     for (int i = 0; i < K; ++i)
         for (int j = 0; j < R; ++j) {
@@ -241,7 +344,7 @@ typedef struct {
 static void* pass_absmax(void* arg) {
     work_t* wk = (work_t*)arg;
     const plan_t* p = wk->p;
-    double V[144];
+    double V[SFO_FMAX];
     for (int64_t t = wk->t0; t < wk->t1; ++t) {
         const int b = (int)(t / ((int64_t)p->th * p->tw));
         const int rem = (int)(t % ((int64_t)p->th * p->tw));
@@ -264,8 +367,8 @@ static void* pass_main(void* arg) {
     const int K = p->K, F = p->F, M = p->s->M, C = p->C;
     const int per_tensor = cfg->act_scope == SFO_ACT_PER_TENSOR;
     int64_t* vq = (int64_t*)malloc(sizeof(int64_t) * (size_t)C * F);
-    int64_t pacc[144];
-    double pd[144], q[7 * 12], V[144];
+    int64_t pacc[SFO_FMAX];
+    double pd[SFO_FMAX], q[SFO_MMAX * SFO_KMAX], V[SFO_FMAX];
     const signed char* A = p->s->a;
     for (int64_t t = wk->t0; t < wk->t1; ++t) {
         const int b = (int)(t / ((int64_t)p->th * p->tw));
@@ -422,7 +525,7 @@ int sfo_quantized_conv(const int8_t* x, int B, int C, int H, int W, const int8_t
     int64_t saturations = 0;
 
     /* --- activation scales (quant.cpp:168-181) --- */
-    double act_scale[144];
+    double act_scale[SFO_FMAX];
     const int n_act = cfg->act_scope == SFO_ACT_PER_TENSOR ? 1 : F;
     double* gall = NULL;
     int64_t vmax = 0;
@@ -436,7 +539,7 @@ int sfo_quantized_conv(const int8_t* x, int B, int C, int H, int W, const int8_t
             wk[i].absmax = am + (size_t)i * F;
         }
         run_threads(pass_absmax, wk, nthreads);
-        double fmaxv[144];
+        double fmaxv[SFO_FMAX];
         for (int f = 0; f < F; ++f) {
             fmaxv[f] = 0.0;
             for (int i = 0; i < nthreads; ++i)
@@ -590,7 +693,7 @@ int sfo_execute_tile(const char* spec, const int64_t* x, const int64_t* f, int64
     const spec_t* s = find_spec(spec);
     if (!s) return -1;
     const int K = s->K, n = s->n, R = s->R, M = s->M;
-    int64_t tmp[12 * 9], V[144], tf[12 * 3], U[144], ta[7 * 12];
+    int64_t tmp[SFO_KMAX * SFO_NMAX], V[SFO_FMAX], tf[SFO_KMAX * SFO_RMAX], U[SFO_FMAX], ta[SFO_MMAX * SFO_KMAX];
     for (int i = 0; i < K; ++i)
         for (int j = 0; j < n; ++j) {
             int64_t acc = 0;

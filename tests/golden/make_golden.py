@@ -22,6 +22,16 @@ sys.path.insert(0, ROOT)
 from oracle import bindings as ob  # noqa: E402
 
 VARIANTS = ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]
+LARGE_R = ["sfc6-6x6-5x5", "sfc6-4x4-7x7"]  # catalog.cpp:249-250
+
+# (tag, B, C, OC, H, W, pad, lo, bits) for the 5x5 / 7x7 variants (their own RNG and file)
+LARGE_CASES = [
+    ("small_p2", 1, 6, 5, 15, 15, 2, -128, 8),
+    ("ragged_p3", 2, 3, 4, 13, 11, 3, -128, 8),
+    ("relu_p1", 1, 9, 3, 12, 12, 1, 0, 8),
+    ("bits4_p0", 1, 4, 3, 14, 14, 0, -128, 4),
+    ("tiny", 1, 2, 2, 7, 7, 3, -128, 8),
+]
 
 # (tag, B, C, OC, H, W, pad, lo, bits, act_scope, filter_scope, search)
 CASES = [
@@ -41,7 +51,53 @@ CASES = [
 ]
 
 
+def exact_texts(js, names):
+    """The exact substring of the reference's catalog export for each algorithm."""
+    full = json.loads(js)
+    sel = [a for a in full["algorithms"] if a["name"] in names]
+    exact = {}
+    for a in sel:
+        tail = js[js.index('{"name":"' + a["name"]):]
+        depth = 0
+        for i, ch in enumerate(tail):
+            depth += ch == "{"
+            depth -= ch == "}"
+            if depth == 0:
+                exact[a["name"]] = tail[: i + 1]
+                break
+    return sel, exact
+
+
+def large_r():
+    """tests/golden/catalog_large_r.json + qconv_large_r.npz for the 5x5 / 7x7 variants."""
+    js, h = ob.ref_catalog_json()
+    sel, exact = exact_texts(js, LARGE_R)
+    with open(os.path.join(HERE, "catalog_large_r.json"), "w") as f:
+        json.dump({"full_catalog_fnv1a64": f"{h:016x}", "algorithms": sel, "exact_text": exact}, f, indent=1)
+    arrays = {}
+    rng = np.random.default_rng(0x5FC1)
+    for tag, B, C, OC, H, W, pad, lo, bits in LARGE_CASES:
+        x = rng.integers(lo, 128, size=(B, C, H, W), dtype=np.int8)
+        arrays[f"{tag}/x"] = x
+        arrays[f"{tag}/meta"] = np.array([pad, bits], np.int64)
+        for v in LARGE_R:
+            R = ob.spec(v, source="ref")["R"]
+            w = rng.integers(-127, 128, size=(OC, C, R, R), dtype=np.int8)
+            arrays[f"{tag}/{v}/w"] = w
+            arrays[f"{tag}/{v}/direct"] = ob.ref_direct_conv2d(x, w, pad)
+            out, rep = ob.ref_quantized_fast_conv2d(x, w, v, pad, bits)
+            arrays[f"{tag}/{v}/out"] = out
+            arrays[f"{tag}/{v}/report"] = np.array([rep["mse"], rep["signal_energy"], rep["snr_db"],
+                                                    rep["saturations"], rep["values_quantized"]], np.float64)
+            if tag == "small_p2":
+                arrays[f"{tag}/{v}/u"] = ob.ref_transform_filters(w, v)
+    np.savez_compressed(os.path.join(HERE, "qconv_large_r.npz"), **arrays)
+    print("wrote", len(arrays), "large-R arrays")
+
+
 def main():
+    if "--large-r" in sys.argv:
+        return large_r()
     if not ob.ref_available():
         raise SystemExit("oracle/_ref/libsfconv_ref.so missing: run `make -C oracle` with /root/reference present")
     js, h = ob.ref_catalog_json()

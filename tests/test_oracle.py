@@ -177,3 +177,65 @@ def test_frequency_energy_reference_dc():
     # test_quant.cpp:97-107: constant input, padding 0 -> DC energy 36^2, every other bin 0
     e = ob.ref_frequency_energy(np.ones((1, 1, 14, 14)), "sfc6-6x6-3x3", 0)
     assert e[0] == 1296.0 and np.all(e[1:] == 0.0)
+
+
+# ------------------------------------------------------------------------------ 5x5 / 7x7 variants
+LARGE_R = ["sfc6-6x6-5x5", "sfc6-4x4-7x7"]  # catalog.cpp:249-250
+GOLD_R = np.load(os.path.join(HERE, "golden", "qconv_large_r.npz"))
+TAGS_R = sorted({k.split("/")[0] for k in GOLD_R.files})
+
+
+@pytest.mark.parametrize("name", LARGE_R)
+def test_oracle_large_r_spec_matches_reference_export(name):
+    cat = json.load(open(os.path.join(HERE, "golden", "catalog_large_r.json")))
+    ref = next(a for a in cat["algorithms"] if a["name"] == name)
+    s = ob.spec(name)
+    assert s["N"] == ref["N"] and s["M"] == ref["tile"] and s["R"] == ref["kernel"]
+    assert s["offset"] == ref["offset"] and s["a_denom"] == ref["denominator"]
+    assert s["mults_full"] == ref["mults_full"] and s["mults_reduced"] == ref["mults_reduced"]
+    for key in ("BT", "G", "A"):
+        assert np.array_equal(s[key], np.array(ref[key], dtype=np.int64)), key
+    assert s["n_corrections"] == len(ref["corrections"])
+    assert ob.check_identity(name) == 0
+
+
+@pytest.mark.parametrize("name", LARGE_R)
+def test_oracle_large_r_execute_tile(name):
+    s = ob.spec(name)
+    rng = np.random.default_rng(78)
+    n, R, M = s["n"], s["R"], s["M"]
+    for trial in range(20):
+        hi = 2000 if trial % 2 else 8
+        x = rng.integers(-hi, hi + 1, size=(n, n))
+        f = rng.integers(-hi, hi + 1, size=(R, R))
+        want = np.array([[np.sum(x[i:i + R, j:j + R] * f) for j in range(M)] for i in range(M)])
+        assert np.array_equal(ob.execute_tile(name, x, f), want)
+
+
+@pytest.mark.parametrize("variant", LARGE_R)
+@pytest.mark.parametrize("tag", TAGS_R)
+def test_oracle_large_r_matches_reference_golden(tag, variant):
+    x, (pad, bits) = GOLD_R[f"{tag}/x"], GOLD_R[f"{tag}/meta"]
+    w = GOLD_R[f"{tag}/{variant}/w"]
+    r = ob.quantized_conv(x, w, variant, int(pad), int(bits), want=("out",), report=True)
+    assert bits_equal(r["out"], GOLD_R[f"{tag}/{variant}/out"])
+    rep = GOLD_R[f"{tag}/{variant}/report"]
+    assert r["report"]["saturations"] == rep[3] and r["report"]["values_quantized"] == rep[4]
+    assert np.array_equal(ob.direct_conv(x, w, int(pad)), GOLD_R[f"{tag}/{variant}/direct"])
+
+
+@needs_ref
+@pytest.mark.parametrize("variant", LARGE_R)
+@pytest.mark.parametrize("seed", [4, 5])
+def test_oracle_large_r_bitwise_vs_live_reference(variant, seed):
+    rng = np.random.default_rng(seed)
+    R = ob.spec(variant)["R"]
+    B, C, OC = 1, int(rng.integers(1, 6)), int(rng.integers(1, 5))
+    H, W = int(rng.integers(R, 18)), int(rng.integers(R, 18))
+    pad = int(rng.integers(0, R))
+    x = rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(OC, C, R, R), dtype=np.int8)
+    out, rep = ob.ref_quantized_fast_conv2d(x, w, variant, pad, 8)
+    r = ob.quantized_conv(x, w, variant, pad, 8, want=("out",), report=True)
+    assert bits_equal(r["out"], out)
+    assert r["report"]["values_quantized"] == rep["values_quantized"]
