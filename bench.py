@@ -248,7 +248,7 @@ def run_b200(args, rank, world, local_rank):
         x_host = torch.from_numpy(np.ascontiguousarray(xg[rank * L.batch:(rank + 1) * L.batch])).pin_memory()
         x = x_host.to(dev)
         w = torch.from_numpy(wl.weights(work.config, i, L)).to(dev)
-        ho = L.hw + 2 * L.pad - 2
+        ho = L.hw + 2 * L.pad - L.r + 1
         for v in work.variants:
             layer = sc.SfcLayer(v, w)
             ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)

@@ -436,7 +436,9 @@ cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, i
     switch (variant) {
         case 0: return act_launch<0, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, vkeep, st, pdl);
         case 1: return act_launch<1, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, vkeep, st, pdl);
-        default: return act_launch<2, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, vkeep, st, pdl);
+        case 2: return act_launch<2, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, vkeep, st, pdl);
+        case 3: return act_launch<3, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, vkeep, st, pdl);
+        default: return act_launch<4, 0>(x, g, vmax, nullptr, 8, nullptr, nullptr, nullptr, vkeep, st, pdl);
     }
 }
 
@@ -445,7 +447,9 @@ cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, co
     switch (variant) {
         case 0: return act_launch<0, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
         case 1: return act_launch<1, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
-        default: return act_launch<2, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
+        case 2: return act_launch<2, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
+        case 3: return act_launch<3, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
+        default: return act_launch<4, 1>(x, g, nullptr, vmax, bits, qp, vqA, sat, nullptr, st, pdl);
     }
 }
 

@@ -1,5 +1,5 @@
 // Offline filter stage and the report / API kernels.
-//   k_filter_prepare     U = G f G^T, per-oc minmax scale, exact RNE quantize into the
+//   k_filter_prepare     U = G f G^T (R x R filters), per-oc minmax scale, exact RNE quantize into the
 //                        GEMM B operand uq[f][oc][ic]   (conv.cpp:352-382, quant.cpp:183-229)
 //   k_direct_conv        exact int8 correlation (int32)  (conv.cpp:320-350, quant.cpp:282)
 //   k_freq_energy        sum of V^2 per frequency, exact (quant.cpp:136-150)
@@ -12,35 +12,37 @@
 
 namespace sfcb200 {
 
-// Row k of U = G f G^T for one 3x3 filter: U[k][l] = sum_j (sum_r G[k][r] f[r][j]) G[l][j].
+// Row k of U = G f G^T for one R x R filter: U[k][l] = sum_j (sum_r G[k][r] f[r][j]) G[l][j].
 template <int V, class Fn>
-__device__ __forceinline__ void filter_rows(const int (&f)[3][3], Fn&& fn) {
+__device__ __forceinline__ void filter_rows(const int (&f)[Tab<V>::R][Tab<V>::R], Fn&& fn) {
     using T = Tab<V>;
+    constexpr int R = T::R;
 #pragma unroll
     for (int k = 0; k < T::K; ++k) {
-        int tmp[3];
+        int tmp[R];
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
+        for (int j = 0; j < R; ++j) {
             int acc = 0;
 #pragma unroll
-            for (int r = 0; r < 3; ++r) acc += T::g(k, r) * f[r][j];
+            for (int r = 0; r < R; ++r) acc += T::g(k, r) * f[r][j];
             tmp[j] = acc;
         }
 #pragma unroll
         for (int l = 0; l < T::K; ++l) {
             int acc = 0;
 #pragma unroll
-            for (int j = 0; j < 3; ++j) acc += tmp[j] * T::g(l, j);
+            for (int j = 0; j < R; ++j) acc += tmp[j] * T::g(l, j);
             fn(k, l, acc);
         }
     }
 }
 
-__device__ __forceinline__ void load_filter(const int8_t* __restrict__ w, size_t base, int (&f)[3][3]) {
+template <int R>
+__device__ __forceinline__ void load_filter(const int8_t* __restrict__ w, size_t base, int (&f)[R][R]) {
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) f[r][c] = w[base + r * 3 + c];
+        for (int c = 0; c < R; ++c) f[r][c] = w[base + r * R + c];
 }
 
 template <int V>
@@ -54,8 +56,8 @@ __global__ void __launch_bounds__(128) k_filter_prepare(const int8_t* __restrict
     __shared__ int s_max[4];
     int local = 0;
     for (int ic = threadIdx.x; ic < IC; ic += blockDim.x) {
-        int f[3][3];
-        load_filter(w, (size_t(oc) * IC + ic) * 9, f);
+        int f[T::R][T::R];
+        load_filter<T::R>(w, (size_t(oc) * IC + ic) * T::R * T::R, f);
         filter_rows<V>(f, [&](int, int, int u) { local = max(local, abs(u)); });
     }
 #pragma unroll
@@ -69,8 +71,8 @@ __global__ void __launch_bounds__(128) k_filter_prepare(const int8_t* __restrict
         if (umax_out) umax_out[oc] = umax;
     }
     for (int ic = threadIdx.x; ic < IC; ic += blockDim.x) {
-        int f[3][3];
-        load_filter(w, (size_t(oc) * IC + ic) * 9, f);
+        int f[T::R][T::R];
+        load_filter<T::R>(w, (size_t(oc) * IC + ic) * T::R * T::R, f);
         filter_rows<V>(f, [&](int k, int l, int u) {
             const int q = clamp_q(exact_q(u, sf), qmax, sat);
             uqB[(size_t(k * T::K + l) * OCpad + oc) * Cpad + ic] = int8_t(q);
@@ -154,8 +156,8 @@ __global__ void __launch_bounds__(128) k_transform_filters(const int8_t* __restr
     using T = Tab<V>;
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (long long)OC * IC) return;
-    int f[3][3];
-    load_filter(w, size_t(idx) * 9, f);
+    int f[T::R][T::R];
+    load_filter<T::R>(w, size_t(idx) * T::R * T::R, f);
     filter_rows<V>(f, [&](int k, int l, int v) { u[idx * T::F + k * T::K + l] = v; });
 }
 
@@ -165,7 +167,9 @@ cudaError_t launch_filter_prepare(int variant, const int8_t* w, int OC, int IC, 
     switch (variant) {
         case 0: k_filter_prepare<0><<<OC, 128, 0, st>>>(w, OC, IC, Cpad, OCpad, bits, sf, umax, uqB, sat); break;
         case 1: k_filter_prepare<1><<<OC, 128, 0, st>>>(w, OC, IC, Cpad, OCpad, bits, sf, umax, uqB, sat); break;
-        default: k_filter_prepare<2><<<OC, 128, 0, st>>>(w, OC, IC, Cpad, OCpad, bits, sf, umax, uqB, sat); break;
+        case 2: k_filter_prepare<2><<<OC, 128, 0, st>>>(w, OC, IC, Cpad, OCpad, bits, sf, umax, uqB, sat); break;
+        case 3: k_filter_prepare<3><<<OC, 128, 0, st>>>(w, OC, IC, Cpad, OCpad, bits, sf, umax, uqB, sat); break;
+        default: k_filter_prepare<4><<<OC, 128, 0, st>>>(w, OC, IC, Cpad, OCpad, bits, sf, umax, uqB, sat); break;
     }
     return cudaGetLastError();
 }
@@ -186,7 +190,9 @@ cudaError_t launch_freq_energy(int variant, const int8_t* x, const ConvGeom& g, 
     switch (variant) {
         case 0: k_freq_energy<0><<<blocks, 256, 0, st>>>(x, g, sum); break;
         case 1: k_freq_energy<1><<<blocks, 256, 0, st>>>(x, g, sum); break;
-        default: k_freq_energy<2><<<blocks, 256, 0, st>>>(x, g, sum); break;
+        case 2: k_freq_energy<2><<<blocks, 256, 0, st>>>(x, g, sum); break;
+        case 3: k_freq_energy<3><<<blocks, 256, 0, st>>>(x, g, sum); break;
+        default: k_freq_energy<4><<<blocks, 256, 0, st>>>(x, g, sum); break;
     }
     return cudaGetLastError();
 }
@@ -197,17 +203,21 @@ cudaError_t launch_transform_filters(int variant, const int8_t* w, int OC, int I
     switch (variant) {
         case 0: k_transform_filters<0><<<blocks, 128, 0, st>>>(w, OC, IC, u); break;
         case 1: k_transform_filters<1><<<blocks, 128, 0, st>>>(w, OC, IC, u); break;
-        default: k_transform_filters<2><<<blocks, 128, 0, st>>>(w, OC, IC, u); break;
+        case 2: k_transform_filters<2><<<blocks, 128, 0, st>>>(w, OC, IC, u); break;
+        case 3: k_transform_filters<3><<<blocks, 128, 0, st>>>(w, OC, IC, u); break;
+        default: k_transform_filters<4><<<blocks, 128, 0, st>>>(w, OC, IC, u); break;
     }
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- geometry
 void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, int OC) {
-    const int M = variant == 0 ? Tab<0>::M : variant == 1 ? Tab<1>::M : Tab<2>::M;
+    static constexpr int kM[5] = {Tab<0>::M, Tab<1>::M, Tab<2>::M, Tab<3>::M, Tab<4>::M};
+    static constexpr int kR[5] = {Tab<0>::R, Tab<1>::R, Tab<2>::R, Tab<3>::R, Tab<4>::R};
+    const int M = kM[variant], R = kR[variant];
     g.B = B, g.C = C, g.H = H, g.W = W, g.pad = pad, g.OC = OC;
-    g.HO = H + 2 * pad - 2;
-    g.WO = W + 2 * pad - 2;
+    g.HO = H + 2 * pad - R + 1;
+    g.WO = W + 2 * pad - R + 1;
     g.th = (g.HO + M - 1) / M;
     g.tw = (g.WO + M - 1) / M;
     g.T = B * g.th * g.tw;

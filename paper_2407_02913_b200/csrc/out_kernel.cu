@@ -36,7 +36,8 @@ template <int V>
 __host__ __device__ constexpr int out_tb() {  // tile columns per block: ~40 KB of P per block
     return (40 * 1024) / (Tab<V>::F * kOcc * 4) < 1 ? 1 : (40 * 1024) / (Tab<V>::F * kOcc * 4);
 }
-static_assert(out_tb<0>() * Tab<0>::M <= 32 && out_tb<1>() * Tab<1>::M <= 32 && out_tb<2>() * Tab<2>::M <= 32,
+static_assert(out_tb<0>() * Tab<0>::M <= 32 && out_tb<1>() * Tab<1>::M <= 32 && out_tb<2>() * Tab<2>::M <= 32 &&
+                  out_tb<3>() * Tab<3>::M <= 32 && out_tb<4>() * Tab<4>::M <= 32,
               "a block's output row segment must fit the 32-entry magic table");
 
 struct OutSmem {
@@ -250,7 +251,9 @@ cudaError_t launch_output(int variant, bool y64, const int32_t* P, const ConvGeo
     switch (variant) {
         case 0: return out_by_width<0>(y64, P, g, qp, sf, o, st, pdl);
         case 1: return out_by_width<1>(y64, P, g, qp, sf, o, st, pdl);
-        default: return out_by_width<2>(y64, P, g, qp, sf, o, st, pdl);
+        case 2: return out_by_width<2>(y64, P, g, qp, sf, o, st, pdl);
+        case 3: return out_by_width<3>(y64, P, g, qp, sf, o, st, pdl);
+        default: return out_by_width<4>(y64, P, g, qp, sf, o, st, pdl);
     }
 }
 

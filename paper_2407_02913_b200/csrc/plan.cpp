@@ -254,7 +254,9 @@ long plan_identity_violations(const SfcPlan& p) {
 }
 
 const std::vector<std::string>& plan_names() {
-    static const std::vector<std::string> names = {"sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"};
+    // the SFC entries of the reference catalog, in its order (catalog.cpp:246-250)
+    static const std::vector<std::string> names = {"sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3", "sfc6-6x6-5x5",
+                                                   "sfc6-4x4-7x7"};
     return names;
 }
 
@@ -266,6 +268,8 @@ const SfcPlan& plan_for(const std::string& name) {
     if (name == "sfc4-4x4-3x3") p = derive(4, 4, 3), p.variant = 0;
     else if (name == "sfc6-6x6-3x3") p = derive(6, 6, 3), p.variant = 1;
     else if (name == "sfc6-7x7-3x3") p = derive(6, 7, 3), p.variant = 2;
+    else if (name == "sfc6-6x6-5x5") p = derive(6, 6, 5), p.variant = 3;
+    else if (name == "sfc6-4x4-7x7") p = derive(6, 4, 7), p.variant = 4;
     else throw std::invalid_argument("unknown algorithm: " + name);
     // Exhaustive exactness gate: the per-axis identity makes every integer
     // tile exact (stronger than the reference's 3 random trials, catalog.cpp:283).
@@ -274,7 +278,9 @@ const SfcPlan& plan_for(const std::string& name) {
                                 " identity violations");
     const bool same = p.variant == 0 ? matches_device_tables<0>(p)
                     : p.variant == 1 ? matches_device_tables<1>(p)
-                                     : matches_device_tables<2>(p);
+                    : p.variant == 2 ? matches_device_tables<2>(p)
+                    : p.variant == 3 ? matches_device_tables<3>(p)
+                                     : matches_device_tables<4>(p);
     if (!same) throw std::domain_error("derived plan differs from the compiled device tables for " + name);
     return cache().emplace(name, std::move(p)).first->second;
 }

@@ -1,4 +1,5 @@
-"""Seeded synthetic workloads for the five BASELINE.json configurations.
+"""Seeded synthetic workloads for the five BASELINE.json configurations (1-5) and the
+5x5 / 7x7 SFC variants at config 2's shape (6, 7, not BASELINE configs).
 
 No public dataset is involved: ImageNet is only cited by the
 paper for accuracy numbers.  Inputs are generated on the host with numpy's
@@ -32,6 +33,7 @@ class Layer:
     act_lo: int = 0          # activations uniform in [act_lo, 127]
     sigma: float = 1.0       # weight N(0, sigma) before per-oc int8 quantization
     pad: int = 1
+    r: int = 3               # filter size (R x R)
 
 
 @dataclass(frozen=True)
@@ -72,6 +74,12 @@ WORKLOADS = {
                 description="VGG-16 13 convs, batch 128, int8 requant"),
     5: Workload(5, "cfg5_n256_c512_14", (Layer("conv", 256, 512, 512, 14, act_lo=-128, sigma=0.5),),
                 description="N=256 512->512 14x14, x~U[-128,127], w~N(0,0.5)"),
+    6: Workload(6, "cfg6_n8_c128_28_r5", (Layer("conv", 8, 128, 128, 28, pad=2, r=5),),
+                variants=("sfc6-6x6-5x5",),
+                description="config 2's shape with 5x5 filters (pad 2), sfc6-6x6-5x5"),
+    7: Workload(7, "cfg7_n8_c128_28_r7", (Layer("conv", 8, 128, 128, 28, pad=3, r=7),),
+                variants=("sfc6-4x4-7x7",),
+                description="config 2's shape with 7x7 filters (pad 3), sfc6-4x4-7x7"),
 }
 
 
@@ -92,7 +100,7 @@ def quantize_weights_per_oc(w: np.ndarray) -> np.ndarray:
 
 def weights(cfg: int, layer_idx: int, layer: Layer) -> np.ndarray:
     rng = np.random.default_rng(BASE_SEED + 1000 * cfg + 2 * layer_idx + 1)
-    w = rng.normal(0.0, layer.sigma, size=(layer.cout, layer.cin, 3, 3))
+    w = rng.normal(0.0, layer.sigma, size=(layer.cout, layer.cin, layer.r, layer.r))
     return quantize_weights_per_oc(w)
 
 
@@ -102,14 +110,14 @@ def requant_scales(cfg: int, n_layers: int) -> np.ndarray:
 
 
 def direct_equivalent_ops(layer: Layer, batch: int | None = None) -> int:
-    """18 * N * Cout * Cin * HO * WO (2 ops per MAC of a direct 3x3 conv)."""
+    """2 R^2 * N * Cout * Cin * HO * WO (2 ops per MAC of a direct R x R conv; 18 for 3x3)."""
     b = layer.batch if batch is None else batch
-    ho = layer.hw + 2 * layer.pad - 2
-    return 18 * b * layer.cout * layer.cin * ho * ho
+    ho = layer.hw + 2 * layer.pad - layer.r + 1
+    return 2 * layer.r * layer.r * b * layer.cout * layer.cin * ho * ho
 
 
 def tile_grid(layer: Layer, m: int, batch: int | None = None):
     b = layer.batch if batch is None else batch
-    ho = layer.hw + 2 * layer.pad - 2
+    ho = layer.hw + 2 * layer.pad - layer.r + 1
     th = -(-ho // m)
     return b * th * th, th, ho

@@ -139,9 +139,11 @@ int main(int argc, char** argv) {
     if (argc > 1 && std::string(argv[1]) == "run") return run_mode(argc, argv);
     g_host_only = argc > 1 && std::string(argv[1]) == "--host-only";
 
-    run_case("catalog holds the 3x3 SFC algorithms (test_catalog.cpp:31-39)", [] {
+    run_case("catalog holds the SFC algorithms (test_catalog.cpp:31-39, catalog.cpp:246-250)", [] {
         const auto& n = catalog_names();
-        CHECK((n == std::vector<std::string>{"sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"}));
+        CHECK((n == std::vector<std::string>{"sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3", "sfc6-6x6-5x5",
+                                             "sfc6-4x4-7x7"}));
+        CHECK(catalog_algorithm("sfc6-6x6-5x5").R == 5 && catalog_algorithm("sfc6-4x4-7x7").R == 7);
         CHECK(throws<std::invalid_argument>([] { catalog_algorithm("wino-9x9-3x3"); }));
     }, false);
 

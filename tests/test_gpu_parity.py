@@ -35,7 +35,8 @@ def run_gpu(x, w, variant, pad=1, bits=8, outs=("y", "f32"), requant=0.0, vmax=N
     layer = sc.SfcLayer(variant, torch.from_numpy(w).to(dev), bits=bits)
     xt = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
     B, C, H, W = x.shape
-    HO, WO = H + 2 * pad - 2, W + 2 * pad - 2
+    R = w.shape[2]
+    HO, WO = H + 2 * pad - R + 1, W + 2 * pad - R + 1
     ws = layer.workspace(B, H, W, pad)
     res = {}
     kw = {}
@@ -303,7 +304,7 @@ def test_repeated_forwards_are_deterministic(cuda, variant):
     L = wl.WORKLOADS[2].layers[0]
     x = torch.from_numpy(wl.activations(2, 0, L)).cuda()
     w = torch.from_numpy(wl.weights(2, 0, L)).cuda()
-    ho = L.hw + 2 * L.pad - 2
+    ho = L.hw + 2 * L.pad - L.r + 1
     first = None
     for _ in range(10):
         layer = sc.SfcLayer(variant, w)
@@ -331,7 +332,7 @@ def test_kept_and_recompute_paths_agree(cuda, variant, monkeypatch):
         x = torch.from_numpy(wl.activations(cfg, li, L)).cuda()
         w = torch.from_numpy(wl.weights(cfg, li, L)).cuda()
         layer = sc.SfcLayer(variant, w)
-        ho = L.hw + 2 * L.pad - 2
+        ho = L.hw + 2 * L.pad - L.r + 1
         res = {}
         for mode in ("forward", "kept", "kept-qfused", "recompute"):
             ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
@@ -361,3 +362,48 @@ def test_kept_and_recompute_paths_agree(cuda, variant, monkeypatch):
             assert torch.equal(ref[1], r[1]), (cfg, mode, "P")
             assert ref[3] == r[3], (cfg, mode, "stats")
         assert torch.equal(ref[2], res["kept"][2]), (cfg, "vq")
+
+
+# ------------------------------------------------------------------------------ 5x5 / 7x7 variants
+LARGE_R = ["sfc6-6x6-5x5", "sfc6-4x4-7x7"]  # catalog.cpp:249-250
+GOLD_R = np.load(os.path.join(HERE, "golden", "qconv_large_r.npz"))
+TAGS_R = sorted({k.split("/")[0] for k in GOLD_R.files})
+CASES_R = [  # (B, C, OC, H, W, pad, lo)
+    (1, 8, 8, 16, 16, 2, -128),
+    (2, 5, 3, 13, 11, 3, -128),
+    (1, 70, 33, 12, 12, 1, 0),
+    (1, 3, 130, 9, 9, 0, -128),
+    (1, 2, 2, 7, 7, 3, -128),
+]
+
+
+@pytest.mark.parametrize("variant", LARGE_R)
+@pytest.mark.parametrize("case", CASES_R, ids=[f"b{c[0]}c{c[1]}o{c[2]}h{c[3]}w{c[4]}p{c[5]}" for c in CASES_R])
+def test_large_r_bit_exact(cuda, variant, case):
+    B, C, OC, H, W, pad, lo = case
+    R = ob.spec(variant)["R"]
+    rng = np.random.default_rng(hash(case) & 0xFFFF)
+    x = rng.integers(lo, 128, size=(B, C, H, W), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(OC, C, R, R), dtype=np.int8)
+    check_against_oracle(x, w, variant, pad)
+
+
+@pytest.mark.parametrize("variant", LARGE_R)
+@pytest.mark.parametrize("tag", TAGS_R)
+def test_large_r_golden_reference_outputs(cuda, tag, variant):
+    """fp32 output vs the reference's own quantized_fast_conv2d (fp64), max-normalised <= 1e-6."""
+    x, (pad, bits) = GOLD_R[f"{tag}/x"], GOLD_R[f"{tag}/meta"]
+    w = GOLD_R[f"{tag}/{variant}/w"]
+    g = run_gpu(x, w, variant, int(pad), int(bits), views=False)
+    assert maxrel(g["f32"], GOLD_R[f"{tag}/{variant}/out"]) <= TOL
+    assert g["stats"]["saturations"] + g["filter_sat"] == 0
+
+
+@pytest.mark.parametrize("variant", LARGE_R)
+def test_large_r_layer_size(cuda, variant):
+    """A 56x56, 64-channel, batch-4 layer against the oracle (y_int bit-exact, fp32 <= 1e-6)."""
+    R = ob.spec(variant)["R"]
+    rng = np.random.default_rng(91)
+    x = rng.integers(0, 128, size=(4, 64, 56, 56), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(64, 64, R, R), dtype=np.int8)
+    check_against_oracle(x, w, variant, R // 2, intermediates=False)

@@ -15,7 +15,8 @@ from paper_2407_02913_b200 import _lib
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CAT = json.load(open(os.path.join(HERE, "golden", "catalog_3x3.json")))
-VARIANTS = ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]
+CAT_R = json.load(open(os.path.join(HERE, "golden", "catalog_large_r.json")))
+VARIANTS = ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3", "sfc6-6x6-5x5", "sfc6-4x4-7x7"]
 
 
 def test_library_exports_every_declared_symbol():
@@ -34,9 +35,10 @@ def test_catalog_json_matches_reference_export_text():
     js, h = sfc.catalog_export_json()
     mine = json.loads(js)["algorithms"]
     assert [a["name"] for a in mine] == VARIANTS
+    exact = dict(CAT["exact_text"], **CAT_R["exact_text"])
     for a in mine:
         text = json.dumps(a, separators=(",", ":"))
-        assert text == CAT["exact_text"][a["name"]]      # byte-identical to the reference's export
+        assert text == exact[a["name"]]      # byte-identical to the reference's export
 
 
 def test_fnv_hash_of_export():

@@ -20,7 +20,7 @@ print(f"{work.name}: layer  variant        shape                 ms      TOPS   
 for i, L in enumerate(work.layers):
     x = torch.from_numpy(wl.activations(work.config, i, L)).cuda()
     w = torch.from_numpy(wl.weights(work.config, i, L)).cuda()
-    ho = L.hw + 2 * L.pad - 2
+    ho = L.hw + 2 * L.pad - L.r + 1
     for v in work.variants:
         layer = sc.SfcLayer(v, w)
         ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)

@@ -16,7 +16,7 @@ L = work.layers[a.layer]
 x = torch.from_numpy(wl.activations(a.workload, a.layer, L)).cuda()
 w = torch.from_numpy(wl.weights(a.workload, a.layer, L)).cuda()
 layer = sc.SfcLayer(a.variant, w)
-ho = L.hw + 2 * L.pad - 2
+ho = L.hw + 2 * L.pad - L.r + 1
 ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
 out = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.float32, device="cuda")
 kw = dict(y_int32=torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int32, device="cuda"), out_f32=out)

@@ -18,7 +18,7 @@ a = ap.parse_args()
 L = wl.WORKLOADS[a.workload].layers[a.layer]
 x = torch.from_numpy(wl.activations(a.workload, a.layer, L)).cuda()
 w = torch.from_numpy(wl.weights(a.workload, a.layer, L)).cuda()
-ho = L.hw + 2 * L.pad - 2
+ho = L.hw + 2 * L.pad - L.r + 1
 ref = None
 bad = 0
 for r in range(a.reps):

@@ -17,7 +17,7 @@ a = ap.parse_args()
 L = wl.WORKLOADS[a.workload].layers[0]
 x = torch.from_numpy(wl.activations(a.workload, 0, L)).cuda()
 w = torch.from_numpy(wl.weights(a.workload, 0, L)).cuda()
-ho = L.hw + 2 * L.pad - 2
+ho = L.hw + 2 * L.pad - L.r + 1
 layer = sc.SfcLayer(a.variant, w)
 ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
 y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int64, device="cuda")

@@ -22,9 +22,9 @@ x = torch.from_numpy(wl.activations(a.workload, a.layer, L)).cuda()
 w = torch.from_numpy(wl.weights(a.workload, a.layer, L)).cuda()
 lib = _lib.lib()
 buf = (ctypes.c_uint64 * 24)()
-ho = L.hw + 2 * L.pad - 2
+ho = L.hw + 2 * L.pad - L.r + 1
 NONE = 2**64 - 1
-for v in ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]:
+for v in wl.WORKLOADS[a.workload].variants:
     layer = sc.SfcLayer(v, w)
     ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
     out = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.float32, device="cuda")
