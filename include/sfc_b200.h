@@ -71,15 +71,26 @@ int sfc_plan_matrices(sfc_plan_t plan, int64_t* bt, int64_t* g, int64_t* a);
 /* ---- layer: offline filter stage of quantized_fast_conv2d
  *      (transform_filters src/conv.cpp:352-382 + filter scales/quantize src/quant.cpp:183-229) */
 
-/* Runs U = G f G^T, the per-output-channel minmax scale and exact RNE
+/* Runs U = G f G^T, the filter scales of `filter_scope` found by `search` and exact RNE
  * quantization on `stream` and keeps the quantized transformed filters on the
- * device.  Synchronous (returns once the layer is ready).  v1 scope: bits in
- * [2, 8], filter_scope PerChannel, search MinMax. */
+ * device.  Synchronous (returns once the layer is ready).  bits in [2, 8] (9-16:
+ * SFC_ERR_UNSUPPORTED); activation scope PerTensor. */
 int sfc_layer_create(sfc_plan_t plan, const int8_t* d_weights, int out_channels, int in_channels, int bits,
                      int filter_scope, int search, void* stream, sfc_layer_t* out);
+/* The whole QuantConfig (quant.hpp:27-34): act_scope SFC_ACT_*, filter_scope SFC_FIL_*,
+ * search SFC_SEARCH_*.  Anything but {PerTensor, PerChannel, MinMax} selects the parity
+ * path: per-frequency dequantisation before the inverse transform in fp64 (quant.cpp:258-278),
+ * scale searches in the reference's order; such layers run through sfc_conv_forward only
+ * and produce out_f32 / out_f64 / out_i8 (y_int is not defined for them). */
+int sfc_layer_create_ex(sfc_plan_t plan, const int8_t* d_weights, int out_channels, int in_channels, int bits,
+                        int act_scope, int filter_scope, int search, void* stream, sfc_layer_t* out);
 int sfc_layer_destroy(sfc_layer_t layer);
 /* Host copies of the filter scales sf[OC] (double) and per-oc max|U| (int32); synchronous. */
 int sfc_layer_filter_scales(sfc_layer_t layer, double* sf, int32_t* umax);
+/* The filter scales as the layer's scope defines them (quant.cpp:193-219): OC (PerChannel),
+ * K*K (PerFrequency) or OC*K*K (PerChannelFrequency) doubles; *count receives the number
+ * (pass scales = NULL to query it).  Synchronous. */
+int sfc_layer_filter_scales_native(sfc_layer_t layer, double* scales, int64_t* count);
 /* Filter-side saturation count (0 by construction for MinMax); synchronous. */
 int sfc_layer_saturations(sfc_layer_t layer, int64_t* count);
 /* Device view of the quantized transformed filters uq[f][oc][ic] with row pitch
@@ -144,6 +155,10 @@ int sfc_conv_forward(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, 
 /* Inspection of the last call's workspace (synchronous on `stream`):
  * stats[0..5] = {sa (as double bits), vmax, activation saturations, fast-quantizer-exact flag,
  *                values_quantized, tiles}. */
+/* Activation scales of the last call: 1 (PerTensor) or K*K (PerFrequency) doubles in *count;
+ * scales may be NULL to query the count.  Synchronous on `stream`. */
+int sfc_conv_act_scales(sfc_layer_t layer, int n, int h, int w, int pad, const void* d_workspace, double* scales,
+                        int64_t* count, void* stream);
 int sfc_conv_stats(sfc_layer_t layer, int n, int h, int w, int pad, const void* d_workspace, int64_t* stats,
                    void* stream);
 /* Device views into the workspace after sfc_conv_int8:

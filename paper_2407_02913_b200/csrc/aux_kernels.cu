@@ -231,7 +231,7 @@ void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, in
 
 size_t workspace_bytes(const ConvGeom& g, int F) {
     auto up = [](size_t v) { return (v + 255) / 256 * 256; };
-    return up(256) + up(size_t(F) * g.Tpad * g.Cpad) + up(size_t(F) * g.Tpad * g.OCpad * 4) +
+    return up(kWsHeader) + up(size_t(F) * g.Tpad * g.Cpad) + up(size_t(F) * g.Tpad * g.OCpad * 4) +
            up(size_t(F) * g.Tpad * g.Cpad * 2);  // kept int16 V
 }
 

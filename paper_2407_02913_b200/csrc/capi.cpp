@@ -30,6 +30,12 @@ struct sfc_layer {
     int* d_umax = nullptr;         // [OC]
     unsigned long long* d_sat = nullptr;
     int64_t max_a_col_l1 = 0;      // for the int32 output bound
+    // QuantConfig beyond PerTensor / PerChannel / MinMax (general_kernels.cu)
+    int act_scope = 0, filter_scope = 0, search = 0;
+    bool general = false;
+    double* d_fil = nullptr;       // [OC][F] filter scale per (oc, f)
+    double* d_fil_native = nullptr;  // scales as the scope defines them (OC, F or OC*F)
+    int n_fil_native = 0;
 };
 
 namespace {
@@ -82,6 +88,8 @@ struct WsView {
     int8_t* vq;
     int32_t* P;
     int16_t* vkeep;  // V kept by sfc_act_transform for the streaming quantizer
+    int* vmaxf;      // general QuantConfig: per-frequency maxima
+    double* act_scale;  // general QuantConfig: activation scales (1 or F)
 };
 WsView carve(void* ws, const ConvGeom& g, int F) {
     auto up = [](size_t v) { return (v + 255) / 256 * 256; };
@@ -90,8 +98,10 @@ WsView carve(void* ws, const ConvGeom& g, int F) {
     v.vmax = reinterpret_cast<int*>(base);
     v.sat = reinterpret_cast<unsigned long long*>(base + 8);
     v.qp = reinterpret_cast<QuantParams*>(base + 64);
-    v.vq = reinterpret_cast<int8_t*>(base + up(256));
-    v.P = reinterpret_cast<int32_t*>(base + up(256) + up(size_t(F) * g.Tpad * g.Cpad));
+    v.vmaxf = reinterpret_cast<int*>(base + 1024);
+    v.act_scale = reinterpret_cast<double*>(base + 2048);
+    v.vq = reinterpret_cast<int8_t*>(base + up(kWsHeader));
+    v.P = reinterpret_cast<int32_t*>(base + up(kWsHeader) + up(size_t(F) * g.Tpad * g.Cpad));
     v.vkeep = reinterpret_cast<int16_t*>(reinterpret_cast<uint8_t*>(v.P) + up(size_t(F) * g.Tpad * g.OCpad * 4));
     return v;
 }
@@ -131,6 +141,8 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
               size_t ws_bytes, const sfc_outputs* o, unsigned mask, bool chained, cudaStream_t st) {
     const bool kept = (mask & SFC_STAGE_KEPT) != 0;
     mask &= SFC_STAGE_ALL;
+    if (L && L->general)
+        throw Unsupported("layers with a non-default QuantConfig run through sfc_conv_forward only (single GPU)");
     check_call(L, kept ? ws : static_cast<const void*>(d_x), n, h, w, pad);
     if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
     const ConvGeom g = geom_of(L, n, h, w, pad);
@@ -173,7 +185,7 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     }
     if (mask & SFC_STAGE_OUTPUT) {
         const OutPtrs op{o->y_int32, o->y_int64, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
-        ck(launch_output(L->variant, need64, v.P, g, v.qp, L->d_sf, op, st, pdl), "output launch");
+        ck(launch_output(L->variant, need64 ? 1 : 0, v.P, g, v.qp, L->d_sf, op, st, pdl), "output launch");
     }
 }
 }  // namespace
@@ -230,15 +242,23 @@ int sfc_plan_matrices(sfc_plan_t plan, int64_t* bt, int64_t* g, int64_t* a) {
 
 int sfc_layer_create(sfc_plan_t plan, const int8_t* d_w, int oc, int ic, int bits, int filter_scope, int search,
                      void* stream, sfc_layer_t* out) {
+    return sfc_layer_create_ex(plan, d_w, oc, ic, bits, SFC_ACT_PER_TENSOR, filter_scope, search, stream, out);
+}
+
+int sfc_layer_create_ex(sfc_plan_t plan, const int8_t* d_w, int oc, int ic, int bits, int act_scope, int filter_scope,
+                        int search, void* stream, sfc_layer_t* out) {
     sfc_layer* L = nullptr;
     int rc = guarded([&] {
         if (!plan || !d_w || !out) throw std::invalid_argument("null argument");
         if (bits < 2 || bits > 16) throw std::invalid_argument("quantization width must be between 2 and 16 bits");
         if (oc <= 0 || ic <= 0) throw std::invalid_argument("bad filter shape");
         if (bits > 8) throw Unsupported("bits > 8 is not on the int8 tensor-core path yet");
-        if (filter_scope != SFC_FIL_PER_CHANNEL) throw Unsupported("only PerChannel filter scales on the device path");
-        if (search != SFC_SEARCH_MINMAX) throw Unsupported("only MinMax scale search on the device path");
+        if (act_scope < 0 || act_scope > 1 || filter_scope < 0 || filter_scope > 2 || search < 0 || search > 1)
+            throw std::invalid_argument("bad quantization config");
         L = new sfc_layer();
+        L->act_scope = act_scope, L->filter_scope = filter_scope, L->search = search;
+        L->general = !(act_scope == SFC_ACT_PER_TENSOR && filter_scope == SFC_FIL_PER_CHANNEL &&
+                       search == SFC_SEARCH_MINMAX);
         L->plan = plan->p;
         qparams_table(true);  // once per device; the kernels derive per CTA if this failed
         L->variant = plan->p->variant;
@@ -261,9 +281,33 @@ int sfc_layer_create(sfc_plan_t plan, const int8_t* d_w, int oc, int ic, int bit
         ck(cudaMalloc(&L->d_sat, sizeof(unsigned long long)), "cudaMalloc sat");
         ck(cudaMemsetAsync(L->d_uq, 0, uq_bytes, S(stream)), "memset uq");
         ck(cudaMemsetAsync(L->d_sat, 0, sizeof(unsigned long long), S(stream)), "memset sat");
-        ck(launch_filter_prepare(L->variant, d_w, oc, ic, L->Cpad, L->OCpad, bits, L->d_sf, L->d_umax, L->d_uq,
-                                 L->d_sat, S(stream)),
-           "filter prepare launch");
+        if (!L->general) {
+            ck(launch_filter_prepare(L->variant, d_w, oc, ic, L->Cpad, L->OCpad, bits, L->d_sf, L->d_umax, L->d_uq,
+                                     L->d_sat, S(stream)),
+               "filter prepare launch");
+        } else {
+            // U exactly, per-group scales in the reference's order, quantize (quant.cpp:183-229)
+            const int F = L->F;
+            L->n_fil_native = filter_scope == SFC_FIL_PER_CHANNEL ? oc : (filter_scope == SFC_FIL_PER_FREQUENCY ? F : oc * F);
+            ck(cudaMalloc(&L->d_fil, sizeof(double) * size_t(oc) * F), "cudaMalloc fil");
+            ck(cudaMalloc(&L->d_fil_native, sizeof(double) * L->n_fil_native), "cudaMalloc fil native");
+            int32_t* U = nullptr;
+            double* err = nullptr;
+            ck(cudaMallocAsync(&U, sizeof(int32_t) * size_t(oc) * ic * F, S(stream)), "alloc U");
+            ck(cudaMallocAsync(&err, sizeof(double) * size_t(L->n_fil_native) * 101, S(stream)), "alloc err");
+            ck(launch_transform_filters(L->variant, d_w, oc, ic, U, S(stream)), "transform filters launch");
+            ck(launch_fil_general(U, oc, ic, F, filter_scope, search == SFC_SEARCH_MSE_GRID, bits, L->Cpad, L->OCpad,
+                                  L->d_fil_native, err, L->d_uq, L->d_fil, L->d_sat, S(stream)),
+               "general filter launch");
+            ck(cudaFreeAsync(U, S(stream)), "free U");
+            ck(cudaFreeAsync(err, S(stream)), "free err");
+            ck(cudaMemsetAsync(L->d_umax, 0, sizeof(int) * oc, S(stream)), "memset umax");
+            if (filter_scope == SFC_FIL_PER_CHANNEL)
+                ck(cudaMemcpyAsync(L->d_sf, L->d_fil_native, sizeof(double) * oc, cudaMemcpyDeviceToDevice, S(stream)),
+                   "copy sf");
+            else
+                ck(cudaMemsetAsync(L->d_sf, 0, sizeof(double) * oc, S(stream)), "memset sf");
+        }
         ck(cudaStreamSynchronize(S(stream)), "filter prepare");
         *out = L;
     });
@@ -277,8 +321,25 @@ int sfc_layer_destroy(sfc_layer_t L) {
     cudaFree(L->d_sf);
     cudaFree(L->d_umax);
     cudaFree(L->d_sat);
+    cudaFree(L->d_fil);
+    cudaFree(L->d_fil_native);
     delete L;
     return SFC_OK;
+}
+
+int sfc_layer_filter_scales_native(sfc_layer_t L, double* scales, int64_t* count) {
+    return guarded([&] {
+        if (!L || !count) throw std::invalid_argument("null argument");
+        if (!L->general) {
+            *count = L->OC;
+            if (scales) ck(cudaMemcpy(scales, L->d_sf, sizeof(double) * L->OC, cudaMemcpyDeviceToHost), "copy sf");
+            return;
+        }
+        *count = L->n_fil_native;
+        if (scales)
+            ck(cudaMemcpy(scales, L->d_fil_native, sizeof(double) * L->n_fil_native, cudaMemcpyDeviceToHost),
+               "copy scales");
+    });
 }
 
 int sfc_layer_filter_scales(sfc_layer_t L, double* sf, int32_t* umax) {
@@ -361,6 +422,22 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
         if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
         WsView v = carve(ws, g, L->F);
         if (!o) throw std::invalid_argument("null outputs");
+        if (L->general) {  // non-default QuantConfig: fp64 parity path (quant.cpp:163-278)
+            if (o->y_int32 || o->y_int64)
+                throw Unsupported("y_int is defined only for PerTensor activation + PerChannel filter MinMax scales");
+            if (L->act_scope == SFC_ACT_PER_FREQUENCY && L->F > 196) throw Unsupported("too many frequencies");
+            ck(cudaMemsetAsync(ws, 0, 1024 + sizeof(int) * L->F, S(stream)), "memset header");
+            ck(launch_act_absmax(L->variant, d_x, g, v.vmax, v.vkeep, S(stream), false), "absmax launch");
+            const bool pf = L->act_scope == SFC_ACT_PER_FREQUENCY;
+            ck(launch_act_general(v.vkeep, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits,
+                                  pf ? v.vmaxf : v.vmax, v.act_scale, v.vq, v.sat, S(stream)),
+               "general activation launch");
+            ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, S(stream), false), "gemm launch");
+            OutPtrs op{nullptr, nullptr, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
+            op.gen_act = v.act_scale, op.gen_per_freq = pf ? 1 : 0, op.gen_fil = L->d_fil;
+            ck(launch_output(L->variant, 2, v.P, g, v.qp, L->d_sf, op, S(stream), false), "output launch");
+            return;
+        }
         needs_y64(L, o);  // refuse before anything is launched
         unsigned mask = SFC_STAGE_ALL & ~SFC_STAGE_QPARAMS;
         if (const char* dbg = std::getenv("SFC_DEBUG_FORWARD_MASK")) mask = unsigned(std::atoi(dbg));  // profiling only
@@ -380,6 +457,11 @@ int sfc_conv_stats(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, 
         unsigned long long sat = 0;
         ck(cudaMemcpyAsync(&qp, v.qp, sizeof qp, cudaMemcpyDeviceToHost, S(stream)), "copy qp");
         ck(cudaMemcpyAsync(&sat, v.sat, sizeof sat, cudaMemcpyDeviceToHost, S(stream)), "copy sat");
+        if (L->general) {  // the activation scale (first if per frequency) and the global max
+            ck(cudaMemcpyAsync(&qp.sa, v.act_scale, sizeof(double), cudaMemcpyDeviceToHost, S(stream)), "copy sa");
+            ck(cudaMemcpyAsync(&qp.vmax, v.vmax, sizeof(int), cudaMemcpyDeviceToHost, S(stream)), "copy vmax");
+            qp.exact = 0;
+        }
         ck(cudaStreamSynchronize(S(stream)), "stats sync");
         std::memcpy(&stats[0], &qp.sa, sizeof(double));
         stats[1] = qp.vmax;
@@ -387,6 +469,27 @@ int sfc_conv_stats(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, 
         stats[3] = qp.exact;
         stats[4] = int64_t(L->OC) * L->IC * L->F + int64_t(g.T) * L->IC * L->F;
         stats[5] = g.T;
+    });
+}
+
+int sfc_conv_act_scales(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, double* scales, int64_t* count,
+                        void* stream) {
+    return guarded([&] {
+        if (!L || !ws || !count) throw std::invalid_argument("null argument");
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        WsView v = carve(const_cast<void*>(ws), g, L->F);
+        *count = L->general && L->act_scope == SFC_ACT_PER_FREQUENCY ? L->F : 1;
+        if (!scales) return;
+        if (L->general) {
+            ck(cudaMemcpyAsync(scales, v.act_scale, sizeof(double) * size_t(*count), cudaMemcpyDeviceToHost, S(stream)),
+               "copy scales");
+        } else {
+            QuantParams qp;
+            ck(cudaMemcpyAsync(&qp, v.qp, sizeof qp, cudaMemcpyDeviceToHost, S(stream)), "copy qp");
+            ck(cudaStreamSynchronize(S(stream)), "sync");
+            scales[0] = qp.sa;
+        }
+        ck(cudaStreamSynchronize(S(stream)), "sync");
     });
 }
 

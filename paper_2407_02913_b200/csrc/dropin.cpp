@@ -415,8 +415,6 @@ QuantReport quantized_fast_conv2d(const DenseTensor& input, const DenseTensor& f
                                   int padding, const QuantConfig& config) {
     if (config.bits < 2 || config.bits > 16)  // quant.cpp:155-156
         throw std::invalid_argument("quantization width must be between 2 and 16 bits");
-    if (config.act_scope != ActScaleScope::PerTensor)
-        throw std::invalid_argument("PerFrequency activation scales are not on the B200 device path");
     check_conv_shapes(input, filters);
     if (filters.dim(2) != spec.R) throw std::invalid_argument("filter shape does not match algorithm");
     const int B = input.dim(0), C = input.dim(1), H = input.dim(2), W = input.dim(3), OC = filters.dim(0);
@@ -426,8 +424,8 @@ QuantReport quantized_fast_conv2d(const DenseTensor& input, const DenseTensor& f
     PlanGuard plan{plan_handle(spec)};
     DevBuf<int8_t> x = to_device_int8(input, "input"), w = to_device_int8(filters, "filters");
     sfc_layer_t layer = nullptr;
-    check(sfc_layer_create(plan.p, w.p, OC, C, config.bits, int(config.filter_scope), int(config.search), stream(),
-                           &layer));
+    check(sfc_layer_create_ex(plan.p, w.p, OC, C, config.bits, int(config.act_scope), int(config.filter_scope),
+                              int(config.search), stream(), &layer));
     struct LayerGuard {
         sfc_layer_t l;
         ~LayerGuard() { sfc_layer_destroy(l); }

@@ -1,0 +1,199 @@
+// Non-default QuantConfig on the device: per-frequency activation
+// scales, per-frequency / per-(channel, frequency) filter scales and the MseGrid scale
+// search (quant.cpp:13-30, 117-134, 163-229, 242-263).
+//
+// Scale search follows the reference bit for bit: a group's MinMax scale is
+// max(absmax / qmax, 1e-8); MseGrid evaluates quant_group_mse for the MinMax scale and 100
+// grid candidates, each as ONE sequential fp64 sum over the group's values in the
+// reference's order, with the reference's rounding steps (__ddiv_rn / __dmul_rn / __dsub_rn /
+// __dadd_rn: no FMA contraction, like the reference's x86-64 build), and keeps the first
+// strict minimum.  Candidates run as the lanes of a warp so every value load is a broadcast.
+// Quantization here is the reference's fp64 nearbyint(v / s) with clamping and saturation
+// counting (these configurations are parity paths, not the tuned default).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "sfc_kernels.hpp"
+
+namespace sfcb200 {
+
+namespace {
+constexpr int kCands = 101;  // the MinMax scale + 100 grid points (quant.cpp:125-131)
+
+__device__ __forceinline__ double grid_scale(double base, int cand) {  // cand 0 = base
+    if (cand == 0) return base;
+    const double t = __dadd_rn(0.3, __ddiv_rn(__dmul_rn(0.7, double(cand - 1)), 99.0));
+    return fmax(__dmul_rn(base, t), 1e-8);
+}
+
+__device__ __forceinline__ double mse_term(double v, double s, double qmax, double qmin) {
+    double q = rint(__ddiv_rn(v, s));
+    q = fmin(qmax, fmax(qmin, q));
+    const double d = __dsub_rn(v, __dmul_rn(q, s));
+    return __dmul_rn(d, d);
+}
+
+// Group g of the transformed filters U[oc][ic][f] (int32, exact) for a filter scope:
+// base offset, element stride and count, in the reference's value order (quant.cpp:193-219).
+struct FilGroup {
+    long long base, stride, count;
+};
+__device__ __forceinline__ FilGroup fil_group(int scope, int g, int OC, int IC, int F) {
+    if (scope == 0) return {(long long)g * IC * F, 1, (long long)IC * F};   // PerChannel: (ic, f)
+    if (scope == 1) return {g, F, (long long)OC * IC};                       // PerFrequency: (oc, ic)
+    return {(long long)(g / F) * IC * F + g % F, F, IC};                     // PerChannelFrequency: ic
+}
+}  // namespace
+
+// One warp per group, lane = candidate chunk: absmax (exact, order-free), then for
+// MseGrid the 101 candidate errors (lanes 0..31 take candidates lane, lane+32, ...).
+// err_out[g * kCands + cand]; scale_out[g] is the MinMax scale (the MseGrid pick follows).
+__global__ void __launch_bounds__(32) k_fil_scales(const int32_t* __restrict__ U, int OC, int IC, int F, int scope,
+                                                   int mse, int bits, double* __restrict__ scale_out,
+                                                   double* __restrict__ err_out) {
+    const int g = blockIdx.x, lane = threadIdx.x;
+    const FilGroup G = fil_group(scope, g, OC, IC, F);
+    int amax = 0;
+    for (long long i = lane; i < G.count; i += 32) amax = max(amax, abs(U[G.base + i * G.stride]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const double qmax = double((1 << (bits - 1)) - 1), qmin = -qmax - 1.0;
+    const double base = fmax(double(amax) / qmax, 1e-8);
+    if (lane == 0) scale_out[g] = base;
+    if (!mse) return;
+    for (int c0 = 0; c0 < kCands; c0 += 32) {
+        const int cand = c0 + lane;
+        const double s = grid_scale(base, cand < kCands ? cand : 0);
+        double err = 0.0;
+        for (long long i = 0; i < G.count; ++i)
+            err = __dadd_rn(err, mse_term(double(U[G.base + i * G.stride]), s, qmax, qmin));
+        if (cand < kCands) err_out[(long long)g * kCands + cand] = err;
+    }
+}
+
+// scale_mse_grid's selection (quant.cpp:122-134): start from the MinMax scale, take a grid
+// point only on a strict improvement, in grid order.
+__global__ void k_pick_best(int groups, const double* __restrict__ err, double* __restrict__ scale) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= groups) return;
+    const double base = scale[g];
+    double best = base, best_err = err[(long long)g * kCands];
+    for (int c = 1; c < kCands; ++c) {
+        const double e = err[(long long)g * kCands + c];
+        if (e < best_err) best_err = e, best = grid_scale(base, c);
+    }
+    scale[g] = best;
+}
+
+// uq[f][oc][ic] = quantize_value(U, fil(oc, f)) (quant.cpp:221-229) and the expanded table
+// fil_full[oc * F + f] the fp64 output epilogue reads.
+__global__ void k_fil_quantize(const int32_t* __restrict__ U, int OC, int IC, int F, int scope,
+                               const double* __restrict__ scale, int bits, int Cpad, int OCpad,
+                               int8_t* __restrict__ uqB, double* __restrict__ fil_full,
+                               unsigned long long* __restrict__ sat) {
+    const long long n = (long long)OC * IC * F;
+    const int qmax = (1 << (bits - 1)) - 1;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int f = int(i % F), ic = int((i / F) % IC), oc = int(i / ((long long)F * IC));
+        const double s = scope == 0 ? scale[oc] : (scope == 1 ? scale[f] : scale[(long long)oc * F + f]);
+        uqB[((long long)f * OCpad + oc) * Cpad + ic] = int8_t(clamp_q(exact_q(U[i], s), qmax, sat));
+        if (ic == 0) fil_full[(long long)oc * F + f] = s;
+    }
+}
+
+// Per-frequency max|V| over the kept V [F][Tpad][Cpad] (t < T, c < C): vmaxf[f].
+__global__ void __launch_bounds__(256) k_act_fmax(const int16_t* __restrict__ V, ConvGeom g, int F,
+                                                  int* __restrict__ vmaxf) {
+    const int f = blockIdx.y;
+    const long long n = (long long)g.T * g.C;
+    int m = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long t = i / g.C, c = i % g.C;
+        m = max(m, abs(int(V[((long long)f * g.Tpad + t) * g.Cpad + c])));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(&vmaxf[f], m);
+}
+
+// Activation scales from the maxima: MinMax, or MseGrid over the group's V in the
+// reference's order (quant.cpp:168-181: PerTensor = all of g.v in (tile, c, f) order,
+// PerFrequency = (tile, c) for one f).  One block of 4 warps per group; lane = candidate.
+__global__ void __launch_bounds__(128) k_act_scales(const int16_t* __restrict__ V, ConvGeom g, int F, int per_freq,
+                                                    const int* __restrict__ vmax, int mse, int bits,
+                                                    double* __restrict__ act_scale) {
+    const int grp = blockIdx.x, cand = threadIdx.x;
+    const double qmax = double((1 << (bits - 1)) - 1), qmin = -qmax - 1.0;
+    const double base = fmax(double(vmax[per_freq ? grp : 0]) / qmax, 1e-8);
+    __shared__ double s_err[kCands];
+    if (!mse) {
+        if (cand == 0) act_scale[grp] = base;
+        return;
+    }
+    const double s = grid_scale(base, cand < kCands ? cand : 0);
+    double err = 0.0;
+    const long long tc = (long long)g.T * g.C;
+    if (per_freq) {
+        const int16_t* Vf = V + (long long)grp * g.Tpad * g.Cpad;
+        for (long long i = 0; i < tc; ++i) {
+            const long long t = i / g.C, c = i - t * g.C;
+            err = __dadd_rn(err, mse_term(double(Vf[t * g.Cpad + c]), s, qmax, qmin));
+        }
+    } else {
+        for (long long i = 0; i < tc; ++i) {
+            const long long t = i / g.C, c = i - t * g.C;
+            for (int f = 0; f < F; ++f)
+                err = __dadd_rn(err, mse_term(double(V[((long long)f * g.Tpad + t) * g.Cpad + c]), s, qmax, qmin));
+        }
+    }
+    if (cand < kCands) s_err[cand] = err;
+    __syncthreads();
+    if (cand == 0) {
+        double best = base, best_err = s_err[0];
+        for (int c = 1; c < kCands; ++c)
+            if (s_err[c] < best_err) best_err = s_err[c], best = grid_scale(base, c);
+        act_scale[grp] = best;
+    }
+}
+
+// vq[f][t][c] = quantize_value(V, sa(f)) (quant.cpp:242-250) for t < T, c < C (else 0).
+__global__ void __launch_bounds__(256) k_quant_general(const int16_t* __restrict__ V, ConvGeom g, int F,
+                                                       int per_freq, const double* __restrict__ act_scale, int bits,
+                                                       int8_t* __restrict__ vqA, unsigned long long* __restrict__ sat) {
+    const int f = blockIdx.y;
+    const double s = act_scale[per_freq ? f : 0];
+    const int qmax = (1 << (bits - 1)) - 1;
+    const long long n = (long long)g.T * g.Cpad;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long t = i / g.Cpad, c = i - t * g.Cpad;
+        const long long off = ((long long)f * g.Tpad + t) * g.Cpad + c;
+        vqA[off] = c < g.C ? int8_t(clamp_q(exact_q(V[off], s), qmax, sat)) : int8_t(0);
+    }
+}
+
+// ============================================================================ host
+cudaError_t launch_fil_general(const int32_t* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
+                               int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
+                               unsigned long long* sat, cudaStream_t st) {
+    const int groups = scope == 0 ? OC : (scope == 1 ? F : OC * F);
+    k_fil_scales<<<groups, 32, 0, st>>>(U, OC, IC, F, scope, mse, bits, scale_native, err_tmp);
+    if (mse) k_pick_best<<<(groups + 127) / 128, 128, 0, st>>>(groups, err_tmp, scale_native);
+    const long long n = (long long)OC * IC * F;
+    const int blocks = int((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+    k_fil_quantize<<<blocks, 256, 0, st>>>(U, OC, IC, F, scope, scale_native, bits, Cpad, OCpad, uqB, fil_full, sat);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
+                               int* vmaxf, double* act_scale, int8_t* vqA, unsigned long long* sat, cudaStream_t st) {
+    const long long n = (long long)g.T * g.C;
+    const int bx = int((n + 255) / 256 < 64 ? (n + 255) / 256 : 64);
+    if (per_freq) k_act_fmax<<<dim3(bx, F), 256, 0, st>>>(V, g, F, vmaxf);
+    k_act_scales<<<per_freq ? F : 1, 128, 0, st>>>(V, g, F, per_freq, vmaxf, mse, bits, act_scale);
+    const long long nq = (long long)g.T * g.Cpad;
+    const int bq = int((nq + 255) / 256 < 64 ? (nq + 255) / 256 : 64);
+    k_quant_general<<<dim3(bq, F), 256, 0, st>>>(V, g, F, per_freq, act_scale, bits, vqA, sat);
+    return cudaGetLastError();
+}
+
+}  // namespace sfcb200

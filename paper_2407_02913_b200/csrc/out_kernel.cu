@@ -45,11 +45,11 @@ struct OutSmem {
     size_t p_bytes, q_off, bar_off, bytes;
 };
 
-template <int V, bool Y64>
+template <int V, int MODE>
 __host__ __device__ inline OutSmem out_smem() {
     using T = Tab<V>;
     constexpr int TB = out_tb<V>();
-    const size_t es = Y64 ? 8 : 4;
+    const size_t es = MODE == 0 ? 4 : 8;
     OutSmem s;
     s.qstride = kOcc | 1;
     s.ystride = (T::M * TB) | 1;
@@ -71,15 +71,18 @@ __constant__ unsigned c_magic32[33] = {  // 0xffffffff / d + 1 (exact for t < 2^
     0x0aaaaaabu, 0x0a3d70a4u, 0x09d89d8au, 0x097b425fu, 0x0924924au, 0x08d3dcb1u, 0x08888889u, 0x08421085u,
     0x08000000u};
 
-template <int V, bool Y64>
+// MODE 0: exact int32 y, 1: exact int64 y, 2: general QuantConfig (P dequantised per
+// (oc, f) before the inverse transform, which then runs in fp64: quant.cpp:258-278).
+template <int V, int MODE>
 __global__ void __launch_bounds__(kOutThreads, 2)
     k_output(const __grid_constant__ CUtensorMap tmP, ConvGeom g, const QuantParams* __restrict__ qpp,
              const double* __restrict__ sf, OutPtrs o) {
     using T = Tab<V>;
     constexpr int K = T::K, M = T::M, TB = out_tb<V>();
-    using acc_t = typename std::conditional<Y64, long long, int>::type;
+    constexpr bool Y64 = MODE == 1;
+    using acc_t = typename std::conditional<MODE == 2, double, typename std::conditional<Y64, long long, int>::type>::type;
     extern __shared__ __align__(128) uint8_t smem[];
-    const OutSmem L = out_smem<V, Y64>();
+    const OutSmem L = out_smem<V, MODE>();
     const int32_t* sp = reinterpret_cast<const int32_t*>(smem);  // [F][TB][kOcc]
     acc_t* s_y = reinterpret_cast<acc_t*>(smem);                 // [M][kOcc] rows of ystride (after stage A)
     acc_t* s_q = reinterpret_cast<acc_t*>(smem + L.q_off);       // [TB][M][K] rows of qstride
@@ -120,6 +123,14 @@ __global__ void __launch_bounds__(kOutThreads, 2)
         acc_t pk[K], qt[M];
 #pragma unroll
         for (int k = 0; k < K; ++k) pk[k] = sp[((k * K + l) * TB + tj) * kOcc + oc];
+        if constexpr (MODE == 2) {  // pd[f] = double(pacc[f]) * sa(f) * fil(oc, f), left to right
+            const int ocg = oc0 + oc < g.OC ? oc0 + oc : 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int f = k * K + l;
+                pk[k] = __dmul_rn(__dmul_rn(pk[k], o.gen_act[o.gen_per_freq ? f : 0]), o.gen_fil[ocg * T::F + f]);
+            }
+        }
         inv1d<V>(pk, qt);
 #pragma unroll
         for (int t1 = 0; t1 < M; ++t1) s_q[((tj * M + t1) * K + l) * L.qstride + oc] = qt[t1];
@@ -164,13 +175,20 @@ __global__ void __launch_bounds__(kOutThreads, 2)
             if (oc >= noc || t1 >= hrows) continue;
             const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
             const acc_t y = s_y[r * L.ystride + c];
-            if constexpr ((MK & 1) != 0) o.y32[x] = int(y);
-            if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y);
-            if constexpr ((MK & 4) != 0)
-                o.f32[x] = Y64 ? float(double(y) * s_scale[oc]) : __int2float_rn(int(y)) * s_scalef[oc];
-            if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * s_scale[oc];
-            if constexpr ((MK & 16) != 0)
-                o.i8[x] = int8_t(fmin(fmax(rint(double(y) * s_scale[oc] * rq), 0.0), 127.0));
+            if constexpr (MODE != 2 && (MK & 1) != 0) o.y32[x] = int(y);
+            if constexpr (MODE != 2 && (MK & 2) != 0) o.y64[x] = int64_t(y);
+            if constexpr (MODE == 2) {  // y = sum A A pd; out = y / N^2 (the reference's a = A / N)
+                const double out = double(y) / double(T::DEN * T::DEN);
+                if constexpr ((MK & 4) != 0) o.f32[x] = float(out);
+                if constexpr ((MK & 8) != 0) o.f64[x] = out;
+                if constexpr ((MK & 16) != 0) o.i8[x] = int8_t(fmin(fmax(rint(out * rq), 0.0), 127.0));
+            } else {
+                if constexpr ((MK & 4) != 0)
+                    o.f32[x] = Y64 ? float(double(y) * s_scale[oc]) : __int2float_rn(int(y)) * s_scalef[oc];
+                if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * s_scale[oc];
+                if constexpr ((MK & 16) != 0)
+                    o.i8[x] = int8_t(fmin(fmax(rint(double(y) * s_scale[oc] * rq), 0.0), 127.0));
+            }
         }
     };
     const int mask = (o.y32 ? 1 : 0) | (o.y64 ? 2 : 0) | (o.f32 ? 4 : 0) | (o.f64 ? 8 : 0) | (o.i8 ? 16 : 0);
@@ -203,7 +221,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int V, bool Y64>
+template <int V, int MODE>
 cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf, const OutPtrs& o,
                        cudaStream_t st, bool pdl) {
     constexpr int TB = out_tb<V>();
@@ -218,8 +236,8 @@ cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* q
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
-    const size_t smem = out_smem<V, Y64>().bytes;
-    auto kern = k_output<V, Y64>;
+    const size_t smem = out_smem<V, MODE>().bytes;
+    auto kern = k_output<V, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     const long rows = long(g.B) * g.th;
@@ -238,11 +256,24 @@ cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* q
 }
 
 template <int V>
-cudaError_t out_by_width(bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
+cudaError_t out_by_width(int mode, const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
                          const OutPtrs& o, cudaStream_t st, bool pdl) {
-    return y64 ? out_launch<V, true>(P, g, qp, sf, o, st, pdl) : out_launch<V, false>(P, g, qp, sf, o, st, pdl);
+    return mode == 0 ? out_launch<V, 0>(P, g, qp, sf, o, st, pdl)
+         : mode == 1 ? out_launch<V, 1>(P, g, qp, sf, o, st, pdl)
+                     : out_launch<V, 2>(P, g, qp, sf, o, st, pdl);
 }
 }  // namespace
+
+cudaError_t launch_output(int variant, int mode, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
+                          const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl) {
+    switch (variant) {
+        case 0: return out_by_width<0>(mode, P, g, qp, sf, o, st, pdl);
+        case 1: return out_by_width<1>(mode, P, g, qp, sf, o, st, pdl);
+        case 2: return out_by_width<2>(mode, P, g, qp, sf, o, st, pdl);
+        case 3: return out_by_width<3>(mode, P, g, qp, sf, o, st, pdl);
+        default: return out_by_width<4>(mode, P, g, qp, sf, o, st, pdl);
+    }
+}
 
 SFC_TL_UNIT_READER(tl_read_out)
 

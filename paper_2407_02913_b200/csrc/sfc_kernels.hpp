@@ -30,6 +30,9 @@ struct QuantParams {
 };
 
 void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, int OC);
+// Workspace header: vmax @0, saturations @8, QuantParams @64, per-frequency maxima @1024
+// (int32 x F), activation scales @2048 (fp64 x F); F <= 196.
+constexpr size_t kWsHeader = 4096;
 size_t workspace_bytes(const ConvGeom& g, int F);
 
 // `pdl`: launch with programmatic stream serialization (overlap the predecessor's tail).
@@ -79,8 +82,14 @@ struct OutPtrs {
     double* f64;
     int8_t* i8;
     double requant;
+    // general QuantConfig (mode 2): per-frequency activation scales and the (oc, f) filter
+    // scale table; the epilogue dequantises P before the inverse transform in fp64
+    const double* gen_act = nullptr;
+    int gen_per_freq = 0;
+    const double* gen_fil = nullptr;  // [OC][F]
 };
-cudaError_t launch_output(int variant, bool y64, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
+// mode 0: exact int32 y, 1: exact int64 y, 2: general QuantConfig (fp64, no y_int)
+cudaError_t launch_output(int variant, int mode, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
 cudaError_t launch_sq_err(const double* out, const int32_t* ref, long long n, double* sums, cudaStream_t st);
 // Device table of verified quantizer parameters (common.cuh, kQpTableMax).  build=true
@@ -95,5 +104,17 @@ cudaError_t launch_direct_conv(const int8_t* x, int B, int C, int H, int W, cons
 cudaError_t launch_freq_energy(int variant, const int8_t* x, const ConvGeom& g, unsigned long long* sum,
                                cudaStream_t st);
 cudaError_t launch_transform_filters(int variant, const int8_t* w, int OC, int IC, int32_t* u, cudaStream_t st);
+
+// General QuantConfig (general_kernels.cu).  Filters: per-group scales of U [OC][IC][F]
+// (scope 0 PerChannel, 1 PerFrequency, 2 PerChannelFrequency; MinMax or MseGrid), uq and the
+// expanded [OC][F] scale table.  err_tmp: groups * 101 doubles.
+cudaError_t launch_fil_general(const int32_t* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
+                               int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
+                               unsigned long long* sat, cudaStream_t st);
+// Activations from the kept V: per-frequency maxima (per_freq), MinMax / MseGrid scales
+// act_scale[1 or F] and vq (exact fp64 quantizer, saturations counted).  vmax: the global
+// max (PerTensor) or F zeroed slots (PerFrequency).
+cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits, int* vmax,
+                               double* act_scale, int8_t* vqA, unsigned long long* sat, cudaStream_t st);
 
 }  // namespace sfcb200

@@ -200,7 +200,8 @@ class SfcLayer:
     """One conv layer on the device: offline-transformed, quantized filters (sfc_layer_t)."""
 
     def __init__(self, spec: AlgorithmSpec | str, filters: torch.Tensor, bits: int = 8,
-                 filter_scope: int = FilterScaleScope.PerChannel, search: int = ScaleSearch.MinMax, stream=None):
+                 filter_scope: int = FilterScaleScope.PerChannel, search: int = ScaleSearch.MinMax, stream=None,
+                 act_scope: int = ActScaleScope.PerTensor):
         self.spec = catalog_algorithm(spec) if isinstance(spec, str) else spec
         if filters.dim() != 4 or filters.shape[2] != self.spec.R or filters.shape[3] != self.spec.R:
             raise ValueError("filter shape does not match algorithm")
@@ -208,11 +209,14 @@ class SfcLayer:
         self.device = w.device
         self.OC, self.IC = int(w.shape[0]), int(w.shape[1])
         self.bits = bits
+        self.act_scope, self.filter_scope, self.search = int(act_scope), int(filter_scope), int(search)
+        # anything but {PerTensor, PerChannel, MinMax} is the fp64 parity path (no y_int)
+        self.general = (self.act_scope, self.filter_scope, self.search) != (0, 0, 0)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            check(lib().sfc_layer_create(ctypes.c_void_p(self.spec._handle), _ptr(w), self.OC, self.IC, bits,
-                                         int(filter_scope), int(search), ctypes.c_void_p(_stream_ptr(stream)),
-                                         ctypes.byref(h)))
+            check(lib().sfc_layer_create_ex(ctypes.c_void_p(self.spec._handle), _ptr(w), self.OC, self.IC, bits,
+                                            self.act_scope, self.filter_scope, self.search,
+                                            ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(h)))
         self._h = h
 
     def __del__(self):
@@ -231,6 +235,25 @@ class SfcLayer:
         check(lib().sfc_layer_filter_scales(self._h, sf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                             um.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
         return sf, um
+
+    def filter_scales_native(self) -> np.ndarray:
+        """Filter scales as the scope defines them (OC, K*K or OC*K*K; quant.cpp:193-219)."""
+        n = ctypes.c_int64()
+        check(lib().sfc_layer_filter_scales_native(self._h, None, ctypes.byref(n)))
+        out = np.zeros(n.value, np.float64)
+        check(lib().sfc_layer_filter_scales_native(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                                   ctypes.byref(n)))
+        return out
+
+    def act_scales(self, n, h, w, pad, ws, stream=None) -> np.ndarray:
+        """Activation scales of the last call (1 or K*K)."""
+        cnt = ctypes.c_int64()
+        check(lib().sfc_conv_act_scales(self._h, n, h, w, pad, _ptr(ws), None, ctypes.byref(cnt),
+                                        ctypes.c_void_p(_stream_ptr(stream))))
+        out = np.zeros(cnt.value, np.float64)
+        check(lib().sfc_conv_act_scales(self._h, n, h, w, pad, _ptr(ws), out.ctypes.data_as(
+            ctypes.POINTER(ctypes.c_double)), ctypes.byref(cnt), ctypes.c_void_p(_stream_ptr(stream))))
+        return out
 
     def filter_saturations(self) -> int:
         c = ctypes.c_int64()
@@ -383,8 +406,6 @@ def quantized_fast_conv2d(input, filters, spec: AlgorithmSpec, padding: int, con
     """quant.cpp:152-293 on the device.  Raises ValueError for bits outside [2, 16] (quant.cpp:155-156)."""
     if config.bits < 2 or config.bits > 16:
         raise ValueError("quantization width must be between 2 and 16 bits")
-    if int(config.act_scope) != ActScaleScope.PerTensor:
-        raise _lib.SfcUnsupported("PerFrequency activation scales are not on the device path yet")
     x = as_int8_device(input, "input")
     if x.dim() != 4 or filters.dim() != 4:
         raise ValueError("conv2d expects 4-d NCHW tensors")
@@ -393,15 +414,25 @@ def quantized_fast_conv2d(input, filters, spec: AlgorithmSpec, padding: int, con
     B, C, H, W = x.shape
     if H + 2 * padding - spec.R + 1 <= 0 or W + 2 * padding - spec.R + 1 <= 0:
         raise ValueError("filter larger than padded input")
-    layer = SfcLayer(spec, filters, config.bits, config.filter_scope, config.search)
+    layer = SfcLayer(spec, filters, config.bits, config.filter_scope, config.search,
+                     act_scope=config.act_scope)
     HO, WO = H + 2 * padding - spec.R + 1, W + 2 * padding - spec.R + 1
     ws = layer.workspace(B, H, W, padding)
-    y = torch.empty((B, layer.OC, HO, WO), dtype=torch.int32, device=x.device)
     out = torch.empty((B, layer.OC, HO, WO), dtype=torch.float32, device=x.device)
-    layer.forward(x, ws, padding, y_int32=y, out_f32=out)
+    y = None
+    if layer.general:  # per-frequency dequantisation in fp64: no integer y (quant.cpp:258-263)
+        layer.forward(x, ws, padding, out_f32=out)
+    else:
+        y = torch.empty((B, layer.OC, HO, WO), dtype=torch.int32, device=x.device)
+        try:
+            layer.forward(x, ws, padding, y_int32=y, out_f32=out)
+        except _lib.SfcUnsupported:  # the int32 bound does not hold for this layer
+            y = torch.empty((B, layer.OC, HO, WO), dtype=torch.int64, device=x.device)
+            layer.forward(x, ws, padding, y_int64=y, out_f32=out)
     st = layer.stats(B, H, W, padding, ws)
-    sf, _ = layer.filter_scales()
-    rep = QuantReport(output=out, y_int=y, act_scale=st["act_scale"], filter_scales=sf,
+    acts = layer.act_scales(B, H, W, padding, ws)
+    rep = QuantReport(output=out, y_int=y, act_scale=float(acts[0]) if len(acts) == 1 else acts,
+                      filter_scales=layer.filter_scales_native(),
                       saturations=st["saturations"] + layer.filter_saturations(),
                       values_quantized=st["values_quantized"])
     if report:

@@ -105,10 +105,11 @@ double max_rel(const DenseTensor& got, const DenseTensor& want) {
 }
 
 int run_mode(int argc, char** argv) {
-    if (argc != 13) {
-        std::fprintf(stderr, "usage: test_dropin run SPEC PAD BITS B C H W OC x.bin w.bin out.bin\n");
+    if (argc != 13 && argc != 16) {
+        std::fprintf(stderr, "usage: test_dropin run SPEC PAD BITS B C H W OC [ACT FIL SEARCH] x.bin w.bin out.bin\n");
         return 2;
     }
+    const int fa = argc == 16 ? 3 : 0;  // optional QuantConfig scopes before the file arguments
     const std::string spec = argv[2];
     const int pad = std::atoi(argv[3]), bits = std::atoi(argv[4]);
     const int B = std::atoi(argv[5]), C = std::atoi(argv[6]), H = std::atoi(argv[7]), W = std::atoi(argv[8]);
@@ -120,13 +121,19 @@ int run_mode(int argc, char** argv) {
         if (!f) throw std::runtime_error(std::string("short read: ") + path);
         for (std::size_t i = 0; i < raw.size(); ++i) t.data[i] = double(raw[i]);
     };
-    DenseTensor x({B, C, H, W}), w({OC, C, 3, 3});
-    load(argv[10], x);
-    load(argv[11], w);
+    const AlgorithmSpec& s = catalog_algorithm(spec);
+    DenseTensor x({B, C, H, W}), w({OC, C, s.R, s.R});
+    load(argv[10 + fa], x);
+    load(argv[11 + fa], w);
     QuantConfig cfg;
     cfg.bits = bits;
-    const QuantReport rep = quantized_fast_conv2d(x, w, catalog_algorithm(spec), pad, cfg);
-    std::ofstream o(argv[12], std::ios::binary);
+    if (fa) {
+        cfg.act_scope = ActScaleScope(std::atoi(argv[10]));
+        cfg.filter_scope = FilterScaleScope(std::atoi(argv[11]));
+        cfg.search = ScaleSearch(std::atoi(argv[12]));
+    }
+    const QuantReport rep = quantized_fast_conv2d(x, w, s, pad, cfg);
+    std::ofstream o(argv[12 + fa], std::ios::binary);
     o.write(reinterpret_cast<const char*>(rep.output.data.data()), std::streamsize(rep.output.data.size() * 8));
     const double tail[5] = {rep.mse, rep.signal_energy, rep.snr_db, double(rep.saturations),
                             double(rep.values_quantized)};

@@ -61,3 +61,30 @@ def test_dropin_quantized_fast_conv2d_matches_oracle(cuda, variant, shape):
     assert tail[0] == pytest.approx(ref["report"]["mse"], rel=1e-9)
     assert tail[2] == pytest.approx(ref["report"]["snr_db"], rel=1e-9)
     assert tail[3] == ref["report"]["saturations"] and tail[4] == ref["report"]["values_quantized"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,cfg", [("sfc6-6x6-3x3", (1, 2, 0)), ("sfc4-4x4-3x3", (0, 0, 1)),
+                                         ("sfc6-6x6-5x5", (0, 0, 0)), ("sfc6-4x4-7x7", (1, 1, 1))])
+def test_dropin_quant_config_and_large_filters(cuda, variant, cfg):
+    """The full QuantConfig (per-frequency scopes, MseGrid) and the 5x5 / 7x7 algorithms through
+    the C++ API: fp64 output vs the oracle (<= 1e-12 relative), counters equal."""
+    _build()
+    R = ob.spec(variant)["R"]
+    B, C, H, W, OC, pad, bits = 1, 6, 14, 13, 5, R // 2, 8
+    rng = np.random.default_rng(R * 7 + sum(cfg))
+    x = rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(OC, C, R, R), dtype=np.int8)
+    with tempfile.TemporaryDirectory() as d:
+        xp, wp, op = (os.path.join(d, n) for n in ("x.bin", "w.bin", "o.bin"))
+        x.tofile(xp)
+        w.tofile(wp)
+        r = subprocess.run([BIN, "run", variant, str(pad), str(bits), str(B), str(C), str(H), str(W), str(OC),
+                            *(str(v) for v in cfg), xp, wp, op], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        raw = np.fromfile(op, np.float64)
+    HO, WO = H + 2 * pad - R + 1, W + 2 * pad - R + 1
+    out, tail = raw[:-5].reshape(B, OC, HO, WO), raw[-5:]
+    ref = ob.quantized_conv(x, w, variant, pad, bits, *cfg, want=("out",), report=True)
+    assert np.abs(out - ref["out"]).max() / np.abs(ref["out"]).max() <= 1e-12
+    assert tail[3] == ref["report"]["saturations"] and tail[4] == ref["report"]["values_quantized"]

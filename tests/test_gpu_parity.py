@@ -135,9 +135,17 @@ GOLD_TAGS = sorted({k.split("/")[0] for k in GOLD.files if k.endswith("/meta")})
 @pytest.mark.parametrize("tag", GOLD_TAGS)
 def test_golden_reference_outputs(cuda, tag, variant):
     pad, bits, asc, fsc, srch = (int(v) for v in GOLD[f"{tag}/meta"])
-    if bits > 8 or asc or fsc or srch:
-        pytest.skip("configuration outside the device path (bits > 8 / per-frequency scopes / MseGrid)")
+    if bits > 8:
+        pytest.skip("bits > 8 is outside the int8 tensor-core path")
     x, w = GOLD[f"{tag}/x"], GOLD[f"{tag}/w"]
+    if asc or fsc or srch:  # the general QuantConfig path (fp64 epilogue, no y_int)
+        rep = sc.quantized_fast_conv2d(torch.from_numpy(x), torch.from_numpy(w), sc.catalog_algorithm(variant), pad,
+                                       sc.QuantConfig(bits, asc, fsc, srch))
+        assert maxrel(rep.output.cpu().numpy(), GOLD[f"{tag}/{variant}/out"]) <= TOL
+        r = GOLD[f"{tag}/{variant}/report"]
+        assert rep.saturations == r[3] and rep.values_quantized == r[4]
+        assert rep.mse == pytest.approx(r[0], rel=1e-6) and rep.snr_db == pytest.approx(r[2], rel=1e-6)
+        return
     ref = GOLD[f"{tag}/{variant}/out"]
     g = run_gpu(x, w, variant, pad, bits)
     assert maxrel(g["f32"], ref) <= TOL
@@ -407,3 +415,45 @@ def test_large_r_layer_size(cuda, variant):
     x = rng.integers(0, 128, size=(4, 64, 56, 56), dtype=np.int8)
     w = rng.integers(-127, 128, size=(64, 64, R, R), dtype=np.int8)
     check_against_oracle(x, w, variant, R // 2, intermediates=False)
+
+
+# ------------------------------------------------------------------------------ general QuantConfig
+GENERAL_CONFIGS = [  # (act_scope, filter_scope, search, bits)
+    (1, 0, 0, 8), (0, 1, 0, 8), (0, 2, 0, 8), (1, 2, 0, 8), (0, 0, 1, 8), (1, 1, 1, 6), (0, 2, 1, 4), (1, 0, 0, 3),
+]
+
+
+@pytest.mark.parametrize("variant", VARIANTS + ["sfc6-6x6-5x5"])
+@pytest.mark.parametrize("cfg", GENERAL_CONFIGS, ids=[f"a{c[0]}f{c[1]}s{c[2]}b{c[3]}" for c in GENERAL_CONFIGS])
+def test_general_quant_config_vs_oracle(cuda, variant, cfg):
+    """Per-frequency activation scales, per-frequency / per-(oc, f) filter scales, MseGrid:
+    the scales are exactly the oracle's (same fp64 search order), vq / uq / pacc bit-exact,
+    fp32 output within 1e-6 (fp64 epilogue, dequantised before A as quant.cpp:258-263)."""
+    asc, fsc, srch, bits = cfg
+    R = ob.spec(variant)["R"]
+    rng = np.random.default_rng(sum(cfg) * 31 + R)
+    B, C, OC, H, W, pad = 2, 6, 5, 13, 12, R // 2
+    x = rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(OC, C, R, R), dtype=np.int8)
+    r = ob.quantized_conv(x, w, variant, pad, bits, asc, fsc, srch, want=("out", "pacc", "vq", "uq"), report=True)
+    dev = torch.device("cuda", 0)
+    layer = sc.SfcLayer(variant, torch.from_numpy(w).to(dev), bits=bits, filter_scope=fsc, search=srch, act_scope=asc)
+    xt = torch.from_numpy(x).to(dev)
+    HO, WO = H + 2 * pad - R + 1, W + 2 * pad - R + 1
+    ws = layer.workspace(B, H, W, pad)
+    out = torch.empty((B, OC, HO, WO), dtype=torch.float32, device=dev)
+    out64 = torch.empty((B, OC, HO, WO), dtype=torch.float64, device=dev)
+    layer.forward(xt, ws, pad, out_f32=out, out_f64=out64)
+    torch.cuda.synchronize()
+    assert np.array_equal(layer.act_scales(B, H, W, pad, ws), r["act_scale"]), "activation scales"
+    assert np.array_equal(layer.filter_scales_native(), r["fil_scale"]), "filter scales"
+    assert np.array_equal(layer.uq().cpu().numpy(), r["uq"].transpose(2, 0, 1)), "uq"
+    vq, pacc = layer.views(B, H, W, pad, ws)
+    assert np.array_equal(vq.cpu().numpy(), r["vq"].transpose(2, 0, 1)), "vq"
+    assert np.array_equal(pacc.cpu().numpy().astype(np.int64), r["pacc"].transpose(2, 0, 1)), "pacc"
+    assert maxrel(out.cpu().numpy(), r["out"]) <= TOL
+    assert maxrel(out64.cpu().numpy(), r["out"]) <= 1e-12
+    st = layer.stats(B, H, W, pad, ws)
+    assert st["saturations"] + layer.filter_saturations() == r["report"]["saturations"]
+    with pytest.raises(_lib.SfcUnsupported):  # y_int is not defined for these configurations
+        layer.forward(xt, ws, pad, y_int32=torch.empty((B, OC, HO, WO), dtype=torch.int32, device=dev))
