@@ -192,6 +192,23 @@ int sfc_report_sq_err(const double* d_out, const int32_t* d_ref, int64_t n, doub
  * sa as double bits}.  Synchronous. */
 int sfc_debug_quantizer(int vmax, int bits, int32_t* d_q, int64_t* info, void* stream);
 
+/* ---- real-valued (fp64) tensors, the reference API's DenseTensor values ---------------- */
+/* sfc_layer_create_ex for fp64 filters [OC][IC][R][R]: U = G f G^T in transform_filters'
+ * arithmetic order (conv.cpp:352-382), then the QuantConfig's scales and quantization. */
+int sfc_layer_create_f64(sfc_plan_t plan, const double* d_weights, int out_channels, int in_channels, int bits,
+                         int act_scope, int filter_scope, int search, void* stream, sfc_layer_t* out);
+/* sfc_conv_forward for fp64 inputs: V = B^T x B in gather_tiles' order (quant.cpp:44-93),
+ * scales, exact quantization, the int8 contraction and the fp64 epilogue (out_f32 / out_f64 /
+ * out_i8; no y_int).  Needs a layer from sfc_layer_create_f64 or a non-default
+ * sfc_layer_create_ex config.  Temporary V buffer stream-ordered (cudaMallocAsync). */
+int sfc_conv_forward_f64(sfc_layer_t layer, const double* d_x, int n, int h, int w, int pad, void* d_workspace,
+                         size_t workspace_bytes, const sfc_outputs* outs, void* stream);
+/* direct_conv2d (conv.cpp:320-350) in fp64 with the reference's summation order. */
+int sfc_direct_conv_f64(const double* d_x, int n, int c, int h, int w, const double* d_weights, int oc, int r,
+                        int stride, int pad, double* d_out, void* stream);
+/* sfc_report_sq_err against an fp64 reference. */
+int sfc_report_sq_err_f64(const double* d_out, const double* d_ref, int64_t n, double* host_sums, void* stream);
+
 /* Profiling hook of the timeline build (libsfc_b200_tl.so, `make TIMELINE=1`): out[8][3] =
  * per kernel {first CTA entry, first CTA past its dependency wait, last CTA exit} in
  * %globaltimer ns (0 / UINT64_MAX when the kernel did not run); reset re-arms the stamps.

@@ -240,7 +240,8 @@ size_t workspace_bytes(const ConvGeom& g, int F) {
 namespace sfcb200 {
 // Report sums for quantized_fast_conv2d (quant.cpp:283-291): sums[0] += sum (out - ref)^2,
 // sums[1] += sum ref^2 in fp64 (ref is the exact int8 direct conv).
-__global__ void __launch_bounds__(256) k_sq_err(const double* __restrict__ out, const int32_t* __restrict__ ref,
+template <class TR>
+__global__ void __launch_bounds__(256) k_sq_err(const double* __restrict__ out, const TR* __restrict__ ref,
                                                 long long n, double* __restrict__ sums) {
     double e = 0.0, s = 0.0;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -291,7 +292,14 @@ cudaError_t launch_zero_words(uint32_t* p, int words, cudaStream_t st) {
 cudaError_t launch_sq_err(const double* out, const int32_t* ref, long long n, double* sums, cudaStream_t st) {
     long long blocks = (n + 255) / 256;
     blocks = blocks > 4 * 148 ? 4 * 148 : (blocks < 1 ? 1 : blocks);
-    k_sq_err<<<int(blocks), 256, 0, st>>>(out, ref, n, sums);
+    k_sq_err<int32_t><<<int(blocks), 256, 0, st>>>(out, ref, n, sums);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sq_err_f64(const double* out, const double* ref, long long n, double* sums, cudaStream_t st) {
+    long long blocks = (n + 255) / 256;
+    blocks = blocks > 148 * 8 ? 148 * 8 : (blocks < 1 ? 1 : blocks);
+    k_sq_err<double><<<int(blocks), 256, 0, st>>>(out, ref, n, sums);
     return cudaGetLastError();
 }
 }  // namespace sfcb200

@@ -88,7 +88,7 @@ struct WsView {
     int8_t* vq;
     int32_t* P;
     int16_t* vkeep;  // V kept by sfc_act_transform for the streaming quantizer
-    int* vmaxf;      // general QuantConfig: per-frequency maxima
+    unsigned long long* vmaxf;  // general QuantConfig: maxima (fp64 bit patterns)
     double* act_scale;  // general QuantConfig: activation scales (1 or F)
 };
 WsView carve(void* ws, const ConvGeom& g, int F) {
@@ -98,8 +98,8 @@ WsView carve(void* ws, const ConvGeom& g, int F) {
     v.vmax = reinterpret_cast<int*>(base);
     v.sat = reinterpret_cast<unsigned long long*>(base + 8);
     v.qp = reinterpret_cast<QuantParams*>(base + 64);
-    v.vmaxf = reinterpret_cast<int*>(base + 1024);
-    v.act_scale = reinterpret_cast<double*>(base + 2048);
+    v.vmaxf = reinterpret_cast<unsigned long long*>(base + kWsMaxima);
+    v.act_scale = reinterpret_cast<double*>(base + kWsActScales);
     v.vq = reinterpret_cast<int8_t*>(base + up(kWsHeader));
     v.P = reinterpret_cast<int32_t*>(base + up(kWsHeader) + up(size_t(F) * g.Tpad * g.Cpad));
     v.vkeep = reinterpret_cast<int16_t*>(reinterpret_cast<uint8_t*>(v.P) + up(size_t(F) * g.Tpad * g.OCpad * 4));
@@ -426,11 +426,11 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
             if (o->y_int32 || o->y_int64)
                 throw Unsupported("y_int is defined only for PerTensor activation + PerChannel filter MinMax scales");
             if (L->act_scope == SFC_ACT_PER_FREQUENCY && L->F > 196) throw Unsupported("too many frequencies");
-            ck(cudaMemsetAsync(ws, 0, 1024 + sizeof(int) * L->F, S(stream)), "memset header");
+            ck(cudaMemsetAsync(ws, 0, kWsMaxima + sizeof(unsigned long long) * L->F, S(stream)), "memset header");
             ck(launch_act_absmax(L->variant, d_x, g, v.vmax, v.vkeep, S(stream), false), "absmax launch");
             const bool pf = L->act_scope == SFC_ACT_PER_FREQUENCY;
-            ck(launch_act_general(v.vkeep, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits,
-                                  pf ? v.vmaxf : v.vmax, v.act_scale, v.vq, v.sat, S(stream)),
+            ck(launch_act_general(v.vkeep, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits, v.vmaxf,
+                                  v.act_scale, v.vq, v.sat, S(stream)),
                "general activation launch");
             ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, S(stream), false), "gemm launch");
             OutPtrs op{nullptr, nullptr, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
@@ -548,6 +548,110 @@ int sfc_report_sq_err(const double* d_out, const int32_t* d_ref, int64_t n, doub
         ck(cudaMemcpyAsync(host_sums, d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, S(stream)), "copy");
         ck(cudaFreeAsync(d_sums, S(stream)), "free");
         ck(cudaStreamSynchronize(S(stream)), "sync");
+    });
+}
+
+int sfc_report_sq_err_f64(const double* d_out, const double* d_ref, int64_t n, double* host_sums, void* stream) {
+    return guarded([&] {
+        if (!d_out || !d_ref || !host_sums || n < 0) throw std::invalid_argument("bad report arguments");
+        void* d_sums = nullptr;
+        ck(cudaMallocAsync(&d_sums, 2 * sizeof(double), S(stream)), "alloc");
+        ck(cudaMemsetAsync(d_sums, 0, 2 * sizeof(double), S(stream)), "memset");
+        ck(launch_sq_err_f64(d_out, d_ref, n, static_cast<double*>(d_sums), S(stream)), "sq_err launch");
+        ck(cudaMemcpyAsync(host_sums, d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, S(stream)), "copy");
+        ck(cudaFreeAsync(d_sums, S(stream)), "free");
+        ck(cudaStreamSynchronize(S(stream)), "sync");
+    });
+}
+
+int sfc_direct_conv_f64(const double* d_x, int n, int c, int h, int w, const double* d_weights, int oc, int r,
+                        int stride, int pad, double* d_out, void* stream) {
+    return guarded([&] {
+        if (!d_x || !d_weights || !d_out) throw std::invalid_argument("null argument");
+        if (n <= 0 || c <= 0 || h <= 0 || w <= 0 || oc <= 0 || r <= 0 || stride < 1 || pad < 0)
+            throw std::invalid_argument("bad direct conv arguments");
+        if ((h + 2 * pad - r) / stride + 1 <= 0 || (w + 2 * pad - r) / stride + 1 <= 0 || h + 2 * pad < r ||
+            w + 2 * pad < r)
+            throw std::invalid_argument("filter larger than padded input");
+        ck(launch_direct_f64(d_x, n, c, h, w, d_weights, oc, r, stride, pad, d_out, S(stream)), "direct conv launch");
+    });
+}
+
+int sfc_layer_create_f64(sfc_plan_t plan, const double* d_w, int oc, int ic, int bits, int act_scope,
+                         int filter_scope, int search, void* stream, sfc_layer_t* out) {
+    sfc_layer* L = nullptr;
+    int rc = guarded([&] {
+        if (!plan || !d_w || !out) throw std::invalid_argument("null argument");
+        if (bits < 2 || bits > 16) throw std::invalid_argument("quantization width must be between 2 and 16 bits");
+        if (oc <= 0 || ic <= 0) throw std::invalid_argument("bad filter shape");
+        if (bits > 8) throw Unsupported("bits > 8 is not on the int8 tensor-core path yet");
+        if (act_scope < 0 || act_scope > 1 || filter_scope < 0 || filter_scope > 2 || search < 0 || search > 1)
+            throw std::invalid_argument("bad quantization config");
+        L = new sfc_layer();
+        L->act_scope = act_scope, L->filter_scope = filter_scope, L->search = search;
+        L->general = true;  // real-valued tensors: the fp64 epilogue (no integer y)
+        L->plan = plan->p;
+        L->variant = plan->p->variant;
+        L->OC = oc, L->IC = ic, L->bits = bits;
+        L->F = plan->p->K * plan->p->K;
+        ConvGeom g;
+        geom_init(g, L->variant, 1, ic, 8, 8, 1, oc);
+        L->BK = g.BK, L->Cpad = g.Cpad, L->BN = g.BN, L->OCpad = g.OCpad;
+        const int F = L->F;
+        L->n_fil_native = filter_scope == SFC_FIL_PER_CHANNEL ? oc : (filter_scope == SFC_FIL_PER_FREQUENCY ? F : oc * F);
+        const size_t uq_bytes = size_t(F) * L->OCpad * L->Cpad;
+        ck(cudaMalloc(&L->d_uq, uq_bytes), "cudaMalloc uq");
+        ck(cudaMalloc(&L->d_sf, sizeof(double) * oc), "cudaMalloc sf");
+        ck(cudaMalloc(&L->d_umax, sizeof(int) * oc), "cudaMalloc umax");
+        ck(cudaMalloc(&L->d_sat, sizeof(unsigned long long)), "cudaMalloc sat");
+        ck(cudaMalloc(&L->d_fil, sizeof(double) * size_t(oc) * F), "cudaMalloc fil");
+        ck(cudaMalloc(&L->d_fil_native, sizeof(double) * L->n_fil_native), "cudaMalloc fil native");
+        ck(cudaMemsetAsync(L->d_uq, 0, uq_bytes, S(stream)), "memset uq");
+        ck(cudaMemsetAsync(L->d_sat, 0, sizeof(unsigned long long), S(stream)), "memset sat");
+        ck(cudaMemsetAsync(L->d_umax, 0, sizeof(int) * oc, S(stream)), "memset umax");
+        ck(cudaMemsetAsync(L->d_sf, 0, sizeof(double) * oc, S(stream)), "memset sf");
+        double *U = nullptr, *err = nullptr;
+        ck(cudaMallocAsync(&U, sizeof(double) * size_t(oc) * ic * F, S(stream)), "alloc U");
+        ck(cudaMallocAsync(&err, sizeof(double) * size_t(L->n_fil_native) * 101, S(stream)), "alloc err");
+        ck(launch_filters_f64(L->variant, d_w, oc, ic, U, S(stream)), "fp64 filter transform launch");
+        ck(launch_fil_general_f64(U, oc, ic, F, filter_scope, search == SFC_SEARCH_MSE_GRID, bits, L->Cpad, L->OCpad,
+                                  L->d_fil_native, err, L->d_uq, L->d_fil, L->d_sat, S(stream)),
+           "general filter launch");
+        ck(cudaFreeAsync(U, S(stream)), "free U");
+        ck(cudaFreeAsync(err, S(stream)), "free err");
+        if (filter_scope == SFC_FIL_PER_CHANNEL)
+            ck(cudaMemcpyAsync(L->d_sf, L->d_fil_native, sizeof(double) * oc, cudaMemcpyDeviceToDevice, S(stream)),
+               "copy sf");
+        ck(cudaStreamSynchronize(S(stream)), "filter prepare");
+        *out = L;
+    });
+    if (rc != SFC_OK && L) sfc_layer_destroy(L);
+    return rc;
+}
+
+int sfc_conv_forward_f64(sfc_layer_t L, const double* d_x, int n, int h, int w, int pad, void* ws, size_t ws_bytes,
+                         const sfc_outputs* o, void* stream) {
+    return guarded([&] {
+        check_call(L, d_x, n, h, w, pad);
+        if (!ws || !o) throw std::invalid_argument("null argument");
+        if (!L->general) throw Unsupported("real-valued inputs need a layer from sfc_layer_create_f64 / _ex");
+        if (o->y_int32 || o->y_int64) throw Unsupported("y_int is not defined for real-valued tensors");
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
+        WsView v = carve(ws, g, L->F);
+        ck(cudaMemsetAsync(ws, 0, kWsMaxima + sizeof(unsigned long long) * L->F, S(stream)), "memset header");
+        double* Vd = nullptr;
+        ck(cudaMallocAsync(&Vd, sizeof(double) * size_t(L->F) * g.Tpad * g.Cpad, S(stream)), "alloc V");
+        ck(launch_act_f64(L->variant, d_x, g, Vd, S(stream)), "fp64 input transform launch");
+        const bool pf = L->act_scope == SFC_ACT_PER_FREQUENCY;
+        ck(launch_act_general_f64(Vd, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits, v.vmaxf, v.act_scale,
+                                  v.vq, v.sat, S(stream)),
+           "general activation launch");
+        ck(cudaFreeAsync(Vd, S(stream)), "free V");
+        ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, S(stream), false), "gemm launch");
+        OutPtrs op{nullptr, nullptr, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
+        op.gen_act = v.act_scale, op.gen_per_freq = pf ? 1 : 0, op.gen_fil = L->d_fil;
+        ck(launch_output(L->variant, 2, v.P, g, v.qp, L->d_sf, op, S(stream), false), "output launch");
     });
 }
 

@@ -156,6 +156,19 @@ DevBuf<int8_t> to_device_int8(const DenseTensor& t, const char* what) {
     return d;
 }
 
+bool int8_valued(const DenseTensor& t) {
+    for (double v : t.data)
+        if (!(v == std::nearbyint(v)) || v < -128.0 || v > 127.0) return false;
+    return true;
+}
+
+DevBuf<double> to_device_f64(const DenseTensor& t) {
+    DevBuf<double> d(t.data.size());
+    ck(cudaMemcpyAsync(d.p, t.data.data(), t.data.size() * sizeof(double), cudaMemcpyHostToDevice, stream()),
+       "copy to device");
+    return d;
+}
+
 template <class T>
 std::vector<T> to_host(const T* d, std::size_t n) {
     std::vector<T> h(n);
@@ -411,6 +424,48 @@ std::vector<double> frequency_energy(const DenseTensor& input, const AlgorithmSp
     return e;
 }
 
+// Real-valued tensors: V, U and the scales in the reference's own fp64 order on the device,
+// the int8 contraction and the fp64 epilogue (sfc_layer_create_f64 / sfc_conv_forward_f64).
+static QuantReport quantized_fast_conv2d_real(const DenseTensor& input, const DenseTensor& filters, const AlgorithmSpec& spec,
+                                       int padding, const QuantConfig& config, sfc_plan_t plan) {
+    const int B = input.dim(0), C = input.dim(1), H = input.dim(2), W = input.dim(3), OC = filters.dim(0);
+    const int HO = H + 2 * padding - spec.R + 1, WO = W + 2 * padding - spec.R + 1;
+    DevBuf<double> x = to_device_f64(input), w = to_device_f64(filters);
+    sfc_layer_t layer = nullptr;
+    check(sfc_layer_create_f64(plan, w.p, OC, C, config.bits, int(config.act_scope), int(config.filter_scope),
+                               int(config.search), stream(), &layer));
+    struct LayerGuard {
+        sfc_layer_t l;
+        ~LayerGuard() { sfc_layer_destroy(l); }
+    } lg{layer};
+    std::size_t ws_bytes = 0;
+    check(sfc_conv_workspace_size(layer, B, H, W, padding, &ws_bytes));
+    DevBuf<uint8_t> ws(ws_bytes);
+    QuantReport rep;
+    rep.output = DenseTensor({B, OC, HO, WO});
+    const std::size_t n = rep.output.data.size();
+    DevBuf<double> out(n), ref(n);
+    sfc_outputs o{};
+    o.out_f64 = out.p;
+    check(sfc_conv_forward_f64(layer, x.p, B, H, W, padding, ws.p, ws_bytes, &o, stream()));
+    check(sfc_direct_conv_f64(x.p, B, C, H, W, w.p, OC, spec.R, 1, padding, ref.p, stream()));
+    double sums[2] = {0.0, 0.0};
+    check(sfc_report_sq_err_f64(out.p, ref.p, int64_t(n), sums, stream()));
+    std::int64_t stats[6] = {};
+    check(sfc_conv_stats(layer, B, H, W, padding, ws.p, stats, stream()));
+    std::int64_t fsat = 0;
+    check(sfc_layer_saturations(layer, &fsat));
+    ck(cudaMemcpyAsync(rep.output.data.data(), out.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream()),
+       "copy output");
+    ck(cudaStreamSynchronize(stream()), "sync");
+    rep.mse = sums[0] / double(n);
+    rep.signal_energy = sums[1] / double(n);
+    rep.snr_db = 10.0 * std::log10(sums[1] / std::max(sums[0], 1e-300));
+    rep.saturations = stats[2] + fsat;
+    rep.values_quantized = stats[4];
+    return rep;
+}
+
 QuantReport quantized_fast_conv2d(const DenseTensor& input, const DenseTensor& filters, const AlgorithmSpec& spec,
                                   int padding, const QuantConfig& config) {
     if (config.bits < 2 || config.bits > 16)  // quant.cpp:155-156
@@ -422,6 +477,8 @@ QuantReport quantized_fast_conv2d(const DenseTensor& input, const DenseTensor& f
     if (HO <= 0 || WO <= 0) throw std::invalid_argument("filter larger than padded input");
 
     PlanGuard plan{plan_handle(spec)};
+    if (!int8_valued(input) || !int8_valued(filters))
+        return quantized_fast_conv2d_real(input, filters, spec, padding, config, plan.p);
     DevBuf<int8_t> x = to_device_int8(input, "input"), w = to_device_int8(filters, "filters");
     sfc_layer_t layer = nullptr;
     check(sfc_layer_create_ex(plan.p, w.p, OC, C, config.bits, int(config.act_scope), int(config.filter_scope),

@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "sfc_kernels.hpp"
+#include "sfc_tables.cuh"
 
 namespace sfcb200 {
 
@@ -48,17 +49,18 @@ __device__ __forceinline__ FilGroup fil_group(int scope, int g, int OC, int IC, 
 // One warp per group, lane = candidate chunk: absmax (exact, order-free), then for
 // MseGrid the 101 candidate errors (lanes 0..31 take candidates lane, lane+32, ...).
 // err_out[g * kCands + cand]; scale_out[g] is the MinMax scale (the MseGrid pick follows).
-__global__ void __launch_bounds__(32) k_fil_scales(const int32_t* __restrict__ U, int OC, int IC, int F, int scope,
+template <class TU>
+__global__ void __launch_bounds__(32) k_fil_scales(const TU* __restrict__ U, int OC, int IC, int F, int scope,
                                                    int mse, int bits, double* __restrict__ scale_out,
                                                    double* __restrict__ err_out) {
     const int g = blockIdx.x, lane = threadIdx.x;
     const FilGroup G = fil_group(scope, g, OC, IC, F);
-    int amax = 0;
-    for (long long i = lane; i < G.count; i += 32) amax = max(amax, abs(U[G.base + i * G.stride]));
+    double amax = 0.0;  // exact and order-free (group_absmax, quant.cpp:13-17)
+    for (long long i = lane; i < G.count; i += 32) amax = fmax(amax, fabs(double(U[G.base + i * G.stride])));
 #pragma unroll
-    for (int o = 16; o; o >>= 1) amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     const double qmax = double((1 << (bits - 1)) - 1), qmin = -qmax - 1.0;
-    const double base = fmax(double(amax) / qmax, 1e-8);
+    const double base = fmax(amax / qmax, 1e-8);
     if (lane == 0) scale_out[g] = base;
     if (!mse) return;
     for (int c0 = 0; c0 < kCands; c0 += 32) {
@@ -87,7 +89,8 @@ __global__ void k_pick_best(int groups, const double* __restrict__ err, double* 
 
 // uq[f][oc][ic] = quantize_value(U, fil(oc, f)) (quant.cpp:221-229) and the expanded table
 // fil_full[oc * F + f] the fp64 output epilogue reads.
-__global__ void k_fil_quantize(const int32_t* __restrict__ U, int OC, int IC, int F, int scope,
+template <class TU>
+__global__ void k_fil_quantize(const TU* __restrict__ U, int OC, int IC, int F, int scope,
                                const double* __restrict__ scale, int bits, int Cpad, int OCpad,
                                int8_t* __restrict__ uqB, double* __restrict__ fil_full,
                                unsigned long long* __restrict__ sat) {
@@ -96,35 +99,40 @@ __global__ void k_fil_quantize(const int32_t* __restrict__ U, int OC, int IC, in
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const int f = int(i % F), ic = int((i / F) % IC), oc = int(i / ((long long)F * IC));
         const double s = scope == 0 ? scale[oc] : (scope == 1 ? scale[f] : scale[(long long)oc * F + f]);
-        uqB[((long long)f * OCpad + oc) * Cpad + ic] = int8_t(clamp_q(exact_q(U[i], s), qmax, sat));
+        uqB[((long long)f * OCpad + oc) * Cpad + ic] =
+            int8_t(clamp_q(int(rint(__ddiv_rn(double(U[i]), s))), qmax, sat));
         if (ic == 0) fil_full[(long long)oc * F + f] = s;
     }
 }
 
 // Per-frequency max|V| over the kept V [F][Tpad][Cpad] (t < T, c < C): vmaxf[f].
-__global__ void __launch_bounds__(256) k_act_fmax(const int16_t* __restrict__ V, ConvGeom g, int F,
-                                                  int* __restrict__ vmaxf) {
+// (maxima as the bit patterns of non-negative doubles, which order like the values)
+template <class TV>
+__global__ void __launch_bounds__(256) k_act_fmax(const TV* __restrict__ V, ConvGeom g, int F, int per_freq,
+                                                  unsigned long long* __restrict__ vmaxf) {
     const int f = blockIdx.y;
     const long long n = (long long)g.T * g.C;
-    int m = 0;
+    double m = 0.0;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const long long t = i / g.C, c = i % g.C;
-        m = max(m, abs(int(V[((long long)f * g.Tpad + t) * g.Cpad + c])));
+        m = fmax(m, fabs(double(V[((long long)f * g.Tpad + t) * g.Cpad + c])));
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(&vmaxf[f], m);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0)
+        atomicMax(&vmaxf[per_freq ? f : 0], (unsigned long long)__double_as_longlong(m));
 }
 
 // Activation scales from the maxima: MinMax, or MseGrid over the group's V in the
 // reference's order (quant.cpp:168-181: PerTensor = all of g.v in (tile, c, f) order,
 // PerFrequency = (tile, c) for one f).  One block of 4 warps per group; lane = candidate.
-__global__ void __launch_bounds__(128) k_act_scales(const int16_t* __restrict__ V, ConvGeom g, int F, int per_freq,
-                                                    const int* __restrict__ vmax, int mse, int bits,
+template <class TV>
+__global__ void __launch_bounds__(128) k_act_scales(const TV* __restrict__ V, ConvGeom g, int F, int per_freq,
+                                                    const unsigned long long* __restrict__ vmax, int mse, int bits,
                                                     double* __restrict__ act_scale) {
     const int grp = blockIdx.x, cand = threadIdx.x;
     const double qmax = double((1 << (bits - 1)) - 1), qmin = -qmax - 1.0;
-    const double base = fmax(double(vmax[per_freq ? grp : 0]) / qmax, 1e-8);
+    const double base = fmax(__longlong_as_double((long long)vmax[per_freq ? grp : 0]) / qmax, 1e-8);
     __shared__ double s_err[kCands];
     if (!mse) {
         if (cand == 0) act_scale[grp] = base;
@@ -134,7 +142,7 @@ __global__ void __launch_bounds__(128) k_act_scales(const int16_t* __restrict__ 
     double err = 0.0;
     const long long tc = (long long)g.T * g.C;
     if (per_freq) {
-        const int16_t* Vf = V + (long long)grp * g.Tpad * g.Cpad;
+        const TV* Vf = V + (long long)grp * g.Tpad * g.Cpad;
         for (long long i = 0; i < tc; ++i) {
             const long long t = i / g.C, c = i - t * g.C;
             err = __dadd_rn(err, mse_term(double(Vf[t * g.Cpad + c]), s, qmax, qmin));
@@ -157,7 +165,8 @@ __global__ void __launch_bounds__(128) k_act_scales(const int16_t* __restrict__ 
 }
 
 // vq[f][t][c] = quantize_value(V, sa(f)) (quant.cpp:242-250) for t < T, c < C (else 0).
-__global__ void __launch_bounds__(256) k_quant_general(const int16_t* __restrict__ V, ConvGeom g, int F,
+template <class TV>
+__global__ void __launch_bounds__(256) k_quant_general(const TV* __restrict__ V, ConvGeom g, int F,
                                                        int per_freq, const double* __restrict__ act_scale, int bits,
                                                        int8_t* __restrict__ vqA, unsigned long long* __restrict__ sat) {
     const int f = blockIdx.y;
@@ -167,32 +176,202 @@ __global__ void __launch_bounds__(256) k_quant_general(const int16_t* __restrict
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const long long t = i / g.Cpad, c = i - t * g.Cpad;
         const long long off = ((long long)f * g.Tpad + t) * g.Cpad + c;
-        vqA[off] = c < g.C ? int8_t(clamp_q(exact_q(V[off], s), qmax, sat)) : int8_t(0);
+        vqA[off] = c < g.C ? int8_t(clamp_q(int(rint(__ddiv_rn(double(V[off]), s))), qmax, sat)) : int8_t(0);
     }
 }
 
+// ---------------------------------------------------------------- real-valued inputs
+// V = B^T x B for fp64 inputs in gather_tiles' exact order (quant.cpp:76-89): sequential
+// sums over k, coefficients in {-1, 0, 1} (exact products, zero terms skipped: adding an
+// exact zero leaves the value unchanged).  One thread per (tile, channel); V [F][Tpad][Cpad].
+template <int V>
+__global__ void __launch_bounds__(128) k_act_f64(const double* __restrict__ x, ConvGeom g, double* __restrict__ Vd) {
+    using T = Tab<V>;
+    constexpr int n = T::n, K = T::K, M = T::M;
+    const long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= (long long)g.T * g.C) return;
+    const int c = int(item % g.C), t = int(item / g.C);
+    const int tj = t % g.tw, ti = (t / g.tw) % g.th, b = t / (g.tw * g.th);
+    const int ih0 = ti * M - g.pad, iw0 = tj * M - g.pad;
+    const double* xc = x + ((size_t)b * g.C + c) * g.H * g.W;
+    double win[n][n];
+#pragma unroll
+    for (int r = 0; r < n; ++r)
+#pragma unroll
+        for (int s2 = 0; s2 < n; ++s2) {
+            const int ih = ih0 + r, iw = iw0 + s2;
+            win[r][s2] = (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W) ? xc[(size_t)ih * g.W + iw] : 0.0;
+        }
+    for (int i = 0; i < K; ++i) {
+        double tmp[n];
+#pragma unroll
+        for (int j = 0; j < n; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < n; ++k) {
+                const int bt = T::bt(i, k);
+                if (bt) acc = __dadd_rn(acc, bt > 0 ? win[k][j] : -win[k][j]);
+            }
+            tmp[j] = acc;
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < n; ++k) {
+                const int bt = T::bt(j, k);
+                if (bt) acc = __dadd_rn(acc, bt > 0 ? tmp[k] : -tmp[k]);
+            }
+            Vd[((size_t)(i * K + j) * g.Tpad + t) * g.Cpad + c] = acc;
+        }
+    }
+}
+
+// U = G f G^T for fp64 filters in transform_filters' order (conv.cpp:362-380); U [OC][IC][F].
+template <int V>
+__global__ void __launch_bounds__(128) k_filters_f64(const double* __restrict__ w, int OC, int IC,
+                                                     double* __restrict__ U) {
+    using T = Tab<V>;
+    constexpr int R = T::R, K = T::K;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)OC * IC) return;
+    const double* f = w + idx * R * R;
+    double tmp[K][R];
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const int gk = T::g(i, k);
+                if (gk) acc = __dadd_rn(acc, gk > 0 ? f[k * R + j] : -f[k * R + j]);
+            }
+            tmp[i][j] = acc;
+        }
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const int gk = T::g(j, k);
+                if (gk) acc = __dadd_rn(acc, gk > 0 ? tmp[i][k] : -tmp[i][k]);
+            }
+            U[idx * T::F + i * K + j] = acc;
+        }
+}
+
+// direct_conv2d (conv.cpp:320-350) in fp64, one output per thread, the reference's loop order.
+__global__ void __launch_bounds__(256) k_direct_f64(const double* __restrict__ x, int B, int C, int H, int W,
+                                                    const double* __restrict__ w, int OC, int R, int stride, int pad,
+                                                    int HO, int WO, double* __restrict__ out) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)B * OC * HO * WO) return;
+    const int ow = int(idx % WO), oh = int((idx / WO) % HO), oc = int((idx / ((long long)WO * HO)) % OC);
+    const int b = int(idx / ((long long)WO * HO * OC));
+    double acc = 0.0;
+    for (int ic = 0; ic < C; ++ic)
+        for (int fr = 0; fr < R; ++fr) {
+            const int ih = oh * stride - pad + fr;
+            if (ih < 0 || ih >= H) continue;
+            for (int fc = 0; fc < R; ++fc) {
+                const int iw = ow * stride - pad + fc;
+                if (iw < 0 || iw >= W) continue;
+                acc = __dadd_rn(acc, __dmul_rn(x[((size_t(b) * C + ic) * H + ih) * W + iw],
+                                               w[((size_t(oc) * C + ic) * R + fr) * R + fc]));
+            }
+        }
+    out[idx] = acc;
+}
+
 // ============================================================================ host
-cudaError_t launch_fil_general(const int32_t* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
-                               int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
-                               unsigned long long* sat, cudaStream_t st) {
+namespace {
+template <class TU>
+cudaError_t fil_general(const TU* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad, int OCpad,
+                        double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full, unsigned long long* sat,
+                        cudaStream_t st) {
     const int groups = scope == 0 ? OC : (scope == 1 ? F : OC * F);
-    k_fil_scales<<<groups, 32, 0, st>>>(U, OC, IC, F, scope, mse, bits, scale_native, err_tmp);
+    k_fil_scales<TU><<<groups, 32, 0, st>>>(U, OC, IC, F, scope, mse, bits, scale_native, err_tmp);
     if (mse) k_pick_best<<<(groups + 127) / 128, 128, 0, st>>>(groups, err_tmp, scale_native);
     const long long n = (long long)OC * IC * F;
     const int blocks = int((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
-    k_fil_quantize<<<blocks, 256, 0, st>>>(U, OC, IC, F, scope, scale_native, bits, Cpad, OCpad, uqB, fil_full, sat);
+    k_fil_quantize<TU><<<blocks, 256, 0, st>>>(U, OC, IC, F, scope, scale_native, bits, Cpad, OCpad, uqB, fil_full,
+                                               sat);
     return cudaGetLastError();
 }
 
-cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
-                               int* vmaxf, double* act_scale, int8_t* vqA, unsigned long long* sat, cudaStream_t st) {
+template <class TV>
+cudaError_t act_general(const TV* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
+                        unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                        cudaStream_t st) {
     const long long n = (long long)g.T * g.C;
     const int bx = int((n + 255) / 256 < 64 ? (n + 255) / 256 : 64);
-    if (per_freq) k_act_fmax<<<dim3(bx, F), 256, 0, st>>>(V, g, F, vmaxf);
-    k_act_scales<<<per_freq ? F : 1, 128, 0, st>>>(V, g, F, per_freq, vmaxf, mse, bits, act_scale);
+    k_act_fmax<TV><<<dim3(bx, F), 256, 0, st>>>(V, g, F, per_freq, vmax);
+    k_act_scales<TV><<<per_freq ? F : 1, 128, 0, st>>>(V, g, F, per_freq, vmax, mse, bits, act_scale);
     const long long nq = (long long)g.T * g.Cpad;
     const int bq = int((nq + 255) / 256 < 64 ? (nq + 255) / 256 : 64);
-    k_quant_general<<<dim3(bq, F), 256, 0, st>>>(V, g, F, per_freq, act_scale, bits, vqA, sat);
+    k_quant_general<TV><<<dim3(bq, F), 256, 0, st>>>(V, g, F, per_freq, act_scale, bits, vqA, sat);
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_fil_general(const int32_t* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
+                               int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
+                               unsigned long long* sat, cudaStream_t st) {
+    return fil_general(U, OC, IC, F, scope, mse, bits, Cpad, OCpad, scale_native, err_tmp, uqB, fil_full, sat, st);
+}
+
+cudaError_t launch_fil_general_f64(const double* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
+                                   int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
+                                   unsigned long long* sat, cudaStream_t st) {
+    return fil_general(U, OC, IC, F, scope, mse, bits, Cpad, OCpad, scale_native, err_tmp, uqB, fil_full, sat, st);
+}
+
+cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
+                               unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                               cudaStream_t st) {
+    return act_general(V, g, F, per_freq, mse, bits, vmax, act_scale, vqA, sat, st);
+}
+
+cudaError_t launch_act_general_f64(const double* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
+                                   unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                                   cudaStream_t st) {
+    return act_general(V, g, F, per_freq, mse, bits, vmax, act_scale, vqA, sat, st);
+}
+
+cudaError_t launch_act_f64(int variant, const double* x, const ConvGeom& g, double* Vd, cudaStream_t st) {
+    const long long n = (long long)g.T * g.C;
+    const int blocks = int((n + 127) / 128);
+    switch (variant) {
+        case 0: k_act_f64<0><<<blocks, 128, 0, st>>>(x, g, Vd); break;
+        case 1: k_act_f64<1><<<blocks, 128, 0, st>>>(x, g, Vd); break;
+        case 2: k_act_f64<2><<<blocks, 128, 0, st>>>(x, g, Vd); break;
+        case 3: k_act_f64<3><<<blocks, 128, 0, st>>>(x, g, Vd); break;
+        default: k_act_f64<4><<<blocks, 128, 0, st>>>(x, g, Vd); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_filters_f64(int variant, const double* w, int OC, int IC, double* U, cudaStream_t st) {
+    const long long n = (long long)OC * IC;
+    const int blocks = int((n + 127) / 128);
+    switch (variant) {
+        case 0: k_filters_f64<0><<<blocks, 128, 0, st>>>(w, OC, IC, U); break;
+        case 1: k_filters_f64<1><<<blocks, 128, 0, st>>>(w, OC, IC, U); break;
+        case 2: k_filters_f64<2><<<blocks, 128, 0, st>>>(w, OC, IC, U); break;
+        case 3: k_filters_f64<3><<<blocks, 128, 0, st>>>(w, OC, IC, U); break;
+        default: k_filters_f64<4><<<blocks, 128, 0, st>>>(w, OC, IC, U); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_direct_f64(const double* x, int B, int C, int H, int W, const double* w, int OC, int R, int stride,
+                              int pad, double* out, cudaStream_t st) {
+    const int HO = (H + 2 * pad - R) / stride + 1, WO = (W + 2 * pad - R) / stride + 1;
+    const long long n = (long long)B * OC * HO * WO;
+    k_direct_f64<<<int((n + 255) / 256), 256, 0, st>>>(x, B, C, H, W, w, OC, R, stride, pad, HO, WO, out);
     return cudaGetLastError();
 }
 

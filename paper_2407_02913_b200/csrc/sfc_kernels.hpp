@@ -30,9 +30,9 @@ struct QuantParams {
 };
 
 void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, int OC);
-// Workspace header: vmax @0, saturations @8, QuantParams @64, per-frequency maxima @1024
-// (int32 x F), activation scales @2048 (fp64 x F); F <= 196.
-constexpr size_t kWsHeader = 4096;
+// Workspace header: vmax @0, saturations @8, QuantParams @64; general QuantConfig:
+// maxima @512 (fp64 bit patterns x F), activation scales @2304 (fp64 x F); F <= 196.
+constexpr size_t kWsHeader = 4096, kWsMaxima = 512, kWsActScales = 2304;
 size_t workspace_bytes(const ConvGeom& g, int F);
 
 // `pdl`: launch with programmatic stream serialization (overlap the predecessor's tail).
@@ -92,6 +92,7 @@ struct OutPtrs {
 cudaError_t launch_output(int variant, int mode, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
 cudaError_t launch_sq_err(const double* out, const int32_t* ref, long long n, double* sums, cudaStream_t st);
+cudaError_t launch_sq_err_f64(const double* out, const double* ref, long long n, double* sums, cudaStream_t st);
 // Device table of verified quantizer parameters (common.cuh, kQpTableMax).  build=true
 // derives it synchronously on a private stream the first time (layer creation -- never
 // inside a graph capture); build=false returns it or nullptr (kernels then derive per CTA).
@@ -111,10 +112,22 @@ cudaError_t launch_transform_filters(int variant, const int8_t* w, int OC, int I
 cudaError_t launch_fil_general(const int32_t* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
                                int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
                                unsigned long long* sat, cudaStream_t st);
-// Activations from the kept V: per-frequency maxima (per_freq), MinMax / MseGrid scales
-// act_scale[1 or F] and vq (exact fp64 quantizer, saturations counted).  vmax: the global
-// max (PerTensor) or F zeroed slots (PerFrequency).
-cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits, int* vmax,
-                               double* act_scale, int8_t* vqA, unsigned long long* sat, cudaStream_t st);
+// Activations from the kept V: maxima (1 or F slots, zeroed on entry; fp64 bit patterns),
+// MinMax / MseGrid scales act_scale[1 or F] and vq (exact fp64 quantizer, saturations counted).
+cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
+                               unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                               cudaStream_t st);
+// Real-valued (fp64) inputs and filters, the reference's own arithmetic order:
+// V [F][Tpad][Cpad] (gather_tiles), U [OC][IC][F] (transform_filters), direct conv.
+cudaError_t launch_act_general_f64(const double* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
+                                   unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                                   cudaStream_t st);
+cudaError_t launch_fil_general_f64(const double* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
+                                   int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
+                                   unsigned long long* sat, cudaStream_t st);
+cudaError_t launch_act_f64(int variant, const double* x, const ConvGeom& g, double* Vd, cudaStream_t st);
+cudaError_t launch_filters_f64(int variant, const double* w, int OC, int IC, double* U, cudaStream_t st);
+cudaError_t launch_direct_f64(const double* x, int B, int C, int H, int W, const double* w, int OC, int R, int stride,
+                              int pad, double* out, cudaStream_t st);
 
 }  // namespace sfcb200

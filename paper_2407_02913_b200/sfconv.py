@@ -183,6 +183,23 @@ def scale_mse_grid(values, bits: int) -> float:
 
 
 # ----------------------------------------------------------------------------------- device
+def is_int8_valued(t) -> bool:
+    """True if every value of t is an integer in [-128, 127] (the int8 fast path applies)."""
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(np.asarray(t))
+    if t.dtype == torch.int8:
+        return True
+    td = t.to(torch.float64)
+    return bool(torch.all(td == torch.round(td))) and not bool((td < -128).any()) and not bool((td > 127).any())
+
+
+def as_f64_device(t, device=None) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(np.asarray(t))
+    dev = device or (t.device if t.is_cuda else torch.device("cuda", torch.cuda.current_device()))
+    return t.to(dev, torch.float64).contiguous()
+
+
 def as_int8_device(t, what: str, device=None) -> torch.Tensor:
     """Accept int8 tensors as-is; accept other dtypes only if every value is an int8 integer."""
     if not isinstance(t, torch.Tensor):
@@ -201,22 +218,25 @@ class SfcLayer:
 
     def __init__(self, spec: AlgorithmSpec | str, filters: torch.Tensor, bits: int = 8,
                  filter_scope: int = FilterScaleScope.PerChannel, search: int = ScaleSearch.MinMax, stream=None,
-                 act_scope: int = ActScaleScope.PerTensor):
+                 act_scope: int = ActScaleScope.PerTensor, real: bool = False):
+        """real=True: fp64 filters of any value (sfc_layer_create_f64, the reference's own
+        arithmetic order); the layer then runs the fp64 epilogue (no y_int)."""
         self.spec = catalog_algorithm(spec) if isinstance(spec, str) else spec
         if filters.dim() != 4 or filters.shape[2] != self.spec.R or filters.shape[3] != self.spec.R:
             raise ValueError("filter shape does not match algorithm")
-        w = as_int8_device(filters, "filters")
+        w = as_f64_device(filters) if real else as_int8_device(filters, "filters")
         self.device = w.device
         self.OC, self.IC = int(w.shape[0]), int(w.shape[1])
         self.bits = bits
         self.act_scope, self.filter_scope, self.search = int(act_scope), int(filter_scope), int(search)
         # anything but {PerTensor, PerChannel, MinMax} is the fp64 parity path (no y_int)
-        self.general = (self.act_scope, self.filter_scope, self.search) != (0, 0, 0)
+        self.general = real or (self.act_scope, self.filter_scope, self.search) != (0, 0, 0)
+        self.real = real
         h = ctypes.c_void_p()
+        create = lib().sfc_layer_create_f64 if real else lib().sfc_layer_create_ex
         with torch.cuda.device(self.device):
-            check(lib().sfc_layer_create_ex(ctypes.c_void_p(self.spec._handle), _ptr(w), self.OC, self.IC, bits,
-                                            self.act_scope, self.filter_scope, self.search,
-                                            ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(h)))
+            check(create(ctypes.c_void_p(self.spec._handle), _ptr(w), self.OC, self.IC, bits, self.act_scope,
+                         self.filter_scope, self.search, ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(h)))
         self._h = h
 
     def __del__(self):
@@ -317,6 +337,17 @@ class SfcLayer:
         check(lib().sfc_conv_forward(self._h, _ptr(x), n, h, w, pad, _ptr(ws), ws.numel(), ctypes.byref(o),
                                      ctypes.c_void_p(_stream_ptr(stream))))
 
+    def forward_f64(self, x: torch.Tensor, ws: torch.Tensor, pad: int, out_f32=None, out_f64=None, out_i8=None,
+                    requant_scale: float = 0.0, stream=None):
+        """Real-valued fp64 input x (sfc_conv_forward_f64)."""
+        n, c, h, w = x.shape
+        if c != self.IC:
+            raise ValueError("input channel count does not match filters")
+        x = as_f64_device(x, self.device)
+        o = Outputs(None, None, _ptr(out_f32), _ptr(out_f64), _ptr(out_i8), float(requant_scale))
+        check(lib().sfc_conv_forward_f64(self._h, _ptr(x), n, h, w, pad, _ptr(ws), ws.numel(), ctypes.byref(o),
+                                         ctypes.c_void_p(_stream_ptr(stream))))
+
     def stats(self, n, h, w, pad, ws, stream=None) -> dict:
         s = np.zeros(6, np.int64)
         check(lib().sfc_conv_stats(self._h, n, h, w, pad, _ptr(ws), s.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
@@ -401,11 +432,19 @@ def frequency_energy(input, spec: AlgorithmSpec, padding: int = 0) -> np.ndarray
     return s.cpu().numpy().astype(np.float64) / float(groups)
 
 
+def _snr_db(sig: float, err: float) -> float:
+    """10 log10(sig / max(err, 1e-300)) with C++ semantics (log10(0) = -inf; quant.cpp:291)."""
+    r = sig / max(err, 1e-300)
+    return 10.0 * math.log10(r) if r > 0 else float("-inf")
+
+
 def quantized_fast_conv2d(input, filters, spec: AlgorithmSpec, padding: int, config: QuantConfig = QuantConfig(),
                           report: bool = True) -> QuantReport:
     """quant.cpp:152-293 on the device.  Raises ValueError for bits outside [2, 16] (quant.cpp:155-156)."""
     if config.bits < 2 or config.bits > 16:
         raise ValueError("quantization width must be between 2 and 16 bits")
+    if not (is_int8_valued(input) and is_int8_valued(filters)):
+        return _quantized_fast_conv2d_real(input, filters, spec, padding, config, report)
     x = as_int8_device(input, "input")
     if x.dim() != 4 or filters.dim() != 4:
         raise ValueError("conv2d expects 4-d NCHW tensors")
@@ -450,5 +489,42 @@ def quantized_fast_conv2d(input, filters, spec: AlgorithmSpec, padding: int, con
         n = out64.numel()
         rep.mse = err / n
         rep.signal_energy = sig / n
-        rep.snr_db = 10.0 * math.log10(sig / max(err, 1e-300))
+        rep.snr_db = _snr_db(sig, err)
+    return rep
+
+
+def _quantized_fast_conv2d_real(input, filters, spec: AlgorithmSpec, padding: int, config: QuantConfig,
+                                report: bool) -> QuantReport:
+    """Real-valued tensors (the reference API's doubles): V, U, scales, vq / uq / pacc exactly
+    as the reference computes them, the fp64 epilogue; output is float64 like DenseTensor."""
+    x = as_f64_device(input)
+    w = as_f64_device(filters, x.device)
+    if x.dim() != 4 or w.dim() != 4:
+        raise ValueError("conv2d expects 4-d NCHW tensors")
+    if w.shape[1] != x.shape[1]:
+        raise ValueError("input channel count does not match filters")
+    B, C, H, W = x.shape
+    if H + 2 * padding - spec.R + 1 <= 0 or W + 2 * padding - spec.R + 1 <= 0:
+        raise ValueError("filter larger than padded input")
+    layer = SfcLayer(spec, w, config.bits, config.filter_scope, config.search, act_scope=config.act_scope, real=True)
+    HO, WO = H + 2 * padding - spec.R + 1, W + 2 * padding - spec.R + 1
+    ws = layer.workspace(B, H, W, padding)
+    out = torch.empty((B, layer.OC, HO, WO), dtype=torch.float64, device=x.device)
+    layer.forward_f64(x, ws, padding, out_f64=out)
+    st = layer.stats(B, H, W, padding, ws)
+    acts = layer.act_scales(B, H, W, padding, ws)
+    rep = QuantReport(output=out, y_int=None, act_scale=float(acts[0]) if len(acts) == 1 else acts,
+                      filter_scales=layer.filter_scales_native(),
+                      saturations=st["saturations"] + layer.filter_saturations(),
+                      values_quantized=st["values_quantized"])
+    if report:  # quant.cpp:282-291 against the fp64 direct conv (reference summation order)
+        ref = torch.empty_like(out)
+        check(lib().sfc_direct_conv_f64(_ptr(x), B, C, H, W, _ptr(w), layer.OC, spec.R, 1, padding, _ptr(ref),
+                                        ctypes.c_void_p(_stream_ptr())))
+        sums = (ctypes.c_double * 2)()
+        check(lib().sfc_report_sq_err_f64(_ptr(out), _ptr(ref), out.numel(), sums, ctypes.c_void_p(_stream_ptr())))
+        n = out.numel()
+        rep.mse = sums[0] / n
+        rep.signal_energy = sums[1] / n
+        rep.snr_db = _snr_db(sums[1], sums[0])
     return rep

@@ -95,9 +95,43 @@ def large_r():
     print("wrote", len(arrays), "large-R arrays")
 
 
+# (tag, B, C, OC, H, W, act_scope, filter_scope, search, bits) with real-valued N(0, 1)
+# inputs and filters, the values the reference CLI's quantsim feeds (sfconv_cli.cpp:299-300)
+REAL_CASES = [
+    ("real_default", 1, 5, 4, 12, 12, 0, 0, 0, 8),
+    ("real_actfreq", 2, 3, 3, 10, 11, 1, 0, 0, 8),
+    ("real_chfreq_mse", 1, 4, 3, 9, 9, 0, 2, 1, 6),
+    ("real_freq_bits4", 1, 3, 2, 11, 10, 1, 1, 0, 4),
+]
+
+
+def real_valued():
+    """tests/golden/qconv_real.npz: real-valued inputs / filters for every SFC variant."""
+    arrays = {}
+    rng = np.random.default_rng(0x5FC2)
+    for tag, B, C, OC, H, W, asc, fsc, srch, bits in REAL_CASES:
+        x = rng.normal(size=(B, C, H, W))
+        arrays[f"{tag}/x"] = x
+        arrays[f"{tag}/meta"] = np.array([asc, fsc, srch, bits], np.int64)
+        for v in VARIANTS + LARGE_R:
+            R = ob.spec(v, source="ref")["R"]
+            w = rng.normal(size=(OC, C, R, R))
+            pad = R // 2
+            out, rep = ob.ref_quantized_fast_conv2d(x, w, v, pad, bits, asc, fsc, srch)
+            arrays[f"{tag}/{v}/w"] = w
+            arrays[f"{tag}/{v}/out"] = out
+            arrays[f"{tag}/{v}/report"] = np.array([rep["mse"], rep["signal_energy"], rep["snr_db"],
+                                                    rep["saturations"], rep["values_quantized"], pad], np.float64)
+            arrays[f"{tag}/{v}/direct"] = ob.ref_direct_conv2d(x, w, pad)
+    np.savez_compressed(os.path.join(HERE, "qconv_real.npz"), **arrays)
+    print("wrote", len(arrays), "real-valued arrays")
+
+
 def main():
     if "--large-r" in sys.argv:
         return large_r()
+    if "--real" in sys.argv:
+        return real_valued()
     if not ob.ref_available():
         raise SystemExit("oracle/_ref/libsfconv_ref.so missing: run `make -C oracle` with /root/reference present")
     js, h = ob.ref_catalog_json()

@@ -281,8 +281,10 @@ def test_errors_like_reference(cuda):
         sc.quantized_fast_conv2d(torch.zeros((1, 2, 8, 8), dtype=torch.int8), f, spec, 1)
     with pytest.raises(ValueError, match="filter larger than padded input"):
         sc.quantized_fast_conv2d(torch.zeros((1, 1, 2, 2), dtype=torch.int8), f, spec, 0)
-    with pytest.raises(ValueError, match="int8-valued"):
-        sc.quantized_fast_conv2d(torch.full((1, 1, 8, 8), 0.5), f, spec, 1)
+    # fractional values take the real-valued path (no longer refused); the reference's output
+    # for a constant 0.5 input and a zero filter is exactly 0
+    rep = sc.quantized_fast_conv2d(torch.full((1, 1, 8, 8), 0.5), f, spec, 1)
+    assert rep.output.dtype == torch.float64 and float(rep.output.abs().max()) == 0.0
     with pytest.raises(_lib.SfcUnsupported):
         sc.quantized_fast_conv2d(x, f, spec, 1, sc.QuantConfig(bits=12))
 
@@ -457,3 +459,36 @@ def test_general_quant_config_vs_oracle(cuda, variant, cfg):
     assert st["saturations"] + layer.filter_saturations() == r["report"]["saturations"]
     with pytest.raises(_lib.SfcUnsupported):  # y_int is not defined for these configurations
         layer.forward(xt, ws, pad, y_int32=torch.empty((B, OC, HO, WO), dtype=torch.int32, device=dev))
+
+
+# ------------------------------------------------------------------------------ real-valued tensors
+GOLD_REAL = np.load(os.path.join(HERE, "golden", "qconv_real.npz"))
+TAGS_REAL = sorted({k.split("/")[0] for k in GOLD_REAL.files})
+
+
+@pytest.mark.parametrize("variant", VARIANTS + LARGE_R)
+@pytest.mark.parametrize("tag", TAGS_REAL)
+def test_real_valued_tensors_vs_reference_golden(cuda, tag, variant):
+    """The reference API's doubles (N(0,1) inputs and filters, as the reference CLI's quantsim
+    feeds): V and U in the reference's arithmetic order, so scales / vq / uq / pacc are the
+    reference's and the fp64 output agrees to the epilogue's rounding (<= 1e-12)."""
+    x = GOLD_REAL[f"{tag}/x"]
+    asc, fsc, srch, bits = (int(v) for v in GOLD_REAL[f"{tag}/meta"])
+    w = GOLD_REAL[f"{tag}/{variant}/w"]
+    r = GOLD_REAL[f"{tag}/{variant}/report"]
+    pad = int(r[5])
+    rep = sc.quantized_fast_conv2d(torch.from_numpy(x), torch.from_numpy(w), sc.catalog_algorithm(variant), pad,
+                                   sc.QuantConfig(bits, asc, fsc, srch))
+    assert rep.output.dtype == torch.float64
+    assert maxrel(rep.output.cpu().numpy(), GOLD_REAL[f"{tag}/{variant}/out"]) <= 1e-12
+    assert rep.saturations == r[3] and rep.values_quantized == r[4]
+    assert rep.mse == pytest.approx(r[0], rel=1e-9) and rep.snr_db == pytest.approx(r[2], rel=1e-9)
+    # the fp64 direct conv in the reference's summation order is bitwise the reference's
+    B, C, H, W = x.shape
+    OC, R = w.shape[0], w.shape[2]
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    out = torch.empty((B, OC, H + 2 * pad - R + 1, W + 2 * pad - R + 1), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().sfc_direct_conv_f64(ctypes.c_void_p(xd.data_ptr()), B, C, H, W,
+                                              ctypes.c_void_p(wd.data_ptr()), OC, R, 1, pad,
+                                              ctypes.c_void_p(out.data_ptr()), None))
+    assert np.array_equal(out.cpu().numpy(), GOLD_REAL[f"{tag}/{variant}/direct"])
