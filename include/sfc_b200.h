@@ -182,6 +182,11 @@ int sfc_frequency_energy_int8(sfc_plan_t plan, const int8_t* d_x, int n, int c, 
 int sfc_transform_filters_int8(sfc_plan_t plan, const int8_t* d_weights, int oc, int ic, int32_t* d_u,
                                void* stream);
 
+/* U = G f G^T for real-valued fp64 filters in the reference's accumulation order, fp64
+ * [OC][IC][K][K] (transform_filters, conv.cpp:352-382, for non-integer filters). */
+int sfc_transform_filters_f64(sfc_plan_t plan, const double* d_weights, int oc, int ic, double* d_u,
+                              void* stream);
+
 /* Report sums of quantized_fast_conv2d (quant.cpp:283-291) on the device: host_sums[0] =
  * sum (out - ref)^2, host_sums[1] = sum ref^2 over n elements (ref = sfc_direct_conv_int8 output).
  * Synchronous. */
@@ -208,6 +213,15 @@ int sfc_direct_conv_f64(const double* d_x, int n, int c, int h, int w, const dou
                         int stride, int pad, double* d_out, void* stream);
 /* sfc_report_sq_err against an fp64 reference. */
 int sfc_report_sq_err_f64(const double* d_out, const double* d_ref, int64_t n, double* host_sums, void* stream);
+
+/* fast_conv2d (conv.cpp:384-553), the fp64 float path, on the device: V and U in the
+ * reference's order, the K^2 per-frequency products as one strided-batched fp64 GEMM,
+ * y = A^T P A / N^2.  d_out [N][OC][HO][WO] fp64.  counters[2] (optional) = {products
+ * formed (full schedule), tiles}.  The reference's paired-product option changes only the
+ * product count, not the result beyond rounding; the device always forms the full set.
+ * Temporary buffers are stream-ordered (cudaMallocAsync). */
+int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, int w, const double* d_weights,
+                      int oc, int pad, double* d_out, int64_t* counters, void* stream);
 
 /* Profiling hook of the timeline build (libsfc_b200_tl.so, `make TIMELINE=1`): out[8][3] =
  * per kernel {first CTA entry, first CTA past its dependency wait, last CTA exit} in

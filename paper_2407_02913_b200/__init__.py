@@ -6,10 +6,10 @@ sfconv:: interface (proj/include/sfconv/*.hpp).  There is no CPU fallback.
 """
 from .sfconv import (ActScaleScope, AlgorithmSpec, FilterScaleScope, QuantConfig, QuantReport, ScaleSearch,  # noqa
                      SfcLayer, catalog_algorithm, catalog_export_json, catalog_names, direct_conv2d,
-                     frequency_energy, quantize_value, quantized_fast_conv2d, scale_minmax, scale_mse_grid,
+                     fast_conv2d, fast_conv2d_counters, frequency_energy, quantize_value, quantized_fast_conv2d, scale_minmax, scale_mse_grid,
                      transform_filters)
 
 __all__ = ["ActScaleScope", "AlgorithmSpec", "FilterScaleScope", "QuantConfig", "QuantReport", "ScaleSearch",
            "SfcLayer", "catalog_algorithm", "catalog_export_json", "catalog_names", "direct_conv2d",
-           "frequency_energy", "quantize_value", "quantized_fast_conv2d", "scale_minmax", "scale_mse_grid",
+           "fast_conv2d", "fast_conv2d_counters", "frequency_energy", "quantize_value", "quantized_fast_conv2d", "scale_minmax", "scale_mse_grid",
            "transform_filters"]

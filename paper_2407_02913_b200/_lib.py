@@ -24,7 +24,7 @@ EXPORTED = (
     "sfc_transform_filters_int8", "sfc_debug_quantizer", "sfc_report_sq_err", "sfc_debug_timeline",
     "sfc_act_transform", "sfc_conv_kept", "sfc_layer_create_ex", "sfc_layer_filter_scales_native",
     "sfc_conv_act_scales", "sfc_layer_create_f64", "sfc_conv_forward_f64", "sfc_direct_conv_f64",
-    "sfc_report_sq_err_f64",
+    "sfc_report_sq_err_f64", "sfc_fast_conv_f64", "sfc_transform_filters_f64",
 )
 
 
@@ -86,12 +86,14 @@ _SIGS = {
     "sfc_conv_forward_f64": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
     "sfc_direct_conv_f64": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp]),
     "sfc_report_sq_err_f64": (_i, [_vp, _vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _vp]),
+    "sfc_fast_conv_f64": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _i, _i, _vp, _i64p, _vp]),
     "sfc_conv_kept": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
     "sfc_conv_stats": (_i, [_vp, _i, _i, _i, _i, _vp, _i64p, _vp]),
     "sfc_conv_views": (_i, [_vp, _i, _i, _i, _i, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64p]),
     "sfc_direct_conv_int8": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp]),
     "sfc_frequency_energy_int8": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "sfc_transform_filters_int8": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
+    "sfc_transform_filters_f64": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "sfc_debug_quantizer": (_i, [_i, _i, _vp, _i64p, _vp]),
     "sfc_debug_timeline": (_i, [_vp, _i]),
     "sfc_report_sq_err": (_i, [_vp, _vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _vp]),

@@ -3,6 +3,7 @@
 // fallback -- a missing / failing device path returns SFC_ERR_CUDA.
 #include "../../include/sfc_b200.h"
 
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -538,6 +539,14 @@ int sfc_transform_filters_int8(sfc_plan_t plan, const int8_t* d_w, int oc, int i
     });
 }
 
+int sfc_transform_filters_f64(sfc_plan_t plan, const double* d_w, int oc, int ic, double* d_u, void* stream) {
+    return guarded([&] {
+        if (!plan || !d_w || !d_u) throw std::invalid_argument("null argument");
+        if (oc <= 0 || ic <= 0) throw std::invalid_argument("bad filter shape");
+        ck(launch_filters_f64(plan->p->variant, d_w, oc, ic, d_u, S(stream)), "fp64 filter transform launch");
+    });
+}
+
 int sfc_report_sq_err(const double* d_out, const int32_t* d_ref, int64_t n, double* host_sums, void* stream) {
     return guarded([&] {
         if (!d_out || !d_ref || !host_sums || n < 0) throw std::invalid_argument("bad report arguments");
@@ -652,6 +661,59 @@ int sfc_conv_forward_f64(sfc_layer_t L, const double* d_x, int n, int h, int w, 
         OutPtrs op{nullptr, nullptr, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
         op.gen_act = v.act_scale, op.gen_per_freq = pf ? 1 : 0, op.gen_fil = L->d_fil;
         ck(launch_output(L->variant, 2, v.P, g, v.qp, L->d_sf, op, S(stream), false), "output launch");
+    });
+}
+
+int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, int w, const double* d_weights,
+                      int oc, int pad, double* d_out, int64_t* counters, void* stream) {
+    return guarded([&] {
+        if (!plan || !d_x || !d_weights || !d_out) throw std::invalid_argument("null argument");
+        if (n <= 0 || c <= 0 || h <= 0 || w <= 0 || oc <= 0 || pad < 0) throw std::invalid_argument("bad shape");
+        const SfcPlan& P = *plan->p;
+        if (h + 2 * pad - P.R + 1 <= 0 || w + 2 * pad - P.R + 1 <= 0)
+            throw std::invalid_argument("filter larger than padded input");
+        if (w > 16384 || h > 16384) throw Unsupported("image sides above 16384");
+        ConvGeom g;
+        geom_init(g, P.variant, n, c, h, w, pad, oc);
+        const int F = P.K * P.K;
+        const cudaStream_t st = S(stream);
+        // per-thread cuBLAS handle (a plain fp64 GEMM: tcgen05 has no fp64 kind)
+        thread_local cublasHandle_t handle = nullptr;
+        if (!handle && cublasCreate(&handle) != CUBLAS_STATUS_SUCCESS) throw CudaFail("cublasCreate failed");
+        if (cublasSetStream(handle, st) != CUBLAS_STATUS_SUCCESS) throw CudaFail("cublasSetStream failed");
+        const size_t nv = size_t(F) * g.Tpad * g.Cpad, nu = size_t(oc) * c * F, nb = size_t(F) * g.OCpad * g.Cpad;
+        const size_t np = size_t(F) * g.Tpad * g.OCpad;
+        double *Vd = nullptr, *U = nullptr, *Ub = nullptr, *Pd = nullptr;
+        void* dummy = nullptr;  // QuantParams / sf the epilogue reads but mode 3 ignores
+        ck(cudaMallocAsync(&Vd, nv * sizeof(double), st), "alloc V");
+        ck(cudaMallocAsync(&U, nu * sizeof(double), st), "alloc U");
+        ck(cudaMallocAsync(&Ub, nb * sizeof(double), st), "alloc Ub");
+        ck(cudaMallocAsync(&Pd, np * sizeof(double), st), "alloc P");
+        ck(cudaMallocAsync(&dummy, 4096, st), "alloc");
+        ck(cudaMemsetAsync(Vd, 0, nv * sizeof(double), st), "memset V");  // padding rows/channels are 0
+        ck(cudaMemsetAsync(Ub, 0, nb * sizeof(double), st), "memset Ub");
+        ck(cudaMemsetAsync(dummy, 0, 4096, st), "memset");
+        ck(launch_act_f64(P.variant, d_x, g, Vd, st), "fp64 input transform launch");
+        ck(launch_filters_f64(P.variant, d_weights, oc, c, U, st), "fp64 filter transform launch");
+        ck(launch_pack_u_f64(U, oc, c, F, g.Cpad, g.OCpad, Ub, st), "pack launch");
+        // P_f[t][o] = sum_c V_f[t][c] Ub_f[o][c] for every f (row-major), i.e. column-major
+        // P_f^T (OCpad x Tpad) = Ub_f (op T of the col-major view) x V_f^T
+        const double one = 1.0, zero = 0.0;
+        if (cublasDgemmStridedBatched(handle, CUBLAS_OP_T, CUBLAS_OP_N, g.OCpad, g.Tpad, g.Cpad, &one, Ub, g.Cpad,
+                                      (long long)g.OCpad * g.Cpad, Vd, g.Cpad, (long long)g.Tpad * g.Cpad, &zero, Pd,
+                                      g.OCpad, (long long)g.Tpad * g.OCpad, F) != CUBLAS_STATUS_SUCCESS)
+            throw CudaFail("cublasDgemmStridedBatched failed");
+        OutPtrs op{nullptr, nullptr, nullptr, d_out, nullptr, 0.0};
+        ck(launch_output(P.variant, 3, Pd, g, static_cast<const QuantParams*>(dummy),
+                         static_cast<const double*>(dummy), op, st, false),
+           "output launch");
+        for (void* p : {static_cast<void*>(Vd), static_cast<void*>(U), static_cast<void*>(Ub), static_cast<void*>(Pd),
+                        dummy})
+            ck(cudaFreeAsync(p, st), "free");
+        if (counters) {  // conv.hpp ConvCounters: products actually formed, tiles
+            counters[0] = int64_t(g.T) * oc * c * F;
+            counters[1] = g.T;
+        }
     });
 }
 

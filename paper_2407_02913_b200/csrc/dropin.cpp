@@ -377,8 +377,15 @@ DenseTensor direct_conv2d(const DenseTensor& input, const DenseTensor& filters, 
     const int HO = (H + 2 * padding - R) / stride + 1, WO = (W + 2 * padding - R) / stride + 1;
     if (HO <= 0 || WO <= 0 || H + 2 * padding < R || W + 2 * padding < R)
         throw std::invalid_argument("filter larger than padded input");
-    DevBuf<int8_t> x = to_device_int8(input, "input"), w = to_device_int8(filters, "filters");
     DenseTensor out({B, OC, HO, WO});
+    if (!int8_valued(input) || !int8_valued(filters)) {
+        // Real-valued tensors: fp64 direct convolution in conv.cpp:62-89's accumulation order.
+        DevBuf<double> xd = to_device_f64(input), wd = to_device_f64(filters), yd(out.data.size());
+        check(sfc_direct_conv_f64(xd.p, B, C, H, W, wd.p, OC, R, stride, padding, yd.p, stream()));
+        out.data = to_host(yd.p, out.data.size());
+        return out;
+    }
+    DevBuf<int8_t> x = to_device_int8(input, "input"), w = to_device_int8(filters, "filters");
     DevBuf<int32_t> y(out.data.size());
     check(sfc_direct_conv_int8(x.p, B, C, H, W, w.p, OC, R, stride, padding, y.p, stream()));
     const auto h = to_host(y.p, out.data.size());
@@ -391,8 +398,14 @@ DenseTensor transform_filters(const DenseTensor& filters, const AlgorithmSpec& s
         throw std::invalid_argument("filter shape does not match algorithm");
     PlanGuard plan{plan_handle(spec)};
     const int OC = filters.dim(0), IC = filters.dim(1), K = spec.K();
-    DevBuf<int8_t> w = to_device_int8(filters, "filters");
     DenseTensor u({OC, IC, K, K});
+    if (!int8_valued(filters)) {
+        DevBuf<double> wd = to_device_f64(filters), ud(u.data.size());
+        check(sfc_transform_filters_f64(plan.p, wd.p, OC, IC, ud.p, stream()));
+        u.data = to_host(ud.p, u.data.size());
+        return u;
+    }
+    DevBuf<int8_t> w = to_device_int8(filters, "filters");
     DevBuf<int32_t> d(u.data.size());
     check(sfc_transform_filters_int8(plan.p, w.p, OC, IC, d.p, stream()));
     const auto h = to_host(d.p, u.data.size());
@@ -400,10 +413,28 @@ DenseTensor transform_filters(const DenseTensor& filters, const AlgorithmSpec& s
     return u;
 }
 
-DenseTensor fast_conv2d(const DenseTensor&, const DenseTensor&, const AlgorithmSpec&, int, const FastConvOptions&) {
-    throw std::logic_error(
-        "fast_conv2d (the reference's fp64 float path, conv.cpp:384-553) is not implemented on the B200 device "
-        "path; use quantized_fast_conv2d");
+DenseTensor fast_conv2d(const DenseTensor& input, const DenseTensor& filters, const AlgorithmSpec& spec, int padding,
+                        const FastConvOptions& opts) {
+    check_conv_shapes(input, filters);
+    if (filters.dim(2) != spec.R) throw std::invalid_argument("filter size does not match algorithm");
+    const int B = input.dim(0), C = input.dim(1), H = input.dim(2), W = input.dim(3), OC = filters.dim(0);
+    const int HO = H + 2 * padding - spec.R + 1, WO = W + 2 * padding - spec.R + 1;
+    if (HO <= 0 || WO <= 0) throw std::invalid_argument("filter larger than padded input");
+    PlanGuard plan{plan_handle(spec)};
+    DevBuf<double> x = to_device_f64(input), w = to_device_f64(filters);
+    DenseTensor out({B, OC, HO, WO});
+    DevBuf<double> d_out(out.data.size());
+    std::int64_t counters[2] = {0, 0};
+    check(sfc_fast_conv_f64(plan.p, x.p, B, C, H, W, w.p, OC, padding, d_out.p, counters, stream()));
+    ck(cudaMemcpyAsync(out.data.data(), d_out.p, out.data.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       stream()),
+       "copy output");
+    ck(cudaStreamSynchronize(stream()), "sync");
+    if (opts.counters) {  // the device forms the full product set (threads / reduced_products: host-CPU knobs)
+        opts.counters->multiplications += counters[0];
+        opts.counters->tiles += counters[1];
+    }
+    return out;
 }
 
 std::vector<double> frequency_energy(const DenseTensor& input, const AlgorithmSpec& spec, int padding) {

@@ -286,6 +286,16 @@ __global__ void __launch_bounds__(256) k_direct_f64(const double* __restrict__ x
     out[idx] = acc;
 }
 
+// U [OC][IC][F] -> the float path's GEMM operand Ub [F][OCpad][Cpad] (zero padding done by the caller).
+__global__ void k_pack_u_f64(const double* __restrict__ U, int OC, int IC, int F, int Cpad, int OCpad,
+                             double* __restrict__ Ub) {
+    const long long n = (long long)OC * IC * F;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int f = int(i % F), ic = int((i / F) % IC), oc = int(i / ((long long)F * IC));
+        Ub[((long long)f * OCpad + oc) * Cpad + ic] = U[i];
+    }
+}
+
 // ============================================================================ host
 namespace {
 template <class TU>
@@ -364,6 +374,14 @@ cudaError_t launch_filters_f64(int variant, const double* w, int OC, int IC, dou
         case 3: k_filters_f64<3><<<blocks, 128, 0, st>>>(w, OC, IC, U); break;
         default: k_filters_f64<4><<<blocks, 128, 0, st>>>(w, OC, IC, U); break;
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_u_f64(const double* U, int OC, int IC, int F, int Cpad, int OCpad, double* Ub,
+                              cudaStream_t st) {
+    const long long n = (long long)OC * IC * F;
+    const int blocks = int((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+    k_pack_u_f64<<<blocks, 256, 0, st>>>(U, OC, IC, F, Cpad, OCpad, Ub);
     return cudaGetLastError();
 }
 

@@ -40,6 +40,15 @@ static_assert(out_tb<0>() * Tab<0>::M <= 32 && out_tb<1>() * Tab<1>::M <= 32 && 
                   out_tb<3>() * Tab<3>::M <= 32 && out_tb<4>() * Tab<4>::M <= 32,
               "a block's output row segment must fit the 32-entry magic table");
 
+// MODE 3 (fp64 P, the float fast_conv2d path) halves the tile columns per block: its P slice
+// is twice as wide per element.
+template <int V, int MODE>
+__host__ __device__ constexpr int out_tbm() {
+    return MODE == 3 ? (out_tb<V>() / 2 < 1 ? 1 : out_tb<V>() / 2) : out_tb<V>();
+}
+template <int MODE>
+using p_elem_t = typename std::conditional<MODE == 3, double, int32_t>::type;
+
 struct OutSmem {
     int qstride, ystride;
     size_t p_bytes, q_off, bar_off, bytes;
@@ -48,13 +57,13 @@ struct OutSmem {
 template <int V, int MODE>
 __host__ __device__ inline OutSmem out_smem() {
     using T = Tab<V>;
-    constexpr int TB = out_tb<V>();
+    constexpr int TB = out_tbm<V, MODE>();
     const size_t es = MODE == 0 ? 4 : 8;
     OutSmem s;
     s.qstride = kOcc | 1;
     s.ystride = (T::M * TB) | 1;
     const size_t y_bytes = size_t(T::M) * kOcc * s.ystride * es;
-    s.p_bytes = size_t(T::F) * TB * kOcc * 4;
+    s.p_bytes = size_t(T::F) * TB * kOcc * sizeof(p_elem_t<MODE>);
     if (y_bytes > s.p_bytes) s.p_bytes = y_bytes;  // s_y reuses the P slice
     s.q_off = (s.p_bytes + 127) & ~size_t(127);
     s.bar_off = (s.q_off + size_t(TB) * T::M * T::K * s.qstride * es + 15) & ~size_t(15);
@@ -72,18 +81,20 @@ __constant__ unsigned c_magic32[33] = {  // 0xffffffff / d + 1 (exact for t < 2^
     0x08000000u};
 
 // MODE 0: exact int32 y, 1: exact int64 y, 2: general QuantConfig (P dequantised per
-// (oc, f) before the inverse transform, which then runs in fp64: quant.cpp:258-278).
+// (oc, f) before the inverse transform, which then runs in fp64: quant.cpp:258-278),
+// 3: fp64 P of the float path (fast_conv2d, conv.cpp:495-510), no dequantisation.
 template <int V, int MODE>
 __global__ void __launch_bounds__(kOutThreads, 2)
     k_output(const __grid_constant__ CUtensorMap tmP, ConvGeom g, const QuantParams* __restrict__ qpp,
              const double* __restrict__ sf, OutPtrs o) {
     using T = Tab<V>;
-    constexpr int K = T::K, M = T::M, TB = out_tb<V>();
+    constexpr int K = T::K, M = T::M, TB = out_tbm<V, MODE>();
     constexpr bool Y64 = MODE == 1;
-    using acc_t = typename std::conditional<MODE == 2, double, typename std::conditional<Y64, long long, int>::type>::type;
+    using acc_t =
+        typename std::conditional<MODE >= 2, double, typename std::conditional<Y64, long long, int>::type>::type;
     extern __shared__ __align__(128) uint8_t smem[];
     const OutSmem L = out_smem<V, MODE>();
-    const int32_t* sp = reinterpret_cast<const int32_t*>(smem);  // [F][TB][kOcc]
+    const p_elem_t<MODE>* sp = reinterpret_cast<const p_elem_t<MODE>*>(smem);  // [F][TB][kOcc]
     acc_t* s_y = reinterpret_cast<acc_t*>(smem);                 // [M][kOcc] rows of ystride (after stage A)
     acc_t* s_q = reinterpret_cast<acc_t*>(smem + L.q_off);       // [TB][M][K] rows of qstride
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -103,7 +114,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     tl_mark(kTlOutput, 1);
     griddep_launch_dependents();
     if (threadIdx.x == 0) {
-        ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 4));
+        ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * sizeof(p_elem_t<MODE>)));
         ptx::tma_load_3d(smem, &tmP, full, oc0, row * g.tw + tc * TB, 0);
     }
     const int b = g.th == 1 ? row : int(__umulhi(unsigned(row), g.th_magic)), ti = row - b * g.th;
@@ -175,9 +186,9 @@ __global__ void __launch_bounds__(kOutThreads, 2)
             if (oc >= noc || t1 >= hrows) continue;
             const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
             const acc_t y = s_y[r * L.ystride + c];
-            if constexpr (MODE != 2 && (MK & 1) != 0) o.y32[x] = int(y);
-            if constexpr (MODE != 2 && (MK & 2) != 0) o.y64[x] = int64_t(y);
-            if constexpr (MODE == 2) {  // y = sum A A pd; out = y / N^2 (the reference's a = A / N)
+            if constexpr (MODE < 2 && (MK & 1) != 0) o.y32[x] = int(y);
+            if constexpr (MODE < 2 && (MK & 2) != 0) o.y64[x] = int64_t(y);
+            if constexpr (MODE >= 2) {  // y = sum A A pd; out = y / N^2 (the reference's a = A / N)
                 const double out = double(y) / double(T::DEN * T::DEN);
                 if constexpr ((MK & 4) != 0) o.f32[x] = float(out);
                 if constexpr ((MK & 8) != 0) o.f64[x] = out;
@@ -222,17 +233,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 template <int V, int MODE>
-cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf, const OutPtrs& o,
+cudaError_t out_launch(const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf, const OutPtrs& o,
                        cudaStream_t st, bool pdl) {
-    constexpr int TB = out_tb<V>();
+    constexpr int TB = out_tbm<V, MODE>();
+    constexpr cuuint64_t es = sizeof(p_elem_t<MODE>);
     auto fn = encode_fn();
     if (!fn) return cudaErrorInvalidValue;
     CUtensorMap tm;
     cuuint64_t dims[3] = {cuuint64_t(g.OCpad), cuuint64_t(g.Tpad), cuuint64_t(Tab<V>::F)};
-    cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * 4, cuuint64_t(g.OCpad) * g.Tpad * 4};
+    cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * es, cuuint64_t(g.OCpad) * g.Tpad * es};
     cuuint32_t box[3] = {kOcc, TB, Tab<V>::F};
     cuuint32_t estr[3] = {1, 1, 1};
-    if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<int32_t*>(P), dims, strides, box, estr,
+    if (fn(&tm, MODE == 3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(P),
+           dims, strides, box, estr,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
@@ -256,15 +269,16 @@ cudaError_t out_launch(const int32_t* P, const ConvGeom& g, const QuantParams* q
 }
 
 template <int V>
-cudaError_t out_by_width(int mode, const int32_t* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
+cudaError_t out_by_width(int mode, const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
                          const OutPtrs& o, cudaStream_t st, bool pdl) {
     return mode == 0 ? out_launch<V, 0>(P, g, qp, sf, o, st, pdl)
          : mode == 1 ? out_launch<V, 1>(P, g, qp, sf, o, st, pdl)
-                     : out_launch<V, 2>(P, g, qp, sf, o, st, pdl);
+         : mode == 2 ? out_launch<V, 2>(P, g, qp, sf, o, st, pdl)
+                     : out_launch<V, 3>(P, g, qp, sf, o, st, pdl);
 }
 }  // namespace
 
-cudaError_t launch_output(int variant, int mode, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
+cudaError_t launch_output(int variant, int mode, const void* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl) {
     switch (variant) {
         case 0: return out_by_width<0>(mode, P, g, qp, sf, o, st, pdl);

@@ -88,8 +88,9 @@ struct OutPtrs {
     int gen_per_freq = 0;
     const double* gen_fil = nullptr;  // [OC][F]
 };
-// mode 0: exact int32 y, 1: exact int64 y, 2: general QuantConfig (fp64, no y_int)
-cudaError_t launch_output(int variant, int mode, const int32_t* P, const ConvGeom& g, const QuantParams* qp,
+// mode 0: exact int32 y, 1: exact int64 y, 2: general QuantConfig (fp64, no y_int),
+// 3: fp64 P [F][Tpad][OCpad] of the float path (no dequantisation)
+cudaError_t launch_output(int variant, int mode, const void* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
 cudaError_t launch_sq_err(const double* out, const int32_t* ref, long long n, double* sums, cudaStream_t st);
 cudaError_t launch_sq_err_f64(const double* out, const double* ref, long long n, double* sums, cudaStream_t st);
@@ -129,5 +130,7 @@ cudaError_t launch_act_f64(int variant, const double* x, const ConvGeom& g, doub
 cudaError_t launch_filters_f64(int variant, const double* w, int OC, int IC, double* U, cudaStream_t st);
 cudaError_t launch_direct_f64(const double* x, int B, int C, int H, int W, const double* w, int OC, int R, int stride,
                               int pad, double* out, cudaStream_t st);
+cudaError_t launch_pack_u_f64(const double* U, int OC, int IC, int F, int Cpad, int OCpad, double* Ub,
+                              cudaStream_t st);
 
 }  // namespace sfcb200

@@ -528,3 +528,31 @@ def _quantized_fast_conv2d_real(input, filters, spec: AlgorithmSpec, padding: in
         rep.signal_energy = sums[1] / n
         rep.snr_db = _snr_db(sums[1], sums[0])
     return rep
+
+
+def fast_conv2d(input, filters, spec: AlgorithmSpec, padding: int = 0) -> torch.Tensor:
+    """conv.cpp:384-553 (the fp64 float path) on the device: fp64 NCHW output.  Returns the
+    output tensor; fast_conv2d_counters() gives the product / tile counts."""
+    out, _ = fast_conv2d_counters(input, filters, spec, padding)
+    return out
+
+
+def fast_conv2d_counters(input, filters, spec: AlgorithmSpec, padding: int = 0):
+    x = as_f64_device(input)
+    w = as_f64_device(filters, x.device)
+    if x.dim() != 4 or w.dim() != 4:
+        raise ValueError("conv2d expects 4-d NCHW tensors")
+    if w.shape[1] != x.shape[1]:
+        raise ValueError("input channel count does not match filters")
+    if w.shape[2] != spec.R or w.shape[3] != spec.R:
+        raise ValueError("filter size does not match algorithm")
+    B, C, H, W = x.shape
+    OC = w.shape[0]
+    HO, WO = H + 2 * padding - spec.R + 1, W + 2 * padding - spec.R + 1
+    if HO <= 0 or WO <= 0:
+        raise ValueError("filter larger than padded input")
+    out = torch.empty((B, OC, HO, WO), dtype=torch.float64, device=x.device)
+    cnt = np.zeros(2, np.int64)
+    check(lib().sfc_fast_conv_f64(ctypes.c_void_p(spec._handle), _ptr(x), B, C, H, W, _ptr(w), OC, padding, _ptr(out),
+                                  cnt.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.c_void_p(_stream_ptr())))
+    return out, {"multiplications": int(cnt[0]), "tiles": int(cnt[1])}

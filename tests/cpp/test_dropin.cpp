@@ -314,7 +314,31 @@ int main(int argc, char** argv) {
         DenseTensor frac = x;  // real values take the fp64 path (not refused)
         frac.data[0] = 0.5;
         CHECK(!throws<std::invalid_argument>([&] { quantized_fast_conv2d(frac, f, s, 1, {}); }));
-        CHECK(throws<std::logic_error>([&] { fast_conv2d(x, f, s, 1); }));
+        CHECK(throws<std::invalid_argument>([&] { fast_conv2d(x, int8_tensor({1, 1, 5, 5}, 2), s, 1); }));
+    });
+
+    run_case("fast_conv2d matches the direct method (test_conv.cpp:78-90)", [] {
+        std::mt19937_64 rng(73);
+        std::normal_distribution<double> nd(0.0, 1.0);
+        for (const std::string& name : catalog_names()) {
+            const AlgorithmSpec& s = catalog_algorithm(name);
+            DenseTensor x({2, 3, 17, 15}), f({4, 3, s.R, s.R});
+            for (auto& v : x.data) v = nd(rng);
+            for (auto& v : f.data) v = nd(rng);
+            const int pad = s.R / 2;
+            ConvCounters cnt;
+            FastConvOptions opts;
+            opts.counters = &cnt;
+            const DenseTensor a = fast_conv2d(x, f, s, pad, opts), b = direct_conv2d(x, f, 1, pad);
+            double md = 0.0, mr = 0.0;
+            for (std::size_t i = 0; i < b.data.size(); ++i) {
+                md = std::max(md, std::abs(a.data[i] - b.data[i]));
+                mr = std::max(mr, std::abs(b.data[i]));
+            }
+            CHECK(md / mr <= 1e-10);
+            const int th = (17 + 2 * pad - s.R + 1 + s.M - 1) / s.M, tw = (15 + 2 * pad - s.R + 1 + s.M - 1) / s.M;
+            CHECK(cnt.tiles == 2 * th * tw && cnt.multiplications == cnt.tiles * 4 * 3 * s.K() * s.K());
+        }
     });
 
     run_case("bitwise determinism across calls and threads (test_conv.cpp:177-192)", [] {

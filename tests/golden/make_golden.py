@@ -123,6 +123,9 @@ def real_valued():
             arrays[f"{tag}/{v}/report"] = np.array([rep["mse"], rep["signal_energy"], rep["snr_db"],
                                                     rep["saturations"], rep["values_quantized"], pad], np.float64)
             arrays[f"{tag}/{v}/direct"] = ob.ref_direct_conv2d(x, w, pad)
+            fo, mults = ob.ref_fast_conv2d(x, w, v, pad)  # the fp64 float path (conv.cpp:384-553)
+            arrays[f"{tag}/{v}/fast"] = fo
+            arrays[f"{tag}/{v}/fast_counts"] = mults
     np.savez_compressed(os.path.join(HERE, "qconv_real.npz"), **arrays)
     print("wrote", len(arrays), "real-valued arrays")
 

@@ -492,3 +492,19 @@ def test_real_valued_tensors_vs_reference_golden(cuda, tag, variant):
                                               ctypes.c_void_p(wd.data_ptr()), OC, R, 1, pad,
                                               ctypes.c_void_p(out.data_ptr()), None))
     assert np.array_equal(out.cpu().numpy(), GOLD_REAL[f"{tag}/{variant}/direct"])
+
+
+
+@pytest.mark.parametrize("variant", VARIANTS + LARGE_R)
+@pytest.mark.parametrize("tag", TAGS_REAL)
+def test_fast_conv2d_float_path(cuda, tag, variant):
+    """fast_conv2d (conv.cpp:384-553) on the device: vs the reference's own float-path output
+    (<= 1e-12) and vs the fp64 direct conv at the reference's bar (<= 1e-10, test_conv.cpp:78-90);
+    the product / tile counters equal the reference's full-schedule counts."""
+    x, w = GOLD_REAL[f"{tag}/x"], GOLD_REAL[f"{tag}/{variant}/w"]
+    pad = int(GOLD_REAL[f"{tag}/{variant}/report"][5])
+    out, cnt = sc.fast_conv2d_counters(torch.from_numpy(x), torch.from_numpy(w), sc.catalog_algorithm(variant), pad)
+    got = out.cpu().numpy()
+    assert maxrel(got, GOLD_REAL[f"{tag}/{variant}/fast"]) <= 1e-12
+    assert maxrel(got, GOLD_REAL[f"{tag}/{variant}/direct"]) <= 1e-10
+    assert [cnt["multiplications"], cnt["tiles"]] == list(GOLD_REAL[f"{tag}/{variant}/fast_counts"])
