@@ -216,12 +216,13 @@ int sfc_report_sq_err_f64(const double* d_out, const double* d_ref, int64_t n, d
 
 /* fast_conv2d (conv.cpp:384-553), the fp64 float path, on the device: V and U in the
  * reference's order, the K^2 per-frequency products as one strided-batched fp64 GEMM,
- * y = A^T P A / N^2.  d_out [N][OC][HO][WO] fp64.  counters[2] (optional) = {products
- * formed (full schedule), tiles}.  The reference's paired-product option changes only the
- * product count, not the result beyond rounding; the device always forms the full set.
- * Temporary buffers are stream-ordered (cudaMallocAsync). */
+ * y = A^T P A / N^2.  reduced != 0 is FastConvOptions::reduced_products (conv.cpp:399-403,
+ * 466-509): each (triple x triple) block's nine products become six evaluation products
+ * folded onto its corners, so the batch shrinks to mults_reduced() slices (88 of 100 for
+ * sfc6-6x6-3x3).  d_out [N][OC][HO][WO] fp64.  counters[2] (optional) = {products formed,
+ * tiles}.  Temporary buffers are stream-ordered (cudaMallocAsync). */
 int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, int w, const double* d_weights,
-                      int oc, int pad, double* d_out, int64_t* counters, void* stream);
+                      int oc, int pad, int reduced, double* d_out, int64_t* counters, void* stream);
 
 /* Profiling hook of the timeline build (libsfc_b200_tl.so, `make TIMELINE=1`): out[8][3] =
  * per kernel {first CTA entry, first CTA past its dependency wait, last CTA exit} in

@@ -86,7 +86,7 @@ _SIGS = {
     "sfc_conv_forward_f64": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
     "sfc_direct_conv_f64": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp]),
     "sfc_report_sq_err_f64": (_i, [_vp, _vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _vp]),
-    "sfc_fast_conv_f64": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _i, _i, _vp, _i64p, _vp]),
+    "sfc_fast_conv_f64": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _i64p, _vp]),
     "sfc_conv_kept": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
     "sfc_conv_stats": (_i, [_vp, _i, _i, _i, _i, _vp, _i64p, _vp]),
     "sfc_conv_views": (_i, [_vp, _i, _i, _i, _i, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64p]),

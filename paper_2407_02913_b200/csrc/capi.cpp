@@ -665,7 +665,7 @@ int sfc_conv_forward_f64(sfc_layer_t L, const double* d_x, int n, int h, int w, 
 }
 
 int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, int w, const double* d_weights,
-                      int oc, int pad, double* d_out, int64_t* counters, void* stream) {
+                      int oc, int pad, int reduced, double* d_out, int64_t* counters, void* stream) {
     return guarded([&] {
         if (!plan || !d_x || !d_weights || !d_out) throw std::invalid_argument("null argument");
         if (n <= 0 || c <= 0 || h <= 0 || w <= 0 || oc <= 0 || pad < 0) throw std::invalid_argument("bad shape");
@@ -699,10 +699,69 @@ int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, i
         // P_f[t][o] = sum_c V_f[t][c] Ub_f[o][c] for every f (row-major), i.e. column-major
         // P_f^T (OCpad x Tpad) = Ub_f (op T of the col-major view) x V_f^T
         const double one = 1.0, zero = 0.0;
-        if (cublasDgemmStridedBatched(handle, CUBLAS_OP_T, CUBLAS_OP_N, g.OCpad, g.Tpad, g.Cpad, &one, Ub, g.Cpad,
-                                      (long long)g.OCpad * g.Cpad, Vd, g.Cpad, (long long)g.Tpad * g.Cpad, &zero, Pd,
-                                      g.OCpad, (long long)g.Tpad * g.OCpad, F) != CUBLAS_STATUS_SUCCESS)
-            throw CudaFail("cublasDgemmStridedBatched failed");
+        auto gemm = [&](const double* Ua, const double* Va, double* Pa, int batch) {
+            if (cublasDgemmStridedBatched(handle, CUBLAS_OP_T, CUBLAS_OP_N, g.OCpad, g.Tpad, g.Cpad, &one, Ua, g.Cpad,
+                                          (long long)g.OCpad * g.Cpad, Va, g.Cpad, (long long)g.Tpad * g.Cpad, &zero,
+                                          Pa, g.OCpad, (long long)g.Tpad * g.OCpad, batch) != CUBLAS_STATUS_SUCCESS)
+                throw CudaFail("cublasDgemmStridedBatched failed");
+        };
+        const PairedSchedule* ps = nullptr;
+        if (reduced) {  // conv.cpp:399-403: no schedule (no triples) means the full product set
+            const PairedSchedule& cand = paired_schedule(P);
+            if (cand.available) ps = &cand;
+        }
+        long products = F;
+        if (!ps) {
+            gemm(Ub, Vd, Pd, F);
+        } else {
+            // reduced batch: the unpaired positions, then six evaluation products per block
+            std::vector<PairSlice> slices;
+            std::vector<PairFold> folds(size_t(F), PairFold{0, 0, {0, 0, 0, 0, 0, 0}});
+            for (int f = 0; f < F; ++f)
+                if (!ps->masked[size_t(f)]) {
+                    folds[size_t(f)] = PairFold{1, int(slices.size()), {0, 0, 0, 0, 0, 0}};
+                    slices.push_back(PairSlice{1, {f, 0, 0, 0}, {1, 0, 0, 0}, {1, 0, 0, 0}});
+                }
+            for (const PairBlock& b : ps->blocks) {
+                const int base = int(slices.size());
+                int corner[4];
+                for (int q = 0; q < 4; ++q) corner[q] = b.r1[q >> 1] * P.K + b.r2[q & 1];
+                for (int l = 0; l < 6; ++l) {
+                    PairSlice sl{4, {corner[0], corner[1], corner[2], corner[3]}, {}, {}};
+                    for (int q = 0; q < 4; ++q) sl.a[q] = b.alpha[l][q], sl.b[q] = b.beta[l][q];
+                    slices.push_back(sl);
+                }
+                for (int q = 0; q < 4; ++q) {
+                    PairFold& fd = folds[size_t(corner[q])];
+                    fd.kind = 2, fd.src = base;
+                    for (int l = 0; l < 6; ++l) fd.w[l] = b.fold[q][l];
+                }
+            }
+            const int ns = int(slices.size());
+            products = ns;
+            const long long ev = (long long)g.Tpad * g.Cpad, eu = (long long)g.OCpad * g.Cpad,
+                            ep = (long long)g.Tpad * g.OCpad;
+            double *Vr = nullptr, *Ur = nullptr, *Pr = nullptr;
+            PairSlice* dsl = nullptr;
+            PairFold* dfd = nullptr;
+            ck(cudaMallocAsync(&Vr, size_t(ns) * ev * sizeof(double), st), "alloc Vr");
+            ck(cudaMallocAsync(&Ur, size_t(ns) * eu * sizeof(double), st), "alloc Ur");
+            ck(cudaMallocAsync(&Pr, size_t(ns) * ep * sizeof(double), st), "alloc Pr");
+            ck(cudaMallocAsync(&dsl, slices.size() * sizeof(PairSlice), st), "alloc slices");
+            ck(cudaMallocAsync(&dfd, folds.size() * sizeof(PairFold), st), "alloc folds");
+            ck(cudaMemcpyAsync(dsl, slices.data(), slices.size() * sizeof(PairSlice), cudaMemcpyHostToDevice, st),
+               "copy slices");
+            ck(cudaMemcpyAsync(dfd, folds.data(), folds.size() * sizeof(PairFold), cudaMemcpyHostToDevice, st),
+               "copy folds");
+            ck(launch_pair_gather(Vd, ev, dsl, ns, false, Vr, st), "pair gather launch");
+            ck(launch_pair_gather(Ub, eu, dsl, ns, true, Ur, st), "pair gather launch");
+            gemm(Ur, Vr, Pr, ns);
+            ck(launch_pair_fold(Pr, ep, dfd, F, Pd, st), "pair fold launch");
+            // the host tables are pageable: the copies above finished staging before returning
+            for (void* p : {static_cast<void*>(Vr), static_cast<void*>(Ur), static_cast<void*>(Pr),
+                            static_cast<void*>(dsl), static_cast<void*>(dfd)})
+                ck(cudaFreeAsync(p, st), "free");
+        }
         OutPtrs op{nullptr, nullptr, nullptr, d_out, nullptr, 0.0};
         ck(launch_output(P.variant, 3, Pd, g, static_cast<const QuantParams*>(dummy),
                          static_cast<const double*>(dummy), op, st, false),
@@ -711,7 +770,7 @@ int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, i
                         dummy})
             ck(cudaFreeAsync(p, st), "free");
         if (counters) {  // conv.hpp ConvCounters: products actually formed, tiles
-            counters[0] = int64_t(g.T) * oc * c * F;
+            counters[0] = int64_t(g.T) * oc * c * products;
             counters[1] = g.T;
         }
     });

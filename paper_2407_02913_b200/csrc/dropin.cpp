@@ -425,12 +425,13 @@ DenseTensor fast_conv2d(const DenseTensor& input, const DenseTensor& filters, co
     DenseTensor out({B, OC, HO, WO});
     DevBuf<double> d_out(out.data.size());
     std::int64_t counters[2] = {0, 0};
-    check(sfc_fast_conv_f64(plan.p, x.p, B, C, H, W, w.p, OC, padding, d_out.p, counters, stream()));
+    check(sfc_fast_conv_f64(plan.p, x.p, B, C, H, W, w.p, OC, padding, opts.reduced_products ? 1 : 0, d_out.p,
+                            counters, stream()));
     ck(cudaMemcpyAsync(out.data.data(), d_out.p, out.data.size() * sizeof(double), cudaMemcpyDeviceToHost,
                        stream()),
        "copy output");
     ck(cudaStreamSynchronize(stream()), "sync");
-    if (opts.counters) {  // the device forms the full product set (threads / reduced_products: host-CPU knobs)
+    if (opts.counters) {  // opts.threads is a host-CPU knob: the device result does not depend on it
         opts.counters->multiplications += counters[0];
         opts.counters->tiles += counters[1];
     }

@@ -296,6 +296,44 @@ __global__ void k_pack_u_f64(const double* __restrict__ U, int OC, int IC, int F
     }
 }
 
+// Reduced batch of the paired schedule: dst[s][e] = sum_k coef[k] * src[f_k][e], the
+// evaluation form accumulated in the reference's order (conv.cpp:482-489).
+__global__ void k_pair_gather(const double* __restrict__ src, long long elems, const PairSlice* __restrict__ tab,
+                              bool filter_side, double* __restrict__ dst) {
+    const PairSlice sl = tab[blockIdx.y];
+    double* out = dst + (long long)blockIdx.y * elems;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < elems;
+         e += (long long)gridDim.x * blockDim.x) {
+        if (sl.n == 1) {
+            out[e] = src[(long long)sl.f[0] * elems + e];
+            continue;
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            acc = __dadd_rn(acc, __dmul_rn(filter_side ? sl.b[k] : sl.a[k], src[(long long)sl.f[k] * elems + e]));
+        out[e] = acc;
+    }
+}
+
+// P[f][e] from the reduced batch: direct copy, zero, or a corner fold (conv.cpp:494-506).
+__global__ void k_pair_fold(const double* __restrict__ Pr, long long elems, const PairFold* __restrict__ tab,
+                            double* __restrict__ P) {
+    const PairFold fd = tab[blockIdx.y];
+    double* out = P + (long long)blockIdx.y * elems;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < elems;
+         e += (long long)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        if (fd.kind == 1) {
+            v = Pr[(long long)fd.src * elems + e];
+        } else if (fd.kind == 2) {
+#pragma unroll
+            for (int l = 0; l < 6; ++l) v = __dadd_rn(v, __dmul_rn(fd.w[l], Pr[(long long)(fd.src + l) * elems + e]));
+        }
+        out[e] = v;
+    }
+}
+
 // ============================================================================ host
 namespace {
 template <class TU>
@@ -382,6 +420,22 @@ cudaError_t launch_pack_u_f64(const double* U, int OC, int IC, int F, int Cpad, 
     const long long n = (long long)OC * IC * F;
     const int blocks = int((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
     k_pack_u_f64<<<blocks, 256, 0, st>>>(U, OC, IC, F, Cpad, OCpad, Ub);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pair_gather(const double* src, long long elems, const PairSlice* tab, int nslices, bool filter_side,
+                               double* dst, cudaStream_t st) {
+    const long long bx = (elems + 255) / 256;
+    const dim3 grid(unsigned(bx < 64 ? bx : 64), unsigned(nslices));
+    k_pair_gather<<<grid, 256, 0, st>>>(src, elems, tab, filter_side, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pair_fold(const double* Pr, long long elems, const PairFold* tab, int F, double* P,
+                             cudaStream_t st) {
+    const long long bx = (elems + 255) / 256;
+    const dim3 grid(unsigned(bx < 64 ? bx : 64), unsigned(F));
+    k_pair_fold<<<grid, 256, 0, st>>>(Pr, elems, tab, P);
     return cudaGetLastError();
 }
 

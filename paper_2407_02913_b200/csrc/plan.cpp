@@ -83,16 +83,21 @@ struct Frac {
     int64_t n = 0, d = 1;
     Frac() = default;
     Frac(int64_t v) : n(v), d(1) {}
-    Frac(int64_t a, int64_t b) : n(a), d(b) { norm(); }
-    void norm() {
-        if (d < 0) n = -n, d = -d;
-        int64_t g = std::gcd(n < 0 ? -n : n, d);
-        if (g > 1) n /= g, d /= g;
+    Frac(__int128 a, __int128 b) {  // normalised; throws if the reduced value leaves int64
+        if (b == 0) throw std::domain_error("exact solve: division by zero");
+        if (b < 0) a = -a, b = -b;
+        __int128 x = a < 0 ? -a : a, y = b;
+        while (y) { const __int128 t = x % y; x = y; y = t; }
+        if (x > 1) a /= x, b /= x;
+        const __int128 lim = __int128(INT64_MAX);
+        if (a > lim || a < -lim || b > lim) throw std::overflow_error("exact solve: rational overflow");
+        n = int64_t(a), d = int64_t(b);
     }
-    Frac operator-(const Frac& o) const { return Frac(n * o.d - o.n * d, d * o.d); }
-    Frac operator*(const Frac& o) const { return Frac(n * o.n, d * o.d); }
-    Frac operator/(const Frac& o) const { return Frac(n * o.d, d * o.n); }
+    Frac operator-(const Frac& o) const { return Frac(__int128(n) * o.d - __int128(o.n) * d, __int128(d) * o.d); }
+    Frac operator*(const Frac& o) const { return Frac(__int128(n) * o.n, __int128(d) * o.d); }
+    Frac operator/(const Frac& o) const { return Frac(__int128(n) * o.d, __int128(d) * o.n); }
     bool zero() const { return n == 0; }
+    double to_double() const { return double(n) / double(d); }
 };
 
 // Solve S x = b exactly (S: rows x cols).  Returns false if inconsistent or
@@ -286,6 +291,76 @@ const SfcPlan& plan_for(const std::string& name) {
 }
 
 namespace {
+// Karatsuba components (c0, c1, c0 + c1) of the block value sum_q V_q z_q for the
+// corner weights z_q = s^r * e^c (q = 2 r + c), e = s or conj(s) = s^(N-1).
+void eval_forms(int N, bool conj2, double out[3][4], Frac outf[3][4]) {
+    for (int q = 0; q < 4; ++q) {
+        const int r = q >> 1, c = q & 1;
+        const Zs z = zs_mul(zs_pow(r, N), zs_pow(conj2 ? c * (N - 1) : c, N), N);
+        const int64_t comp[3] = {z.c0, z.c1, z.c0 + z.c1};
+        for (int l = 0; l < 3; ++l) out[l][q] = double(comp[l]), outf[l][q] = Frac(comp[l]);
+    }
+}
+
+PairBlock derive_block(const SfcPlan& p, const int* t1, const int* t2) {
+    PairBlock b{};
+    for (int i = 0; i < 3; ++i) b.r1[i] = t1[i], b.r2[i] = t2[i];
+    // each block row must be additive (row c = row a + row b) in B^T and G on both axes
+    for (const int* t : {t1, t2}) {
+        for (int j = 0; j < p.n_in; ++j)
+            if (p.bt(t[0], j) + p.bt(t[1], j) != p.bt(t[2], j)) throw std::domain_error("block rows not additive");
+        for (int j = 0; j < p.R; ++j)
+            if (p.g(t[0], j) + p.g(t[1], j) != p.g(t[2], j)) throw std::domain_error("block rows not additive");
+    }
+    Frac af[6][4];
+    {
+        double d[3][4];
+        Frac f[3][4];
+        eval_forms(p.N, false, d, f);
+        for (int l = 0; l < 3; ++l)
+            for (int q = 0; q < 4; ++q) b.alpha[l][q] = d[l][q], af[l][q] = f[l][q];
+        eval_forms(p.N, true, d, f);
+        for (int l = 0; l < 3; ++l)
+            for (int q = 0; q < 4; ++q) b.alpha[3 + l][q] = d[l][q], af[3 + l][q] = f[l][q];
+    }
+    for (int l = 0; l < 6; ++l)
+        for (int q = 0; q < 4; ++q) b.beta[l][q] = b.alpha[l][q];
+    // position (i, j) in corner coordinates: row i of {a, b, c} = (1,0), (0,1), (1,1)
+    const int ex[3][2] = {{1, 0}, {0, 1}, {1, 1}};
+    const int M = p.M;
+    std::vector<std::vector<Frac>> S;
+    std::vector<Frac> rhs;
+    for (int o1 = 0; o1 < M; ++o1)
+        for (int o2 = 0; o2 < M; ++o2)
+            for (int qv = 0; qv < 4; ++qv)
+                for (int qu = 0; qu < 4; ++qu) {
+                    int64_t target = 0;
+                    for (int i = 0; i < 3; ++i)
+                        for (int j = 0; j < 3; ++j) {
+                            const int64_t ev = ex[i][qv >> 1] * ex[j][qv & 1], eu = ex[i][qu >> 1] * ex[j][qu & 1];
+                            target += p.a(t1[i], o1) * p.a(t2[j], o2) * ev * eu;
+                        }
+                    std::vector<Frac> row(24);
+                    for (int q = 0; q < 4; ++q) {
+                        const Frac w(p.a(t1[q >> 1], o1) * p.a(t2[q & 1], o2));
+                        for (int l = 0; l < 6; ++l) row[size_t(q) * 6 + l] = w * af[l][qv] * af[l][qu];
+                    }
+                    S.push_back(std::move(row));
+                    rhs.push_back(Frac(target));
+                }
+    std::vector<Frac> sol;
+    if (!solve_unique(S, rhs, sol)) throw std::domain_error("paired block: fold not uniquely determined");
+    for (int q = 0; q < 4; ++q)
+        for (int l = 0; l < 6; ++l) b.fold[q][l] = sol[size_t(q) * 6 + l].to_double();
+    return b;
+}
+
+std::mutex g_pair_mu;
+std::map<std::string, PairedSchedule>& pair_cache() {
+    static std::map<std::string, PairedSchedule> c;
+    return c;
+}
+
 void matrix_json(std::ostringstream& os, const char* key, const std::vector<int64_t>& m, int rows, int cols) {
     os << '"' << key << "\":[";
     for (int i = 0; i < rows; ++i) {
@@ -296,6 +371,27 @@ void matrix_json(std::ostringstream& os, const char* key, const std::vector<int6
     os << ']';
 }
 }  // namespace
+
+const PairedSchedule& paired_schedule(const SfcPlan& p) {
+    std::lock_guard<std::mutex> lock(g_pair_mu);
+    auto it = pair_cache().find(p.name);
+    if (it != pair_cache().end()) return it->second;
+    PairedSchedule ps;
+    const int nt = int(p.triples.size() / 3);
+    if (nt > 0) {
+        ps.masked.assign(size_t(p.K) * p.K, 0);
+        for (int u = 0; u < nt; ++u)
+            for (int v = 0; v < nt; ++v) {
+                const int* t1 = &p.triples[size_t(u) * 3];
+                const int* t2 = &p.triples[size_t(v) * 3];
+                ps.blocks.push_back(derive_block(p, t1, t2));
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) ps.masked[size_t(t1[i]) * p.K + t2[j]] = 1;
+            }
+        ps.available = true;
+    }
+    return pair_cache().emplace(p.name, std::move(ps)).first->second;
+}
 
 std::string plan_export_json(const std::vector<std::string>& names) {
     std::ostringstream os;

@@ -46,6 +46,28 @@ struct SfcPlan {
     int64_t a(int k, int t) const { return A[size_t(k) * M + t]; }
 };
 
+// Paired-product schedule of fast_conv2d's reduced_products option (conv.cpp:39-295,
+// 466-509): on each (axis-1 triple) x (axis-2 triple) block the nine positionwise
+// products collapse to six -- the block's 2-D value evaluated at (s, s) and (s, conj s),
+// each multiplied Karatsuba-style -- folded back onto the four corner positions.
+struct PairBlock {
+    int r1[3], r2[3];    // (a, b, c) transform rows per axis; corners are a/b x a/b
+    double alpha[6][4];  // product l = (alpha[l] . V corners) * (beta[l] . U corners)
+    double beta[6][4];
+    double fold[4][6];   // corner q = 2 r + c gets sum_l fold[q][l] * product l
+};
+struct PairedSchedule {
+    bool available = false;
+    std::vector<uint8_t> masked;  // K*K: position inside some block (no direct product)
+    std::vector<PairBlock> blocks;
+};
+// Derived here (not transcribed): alpha/beta are the Karatsuba components of the two
+// evaluations, and fold is the unique exact solution of the block's output identity
+//   sum_{ij in block} A_i(o1) A_j(o2) V_ij U_ij = sum_{corners} A_r(o1) A_c(o2) fold . products
+// for every output pair (o1, o2) and every V, U.  Throws std::domain_error if the
+// identity has no unique solution.
+const PairedSchedule& paired_schedule(const SfcPlan& p);
+
 // Throws std::invalid_argument for unknown names and std::domain_error when the
 // exactness gate fails.  Returned references live for the process lifetime.
 const SfcPlan& plan_for(const std::string& name);

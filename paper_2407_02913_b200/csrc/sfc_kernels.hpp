@@ -132,5 +132,22 @@ cudaError_t launch_direct_f64(const double* x, int B, int C, int H, int W, const
                               int pad, double* out, cudaStream_t st);
 cudaError_t launch_pack_u_f64(const double* U, int OC, int IC, int F, int Cpad, int OCpad, double* Ub,
                               cudaStream_t st);
+// Paired-product schedule of fast_conv2d (plan.hpp PairedSchedule): slice s of the
+// reduced batch is sum_k a[k] * src[f[k]] (V side) / sum_k b[k] * src[f[k]] (U side);
+// n == 1 is a direct (unpaired) position.
+struct PairSlice {
+    int n, f[4];
+    double a[4], b[4];
+};
+// Position f of P after the reduced batch: kind 0 zero (inside a block, not a corner),
+// 1 copy of slice src, 2 corner: sum_l w[l] * slice (src + l).
+struct PairFold {
+    int kind, src;
+    double w[6];
+};
+cudaError_t launch_pair_gather(const double* src, long long elems, const PairSlice* tab, int nslices, bool filter_side,
+                               double* dst, cudaStream_t st);
+cudaError_t launch_pair_fold(const double* Pr, long long elems, const PairFold* tab, int F, double* P,
+                             cudaStream_t st);
 
 }  // namespace sfcb200

@@ -530,14 +530,15 @@ def _quantized_fast_conv2d_real(input, filters, spec: AlgorithmSpec, padding: in
     return rep
 
 
-def fast_conv2d(input, filters, spec: AlgorithmSpec, padding: int = 0) -> torch.Tensor:
+def fast_conv2d(input, filters, spec: AlgorithmSpec, padding: int = 0, reduced_products: bool = False) -> torch.Tensor:
     """conv.cpp:384-553 (the fp64 float path) on the device: fp64 NCHW output.  Returns the
-    output tensor; fast_conv2d_counters() gives the product / tile counts."""
-    out, _ = fast_conv2d_counters(input, filters, spec, padding)
+    output tensor; fast_conv2d_counters() gives the product / tile counts.  reduced_products
+    is FastConvOptions::reduced_products (the paired 6-for-9 block schedule)."""
+    out, _ = fast_conv2d_counters(input, filters, spec, padding, reduced_products)
     return out
 
 
-def fast_conv2d_counters(input, filters, spec: AlgorithmSpec, padding: int = 0):
+def fast_conv2d_counters(input, filters, spec: AlgorithmSpec, padding: int = 0, reduced_products: bool = False):
     x = as_f64_device(input)
     w = as_f64_device(filters, x.device)
     if x.dim() != 4 or w.dim() != 4:
@@ -553,6 +554,7 @@ def fast_conv2d_counters(input, filters, spec: AlgorithmSpec, padding: int = 0):
         raise ValueError("filter larger than padded input")
     out = torch.empty((B, OC, HO, WO), dtype=torch.float64, device=x.device)
     cnt = np.zeros(2, np.int64)
-    check(lib().sfc_fast_conv_f64(ctypes.c_void_p(spec._handle), _ptr(x), B, C, H, W, _ptr(w), OC, padding, _ptr(out),
+    check(lib().sfc_fast_conv_f64(ctypes.c_void_p(spec._handle), _ptr(x), B, C, H, W, _ptr(w), OC, padding,
+                                  int(bool(reduced_products)), _ptr(out),
                                   cnt.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.c_void_p(_stream_ptr())))
     return out, {"multiplications": int(cnt[0]), "tiles": int(cnt[1])}

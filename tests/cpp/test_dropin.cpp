@@ -341,6 +341,33 @@ int main(int argc, char** argv) {
         }
     });
 
+    run_case("reduced schedule skips the paired products and changes nothing else (test_conv.cpp:140-162)", [] {
+        std::mt19937_64 rng(91);
+        std::normal_distribution<double> nd(0.0, 1.0);
+        DenseTensor x({1, 2, 20, 20});
+        for (auto& v : x.data) v = nd(rng);
+        for (const std::string& name : catalog_names()) {
+            const AlgorithmSpec& s = catalog_algorithm(name);
+            DenseTensor f({3, 2, s.R, s.R});
+            for (auto& v : f.data) v = nd(rng);
+            ConvCounters full_ctr, red_ctr;
+            FastConvOptions full_opts, red_opts;
+            full_opts.counters = &full_ctr;
+            red_opts.counters = &red_ctr;
+            red_opts.reduced_products = true;
+            const DenseTensor yf = fast_conv2d(x, f, s, 1, full_opts), yr = fast_conv2d(x, f, s, 1, red_opts);
+            double md = 0.0, mr = 0.0;
+            for (std::size_t i = 0; i < yf.data.size(); ++i) {
+                md = std::max(md, std::abs(yr.data[i] - yf.data[i]));
+                mr = std::max(mr, std::abs(yf.data[i]));
+            }
+            CHECK(md / mr < 1e-12);
+            CHECK(full_ctr.multiplications == s.mults_full() * full_ctr.tiles * 2 * 3);
+            CHECK(red_ctr.multiplications == s.mults_reduced() * red_ctr.tiles * 2 * 3);
+            CHECK(red_ctr.multiplications < full_ctr.multiplications);
+        }
+    });
+
     run_case("bitwise determinism across calls and threads (test_conv.cpp:177-192)", [] {
         const DenseTensor x = int8_tensor({2, 16, 20, 20}, 70), f = int8_tensor({8, 16, 3, 3}, 71, -127, 127);
         const AlgorithmSpec& s = catalog_algorithm("sfc6-7x7-3x3");

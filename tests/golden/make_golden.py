@@ -126,6 +126,9 @@ def real_valued():
             fo, mults = ob.ref_fast_conv2d(x, w, v, pad)  # the fp64 float path (conv.cpp:384-553)
             arrays[f"{tag}/{v}/fast"] = fo
             arrays[f"{tag}/{v}/fast_counts"] = mults
+            fo, mults = ob.ref_fast_conv2d(x, w, v, pad, reduced=True)  # paired schedule (conv.cpp:466-509)
+            arrays[f"{tag}/{v}/fast_red"] = fo
+            arrays[f"{tag}/{v}/fast_red_counts"] = mults
     np.savez_compressed(os.path.join(HERE, "qconv_real.npz"), **arrays)
     print("wrote", len(arrays), "real-valued arrays")
 

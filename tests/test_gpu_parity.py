@@ -508,3 +508,21 @@ def test_fast_conv2d_float_path(cuda, tag, variant):
     assert maxrel(got, GOLD_REAL[f"{tag}/{variant}/fast"]) <= 1e-12
     assert maxrel(got, GOLD_REAL[f"{tag}/{variant}/direct"]) <= 1e-10
     assert [cnt["multiplications"], cnt["tiles"]] == list(GOLD_REAL[f"{tag}/{variant}/fast_counts"])
+
+
+@pytest.mark.parametrize("variant", VARIANTS + LARGE_R)
+@pytest.mark.parametrize("tag", TAGS_REAL)
+def test_fast_conv2d_paired_schedule(cuda, tag, variant):
+    """reduced_products (conv.cpp:466-509): six evaluation products per (triple x triple) block
+    folded onto its corners.  Matches the reference's own paired output (<= 1e-12), the full
+    schedule (<= 1e-12, test_conv.cpp:140-162) and the reference's paired product count."""
+    x, w = GOLD_REAL[f"{tag}/x"], GOLD_REAL[f"{tag}/{variant}/w"]
+    pad = int(GOLD_REAL[f"{tag}/{variant}/report"][5])
+    spec = sc.catalog_algorithm(variant)
+    out, cnt = sc.fast_conv2d_counters(torch.from_numpy(x), torch.from_numpy(w), spec, pad, reduced_products=True)
+    got = out.cpu().numpy()
+    assert maxrel(got, GOLD_REAL[f"{tag}/{variant}/fast_red"]) <= 1e-12
+    assert maxrel(got, GOLD_REAL[f"{tag}/{variant}/fast"]) <= 1e-12
+    assert [cnt["multiplications"], cnt["tiles"]] == list(GOLD_REAL[f"{tag}/{variant}/fast_red_counts"])
+    B, C = x.shape[:2]
+    assert cnt["multiplications"] == spec.mults_reduced() * cnt["tiles"] * w.shape[0] * C
