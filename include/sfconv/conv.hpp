@@ -1,8 +1,11 @@
 // sfconv:: drop-in (B200 build) -- convolution entry points of the reference
-// (include/sfconv/conv.hpp:12-36).  direct_conv2d and transform_filters run on
-// the device for int8-valued tensors (exact int32 arithmetic); fast_conv2d, the
-// reference's fp64 float path (conv.cpp:384-553), is not part of this build's
-// device path yet and throws std::logic_error instead of falling back to a CPU.
+// (include/sfconv/conv.hpp:12-36), all on the device.  direct_conv2d and
+// transform_filters are exact int32 for int8-valued tensors and fp64 in the
+// reference's summation order otherwise; fast_conv2d, the reference's fp64 float
+// path (conv.cpp:384-553), forms V and U in the reference's order, contracts the
+// K^2 frequencies (or the paired schedule's mults_reduced() slices when
+// opts.reduced_products) as one batched fp64 GEMM and reports the counters.
+// opts.threads is a host-CPU knob of the reference: accepted, without effect.
 #pragma once
 
 #include <cstdint>

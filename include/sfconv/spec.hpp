@@ -1,8 +1,8 @@
 // sfconv:: drop-in (B200 build) -- algorithm specs and the catalog.
 // Declarations match the reference's include/sfconv/spec.hpp (AlgorithmSpec
 // spec.hpp:36-62, catalog spec.hpp:76-79, validation spec.hpp:85-99).  The
-// catalog of this build serves the device path: the three 3x3 SFC algorithms
-// ("sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"), derived by the plan layer
+// catalog of this build serves the device path: the five SFC algorithms
+// ("sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3", "sfc6-6x6-5x5", "sfc6-4x4-7x7"), derived by the plan layer
 // (paper_2407_02913_b200/csrc/plan.cpp), exactness-gated, and identical to the
 // reference's entries.  Other names throw std::invalid_argument("unknown
 // algorithm: ...") exactly like an unknown name in the reference.

@@ -130,11 +130,12 @@ def catalog_algorithm(name: str) -> AlgorithmSpec:
 
 
 def catalog_names():
-    return ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]
+    """The SFC entries of the reference catalog, in its order (catalog.cpp:246-250)."""
+    return ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3", "sfc6-6x6-5x5", "sfc6-4x4-7x7"]
 
 
 def catalog_export_json() -> tuple[str, int]:
-    buf = ctypes.create_string_buffer(1 << 16)
+    buf = ctypes.create_string_buffer(1 << 18)
     h = ctypes.c_uint64()
     check(lib().sfc_catalog_json(buf, len(buf), ctypes.byref(h)))
     return buf.value.decode(), h.value

@@ -11,6 +11,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <iterator>
+#include <limits>
 #include <fstream>
 #include <functional>
 #include <random>
@@ -20,8 +23,10 @@
 #include <vector>
 
 #include "sfconv/conv.hpp"
+#include "sfconv/manifest.hpp"
 #include "sfconv/quant.hpp"
 #include "sfconv/spec.hpp"
+#include "sfconv/tensor.hpp"
 
 using namespace sfconv;
 
@@ -148,8 +153,21 @@ int run_mode(int argc, char** argv) {
 }
 }  // namespace
 
+// test_dropin sfct-copy IN OUT: load_sfct then save_sfct (cross-checked against the Python writer)
+int sfct_copy(int argc, char** argv) {
+    if (argc != 4) return 2;
+    try {
+        save_sfct(argv[3], load_sfct(argv[2]));
+    } catch (const std::runtime_error& e) {
+        std::printf("%s\n", e.what());
+        return 1;
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
     if (argc > 1 && std::string(argv[1]) == "run") return run_mode(argc, argv);
+    if (argc > 1 && std::string(argv[1]) == "sfct-copy") return sfct_copy(argc, argv);
     g_host_only = argc > 1 && std::string(argv[1]) == "--host-only";
 
     run_case("catalog holds the SFC algorithms (test_catalog.cpp:31-39, catalog.cpp:246-250)", [] {
@@ -158,6 +176,77 @@ int main(int argc, char** argv) {
                                              "sfc6-4x4-7x7"}));
         CHECK(catalog_algorithm("sfc6-6x6-5x5").R == 5 && catalog_algorithm("sfc6-4x4-7x7").R == 7);
         CHECK(throws<std::invalid_argument>([] { catalog_algorithm("wino-9x9-3x3"); }));
+    }, false);
+
+    run_case("SFCT round trip and error messages (test_tensor.cpp:38-83)", [] {
+        const std::string path = "/tmp/sfc_dropin_test.sfct";
+        DenseTensor t({2, 3, 4, 5});
+        for (std::size_t i = 0; i < t.data.size(); ++i) t.data[i] = std::ldexp(double(i) - 60.5, int(i % 7) - 3);
+        t.data[7] = -0.0;
+        t.data[8] = 1e-308;
+        t.data[9] = std::numeric_limits<double>::denorm_min();
+        save_sfct(path, t);
+        const DenseTensor u = load_sfct(path);
+        CHECK(u.shape == t.shape);
+        CHECK(std::memcmp(u.data.data(), t.data.data(), t.data.size() * 8) == 0);
+        std::ifstream raw(path, std::ios::binary);
+        std::string bytes((std::istreambuf_iterator<char>(raw)), std::istreambuf_iterator<char>());
+        const std::string header = "{\"dtype\":\"f64\",\"layout\":\"row-major-nchw\",\"shape\":[2,3,4,5]}";
+        CHECK(bytes.compare(0, 8, "SFCT0001") == 0);
+        CHECK(std::uint8_t(bytes[8]) == header.size() && bytes[9] == 0 && bytes[10] == 0 && bytes[11] == 0);
+        CHECK(bytes.compare(12, header.size(), header) == 0);
+        CHECK(bytes.size() == 12 + header.size() + t.data.size() * 8);
+        auto message = [](const std::string& p) {
+            try {
+                load_sfct(p);
+            } catch (const std::runtime_error& e) {
+                return std::string(e.what());
+            }
+            return std::string("no error");
+        };
+        { std::ofstream(path, std::ios::binary) << "NOTSFCT!xxxx"; }
+        CHECK(message(path) == "not an SFCT file: " + path);
+        { std::ofstream(path, std::ios::binary) << bytes.substr(0, 10); }
+        CHECK(message(path) == "truncated SFCT header: " + path);
+        { std::ofstream(path, std::ios::binary) << bytes.substr(0, bytes.size() - 1); }
+        CHECK(message(path) == "truncated SFCT payload: " + path);
+        std::string f32 = bytes;
+        f32.replace(12 + 10, 3, "f32");
+        { std::ofstream(path, std::ios::binary) << f32; }
+        CHECK(message(path) == "unsupported SFCT dtype: f32");
+        CHECK(message("/tmp/definitely_not_here.sfct") == "cannot open: /tmp/definitely_not_here.sfct");
+        std::remove(path.c_str());
+    }, false);
+
+    run_case("layer lists and run manifests (test_tensor.cpp:85-131, manifest.cpp:7-16)", [] {
+        const std::string path = "/tmp/sfc_dropin_layers.json";
+        {
+            std::ofstream o(path);
+            o << "[{\"name\": \"a\", \"in_channels\": 3, \"out_channels\": 8, \"height\": 32, \"width\": 30,"
+                 " \"kernel\": 3, \"padding\": 1}, {\"in_channels\": 2, \"out_channels\": 2, \"height\": 9,"
+                 " \"width\": 9, \"kernel\": 5, \"stride\": 2}]";
+        }
+        const std::vector<LayerConfig> ls = load_layer_configs(path);
+        CHECK(ls.size() == 2 && ls[0].name == "a" && ls[0].width == 30 && ls[0].padding == 1 && ls[0].stride == 1);
+        CHECK(ls[1].name == "layer1" && ls[1].kernel == 5 && ls[1].stride == 2 && ls[1].padding == 0);
+        const std::string js = layer_configs_to_json(ls);
+        CHECK(js.rfind("[\n  {\n    \"height\": 32,\n    \"in_channels\": 3,\n    \"kernel\": 3,\n    \"name\": \"a\",", 0) == 0);
+        { std::ofstream(path) << js; }
+        const std::vector<LayerConfig> again = load_layer_configs(path);
+        CHECK(again.size() == 2 && again[1].name == "layer1" && again[1].stride == 2);
+        { std::ofstream(path) << "[{\"in_channels\": 0, \"out_channels\": 1, \"height\": 1, \"width\": 1, \"kernel\": 3}]"; }
+        CHECK(throws<std::runtime_error>([&] { load_layer_configs(path); }));
+        { std::ofstream(path) << "{\"in_channels\": 1}"; }
+        CHECK(throws<std::runtime_error>([&] { load_layer_configs(path); }));
+        CHECK(throws<std::runtime_error>([] { load_layer_configs("/nonexistent/layers.json"); }));
+        std::remove(path.c_str());
+        RunManifest m;
+        m.command = "quantsim";
+        m.seed = 0x5fc07751u;
+        m.output_dir = "out";
+        m.catalog_hash = 18446744073709551615ull;
+        CHECK(m.to_json() == "{\n  \"catalog_hash\": 18446744073709551615,\n  \"command\": \"quantsim\",\n"
+                             "  \"config_path\": \"\",\n  \"output_dir\": \"out\",\n  \"seed\": 1606448977\n}");
     }, false);
 
     run_case("channel and product counts (test_catalog.cpp:101-126)", [] {

@@ -1,7 +1,10 @@
 """Generate the committed golden fixtures from the *reference itself* (oracle/_ref, built
 from /root/reference/proj/src by oracle/Makefile).  Run in the build container:
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py            (qconv_cases.npz, catalog_3x3.json)
+    python tests/golden/make_golden.py --large-r  (qconv_large_r.npz, catalog_large_r.json)
+    python tests/golden/make_golden.py --real     (qconv_real.npz)
+    python tests/golden/make_golden.py --cli      (cli_golden.json, cli_layers.json)
 
 Writes tests/golden/catalog_3x3.json (the reference's catalog export restricted to the
 three 3x3 SFC specs + the full-catalog FNV hash) and tests/golden/qconv_cases.npz (seeded
@@ -133,7 +136,107 @@ def real_valued():
     print("wrote", len(arrays), "real-valued arrays")
 
 
+# ------------------------------------------------------------------ command-line drop-in
+# quantsim cases: CLI options (None = the CLI default) -> the reference's report per layer
+CLI_QUANTSIM = [
+    {"name": "defaults"},
+    {"name": "sfc4_bits6_actfreq", "seed": "7", "algo": "sfc4-4x4-3x3", "bits": 6, "act": "frequency"},
+    {"name": "sfc7_chfreq_mse_onef", "seed": "11", "algo": "sfc6-7x7-3x3", "fil": "channel-frequency",
+     "search": "mse", "gen": "onef", "channels": 6, "out_channels": 5, "size": 30},
+    {"name": "sfc5x5_freq_bits4", "seed": "0x2a", "algo": "sfc6-6x6-5x5", "bits": 4, "fil": "frequency",
+     "padding": 2, "size": 19},
+    {"name": "sfc7x7_onef", "seed": "99", "algo": "sfc6-4x4-7x7", "gen": "onef", "padding": 3, "size": 20},
+    {"name": "bits2_saturating", "seed": "5", "bits": 2, "search": "mse", "channels": 3, "out_channels": 2},
+    {"name": "layers_file", "seed": "1234", "bits": 7, "search": "mse", "layers": "cli_layers.json"},
+    {"name": "env_seed", "env_seed": "12345", "act": "frequency", "fil": "channel-frequency"},
+]
+CLI_LAYERS = [  # tests/golden/cli_layers.json (the reference's layer-list format, tensor.cpp:66-90)
+    {"name": "conv1", "in_channels": 3, "out_channels": 8, "height": 32, "width": 32, "kernel": 3, "padding": 1},
+    {"name": "conv2", "in_channels": 8, "out_channels": 4, "height": 17, "width": 23, "kernel": 3},
+    {"in_channels": 4, "out_channels": 4, "height": 12, "width": 12, "kernel": 3, "stride": 1, "padding": 1},
+]
+CLI_BENCH = [
+    {"name": "defaults"},
+    {"name": "reduced", "reduced": True},
+    {"name": "sfc4_onef_reduced", "seed": "3", "algo": "sfc4-4x4-3x3", "gen": "onef", "size": 30,
+     "channels": 5, "out_channels": 3, "reduced": True},
+    {"name": "sfc5x5", "algo": "sfc6-6x6-5x5", "padding": 2, "size": 26, "channels": 4, "out_channels": 6},
+]
+CLI_DEFAULT_SEED = "0x5fc07751"  # sfconv_cli.cpp:30
+
+
+def cli_quantsim_argv(c):
+    """Command line of the drop-in CLI for a quantsim case (the environment goes separately)."""
+    argv = (["--seed", c["seed"]] if "seed" in c else []) + ["quantsim"]
+    for key, flag in [("algo", "--algo"), ("bits", "--bits"), ("act", "--act-scope"), ("fil", "--filter-scope"),
+                      ("search", "--search"), ("gen", "--gen"), ("channels", "--channels"),
+                      ("out_channels", "--out-channels"), ("size", "--size"), ("padding", "--padding")]:
+        if key in c:
+            argv += [flag, str(c[key])]
+    if "layers" in c:
+        argv += ["--layers", os.path.join("tests", "golden", c["layers"])]
+    return argv
+
+
+def cli_bench_argv(c):
+    argv = (["--seed", c["seed"]] if "seed" in c else []) + ["bench"]
+    for key, flag in [("algo", "--algo"), ("gen", "--gen"), ("channels", "--channels"),
+                      ("out_channels", "--out-channels"), ("size", "--size"), ("padding", "--padding")]:
+        if key in c:
+            argv += [flag, str(c[key])]
+    if c.get("reduced"):
+        argv.append("--reduced")
+    return argv
+
+
+def cli_golden():
+    """tests/golden/cli_golden.json: the reference library's quantsim reports / bench counters
+    for the CLI cases, through oracle/_ref/cli_golden (inputs drawn as sfconv_cli.cpp does)."""
+    import subprocess
+    drv = os.path.join(ROOT, "oracle", "_ref", "cli_golden")
+    if not os.path.exists(drv):
+        raise SystemExit("oracle/_ref/cli_golden missing: run `make -C oracle` with /root/reference present")
+    with open(os.path.join(HERE, "cli_layers.json"), "w") as f:
+        json.dump(CLI_LAYERS, f, indent=2)
+    out = {"quantsim": [], "bench": []}
+    for c in CLI_QUANTSIM:
+        algo = c.get("algo", "sfc6-6x6-3x3")
+        R = ob.spec(algo, source="ref")["R"]
+        if "layers" in c:
+            specs = [f"{lc.get('name', f'layer{i}')}:{lc['in_channels']}:{lc['out_channels']}:{lc['height']}:"
+                     f"{lc['width']}:{lc['kernel']}:{lc.get('padding', 0)}" for i, lc in enumerate(CLI_LAYERS)]
+        else:
+            size = c.get("size", 24)
+            specs = [f"inline:{c.get('channels', 4)}:{c.get('out_channels', 4)}:{size}:{size}:{R}:{c.get('padding', 1)}"]
+        seed = c.get("seed", c.get("env_seed", CLI_DEFAULT_SEED))
+        res = subprocess.run([drv, "quantsim", seed, algo, str(c.get("bits", 8)), c.get("act", "tensor"),
+                              c.get("fil", "channel"), c.get("search", "minmax"), c.get("gen", "gaussian"),
+                              ",".join(specs)], check=True, capture_output=True, text=True).stdout
+        rows = []
+        for line in res.strip().splitlines():
+            name, mse, snr, sat, vq = line.split()
+            rows.append({"layer": name, "mse": float(mse), "snr_db": float(snr), "saturations": int(sat),
+                         "values_quantized": int(vq)})
+        env = {"SFC_SEED": c["env_seed"]} if "env_seed" in c else {}
+        out["quantsim"].append({"name": c["name"], "argv": cli_quantsim_argv(c), "env": env, "seed": int(seed, 0),
+                                "results": rows})
+    for c in CLI_BENCH:
+        algo = c.get("algo", "sfc6-6x6-3x3")
+        seed = c.get("seed", CLI_DEFAULT_SEED)
+        res = subprocess.run([drv, "bench", seed, algo, c.get("gen", "gaussian"), str(c.get("channels", 8)),
+                              str(c.get("out_channels", 8)), str(c.get("size", 56)), str(c.get("padding", 1)),
+                              "1" if c.get("reduced") else "0"], check=True, capture_output=True, text=True).stdout
+        rel, mults, tiles = res.split()
+        out["bench"].append({"name": c["name"], "argv": cli_bench_argv(c), "rel": float(rel),
+                             "multiplications": int(mults), "tiles": int(tiles)})
+    with open(os.path.join(HERE, "cli_golden.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote", len(out["quantsim"]), "quantsim and", len(out["bench"]), "bench cases")
+
+
 def main():
+    if "--cli" in sys.argv:
+        return cli_golden()
     if "--large-r" in sys.argv:
         return large_r()
     if "--real" in sys.argv:
