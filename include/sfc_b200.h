@@ -73,15 +73,17 @@ int sfc_plan_matrices(sfc_plan_t plan, int64_t* bt, int64_t* g, int64_t* a);
 
 /* Runs U = G f G^T, the filter scales of `filter_scope` found by `search` and exact RNE
  * quantization on `stream` and keeps the quantized transformed filters on the
- * device.  Synchronous (returns once the layer is ready).  bits in [2, 8] (9-16:
- * SFC_ERR_UNSUPPORTED); activation scope PerTensor. */
+ * device.  Synchronous (returns once the layer is ready).  bits in [2, 16]; 9-16 bits
+ * take the parity path below (operands exceed int8); activation scope PerTensor. */
 int sfc_layer_create(sfc_plan_t plan, const int8_t* d_weights, int out_channels, int in_channels, int bits,
                      int filter_scope, int search, void* stream, sfc_layer_t* out);
 /* The whole QuantConfig (quant.hpp:27-34): act_scope SFC_ACT_*, filter_scope SFC_FIL_*,
  * search SFC_SEARCH_*.  Anything but {PerTensor, PerChannel, MinMax} selects the parity
  * path: per-frequency dequantisation before the inverse transform in fp64 (quant.cpp:258-278),
  * scale searches in the reference's order; such layers run through sfc_conv_forward only
- * and produce out_f32 / out_f64 / out_i8 (y_int is not defined for them). */
+ * and produce out_f32 / out_f64 / out_i8 (y_int is not defined for them).  bits 9-16 (any
+ * scope) keep vq / uq as integer-valued doubles and contract them with an exact fp64
+ * batched GEMM (|pacc| <= C * 2^30 < 2^53, so pacc is the reference's int64 exactly). */
 int sfc_layer_create_ex(sfc_plan_t plan, const int8_t* d_weights, int out_channels, int in_channels, int bits,
                         int act_scope, int filter_scope, int search, void* stream, sfc_layer_t* out);
 int sfc_layer_destroy(sfc_layer_t layer);

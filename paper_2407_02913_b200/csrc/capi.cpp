@@ -37,6 +37,9 @@ struct sfc_layer {
     double* d_fil = nullptr;       // [OC][F] filter scale per (oc, f)
     double* d_fil_native = nullptr;  // scales as the scope defines them (OC, F or OC*F)
     int n_fil_native = 0;
+    // bits 9-16 (the reference's full width range): uq as integer-valued doubles
+    // [F][OCpad][Cpad], contracted by an exact fp64 GEMM (|P| <= IC * 2^30 < 2^53)
+    double* d_uqw = nullptr;
 };
 
 namespace {
@@ -80,6 +83,43 @@ struct Unsupported : std::length_error {
 };
 
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// cuBLAS for the fp64 contractions (tcgen05 has no fp64 kind): one handle per host thread.
+cublasHandle_t cublas_on(cudaStream_t st) {
+    thread_local cublasHandle_t handle = nullptr;
+    if (!handle && cublasCreate(&handle) != CUBLAS_STATUS_SUCCESS) throw CudaFail("cublasCreate failed");
+    if (cublasSetStream(handle, st) != CUBLAS_STATUS_SUCCESS) throw CudaFail("cublasSetStream failed");
+    return handle;
+}
+
+// P_f[t][o] = sum_c V_f[t][c] U_f[o][c] for `batch` frequency slices (row-major), i.e. the
+// column-major P_f^T (OCpad x Tpad) = U_f (op T of the col-major view) x V_f^T.
+void dgemm_freq(const double* U, const double* V, double* P, const ConvGeom& g, int batch, cudaStream_t st) {
+    const double one = 1.0, zero = 0.0;
+    if (cublasDgemmStridedBatched(cublas_on(st), CUBLAS_OP_T, CUBLAS_OP_N, g.OCpad, g.Tpad, g.Cpad, &one, U, g.Cpad,
+                                  (long long)g.OCpad * g.Cpad, V, g.Cpad, (long long)g.Tpad * g.Cpad, &zero, P, g.OCpad,
+                                  (long long)g.Tpad * g.OCpad, batch) != CUBLAS_STATUS_SUCCESS)
+        throw CudaFail("cublasDgemmStridedBatched failed");
+}
+
+// The wide (9-16 bit) tail of a general forward: vq as integer-valued doubles from the
+// activation quantizer, the exact fp64 contraction, then the mode-4 epilogue (fp64 P
+// dequantised per (oc, f) in the reference's order, quant.cpp:251-278).  `quantize`
+// fills vq (already zeroed, [F][Tpad][Cpad]).
+template <class Q>
+void wide_tail(const sfc_layer* L, const ConvGeom& g, const OutPtrs& op, const QuantParams* qp, Q&& quantize,
+               cudaStream_t st) {
+    const size_t nv = size_t(L->F) * g.Tpad * g.Cpad, np = size_t(L->F) * g.Tpad * g.OCpad;
+    double *vq = nullptr, *P = nullptr;
+    ck(cudaMallocAsync(&vq, nv * sizeof(double), st), "alloc wide vq");
+    ck(cudaMallocAsync(&P, np * sizeof(double), st), "alloc wide P");
+    ck(cudaMemsetAsync(vq, 0, nv * sizeof(double), st), "memset wide vq");
+    quantize(vq);
+    dgemm_freq(L->d_uqw, vq, P, g, L->F, st);
+    ck(launch_output(L->variant, 4, P, g, qp, L->d_sf, op, st, false), "output launch");
+    ck(cudaFreeAsync(vq, st), "free wide vq");
+    ck(cudaFreeAsync(P, st), "free wide P");
+}
 
 // Workspace carve-up (kept in sync with workspace_bytes()).
 struct WsView {
@@ -253,13 +293,13 @@ int sfc_layer_create_ex(sfc_plan_t plan, const int8_t* d_w, int oc, int ic, int 
         if (!plan || !d_w || !out) throw std::invalid_argument("null argument");
         if (bits < 2 || bits > 16) throw std::invalid_argument("quantization width must be between 2 and 16 bits");
         if (oc <= 0 || ic <= 0) throw std::invalid_argument("bad filter shape");
-        if (bits > 8) throw Unsupported("bits > 8 is not on the int8 tensor-core path yet");
         if (act_scope < 0 || act_scope > 1 || filter_scope < 0 || filter_scope > 2 || search < 0 || search > 1)
             throw std::invalid_argument("bad quantization config");
         L = new sfc_layer();
         L->act_scope = act_scope, L->filter_scope = filter_scope, L->search = search;
-        L->general = !(act_scope == SFC_ACT_PER_TENSOR && filter_scope == SFC_FIL_PER_CHANNEL &&
-                       search == SFC_SEARCH_MINMAX);
+        // bits 9-16 exceed the int8 operands: every scope then takes the fp64 parity path
+        L->general = bits > 8 || !(act_scope == SFC_ACT_PER_TENSOR && filter_scope == SFC_FIL_PER_CHANNEL &&
+                                   search == SFC_SEARCH_MINMAX);
         L->plan = plan->p;
         qparams_table(true);  // once per device; the kernels derive per CTA if this failed
         L->variant = plan->p->variant;
@@ -297,8 +337,15 @@ int sfc_layer_create_ex(sfc_plan_t plan, const int8_t* d_w, int oc, int ic, int 
             ck(cudaMallocAsync(&U, sizeof(int32_t) * size_t(oc) * ic * F, S(stream)), "alloc U");
             ck(cudaMallocAsync(&err, sizeof(double) * size_t(L->n_fil_native) * 101, S(stream)), "alloc err");
             ck(launch_transform_filters(L->variant, d_w, oc, ic, U, S(stream)), "transform filters launch");
+            void* uq_out = L->d_uq;
+            if (bits > 8) {
+                const size_t n = size_t(F) * L->OCpad * L->Cpad;
+                ck(cudaMalloc(&L->d_uqw, n * sizeof(double)), "cudaMalloc wide uq");
+                ck(cudaMemsetAsync(L->d_uqw, 0, n * sizeof(double), S(stream)), "memset wide uq");
+                uq_out = L->d_uqw;
+            }
             ck(launch_fil_general(U, oc, ic, F, filter_scope, search == SFC_SEARCH_MSE_GRID, bits, L->Cpad, L->OCpad,
-                                  L->d_fil_native, err, L->d_uq, L->d_fil, L->d_sat, S(stream)),
+                                  L->d_fil_native, err, uq_out, L->d_fil, L->d_sat, S(stream)),
                "general filter launch");
             ck(cudaFreeAsync(U, S(stream)), "free U");
             ck(cudaFreeAsync(err, S(stream)), "free err");
@@ -324,6 +371,7 @@ int sfc_layer_destroy(sfc_layer_t L) {
     cudaFree(L->d_sat);
     cudaFree(L->d_fil);
     cudaFree(L->d_fil_native);
+    cudaFree(L->d_uqw);
     delete L;
     return SFC_OK;
 }
@@ -430,12 +478,16 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
             ck(cudaMemsetAsync(ws, 0, kWsMaxima + sizeof(unsigned long long) * L->F, S(stream)), "memset header");
             ck(launch_act_absmax(L->variant, d_x, g, v.vmax, v.vkeep, S(stream), false), "absmax launch");
             const bool pf = L->act_scope == SFC_ACT_PER_FREQUENCY;
-            ck(launch_act_general(v.vkeep, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits, v.vmaxf,
-                                  v.act_scale, v.vq, v.sat, S(stream)),
-               "general activation launch");
-            ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, S(stream), false), "gemm launch");
             OutPtrs op{nullptr, nullptr, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
             op.gen_act = v.act_scale, op.gen_per_freq = pf ? 1 : 0, op.gen_fil = L->d_fil;
+            auto quantize = [&](void* vq) {
+                ck(launch_act_general(v.vkeep, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits, v.vmaxf,
+                                      v.act_scale, vq, v.sat, S(stream)),
+                   "general activation launch");
+            };
+            if (L->bits > 8) return wide_tail(L, g, op, v.qp, quantize, S(stream));
+            quantize(v.vq);
+            ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, S(stream), false), "gemm launch");
             ck(launch_output(L->variant, 2, v.P, g, v.qp, L->d_sf, op, S(stream), false), "output launch");
             return;
         }
@@ -593,7 +645,6 @@ int sfc_layer_create_f64(sfc_plan_t plan, const double* d_w, int oc, int ic, int
         if (!plan || !d_w || !out) throw std::invalid_argument("null argument");
         if (bits < 2 || bits > 16) throw std::invalid_argument("quantization width must be between 2 and 16 bits");
         if (oc <= 0 || ic <= 0) throw std::invalid_argument("bad filter shape");
-        if (bits > 8) throw Unsupported("bits > 8 is not on the int8 tensor-core path yet");
         if (act_scope < 0 || act_scope > 1 || filter_scope < 0 || filter_scope > 2 || search < 0 || search > 1)
             throw std::invalid_argument("bad quantization config");
         L = new sfc_layer();
@@ -623,8 +674,15 @@ int sfc_layer_create_f64(sfc_plan_t plan, const double* d_w, int oc, int ic, int
         ck(cudaMallocAsync(&U, sizeof(double) * size_t(oc) * ic * F, S(stream)), "alloc U");
         ck(cudaMallocAsync(&err, sizeof(double) * size_t(L->n_fil_native) * 101, S(stream)), "alloc err");
         ck(launch_filters_f64(L->variant, d_w, oc, ic, U, S(stream)), "fp64 filter transform launch");
+        void* uq_out = L->d_uq;
+        if (bits > 8) {
+            const size_t nw = size_t(F) * L->OCpad * L->Cpad;
+            ck(cudaMalloc(&L->d_uqw, nw * sizeof(double)), "cudaMalloc wide uq");
+            ck(cudaMemsetAsync(L->d_uqw, 0, nw * sizeof(double), S(stream)), "memset wide uq");
+            uq_out = L->d_uqw;
+        }
         ck(launch_fil_general_f64(U, oc, ic, F, filter_scope, search == SFC_SEARCH_MSE_GRID, bits, L->Cpad, L->OCpad,
-                                  L->d_fil_native, err, L->d_uq, L->d_fil, L->d_sat, S(stream)),
+                                  L->d_fil_native, err, uq_out, L->d_fil, L->d_sat, S(stream)),
            "general filter launch");
         ck(cudaFreeAsync(U, S(stream)), "free U");
         ck(cudaFreeAsync(err, S(stream)), "free err");
@@ -653,13 +711,21 @@ int sfc_conv_forward_f64(sfc_layer_t L, const double* d_x, int n, int h, int w, 
         ck(cudaMallocAsync(&Vd, sizeof(double) * size_t(L->F) * g.Tpad * g.Cpad, S(stream)), "alloc V");
         ck(launch_act_f64(L->variant, d_x, g, Vd, S(stream)), "fp64 input transform launch");
         const bool pf = L->act_scope == SFC_ACT_PER_FREQUENCY;
-        ck(launch_act_general_f64(Vd, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits, v.vmaxf, v.act_scale,
-                                  v.vq, v.sat, S(stream)),
-           "general activation launch");
-        ck(cudaFreeAsync(Vd, S(stream)), "free V");
-        ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, S(stream), false), "gemm launch");
         OutPtrs op{nullptr, nullptr, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
         op.gen_act = v.act_scale, op.gen_per_freq = pf ? 1 : 0, op.gen_fil = L->d_fil;
+        auto quantize = [&](void* vq) {
+            ck(launch_act_general_f64(Vd, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits, v.vmaxf, v.act_scale,
+                                      vq, v.sat, S(stream)),
+               "general activation launch");
+        };
+        if (L->bits > 8) {
+            wide_tail(L, g, op, v.qp, quantize, S(stream));
+            ck(cudaFreeAsync(Vd, S(stream)), "free V");
+            return;
+        }
+        quantize(v.vq);
+        ck(cudaFreeAsync(Vd, S(stream)), "free V");
+        ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, S(stream), false), "gemm launch");
         ck(launch_output(L->variant, 2, v.P, g, v.qp, L->d_sf, op, S(stream), false), "output launch");
     });
 }
@@ -677,10 +743,6 @@ int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, i
         geom_init(g, P.variant, n, c, h, w, pad, oc);
         const int F = P.K * P.K;
         const cudaStream_t st = S(stream);
-        // per-thread cuBLAS handle (a plain fp64 GEMM: tcgen05 has no fp64 kind)
-        thread_local cublasHandle_t handle = nullptr;
-        if (!handle && cublasCreate(&handle) != CUBLAS_STATUS_SUCCESS) throw CudaFail("cublasCreate failed");
-        if (cublasSetStream(handle, st) != CUBLAS_STATUS_SUCCESS) throw CudaFail("cublasSetStream failed");
         const size_t nv = size_t(F) * g.Tpad * g.Cpad, nu = size_t(oc) * c * F, nb = size_t(F) * g.OCpad * g.Cpad;
         const size_t np = size_t(F) * g.Tpad * g.OCpad;
         double *Vd = nullptr, *U = nullptr, *Ub = nullptr, *Pd = nullptr;
@@ -696,14 +758,8 @@ int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, i
         ck(launch_act_f64(P.variant, d_x, g, Vd, st), "fp64 input transform launch");
         ck(launch_filters_f64(P.variant, d_weights, oc, c, U, st), "fp64 filter transform launch");
         ck(launch_pack_u_f64(U, oc, c, F, g.Cpad, g.OCpad, Ub, st), "pack launch");
-        // P_f[t][o] = sum_c V_f[t][c] Ub_f[o][c] for every f (row-major), i.e. column-major
-        // P_f^T (OCpad x Tpad) = Ub_f (op T of the col-major view) x V_f^T
-        const double one = 1.0, zero = 0.0;
         auto gemm = [&](const double* Ua, const double* Va, double* Pa, int batch) {
-            if (cublasDgemmStridedBatched(handle, CUBLAS_OP_T, CUBLAS_OP_N, g.OCpad, g.Tpad, g.Cpad, &one, Ua, g.Cpad,
-                                          (long long)g.OCpad * g.Cpad, Va, g.Cpad, (long long)g.Tpad * g.Cpad, &zero,
-                                          Pa, g.OCpad, (long long)g.Tpad * g.OCpad, batch) != CUBLAS_STATUS_SUCCESS)
-                throw CudaFail("cublasDgemmStridedBatched failed");
+            dgemm_freq(Ua, Va, Pa, g, batch, st);
         };
         const PairedSchedule* ps = nullptr;
         if (reduced) {  // conv.cpp:399-403: no schedule (no triples) means the full product set

@@ -88,19 +88,19 @@ __global__ void k_pick_best(int groups, const double* __restrict__ err, double* 
 }
 
 // uq[f][oc][ic] = quantize_value(U, fil(oc, f)) (quant.cpp:221-229) and the expanded table
-// fil_full[oc * F + f] the fp64 output epilogue reads.
-template <class TU>
+// fil_full[oc * F + f] the fp64 output epilogue reads.  QT = int8_t (bits <= 8, the
+// tensor-core operand) or double (bits 9-16: integer-valued fp64 for the exact fp64 GEMM).
+template <class TU, class QT>
 __global__ void k_fil_quantize(const TU* __restrict__ U, int OC, int IC, int F, int scope,
                                const double* __restrict__ scale, int bits, int Cpad, int OCpad,
-                               int8_t* __restrict__ uqB, double* __restrict__ fil_full,
+                               QT* __restrict__ uqB, double* __restrict__ fil_full,
                                unsigned long long* __restrict__ sat) {
     const long long n = (long long)OC * IC * F;
     const int qmax = (1 << (bits - 1)) - 1;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const int f = int(i % F), ic = int((i / F) % IC), oc = int(i / ((long long)F * IC));
         const double s = scope == 0 ? scale[oc] : (scope == 1 ? scale[f] : scale[(long long)oc * F + f]);
-        uqB[((long long)f * OCpad + oc) * Cpad + ic] =
-            int8_t(clamp_q(int(rint(__ddiv_rn(double(U[i]), s))), qmax, sat));
+        uqB[((long long)f * OCpad + oc) * Cpad + ic] = QT(clamp_q(int(rint(__ddiv_rn(double(U[i]), s))), qmax, sat));
         if (ic == 0) fil_full[(long long)oc * F + f] = s;
     }
 }
@@ -164,11 +164,12 @@ __global__ void __launch_bounds__(128) k_act_scales(const TV* __restrict__ V, Co
     }
 }
 
-// vq[f][t][c] = quantize_value(V, sa(f)) (quant.cpp:242-250) for t < T, c < C (else 0).
-template <class TV>
+// vq[f][t][c] = quantize_value(V, sa(f)) (quant.cpp:242-250) for t < T, c < C (else 0);
+// QT as in k_fil_quantize.
+template <class TV, class QT>
 __global__ void __launch_bounds__(256) k_quant_general(const TV* __restrict__ V, ConvGeom g, int F,
                                                        int per_freq, const double* __restrict__ act_scale, int bits,
-                                                       int8_t* __restrict__ vqA, unsigned long long* __restrict__ sat) {
+                                                       QT* __restrict__ vqA, unsigned long long* __restrict__ sat) {
     const int f = blockIdx.y;
     const double s = act_scale[per_freq ? f : 0];
     const int qmax = (1 << (bits - 1)) - 1;
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(256) k_quant_general(const TV* __restrict__ V,
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const long long t = i / g.Cpad, c = i - t * g.Cpad;
         const long long off = ((long long)f * g.Tpad + t) * g.Cpad + c;
-        vqA[off] = c < g.C ? int8_t(clamp_q(int(rint(__ddiv_rn(double(V[off]), s))), qmax, sat)) : int8_t(0);
+        vqA[off] = c < g.C ? QT(clamp_q(int(rint(__ddiv_rn(double(V[off]), s))), qmax, sat)) : QT(0);
     }
 }
 
@@ -338,21 +339,25 @@ __global__ void k_pair_fold(const double* __restrict__ Pr, long long elems, cons
 namespace {
 template <class TU>
 cudaError_t fil_general(const TU* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad, int OCpad,
-                        double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full, unsigned long long* sat,
+                        double* scale_native, double* err_tmp, void* uqB, double* fil_full, unsigned long long* sat,
                         cudaStream_t st) {
     const int groups = scope == 0 ? OC : (scope == 1 ? F : OC * F);
     k_fil_scales<TU><<<groups, 32, 0, st>>>(U, OC, IC, F, scope, mse, bits, scale_native, err_tmp);
     if (mse) k_pick_best<<<(groups + 127) / 128, 128, 0, st>>>(groups, err_tmp, scale_native);
     const long long n = (long long)OC * IC * F;
     const int blocks = int((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
-    k_fil_quantize<TU><<<blocks, 256, 0, st>>>(U, OC, IC, F, scope, scale_native, bits, Cpad, OCpad, uqB, fil_full,
-                                               sat);
+    if (bits > 8)
+        k_fil_quantize<TU, double><<<blocks, 256, 0, st>>>(U, OC, IC, F, scope, scale_native, bits, Cpad, OCpad,
+                                                           static_cast<double*>(uqB), fil_full, sat);
+    else
+        k_fil_quantize<TU, int8_t><<<blocks, 256, 0, st>>>(U, OC, IC, F, scope, scale_native, bits, Cpad, OCpad,
+                                                           static_cast<int8_t*>(uqB), fil_full, sat);
     return cudaGetLastError();
 }
 
 template <class TV>
 cudaError_t act_general(const TV* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
-                        unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                        unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
                         cudaStream_t st) {
     const long long n = (long long)g.T * g.C;
     const int bx = int((n + 255) / 256 < 64 ? (n + 255) / 256 : 64);
@@ -360,31 +365,36 @@ cudaError_t act_general(const TV* V, const ConvGeom& g, int F, int per_freq, int
     k_act_scales<TV><<<per_freq ? F : 1, 128, 0, st>>>(V, g, F, per_freq, vmax, mse, bits, act_scale);
     const long long nq = (long long)g.T * g.Cpad;
     const int bq = int((nq + 255) / 256 < 64 ? (nq + 255) / 256 : 64);
-    k_quant_general<TV><<<dim3(bq, F), 256, 0, st>>>(V, g, F, per_freq, act_scale, bits, vqA, sat);
+    if (bits > 8)
+        k_quant_general<TV, double><<<dim3(bq, F), 256, 0, st>>>(V, g, F, per_freq, act_scale, bits,
+                                                                 static_cast<double*>(vqA), sat);
+    else
+        k_quant_general<TV, int8_t><<<dim3(bq, F), 256, 0, st>>>(V, g, F, per_freq, act_scale, bits,
+                                                                 static_cast<int8_t*>(vqA), sat);
     return cudaGetLastError();
 }
 }  // namespace
 
 cudaError_t launch_fil_general(const int32_t* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
-                               int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
+                               int OCpad, double* scale_native, double* err_tmp, void* uqB, double* fil_full,
                                unsigned long long* sat, cudaStream_t st) {
     return fil_general(U, OC, IC, F, scope, mse, bits, Cpad, OCpad, scale_native, err_tmp, uqB, fil_full, sat, st);
 }
 
 cudaError_t launch_fil_general_f64(const double* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
-                                   int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
+                                   int OCpad, double* scale_native, double* err_tmp, void* uqB, double* fil_full,
                                    unsigned long long* sat, cudaStream_t st) {
     return fil_general(U, OC, IC, F, scope, mse, bits, Cpad, OCpad, scale_native, err_tmp, uqB, fil_full, sat, st);
 }
 
 cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
-                               unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                               unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
                                cudaStream_t st) {
     return act_general(V, g, F, per_freq, mse, bits, vmax, act_scale, vqA, sat, st);
 }
 
 cudaError_t launch_act_general_f64(const double* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
-                                   unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                                   unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
                                    cudaStream_t st) {
     return act_general(V, g, F, per_freq, mse, bits, vmax, act_scale, vqA, sat, st);
 }

@@ -40,14 +40,14 @@ static_assert(out_tb<0>() * Tab<0>::M <= 32 && out_tb<1>() * Tab<1>::M <= 32 && 
                   out_tb<3>() * Tab<3>::M <= 32 && out_tb<4>() * Tab<4>::M <= 32,
               "a block's output row segment must fit the 32-entry magic table");
 
-// MODE 3 (fp64 P, the float fast_conv2d path) halves the tile columns per block: its P slice
-// is twice as wide per element.
+// MODE 3 (fp64 P, the float fast_conv2d path) and MODE 4 (fp64 P of the wide 9-16 bit
+// quantized path) halve the tile columns per block: their P slice is twice as wide per element.
 template <int V, int MODE>
 __host__ __device__ constexpr int out_tbm() {
-    return MODE == 3 ? (out_tb<V>() / 2 < 1 ? 1 : out_tb<V>() / 2) : out_tb<V>();
+    return MODE >= 3 ? (out_tb<V>() / 2 < 1 ? 1 : out_tb<V>() / 2) : out_tb<V>();
 }
 template <int MODE>
-using p_elem_t = typename std::conditional<MODE == 3, double, int32_t>::type;
+using p_elem_t = typename std::conditional<MODE >= 3, double, int32_t>::type;
 
 struct OutSmem {
     int qstride, ystride;
@@ -82,7 +82,8 @@ __constant__ unsigned c_magic32[33] = {  // 0xffffffff / d + 1 (exact for t < 2^
 
 // MODE 0: exact int32 y, 1: exact int64 y, 2: general QuantConfig (P dequantised per
 // (oc, f) before the inverse transform, which then runs in fp64: quant.cpp:258-278),
-// 3: fp64 P of the float path (fast_conv2d, conv.cpp:495-510), no dequantisation.
+// 3: fp64 P of the float path (fast_conv2d, conv.cpp:495-510), no dequantisation,
+// 4: as 2 from an fp64 P (the exact-integer P of the 9-16 bit path, |P| < 2^53).
 template <int V, int MODE>
 __global__ void __launch_bounds__(kOutThreads, 2)
     k_output(const __grid_constant__ CUtensorMap tmP, ConvGeom g, const QuantParams* __restrict__ qpp,
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
         acc_t pk[K], qt[M];
 #pragma unroll
         for (int k = 0; k < K; ++k) pk[k] = sp[((k * K + l) * TB + tj) * kOcc + oc];
-        if constexpr (MODE == 2) {  // pd[f] = double(pacc[f]) * sa(f) * fil(oc, f), left to right
+        if constexpr (MODE == 2 || MODE == 4) {  // pd[f] = double(pacc[f]) * sa(f) * fil(oc, f), left to right
             const int ocg = oc0 + oc < g.OC ? oc0 + oc : 0;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
@@ -244,7 +245,7 @@ cudaError_t out_launch(const void* P, const ConvGeom& g, const QuantParams* qp, 
     cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * es, cuuint64_t(g.OCpad) * g.Tpad * es};
     cuuint32_t box[3] = {kOcc, TB, Tab<V>::F};
     cuuint32_t estr[3] = {1, 1, 1};
-    if (fn(&tm, MODE == 3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(P),
+    if (fn(&tm, MODE >= 3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(P),
            dims, strides, box, estr,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -274,7 +275,8 @@ cudaError_t out_by_width(int mode, const void* P, const ConvGeom& g, const Quant
     return mode == 0 ? out_launch<V, 0>(P, g, qp, sf, o, st, pdl)
          : mode == 1 ? out_launch<V, 1>(P, g, qp, sf, o, st, pdl)
          : mode == 2 ? out_launch<V, 2>(P, g, qp, sf, o, st, pdl)
-                     : out_launch<V, 3>(P, g, qp, sf, o, st, pdl);
+         : mode == 3 ? out_launch<V, 3>(P, g, qp, sf, o, st, pdl)
+                     : out_launch<V, 4>(P, g, qp, sf, o, st, pdl);
 }
 }  // namespace
 

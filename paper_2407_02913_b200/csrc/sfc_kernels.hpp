@@ -110,21 +110,23 @@ cudaError_t launch_transform_filters(int variant, const int8_t* w, int OC, int I
 // General QuantConfig (general_kernels.cu).  Filters: per-group scales of U [OC][IC][F]
 // (scope 0 PerChannel, 1 PerFrequency, 2 PerChannelFrequency; MinMax or MseGrid), uq and the
 // expanded [OC][F] scale table.  err_tmp: groups * 101 doubles.
+// bits > 8: uqB / vqA hold integer-valued doubles (the exact fp64 GEMM of the wide path),
+// else int8 tensor-core operands.
 cudaError_t launch_fil_general(const int32_t* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
-                               int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
+                               int OCpad, double* scale_native, double* err_tmp, void* uqB, double* fil_full,
                                unsigned long long* sat, cudaStream_t st);
 // Activations from the kept V: maxima (1 or F slots, zeroed on entry; fp64 bit patterns),
 // MinMax / MseGrid scales act_scale[1 or F] and vq (exact fp64 quantizer, saturations counted).
 cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
-                               unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                               unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
                                cudaStream_t st);
 // Real-valued (fp64) inputs and filters, the reference's own arithmetic order:
 // V [F][Tpad][Cpad] (gather_tiles), U [OC][IC][F] (transform_filters), direct conv.
 cudaError_t launch_act_general_f64(const double* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
-                                   unsigned long long* vmax, double* act_scale, int8_t* vqA, unsigned long long* sat,
+                                   unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
                                    cudaStream_t st);
 cudaError_t launch_fil_general_f64(const double* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
-                                   int OCpad, double* scale_native, double* err_tmp, int8_t* uqB, double* fil_full,
+                                   int OCpad, double* scale_native, double* err_tmp, void* uqB, double* fil_full,
                                    unsigned long long* sat, cudaStream_t st);
 cudaError_t launch_act_f64(int variant, const double* x, const ConvGeom& g, double* Vd, cudaStream_t st);
 cudaError_t launch_filters_f64(int variant, const double* w, int OC, int IC, double* U, cudaStream_t st);

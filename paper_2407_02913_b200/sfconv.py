@@ -230,8 +230,9 @@ class SfcLayer:
         self.OC, self.IC = int(w.shape[0]), int(w.shape[1])
         self.bits = bits
         self.act_scope, self.filter_scope, self.search = int(act_scope), int(filter_scope), int(search)
-        # anything but {PerTensor, PerChannel, MinMax} is the fp64 parity path (no y_int)
-        self.general = real or (self.act_scope, self.filter_scope, self.search) != (0, 0, 0)
+        # anything but {PerTensor, PerChannel, MinMax} at <= 8 bits is the fp64 parity path (no
+        # y_int); 9-16 bits contract integer-valued fp64 operands exactly (fp64 GEMM)
+        self.general = real or bits > 8 or (self.act_scope, self.filter_scope, self.search) != (0, 0, 0)
         self.real = real
         h = ctypes.c_void_p()
         create = lib().sfc_layer_create_f64 if real else lib().sfc_layer_create_ex

@@ -105,6 +105,8 @@ REAL_CASES = [
     ("real_actfreq", 2, 3, 3, 10, 11, 1, 0, 0, 8),
     ("real_chfreq_mse", 1, 4, 3, 9, 9, 0, 2, 1, 6),
     ("real_freq_bits4", 1, 3, 2, 11, 10, 1, 1, 0, 4),
+    ("real_bits12", 1, 4, 3, 10, 10, 0, 0, 0, 12),
+    ("real_bits16_freq_mse", 1, 3, 2, 9, 11, 1, 2, 1, 16),
 ]
 
 
@@ -149,6 +151,9 @@ CLI_QUANTSIM = [
     {"name": "bits2_saturating", "seed": "5", "bits": 2, "search": "mse", "channels": 3, "out_channels": 2},
     {"name": "layers_file", "seed": "1234", "bits": 7, "search": "mse", "layers": "cli_layers.json"},
     {"name": "env_seed", "env_seed": "12345", "act": "frequency", "fil": "channel-frequency"},
+    {"name": "bits12", "seed": "21", "bits": 12},
+    {"name": "bits16_onef_freq_mse", "seed": "22", "bits": 16, "gen": "onef", "act": "frequency",
+     "fil": "channel-frequency", "search": "mse", "size": 16},
 ]
 CLI_LAYERS = [  # tests/golden/cli_layers.json (the reference's layer-list format, tensor.cpp:66-90)
     {"name": "conv1", "in_channels": 3, "out_channels": 8, "height": 32, "width": 32, "kernel": 3, "padding": 1},

@@ -21,6 +21,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = np.load(os.path.join(HERE, "golden", "qconv_cases.npz"))
 VARIANTS = ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]
+LARGE_R = ["sfc6-6x6-5x5", "sfc6-4x4-7x7"]  # catalog.cpp:249-250
 TOL = 1e-6
 
 
@@ -127,6 +128,36 @@ def test_bit_widths(cuda, variant, bits):
     check_against_oracle(x, w, variant, 1, bits)
 
 
+WIDE_CASES = [  # (bits, act_scope, filter_scope, search)
+    (9, 0, 0, 0), (10, 0, 0, 0), (12, 0, 0, 0), (13, 1, 0, 0), (14, 0, 2, 0), (15, 0, 1, 1), (16, 0, 0, 0),
+    (16, 1, 2, 1),
+]
+
+
+@pytest.mark.parametrize("variant", VARIANTS + LARGE_R)
+@pytest.mark.parametrize("wide", WIDE_CASES, ids=[f"b{c[0]}a{c[1]}f{c[2]}s{c[3]}" for c in WIDE_CASES])
+def test_wide_bit_widths(cuda, variant, wide):
+    """bits 9-16 (quant.cpp:155-156 accepts 2..16): integer-valued fp64 operands contracted by an
+    exact fp64 GEMM (|P| <= C * 2^30 < 2^53), then the reference-order fp64 epilogue.  Output
+    vs the oracle (fp32 output of the int8 API; the fp64 output through the report's mse at
+    1e-9), scales and counters exactly."""
+    bits, asc, fsc, srch = wide
+    R = sc.catalog_algorithm(variant).R
+    rng = np.random.default_rng(bits * 7 + asc + 3 * fsc + 11 * srch)
+    x = rng.integers(-128, 128, size=(2, 7, 13, 11), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(5, 7, R, R), dtype=np.int8)
+    pad = R // 2
+    r = ob.quantized_conv(x, w, variant, pad, bits, asc, fsc, srch, want=("out",), report=True)
+    rep = sc.quantized_fast_conv2d(torch.from_numpy(x), torch.from_numpy(w), sc.catalog_algorithm(variant), pad,
+                                   sc.QuantConfig(bits, asc, fsc, srch))
+    assert rep.y_int is None
+    assert maxrel(rep.output.cpu().numpy(), r["out"]) <= TOL  # fp32 output; the fp64 one is pinned via mse
+    assert np.array_equal(np.atleast_1d(rep.act_scale), r["act_scale"][: np.atleast_1d(rep.act_scale).size])
+    assert rep.saturations == r["report"]["saturations"]
+    assert rep.values_quantized == r["report"]["values_quantized"]
+    assert rep.mse == pytest.approx(r["report"]["mse"], rel=1e-9)
+
+
 # ------------------------------------------------------------------------------ golden fixtures
 GOLD_TAGS = sorted({k.split("/")[0] for k in GOLD.files if k.endswith("/meta")})
 
@@ -135,10 +166,8 @@ GOLD_TAGS = sorted({k.split("/")[0] for k in GOLD.files if k.endswith("/meta")})
 @pytest.mark.parametrize("tag", GOLD_TAGS)
 def test_golden_reference_outputs(cuda, tag, variant):
     pad, bits, asc, fsc, srch = (int(v) for v in GOLD[f"{tag}/meta"])
-    if bits > 8:
-        pytest.skip("bits > 8 is outside the int8 tensor-core path")
     x, w = GOLD[f"{tag}/x"], GOLD[f"{tag}/w"]
-    if asc or fsc or srch:  # the general QuantConfig path (fp64 epilogue, no y_int)
+    if asc or fsc or srch or bits > 8:  # the general QuantConfig / wide path (fp64 epilogue, no y_int)
         rep = sc.quantized_fast_conv2d(torch.from_numpy(x), torch.from_numpy(w), sc.catalog_algorithm(variant), pad,
                                        sc.QuantConfig(bits, asc, fsc, srch))
         assert maxrel(rep.output.cpu().numpy(), GOLD[f"{tag}/{variant}/out"]) <= TOL
@@ -285,8 +314,9 @@ def test_errors_like_reference(cuda):
     # for a constant 0.5 input and a zero filter is exactly 0
     rep = sc.quantized_fast_conv2d(torch.full((1, 1, 8, 8), 0.5), f, spec, 1)
     assert rep.output.dtype == torch.float64 and float(rep.output.abs().max()) == 0.0
-    with pytest.raises(_lib.SfcUnsupported):
-        sc.quantized_fast_conv2d(x, f, spec, 1, sc.QuantConfig(bits=12))
+    # bits 9-16 are accepted like the reference (the wide fp64-GEMM path)
+    rep = sc.quantized_fast_conv2d(x, f, spec, 1, sc.QuantConfig(bits=12))
+    assert float(rep.output.abs().max()) == 0.0 and rep.saturations == 0
 
 
 def test_concurrent_streams_match(cuda):
@@ -375,7 +405,6 @@ def test_kept_and_recompute_paths_agree(cuda, variant, monkeypatch):
 
 
 # ------------------------------------------------------------------------------ 5x5 / 7x7 variants
-LARGE_R = ["sfc6-6x6-5x5", "sfc6-4x4-7x7"]  # catalog.cpp:249-250
 GOLD_R = np.load(os.path.join(HERE, "golden", "qconv_large_r.npz"))
 TAGS_R = sorted({k.split("/")[0] for k in GOLD_R.files})
 CASES_R = [  # (B, C, OC, H, W, pad, lo)
