@@ -165,7 +165,9 @@ int sfc_conv_stats(sfc_layer_t layer, int n, int h, int w, int pad, const void* 
                    void* stream);
 /* Device views into the workspace after sfc_conv_int8:
  *   vq   int8  [F][Tpad][Cpad]   quantized transformed activations
- *   pacc int32 [F][Tpad][OCpad]  per-frequency channel contractions
+ *   pacc int32 [F][Tpad][OCpad]  per-frequency channel contractions; NULL when P is
+ *                                chunked (opt-in SFC_PCHUNK_MB budget exceeded: each chunk
+ *                                is consumed from L2 and never materialised whole)
  * geom[6] = {T, Tpad, Cpad, OCpad, th, tw}. */
 int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_workspace, int8_t** d_vq,
                    int32_t** d_pacc, int64_t* geom);

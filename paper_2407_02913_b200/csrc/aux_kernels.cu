@@ -4,6 +4,8 @@
 //   k_direct_conv        exact int8 correlation (int32)  (conv.cpp:320-350, quant.cpp:282)
 //   k_freq_energy        sum of V^2 per frequency, exact (quant.cpp:136-150)
 //   k_transform_filters  U as int32                      (conv.cpp:352-382)
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -227,11 +229,29 @@ void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, in
     g.BN = OC <= 64 ? 64 : (OC <= 128 ? 128 : 256);
     g.OCpad = (OC + g.BN - 1) / g.BN * g.BN;
     g.th_magic = g.th == 1 ? 0u : 0xffffffffu / unsigned(g.th) + 1u;
+    g.row0 = 0;
+    g.nrows = B * g.th;
+}
+
+PChunk p_chunk(const ConvGeom& g, int F) {
+    size_t budget = 0;  // opt-in (see sfc_kernels.hpp)
+    if (const char* e = std::getenv("SFC_PCHUNK_MB")) budget = size_t(std::atol(e)) << 20;
+    const size_t per_row = size_t(F) * g.OCpad * 4;  // P bytes per tile
+    const int rows_total = g.B * g.th;
+    if (budget == 0 || per_row * g.Tpad <= budget) return PChunk{rows_total, g.Tpad, 1};
+    size_t max_tiles = budget / per_row / kRowsPerTile * kRowsPerTile;
+    if (max_tiles < size_t(kRowsPerTile)) max_tiles = kRowsPerTile;
+    int rows_max = int(max_tiles / size_t(g.tw));
+    if (rows_max < 1) rows_max = 1;
+    const int n = (rows_total + rows_max - 1) / rows_max;
+    const int rows = (rows_total + n - 1) / n;  // balanced chunks
+    const int tcpad = (rows * g.tw + kRowsPerTile - 1) / kRowsPerTile * kRowsPerTile;
+    return PChunk{rows, tcpad, (rows_total + rows - 1) / rows};
 }
 
 size_t workspace_bytes(const ConvGeom& g, int F) {
     auto up = [](size_t v) { return (v + 255) / 256 * 256; };
-    return up(kWsHeader) + up(size_t(F) * g.Tpad * g.Cpad) + up(size_t(F) * g.Tpad * g.OCpad * 4) +
+    return up(kWsHeader) + up(size_t(F) * g.Tpad * g.Cpad) + up(size_t(F) * p_chunk(g, F).tcpad * g.OCpad * 4) +
            up(size_t(F) * g.Tpad * g.Cpad * 2);  // kept int16 V
 }
 
@@ -257,12 +277,21 @@ __global__ void __launch_bounds__(256) k_sq_err(const double* __restrict__ out, 
     }
     if ((threadIdx.x & 31) == 0) se[threadIdx.x >> 5] = e, ss[threadIdx.x >> 5] = s;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // per-block partials; k_sum_partials adds them in block order
         double a = 0.0, b = 0.0;
         for (int w = 0; w < 8; ++w) a += se[w], b += ss[w];
-        atomicAdd(&sums[0], a);
-        atomicAdd(&sums[1], b);
+        sums[2 + 2 * blockIdx.x] = a;
+        sums[3 + 2 * blockIdx.x] = b;
     }
+}
+
+// sums[0..1] = the block partials summed in a fixed order: the report is bitwise
+// repeatable (the grid size depends on n only).
+__global__ void k_sum_partials(double* __restrict__ sums, int blocks) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < blocks; ++i) a += sums[2 + 2 * i], b += sums[3 + 2 * i];
+    sums[0] = a;
+    sums[1] = b;
 }
 
 __global__ void k_zero_words(uint32_t* __restrict__ p, int words) {
@@ -291,15 +320,17 @@ cudaError_t launch_zero_words(uint32_t* p, int words, cudaStream_t st) {
 
 cudaError_t launch_sq_err(const double* out, const int32_t* ref, long long n, double* sums, cudaStream_t st) {
     long long blocks = (n + 255) / 256;
-    blocks = blocks > 4 * 148 ? 4 * 148 : (blocks < 1 ? 1 : blocks);
+    blocks = blocks > kSqErrBlocks ? kSqErrBlocks : (blocks < 1 ? 1 : blocks);
     k_sq_err<int32_t><<<int(blocks), 256, 0, st>>>(out, ref, n, sums);
+    k_sum_partials<<<1, 1, 0, st>>>(sums, int(blocks));
     return cudaGetLastError();
 }
 
 cudaError_t launch_sq_err_f64(const double* out, const double* ref, long long n, double* sums, cudaStream_t st) {
     long long blocks = (n + 255) / 256;
-    blocks = blocks > 148 * 8 ? 148 * 8 : (blocks < 1 ? 1 : blocks);
+    blocks = blocks > kSqErrBlocks ? kSqErrBlocks : (blocks < 1 ? 1 : blocks);
     k_sq_err<double><<<int(blocks), 256, 0, st>>>(out, ref, n, sums);
+    k_sum_partials<<<1, 1, 0, st>>>(sums, int(blocks));
     return cudaGetLastError();
 }
 }  // namespace sfcb200

@@ -143,8 +143,33 @@ WsView carve(void* ws, const ConvGeom& g, int F) {
     v.act_scale = reinterpret_cast<double*>(base + kWsActScales);
     v.vq = reinterpret_cast<int8_t*>(base + up(kWsHeader));
     v.P = reinterpret_cast<int32_t*>(base + up(kWsHeader) + up(size_t(F) * g.Tpad * g.Cpad));
-    v.vkeep = reinterpret_cast<int16_t*>(reinterpret_cast<uint8_t*>(v.P) + up(size_t(F) * g.Tpad * g.OCpad * 4));
+    v.vkeep = reinterpret_cast<int16_t*>(reinterpret_cast<uint8_t*>(v.P) +
+                                         up(size_t(F) * p_chunk(g, F).tcpad * g.OCpad * 4));
     return v;
+}
+
+// GEMM and output transform over P chunks (PChunk): one pair of launches when P fits the
+// chunk budget, else for each chunk of image tile rows the GEMM writes that chunk's P
+// rows into the chunk buffer and the output kernel consumes and discards them from L2.
+// `pdl` is the PDL flag of the next launch and is left as the caller's chain expects.
+void gemm_output(const sfc_layer* L, const ConvGeom& g, const WsView& v, int mode, const OutPtrs& op, bool do_gemm,
+                 bool do_out, cudaStream_t st, bool& pdl, bool full_pdl) {
+    const PChunk pc = p_chunk(g, L->F);
+    for (int c = 0; c < pc.n; ++c) {
+        const int r0 = c * pc.rows, nr = std::min(pc.rows, g.nrows - r0);
+        if (do_gemm) {
+            if (pc.n == 1) ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st, pdl), "gemm launch");
+            else ck(launch_gemm_rows(v.vq, L->d_uq, v.P, g, L->F, r0 * g.tw, pc.tcpad, st, pdl), "gemm launch");
+            pdl = full_pdl;
+        }
+        if (do_out) {
+            ConvGeom gc = g;
+            OutPtrs oc = op;
+            if (pc.n > 1) gc.row0 = r0, gc.nrows = nr, gc.Tpad = pc.tcpad, oc.p_discard = v.P;
+            ck(launch_output(L->variant, mode, v.P, gc, v.qp, L->d_sf, oc, st, pdl), "output launch");
+            pdl = full_pdl;
+        }
+    }
 }
 
 void check_call(const sfc_layer* L, const void* x, int n, int h, int w, int pad) {
@@ -206,6 +231,8 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     // (one oc block: every A tile is converted once; several: only if V is L2-sized)
     bool qfuse = kept && (g.OCpad == g.BN || size_t(L->F) * g.Tpad * g.Cpad * 2 <= (size_t(64) << 20));
     if (const char* q = std::getenv("SFC_QFUSE")) qfuse = kept && q[0] == '1';
+    const bool chunked = p_chunk(g, L->F).n > 1;
+    qfuse = qfuse && !chunked;  // the converter GEMM covers the whole tile range
     if (mask & SFC_STAGE_ACT) {
         if (!kept) {
             ck(launch_act_quant(L->variant, d_x, g, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "act launch");
@@ -215,19 +242,20 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
             pdl = full_pdl;
         }
     }
-    if (mask & SFC_STAGE_GEMM) {
-        if (qfuse)
+    const OutPtrs op{o->y_int32, o->y_int64, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
+    if (qfuse) {
+        if (mask & SFC_STAGE_GEMM) {
             ck(launch_gemm_qfused(QFuse{v.vkeep, d_vmax, qparams_table(false), v.qp, v.sat, L->bits}, L->d_uq, v.P, g,
                                   L->F, st, pdl),
                "fused quantize + gemm launch");
-        else
-            ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, st, pdl), "gemm launch");
-        pdl = full_pdl;
+            pdl = full_pdl;
+        }
+        if (mask & SFC_STAGE_OUTPUT)
+            ck(launch_output(L->variant, need64 ? 1 : 0, v.P, g, v.qp, L->d_sf, op, st, pdl), "output launch");
+        return;
     }
-    if (mask & SFC_STAGE_OUTPUT) {
-        const OutPtrs op{o->y_int32, o->y_int64, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
-        ck(launch_output(L->variant, need64 ? 1 : 0, v.P, g, v.qp, L->d_sf, op, st, pdl), "output launch");
-    }
+    gemm_output(L, g, v, need64 ? 1 : 0, op, (mask & SFC_STAGE_GEMM) != 0, (mask & SFC_STAGE_OUTPUT) != 0, st, pdl,
+                full_pdl);
 }
 }  // namespace
 
@@ -487,8 +515,8 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
             };
             if (L->bits > 8) return wide_tail(L, g, op, v.qp, quantize, S(stream));
             quantize(v.vq);
-            ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, S(stream), false), "gemm launch");
-            ck(launch_output(L->variant, 2, v.P, g, v.qp, L->d_sf, op, S(stream), false), "output launch");
+            bool pdl = false;
+            gemm_output(L, g, v, 2, op, true, true, S(stream), pdl, false);
             return;
         }
         needs_y64(L, o);  // refuse before anything is launched
@@ -553,7 +581,7 @@ int sfc_conv_views(sfc_layer_t L, int n, int h, int w, int pad, void* ws, int8_t
         const ConvGeom g = geom_of(L, n, h, w, pad);
         WsView v = carve(ws, g, L->F);
         if (d_vq) *d_vq = v.vq;
-        if (d_pacc) *d_pacc = v.P;
+        if (d_pacc) *d_pacc = p_chunk(g, L->F).n > 1 ? nullptr : v.P;
         if (geom) {
             geom[0] = g.T, geom[1] = g.Tpad, geom[2] = g.Cpad, geom[3] = g.OCpad, geom[4] = g.th, geom[5] = g.tw;
         }
@@ -603,8 +631,7 @@ int sfc_report_sq_err(const double* d_out, const int32_t* d_ref, int64_t n, doub
     return guarded([&] {
         if (!d_out || !d_ref || !host_sums || n < 0) throw std::invalid_argument("bad report arguments");
         void* d_sums = nullptr;
-        ck(cudaMallocAsync(&d_sums, 2 * sizeof(double), S(stream)), "alloc");
-        ck(cudaMemsetAsync(d_sums, 0, 2 * sizeof(double), S(stream)), "memset");
+        ck(cudaMallocAsync(&d_sums, (2 + 2 * kSqErrBlocks) * sizeof(double), S(stream)), "alloc");
         ck(launch_sq_err(d_out, d_ref, n, static_cast<double*>(d_sums), S(stream)), "sq_err launch");
         ck(cudaMemcpyAsync(host_sums, d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, S(stream)), "copy");
         ck(cudaFreeAsync(d_sums, S(stream)), "free");
@@ -616,8 +643,7 @@ int sfc_report_sq_err_f64(const double* d_out, const double* d_ref, int64_t n, d
     return guarded([&] {
         if (!d_out || !d_ref || !host_sums || n < 0) throw std::invalid_argument("bad report arguments");
         void* d_sums = nullptr;
-        ck(cudaMallocAsync(&d_sums, 2 * sizeof(double), S(stream)), "alloc");
-        ck(cudaMemsetAsync(d_sums, 0, 2 * sizeof(double), S(stream)), "memset");
+        ck(cudaMallocAsync(&d_sums, (2 + 2 * kSqErrBlocks) * sizeof(double), S(stream)), "alloc");
         ck(launch_sq_err_f64(d_out, d_ref, n, static_cast<double*>(d_sums), S(stream)), "sq_err launch");
         ck(cudaMemcpyAsync(host_sums, d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, S(stream)), "copy");
         ck(cudaFreeAsync(d_sums, S(stream)), "free");
@@ -725,8 +751,8 @@ int sfc_conv_forward_f64(sfc_layer_t L, const double* d_x, int n, int h, int w, 
         }
         quantize(v.vq);
         ck(cudaFreeAsync(Vd, S(stream)), "free V");
-        ck(launch_gemm(v.vq, L->d_uq, v.P, g, L->F, S(stream), false), "gemm launch");
-        ck(launch_output(L->variant, 2, v.P, g, v.qp, L->d_sf, op, S(stream), false), "output launch");
+        bool pdl = false;
+        gemm_output(L, g, v, 2, op, true, true, S(stream), pdl, false);
     });
 }
 

@@ -284,11 +284,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool make_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base, uint64_t d0, uint64_t d1,
-                  uint64_t d2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw) {
+                  uint64_t d2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw, uint64_t plane_rows = 0) {
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[3] = {d0, d1, d2};
-    cuuint64_t strides[2] = {d0 * esize, d0 * d1 * esize};
+    cuuint64_t strides[2] = {d0 * esize, d0 * (plane_rows ? plane_rows : d1) * esize};
     cuuint32_t box[3] = {b0, b1, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     return fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
@@ -370,6 +370,29 @@ cudaError_t gemm_dispatch(const int8_t* vqA, const int8_t* uqB, int32_t* P, cons
 cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
                         bool pdl) {
     return gemm_dispatch<false>(vqA, uqB, P, g, F, QFuse{}, st, pdl);
+}
+
+cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, int t0,
+                             int tcpad, cudaStream_t st, bool pdl) {
+    // A: rows [t0, t0 + tcpad) of every frequency plane of vq (rows past the planes' Tpad
+    // read as zeros); P: a buffer of tcpad rows per frequency
+    CUtensorMap ta, tb, tp;
+    const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    const int arows = tcpad < g.Tpad - t0 ? tcpad : g.Tpad - t0;
+    if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, vqA + size_t(t0) * g.Cpad, g.Cpad, arows, F, g.BK,
+                      kRowsPerTile, sw, g.Tpad) ||
+        !make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
+        !make_tmap_3d(&tp, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, tcpad, F, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+    ConvGeom gc = g;
+    gc.Tpad = tcpad;
+    const int nk = g.Cpad / g.BK;
+    const QFuse none{};
+    if (g.BK == 128)
+        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, gc, F, none, st, pdl)
+                       : gemm_by_bn<128, 3, false>(ta, tb, tp, gc, F, none, st, pdl);
+    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, gc, F, none, st, pdl)
+                   : gemm_by_bn<64, 4, false>(ta, tb, tp, gc, F, none, st, pdl);
 }
 
 cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,

@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     __shared__ double s_scale[kOcc];
     __shared__ float s_scalef[kOcc];
 
-    // grid = (oc blocks, tile-column blocks, image rows b * th + ti)
+    // grid = (oc blocks, tile-column blocks, image rows b * th + ti of the chunk); P rows are
+    // chunk-relative, the output position uses the absolute row g.row0 + row
     const int oc0 = blockIdx.x * kOcc, tc = blockIdx.y, row = blockIdx.z;
     tl_mark(kTlOutput, 0);
     if (threadIdx.x == 0) {
@@ -118,7 +119,8 @@ __global__ void __launch_bounds__(kOutThreads, 2)
         ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * sizeof(p_elem_t<MODE>)));
         ptx::tma_load_3d(smem, &tmP, full, oc0, row * g.tw + tc * TB, 0);
     }
-    const int b = g.th == 1 ? row : int(__umulhi(unsigned(row), g.th_magic)), ti = row - b * g.th;
+    const int arow = g.row0 + row;
+    const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
     const int noc = min(kOcc, g.OC - oc0);
     const int ntb = min(TB, g.tw - tc * TB);
     if (threadIdx.x < kOcc && int(threadIdx.x) < noc) {
@@ -127,6 +129,15 @@ __global__ void __launch_bounds__(kOutThreads, 2)
         s_scalef[threadIdx.x] = float(sc);
     }
     ptx::mbar_wait(full, 0);
+    if (o.p_discard) {  // this block is the only reader of its rows' lines: drop them from L2 unwritten
+        constexpr int kLines = int(kOcc * sizeof(p_elem_t<MODE>) / 128);
+        const char* pb = static_cast<const char*>(o.p_discard);
+        for (int i = threadIdx.x; i < T::F * ntb * kLines; i += kOutThreads) {
+            const int l = i % kLines, j = (i / kLines) % ntb, f = i / (kLines * ntb);
+            const size_t e = (size_t(f) * g.Tpad + size_t(row) * g.tw + tc * TB + j) * g.OCpad + oc0;
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(pb + e * sizeof(p_elem_t<MODE>) + l * 128) : "memory");
+        }
+    }
 
     // stage A: items (tj, l, oc)
     for (int it = threadIdx.x; it < TB * K * kOcc; it += kOutThreads) {
@@ -254,7 +265,7 @@ cudaError_t out_launch(const void* P, const ConvGeom& g, const QuantParams* qp, 
     auto kern = k_output<V, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    const long rows = long(g.B) * g.th;
+    const long rows = g.nrows;
     if (rows > 65535 || (g.tw + TB - 1) / TB > 65535) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned((g.OC + kOcc - 1) / kOcc), unsigned((g.tw + TB - 1) / TB), unsigned(rows));

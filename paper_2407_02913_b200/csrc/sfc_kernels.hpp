@@ -16,7 +16,26 @@ struct ConvGeom {
     int BK;     // 64 or 128 bytes of K per pipeline stage
     int OC, OCpad, BN;
     unsigned th_magic;  // r / th == umulhi(r, th_magic) for r < 2^16 (th == 1: 0, divide by identity)
+    // output-transform launches over a chunk of image tile rows (P chunked, see PChunk):
+    // rows [row0, row0 + nrows) of the B * th rows; geom_init sets the whole range
+    int row0, nrows;
 };
+
+// P chunking (opt-in: SFC_PCHUNK_MB = budget in MB; unset or 0 = never chunk).  P (4 B per
+// (frequency, tile, oc)) is the largest intermediate; when the whole of it exceeds the
+// budget, GEMM and output transform alternate over chunks of `rows` image tile rows so
+// each chunk's P is consumed from L2 and discarded there (never written back to HBM), and
+// the workspace holds one chunk (config 5: 52 MB instead of 472 MB).  Measured on config
+// 5 it is slower (0.49 ms at 64 MB vs 0.41 ms whole): the serialised per-chunk ramp-up /
+// drain of two bandwidth kernels costs more than the HBM traffic it saves, so it is a
+// workspace-memory cap, not the default; overlapping chunk i's output transform with
+// chunk i+1's GEMM is the open follow-up.
+struct PChunk {
+    int rows;   // image tile rows per chunk (last chunk may be shorter)
+    int tcpad;  // P rows per chunk buffer: rows * tw rounded up to the GEMM row block
+    int n;      // chunks
+};
+PChunk p_chunk(const ConvGeom& g, int F);
 
 // Activation quantizer derived on device from the global absmax (so multi-GPU
 // callers can all-reduce the absmax first).
@@ -72,6 +91,9 @@ cudaError_t tl_read_out(unsigned long long* out, bool reset);
 cudaError_t tl_read_aux(unsigned long long* out, bool reset);
 cudaError_t launch_act_quant(int variant, const int8_t* x, const ConvGeom& g, const int* vmax, int bits,
                              QuantParams* qp, int8_t* vqA, unsigned long long* sat, cudaStream_t st, bool pdl);
+// P rows [t0, t0 + tcpad) of the full problem into a P buffer of tcpad rows (a P chunk).
+cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, int t0,
+                             int tcpad, cudaStream_t st, bool pdl);
 cudaError_t launch_gemm(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
                         bool pdl);
 // Output pointers of the output-transform kernel (any may be null).
@@ -87,11 +109,16 @@ struct OutPtrs {
     const double* gen_act = nullptr;
     int gen_per_freq = 0;
     const double* gen_fil = nullptr;  // [OC][F]
+    // when set (the P chunk buffer): every block discards the P lines it consumed from L2
+    // (discard.global.L2), so chunked P is never written back to HBM
+    const void* p_discard = nullptr;
 };
 // mode 0: exact int32 y, 1: exact int64 y, 2: general QuantConfig (fp64, no y_int),
 // 3: fp64 P [F][Tpad][OCpad] of the float path (no dequantisation)
 cudaError_t launch_output(int variant, int mode, const void* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
+// report sums: `sums` holds 2 + 2 * kSqErrBlocks doubles (result in [0..1], block partials after)
+constexpr int kSqErrBlocks = 148 * 8;
 cudaError_t launch_sq_err(const double* out, const int32_t* ref, long long n, double* sums, cudaStream_t st);
 cudaError_t launch_sq_err_f64(const double* out, const double* ref, long long n, double* sums, cudaStream_t st);
 // Device table of verified quantizer parameters (common.cuh, kQpTableMax).  build=true

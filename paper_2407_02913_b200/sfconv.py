@@ -358,7 +358,8 @@ class SfcLayer:
                     fast_quantizer_exact=bool(s[3]), values_quantized=int(s[4]), tiles=int(s[5]))
 
     def views(self, n, h, w, pad, ws):
-        """(vq int8 [F, T, IC], pacc int32 [F, T, OC]) views of the workspace after conv()."""
+        """(vq int8 [F, T, IC], pacc int32 [F, T, OC]) views of the workspace after conv();
+        pacc is None when the layer's P is chunked (never materialised whole)."""
         vq, pa = ctypes.c_void_p(), ctypes.c_void_p()
         geom = np.zeros(6, np.int64)
         check(lib().sfc_conv_views(self._h, n, h, w, pad, _ptr(ws), ctypes.byref(vq), ctypes.byref(pa),
@@ -366,6 +367,8 @@ class SfcLayer:
         T, Tpad, Cpad, OCpad = (int(v) for v in geom[:4])
         F = self.spec.K ** 2
         vqt = _wrap_device(vq.value, (F, Tpad, Cpad), torch.int8, self.device)[:, :T, : self.IC]
+        if not pa.value:
+            return vqt, None
         pat = _wrap_device(pa.value, (F, Tpad, OCpad), torch.int32, self.device)[:, :T, : self.OC]
         return vqt, pat
 

@@ -394,14 +394,53 @@ def test_kept_and_recompute_paths_agree(cuda, variant, monkeypatch):
                     layer.absmax(x, vmax, L.pad)
                     layer.conv(x, vmax, ws, L.pad, y_int64=y)
             vq, p = layer.views(L.batch, L.hw, L.hw, L.pad, ws)
-            res[mode] = (y.clone(), p.clone(), vq.clone(), layer.stats(L.batch, L.hw, L.hw, L.pad, ws))
+            res[mode] = (y.clone(), None if p is None else p.clone(), vq.clone(),
+                         layer.stats(L.batch, L.hw, L.hw, L.pad, ws))
         monkeypatch.delenv("SFC_QFUSE", raising=False)
         ref = res["recompute"]
         for mode, r in res.items():
             assert torch.equal(ref[0], r[0]), (cfg, mode, "y")
-            assert torch.equal(ref[1], r[1]), (cfg, mode, "P")
+            if ref[1] is not None:  # (chunked P is consumed from L2 and never materialised)
+                assert torch.equal(ref[1], r[1]), (cfg, mode, "P")
             assert ref[3] == r[3], (cfg, mode, "stats")
         assert torch.equal(ref[2], res["kept"][2]), (cfg, "vq")
+
+
+@pytest.mark.parametrize("variant", VARIANTS + LARGE_R)
+@pytest.mark.parametrize("budget_mb", [2])
+def test_chunked_p_matches_whole(cuda, variant, budget_mb, monkeypatch):
+    """P chunking (GEMM -> output transform per chunk of image tile rows, each chunk's P
+    consumed from L2 and discarded): a small budget forces 2..many chunks, ragged last chunk
+    included; y, fp32 out and stats equal the unchunked run bit for bit and y the oracle's.
+    The general QuantConfig path chunks the same way."""
+    R = sc.catalog_algorithm(variant).R
+    rng = np.random.default_rng(budget_mb * 31 + R)
+    B, C, OC, H = 20, 40, 96, 22
+    x = rng.integers(-128, 128, size=(B, C, H, H), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(OC, C, R, R), dtype=np.int8)
+    pad = R // 2
+    xt, wt = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    res = {}
+    for mode in ("whole", "chunked"):
+        if mode == "chunked":
+            monkeypatch.setenv("SFC_PCHUNK_MB", str(budget_mb))
+        else:
+            monkeypatch.setenv("SFC_PCHUNK_MB", "0")
+        layer = sc.SfcLayer(variant, wt)
+        ws = layer.workspace(B, H, H, pad)
+        y = torch.empty((B, OC, H, H), dtype=torch.int64, device="cuda")
+        out = torch.empty((B, OC, H, H), dtype=torch.float32, device="cuda")
+        layer.forward(xt, ws, pad, y_int64=y, out_f32=out)
+        _, pacc = layer.views(B, H, H, pad, ws)
+        gen = sc.quantized_fast_conv2d(xt, wt, sc.catalog_algorithm(variant), pad, sc.QuantConfig(8, 1, 2, 0))
+        res[mode] = (y.cpu(), out.cpu(), layer.stats(B, H, H, pad, ws), pacc is None, gen.output.cpu(), gen.mse)
+    monkeypatch.delenv("SFC_PCHUNK_MB")
+    whole, chunked = res["whole"], res["chunked"]
+    assert not whole[3] and chunked[3]  # the budget really chunked P
+    assert torch.equal(whole[0], chunked[0]) and torch.equal(whole[1], chunked[1]) and whole[2] == chunked[2]
+    assert torch.equal(whole[4], chunked[4]) and whole[5] == chunked[5]
+    r = ob.quantized_conv(x, w, variant, pad, want=("y_int",))
+    assert np.array_equal(chunked[0].numpy(), r["y_int"])
 
 
 # ------------------------------------------------------------------------------ 5x5 / 7x7 variants
