@@ -15,6 +15,7 @@
 // warp touches distinct banks, and item decompositions divide by compile-time constants.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -242,6 +243,175 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     tl_mark(kTl, 2);
 }
 
+// ---------------------------------------------------------------------------------------
+// Two-channel SWAR absmax / keep-V pass for the 3x3 variants (MODE 0 of k_act, reworked).
+// One thread owns one tile and one adjacent channel pair (c, c+1), packed into one 32-bit
+// register as P = x_c + 2^16 x_{c+1}.  The transforms are integer-linear and every value
+// they form (window samples, row-transform Z, V) stays inside (-2^15, 2^15)
+// (|V| <= 4608), so a 32-bit add of two packed values is the exact packed sum of both
+// lanes: every addition of the scheduled transforms serves two channels.  The row
+// transforms write Z to the warp's own shared-memory slab (lane-contiguous words:
+// conflict-free, one word per channel pair), the column transforms read it back; both
+// loops stay rolled so the code fits the instruction cache.  A V pair becomes its int16x2
+// memory word (low lane's borrow undone: P + 2^16 [lane0 < 0]), is reduced with
+// max/min.s16x2 and stored as one 32-bit word -- a warp (32 pairs = 64 channels of one
+// tile) writes 128 contiguous bytes of the kept V row per frequency.
+constexpr int kPairCC = 64;  // channels per CTA (one warp of pairs per tile)
+constexpr int kPairMaxTiles = 4;
+
+struct PairSmem {
+    int nwp, chw;  // as ActSmem: words per staged row piece, words per staged channel (odd)
+    size_t z_off, bytes;
+};
+template <int V>
+__host__ __device__ inline PairSmem pair_smem(int W, int twc) {
+    using T = Tab<V>;
+    PairSmem s;
+    const int pw = min((twc - 1) * T::M + T::n, W);
+    s.nwp = (pw + 6) >> 2;
+    s.chw = T::n * s.nwp;
+    if ((s.chw & 1) == 0) s.chw += 1;
+    s.z_off = (size_t(s.chw) * 4 * kPairCC + 15) & ~size_t(15);
+    s.bytes = s.z_off + size_t(twc) * T::K * T::n * 32 * 4;
+    return s;
+}
+
+// Grid: x = tile row * column chunks + chunk (twc tiles), y = image, z = 64-channel block;
+// block = 32 * twc threads (warp w = tile column tj0 + w, lane = channel pair).
+template <int V>
+__global__ void __launch_bounds__(32 * kPairMaxTiles) k_act_pair(const int8_t* __restrict__ x, ConvGeom g, int twc,
+                                                                int* __restrict__ vmax, int16_t* __restrict__ vkeep) {
+    using T = Tab<V>;
+    constexpr int n = T::n, K = T::K, M = T::M;
+    extern __shared__ __align__(16) uint8_t smem[];
+    tl_mark(kTlAbsmax, 0);
+    griddep_launch_dependents();
+
+    const int W = g.W;
+    const int nchunk = (g.tw + twc - 1) / twc;
+    const int ti = blockIdx.x / nchunk, tj0 = (blockIdx.x - ti * nchunk) * twc;
+    const int ntj = min(twc, g.tw - tj0);
+    const int b = blockIdx.y, c0 = blockIdx.z * kPairCC;
+    const int nch = min(kPairCC, g.C - c0);
+    const PairSmem L = pair_smem<V>(W, twc);
+    uint32_t* s_xw = reinterpret_cast<uint32_t*>(smem);
+    // staged plane of channel ch: even channels first, then odd ones, so lane p's two loads
+    // (channels 2p, 2p+1) step through planes with the odd word stride chw: no bank conflicts
+    auto plane = [&](int ch) { return ((ch & 1) * (kPairCC / 2) + (ch >> 1)) * L.chw; };
+
+    // ---- stage 0: window rows [r_lo, r_lo + nrows) x columns [cb_lo, cb_lo + pw) of each
+    // channel; word w of a staged row holds columns cb_lo + 4w .. +3 (funnel-shifted from the
+    // two aligned words that cover them), so a sample's shared address needs no per-row
+    // alignment term.  Words past the end of x read as zero.
+    const int ih0 = ti * M - g.pad;
+    const int r_lo = max(ih0, 0), nrows = min(ih0 + n, g.H) - r_lo;
+    const int cb_lo = max(tj0 * M - g.pad, 0);
+    const int pw = min((tj0 + ntj - 1) * M - g.pad + n, W) - cb_lo;
+    const int HW = g.H * W;
+    const int8_t* base = x + (size_t(b) * g.C + c0) * size_t(HW);
+    {
+        const uint32_t* xw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(base) & ~uintptr_t(3));
+        const int bmis = int(reinterpret_cast<uintptr_t>(base) & 3);
+        const long long availw64 = ((long long)(size_t(g.B) * g.C * HW) - (long long)(base - x) + bmis + 3) >> 2;
+        const int availw = availw64 > 0x7fffffffll ? 0x7fffffff : int(availw64);  // readable words from xw
+        const int nwp = (pw + 3) >> 2;
+        const unsigned wmag = 0xffffffffu / unsigned(nwp) + 1u, rmag = 0xffffffffu / unsigned(nrows) + 1u;
+        const int total = nch * nrows * nwp;
+        constexpr int kJ = 8;  // loads in flight per thread
+        for (int k0 = 0; k0 < total; k0 += kJ * int(blockDim.x)) {
+            uint32_t lo[kJ], hi[kJ];
+            int dst[kJ], sh[kJ];
+#pragma unroll
+            for (int jj = 0; jj < kJ; ++jj) {
+                const int k = k0 + jj * int(blockDim.x) + int(threadIdx.x);
+                const int cr = nwp == 1 ? k : int(__umulhi(unsigned(k), wmag)), w = k - cr * nwp;
+                const int ch = nrows == 1 ? cr : int(__umulhi(unsigned(cr), rmag)), r = cr - ch * nrows;
+                const int byte = bmis + ch * HW + (r_lo + r) * W + cb_lo + 4 * w;  // from xw
+                const int a = byte >> 2;
+                sh[jj] = (byte & 3) * 8;
+                dst[jj] = k < total ? plane(ch) + r * L.nwp + w : -1;
+                lo[jj] = (dst[jj] >= 0 && a < availw) ? __ldg(xw + a) : 0u;
+                hi[jj] = (dst[jj] >= 0 && sh[jj] && a + 1 < availw) ? __ldg(xw + a + 1) : 0u;
+            }
+#pragma unroll
+            for (int jj = 0; jj < kJ; ++jj)
+                if (dst[jj] >= 0) s_xw[dst[jj]] = __funnelshift_r(lo[jj], hi[jj], sh[jj]);
+        }
+    }
+    __syncthreads();
+
+    const int tjl = threadIdx.x >> 5, p = threadIdx.x & 31, c = 2 * p;
+    int mx = 0, mn = 0;  // int16x2 running max / min of V over this thread's two channels
+    if (tjl < ntj) {
+        const int col0 = (tj0 + tjl) * M - g.pad;
+        // interior tile with both channels present: no per-sample predicates
+        const bool fast = col0 >= 0 && col0 + n <= W && c + 1 < nch;
+        const int8_t* px0 = reinterpret_cast<const int8_t*>(s_xw + plane(c)) + (col0 - cb_lo);
+        const int8_t* px1 = reinterpret_cast<const int8_t*>(s_xw + plane(c + 1)) + (col0 - cb_lo);
+        const bool ok0 = c < nch, ok1 = c + 1 < nch;
+        int* sz = reinterpret_cast<int*>(smem + L.z_off) + tjl * (K * n * 32) + p;  // [l][r][lane]
+        // ---- rows: Z[r][l] = sum_s BT[l][s] x[r][s], both channels at once
+#pragma unroll 1
+        for (int r = 0; r < n; ++r) {
+            const int ir = ih0 + r - r_lo;  // row within the staged window
+            int xs[n], z[K];
+            if (ir < 0 || ir >= nrows) {
+#pragma unroll
+                for (int s2 = 0; s2 < n; ++s2) xs[s2] = 0;
+            } else if (fast) {
+                const int8_t* s0 = px0 + ir * L.nwp * 4;
+                const int8_t* s1 = px1 + ir * L.nwp * 4;
+#pragma unroll
+                for (int s2 = 0; s2 < n; ++s2) xs[s2] = int(s0[s2]) + (int(s1[s2]) << 16);
+            } else {
+                const int8_t* s0 = px0 + ir * L.nwp * 4;
+                const int8_t* s1 = px1 + ir * L.nwp * 4;
+#pragma unroll
+                for (int s2 = 0; s2 < n; ++s2) {
+                    const bool in = unsigned(col0 + s2) < unsigned(W);
+                    const int a = (ok0 && in) ? int(s0[s2]) : 0;
+                    const int h = (ok1 && in) ? int(s1[s2]) : 0;
+                    xs[s2] = a + (h << 16);
+                }
+            }
+            fwd1d<V>(xs, z);
+#pragma unroll
+            for (int l = 0; l < K; ++l) sz[(l * n + r) * 32] = z[l];
+        }
+        __syncwarp();
+        // ---- columns: V[k][l] = sum_r BT[k][r] Z[r][l]; keep as int16x2 words
+        const int t = (b * g.th + ti) * g.tw + tj0 + tjl;
+        const size_t fstride = size_t(g.Tpad) * g.Cpad / 2;  // words between frequency planes
+        int* vk = vkeep ? reinterpret_cast<int*>(vkeep + size_t(t) * g.Cpad + c0 + c) : nullptr;
+#pragma unroll 1
+        for (int l = 0; l < K; ++l) {
+            int zr[n], v[K];
+#pragma unroll
+            for (int r = 0; r < n; ++r) zr[r] = sz[(l * n + r) * 32];
+            fwd1d<V>(zr, v);
+            int* q = vk;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int w = v[k] + ((v[k] & 0x8000) << 1);  // P -> int16x2 word
+                mx = __vmaxs2(mx, w);
+                mn = __vmins2(mn, w);
+                if (vk) {
+                    *q = w;
+                    q += K * fstride;  // f = k * K + l: next k
+                }
+            }
+            if (vk) vk += fstride;  // next l
+        }
+    }
+    int local = max(max(int(int16_t(mx)), mx >> 16), -min(int(int16_t(mn)), mn >> 16));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+    griddep_wait();  // under PDL: *vmax has been zeroed by the predecessor
+    tl_mark(kTlAbsmax, 1);
+    if (p == 0 && local > 0) atomicMax(vmax, local);
+    tl_mark(kTlAbsmax, 2);
+}
+
 // Streaming quantizer over the V kept by the absmax pass: vq[f][t][c] = q(V[f][t][c]) for
 // t < T, 16 channels per item (two 16-byte loads, one 16-byte store); channels >= C are
 // written as 0.  HBM-bound: 3 bytes per value.
@@ -416,9 +586,47 @@ void pick_shape(const ConvGeom& g, int& cc, int& twc) {
     while (cc > 4 && bytes(cc, twc) > 96 * 1024) cc /= 2;
 }
 
+// k_act_pair: tiles per CTA halved until the grid has two waves over the 148 SMs.
+template <int V>
+cudaError_t act_pair_launch(const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep, cudaStream_t st, bool pdl) {
+    int twc = g.tw < kPairMaxTiles ? g.tw : kPairMaxTiles;
+    const long blocks_c = (g.C + kPairCC - 1) / kPairCC;
+    auto ctas = [&](int t) { return long(g.th) * ((g.tw + t - 1) / t) * g.B * blocks_c; };
+    while (twc > 1 && ctas(twc) < 2 * 148) twc = (twc + 1) / 2;
+    const size_t smem = pair_smem<V>(g.W, twc).bytes;
+    auto kern = k_act_pair<V>;
+    static size_t attr_bytes = 0;
+    if (smem > attr_bytes) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        attr_bytes = smem;
+    }
+    const long gx = long(g.th) * ((g.tw + twc - 1) / twc);
+    if (gx > 0x7fffffffL || g.B > 65535 || blocks_c > 65535) return cudaErrorInvalidConfiguration;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(gx), g.B, unsigned(blocks_c));
+    cfg.blockDim = dim3(32 * twc);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, x, g, twc, vmax, vkeep);
+}
+
 template <int V, int MODE>
 cudaError_t act_launch(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits, QuantParams* qp,
                        int8_t* vqA, unsigned long long* sat, int16_t* vkeep, cudaStream_t st, bool pdl) {
+    if constexpr (MODE == 0 && V <= 2) {
+        // the SWAR kernel has one thread per (tile, channel pair): it needs >= 32k of them to
+        // fill the GPU (measured: config 5 absmax 0.121 -> 0.091 ms, ResNet-18 layers 0.435 ->
+        // 0.382 ms); smaller layers (config 2) keep the item-parallel kernel
+        const char* force = std::getenv("SFC_ACT_PAIR");  // "0" / "1": A/B measurement / test knob
+        const bool big = long(g.T) * ((g.C + 1) / 2) >= 32768;
+        if (force ? force[0] == '1' : big) return act_pair_launch<V>(x, g, vmax, vkeep, st, pdl);
+    }
     int cc, twc;
     pick_shape<V>(g, cc, twc);
     switch (cc) {

@@ -119,6 +119,26 @@ def test_small_cases_bit_exact(cuda, variant, case):
     check_against_oracle(x, w, variant, pad)
 
 
+SWAR_CASES = [  # (B, C, OC, H, W, pad): odd / small / non-multiple-of-64 channel counts, border tiles
+    (2, 5, 3, 13, 11, 1), (1, 64, 8, 14, 14, 1), (3, 130, 9, 9, 17, 0), (1, 1, 2, 7, 7, 1), (2, 67, 16, 20, 6, 2),
+    (1, 128, 32, 29, 31, 1),
+]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("case", SWAR_CASES, ids=[f"b{c[0]}c{c[1]}o{c[2]}h{c[3]}w{c[4]}p{c[5]}" for c in SWAR_CASES])
+def test_swar_absmax_kernel_bit_exact(cuda, variant, case, monkeypatch):
+    """The two-channel SWAR absmax / keep-V kernel (k_act_pair, used for large layers) forced on
+    small ragged cases: vmax, vq, uq, pacc and y_int bit-exact against the oracle."""
+    monkeypatch.setenv("SFC_ACT_PAIR", "1")
+    B, C, OC, H, W, pad = case
+    rng = np.random.default_rng(sum(case) + len(variant))
+    x = rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(OC, C, 3, 3), dtype=np.int8)
+    g, r = check_against_oracle(x, w, variant, pad)
+    assert g["stats"]["vmax"] == r["report"]["vmax"]
+
+
 @pytest.mark.parametrize("bits", [2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_bit_widths(cuda, variant, bits):
