@@ -278,14 +278,19 @@ __host__ __device__ inline PairSmem pair_smem(int W, int twc) {
 
 // Grid: x = tile row * column chunks + chunk (twc tiles), y = image, z = 64-channel block;
 // block = 32 * twc threads (warp w = tile column tj0 + w, lane = channel pair).
-template <int V>
-__global__ void __launch_bounds__(32 * kPairMaxTiles) k_act_pair(const int8_t* __restrict__ x, ConvGeom g, int twc,
-                                                                int* __restrict__ vmax, int16_t* __restrict__ vkeep) {
+// MODE 0: max|V| (+ kept V when vkeep); MODE 1: quantize with the scale of *vmax_in and write
+// vq[f][t][c] (both channels of a pair as one 16-bit store: 64 contiguous bytes per warp).
+template <int V, int MODE>
+__global__ void __launch_bounds__(32 * kPairMaxTiles)
+    k_act_pair(const int8_t* __restrict__ x, ConvGeom g, int twc, int* __restrict__ vmax, int16_t* __restrict__ vkeep,
+               const int* __restrict__ vmax_in, int bits, QuantParams* __restrict__ qp_out,
+               int8_t* __restrict__ vqA, unsigned long long* __restrict__ sat, const QuantParams* __restrict__ qtab) {
     using T = Tab<V>;
     constexpr int n = T::n, K = T::K, M = T::M;
+    constexpr int kTl = MODE == 1 ? kTlQuant : kTlAbsmax;
     extern __shared__ __align__(16) uint8_t smem[];
-    tl_mark(kTlAbsmax, 0);
-    griddep_launch_dependents();
+    tl_mark(kTl, 0);
+    if (MODE == 0) griddep_launch_dependents();
 
     const int W = g.W;
     const int nchunk = (g.tw + twc - 1) / twc;
@@ -342,6 +347,7 @@ __global__ void __launch_bounds__(32 * kPairMaxTiles) k_act_pair(const int8_t* _
 
     const int tjl = threadIdx.x >> 5, p = threadIdx.x & 31, c = 2 * p;
     int mx = 0, mn = 0;  // int16x2 running max / min of V over this thread's two channels
+    int* sz = reinterpret_cast<int*>(smem + L.z_off) + tjl * (K * n * 32) + p;  // [l][r][lane]
     if (tjl < ntj) {
         const int col0 = (tj0 + tjl) * M - g.pad;
         // interior tile with both channels present: no per-sample predicates
@@ -349,7 +355,6 @@ __global__ void __launch_bounds__(32 * kPairMaxTiles) k_act_pair(const int8_t* _
         const int8_t* px0 = reinterpret_cast<const int8_t*>(s_xw + plane(c)) + (col0 - cb_lo);
         const int8_t* px1 = reinterpret_cast<const int8_t*>(s_xw + plane(c + 1)) + (col0 - cb_lo);
         const bool ok0 = c < nch, ok1 = c + 1 < nch;
-        int* sz = reinterpret_cast<int*>(smem + L.z_off) + tjl * (K * n * 32) + p;  // [l][r][lane]
         // ---- rows: Z[r][l] = sum_s BT[l][s] x[r][s], both channels at once
 #pragma unroll 1
         for (int r = 0; r < n; ++r) {
@@ -378,7 +383,48 @@ __global__ void __launch_bounds__(32 * kPairMaxTiles) k_act_pair(const int8_t* _
 #pragma unroll
             for (int l = 0; l < K; ++l) sz[(l * n + r) * 32] = z[l];
         }
-        __syncwarp();
+    }
+    QuantParams qp{};
+    if (MODE == 1) {  // every thread: the table fallback derives cooperatively over the block
+        griddep_wait();  // the absmax pre-pass (and any multi-GPU MAX exchange) is complete
+        tl_mark(kTl, 1);
+        qp = qparams_for(*vmax_in, bits, qtab);
+        if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *qp_out = qp;
+        griddep_launch_dependents();
+    }
+    __syncwarp();
+    if (MODE == 1 && tjl < ntj) {
+        // ---- columns, quantized: vq[f][t][c, c+1] (one 16-bit store per pair)
+        const int t = (b * g.th + ti) * g.tw + tj0 + tjl;
+        const size_t fstride = size_t(g.Tpad) * g.Cpad / 2;  // 16-bit units between frequency planes
+        int16_t* vq = reinterpret_cast<int16_t*>(vqA + size_t(t) * g.Cpad + c0 + c);
+        auto columns = [&](auto quantize) {
+#pragma unroll 1
+            for (int l = 0; l < K; ++l) {
+                int zr[n], v[K];
+#pragma unroll
+                for (int r = 0; r < n; ++r) zr[r] = sz[(l * n + r) * 32];
+                fwd1d<V>(zr, v);
+                int16_t* q = vq;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int lo = int(int16_t(v[k])), hi = (v[k] - lo) >> 16;  // unpack the pair
+                    *q = int16_t((quantize(lo) & 0xff) | (quantize(hi) << 8));
+                    q += K * fstride;  // f = k * K + l: next k
+                }
+                vq += fstride;  // next l
+            }
+        };
+        if (qp.exact) {  // uniform over the grid: no per-value branch
+            const int mul = int(qp.mul);
+            const long long half = 1ll << (qp.shift - 1);
+            const int shift = qp.shift;
+            columns([=](int v) { return quant_fast(v, mul, half, shift); });
+        } else {
+            columns([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, sat); });
+        }
+    }
+    if (MODE == 0 && tjl < ntj) {
         // ---- columns: V[k][l] = sum_r BT[k][r] Z[r][l]; keep as int16x2 words
         const int t = (b * g.th + ti) * g.tw + tj0 + tjl;
         const size_t fstride = size_t(g.Tpad) * g.Cpad / 2;  // words between frequency planes
@@ -403,13 +449,15 @@ __global__ void __launch_bounds__(32 * kPairMaxTiles) k_act_pair(const int8_t* _
             if (vk) vk += fstride;  // next l
         }
     }
-    int local = max(max(int(int16_t(mx)), mx >> 16), -min(int(int16_t(mn)), mn >> 16));
+    if (MODE == 0) {
+        int local = max(max(int(int16_t(mx)), mx >> 16), -min(int(int16_t(mn)), mn >> 16));
 #pragma unroll
-    for (int o = 16; o; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
-    griddep_wait();  // under PDL: *vmax has been zeroed by the predecessor
-    tl_mark(kTlAbsmax, 1);
-    if (p == 0 && local > 0) atomicMax(vmax, local);
-    tl_mark(kTlAbsmax, 2);
+        for (int o = 16; o; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+        griddep_wait();  // under PDL: *vmax has been zeroed by the predecessor
+        tl_mark(kTl, 1);
+        if (p == 0 && local > 0) atomicMax(vmax, local);
+    }
+    tl_mark(kTl, 2);
 }
 
 // Streaming quantizer over the V kept by the absmax pass: vq[f][t][c] = q(V[f][t][c]) for
@@ -460,17 +508,17 @@ __global__ void __launch_bounds__(kActThreads) k_quant_kept(const int16_t* __res
             uint4 out = make_uint4(0, 0, 0, 0);
             const int cbase = cb[u];
             if (cbase < g.C) {
-                const uint32_t w[8] = {a[u].x, a[u].y, a[u].z, a[u].w, b[u].x, b[u].y, b[u].z, b[u].w};
-                uint32_t o[4] = {0, 0, 0, 0};
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
-                    o[e >> 2] |= uint32_t(uint8_t(int8_t(quantize(v)))) << (8 * (e & 3));
-                }
-                if (cbase + 16 > g.C) {  // channels >= C within the chunk are 0 (V holds 0 there too)
+                uint32_t w[8] = {a[u].x, a[u].y, a[u].z, a[u].w, b[u].x, b[u].y, b[u].z, b[u].w};
+                if (cbase + 16 > g.C) {  // channels >= C of the tail chunk: V there is not defined
 #pragma unroll
                     for (int e = 0; e < 16; ++e)
-                        if (cbase + e >= g.C) o[e >> 2] &= ~(0xffu << (8 * (e & 3)));
+                        if (cbase + e >= g.C) w[e >> 1] &= ~(0xffffu << (16 * (e & 1)));
+                }
+                uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {  // (quantize(0) == 0: no saturation from padding)
+                    const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
+                    o[e >> 2] |= uint32_t(uint8_t(int8_t(quantize(v)))) << (8 * (e & 3));
                 }
                 out = make_uint4(o[0], o[1], o[2], o[3]);
             }
@@ -586,15 +634,25 @@ void pick_shape(const ConvGeom& g, int& cc, int& twc) {
     while (cc > 4 && bytes(cc, twc) > 96 * 1024) cc /= 2;
 }
 
+}  // namespace
+
+bool act_pair_wanted(const ConvGeom& g) {
+    const char* force = std::getenv("SFC_ACT_PAIR");  // "0" / "1": A/B measurement / test knob
+    return force ? force[0] == '1' : long(g.T) * ((g.C + 1) / 2) >= 32768;
+}
+
+namespace {
 // k_act_pair: tiles per CTA halved until the grid has two waves over the 148 SMs.
-template <int V>
-cudaError_t act_pair_launch(const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep, cudaStream_t st, bool pdl) {
+template <int V, int MODE>
+cudaError_t act_pair_launch(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits,
+                            QuantParams* qp, int8_t* vqA, unsigned long long* sat, int16_t* vkeep, cudaStream_t st,
+                            bool pdl) {
     int twc = g.tw < kPairMaxTiles ? g.tw : kPairMaxTiles;
     const long blocks_c = (g.C + kPairCC - 1) / kPairCC;
     auto ctas = [&](int t) { return long(g.th) * ((g.tw + t - 1) / t) * g.B * blocks_c; };
     while (twc > 1 && ctas(twc) < 2 * 148) twc = (twc + 1) / 2;
     const size_t smem = pair_smem<V>(g.W, twc).bytes;
-    auto kern = k_act_pair<V>;
+    auto kern = k_act_pair<V, MODE>;
     static size_t attr_bytes = 0;
     if (smem > attr_bytes) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -613,19 +671,19 @@ cudaError_t act_pair_launch(const int8_t* x, const ConvGeom& g, int* vmax, int16
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, x, g, twc, vmax, vkeep);
+    return cudaLaunchKernelEx(&cfg, kern, x, g, twc, vmax, vkeep, vmax_in, bits, qp, vqA, sat,
+                              MODE == 0 ? nullptr : qparams_table(false));
 }
 
 template <int V, int MODE>
 cudaError_t act_launch(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits, QuantParams* qp,
                        int8_t* vqA, unsigned long long* sat, int16_t* vkeep, cudaStream_t st, bool pdl) {
-    if constexpr (MODE == 0 && V <= 2) {
+    if constexpr (V <= 2) {
         // the SWAR kernel has one thread per (tile, channel pair): it needs >= 32k of them to
         // fill the GPU (measured: config 5 absmax 0.121 -> 0.091 ms, ResNet-18 layers 0.435 ->
         // 0.382 ms); smaller layers (config 2) keep the item-parallel kernel
-        const char* force = std::getenv("SFC_ACT_PAIR");  // "0" / "1": A/B measurement / test knob
-        const bool big = long(g.T) * ((g.C + 1) / 2) >= 32768;
-        if (force ? force[0] == '1' : big) return act_pair_launch<V>(x, g, vmax, vkeep, st, pdl);
+        if (act_pair_wanted(g))
+            return act_pair_launch<V, MODE>(x, g, vmax, vmax_in, bits, qp, vqA, sat, vkeep, st, pdl);
     }
     int cc, twc;
     pick_shape<V>(g, cc, twc);

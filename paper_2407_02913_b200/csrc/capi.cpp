@@ -522,10 +522,18 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
         needs_y64(L, o);  // refuse before anything is launched
         unsigned mask = SFC_STAGE_ALL & ~SFC_STAGE_QPARAMS;
         if (const char* dbg = std::getenv("SFC_DEBUG_FORWARD_MASK")) mask = unsigned(std::atoi(dbg));  // profiling only
+        // The absmax pass keeps V and the quantizer streams it (or runs inside the GEMM).
+        // Recomputing V from x in a quantizing transform instead (no int16 V round trip) was
+        // measured slower even with the SWAR kernels (config 5 0.390 vs 0.385 ms, ResNet-18
+        // 1.30 vs 1.19, VGG-16 18.3 vs 15.8); SFC_FORWARD_RECOMPUTE=1 selects it.
+        bool recompute = false;
+        if (const char* e = std::getenv("SFC_FORWARD_RECOMPUTE")) recompute = e[0] == '1';
         // vmax and the saturation counter share the first 16 bytes of the workspace
         ck(launch_zero_words(reinterpret_cast<uint32_t*>(v.vmax), 4, S(stream)), "workspace reset launch");
-        ck(launch_act_absmax(L->variant, d_x, g, v.vmax, v.vkeep, S(stream), true), "absmax launch");
-        run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, mask | SFC_STAGE_KEPT, true, S(stream));
+        ck(launch_act_absmax(L->variant, d_x, g, v.vmax, recompute ? nullptr : v.vkeep, S(stream), true),
+           "absmax launch");
+        run_conv(L, d_x, n, h, w, pad, v.vmax, ws, ws_bytes, o, recompute ? mask : mask | SFC_STAGE_KEPT, true,
+                 S(stream));
     });
 }
 

@@ -229,17 +229,17 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                     const int i = ct + j * (32 * kConvWarps);
                     const int r = i / kCh, qc = i % kCh;
                     const int valid = g.C - (kc * BK + qc * 16);  // channels >= C (and rows >= T, loaded as 0) give 0
-                    const uint32_t w[8] = {ca[j].x, ca[j].y, ca[j].z, ca[j].w, cb[j].x, cb[j].y, cb[j].z, cb[j].w};
-                    uint32_t o[4] = {0, 0, 0, 0};
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
-                        o[e >> 2] |= uint32_t(uint8_t(int8_t(quant(v)))) << (8 * (e & 3));
-                    }
-                    if (valid < 16) {  // the channel tail of the last chunk (V was loaded as 0 there)
+                    uint32_t w[8] = {ca[j].x, ca[j].y, ca[j].z, ca[j].w, cb[j].x, cb[j].y, cb[j].z, cb[j].w};
+                    if (valid < 16) {  // the channel tail of the last chunk: V there is not defined
 #pragma unroll
                         for (int e = 0; e < 16; ++e)
-                            if (e >= valid) o[e >> 2] &= ~(0xffu << (8 * (e & 3)));
+                            if (e >= valid) w[e >> 1] &= ~(0xffffu << (16 * (e & 1)));
+                    }
+                    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {  // (quant(0) == 0: no saturation from padding)
+                        const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
+                        o[e >> 2] |= uint32_t(uint8_t(int8_t(quant(v)))) << (8 * (e & 3));
                     }
                     const int sw = BK == 128 ? (qc ^ (r & 7)) : (qc ^ ((r >> 1) & 3));
                     *reinterpret_cast<uint4*>(a_st + r * BK + (sw << 4)) = make_uint4(o[0], o[1], o[2], o[3]);

@@ -60,6 +60,9 @@ cudaError_t launch_filter_prepare(int variant, const int8_t* w, int OC, int IC, 
 // pdl: launched under programmatic stream serialization; the CTAs stage and transform
 // their tiles before waiting on the predecessor (which zeroes *vmax).
 // vkeep != nullptr: also keep V as int16 [F][Tpad][Cpad] for launch_quant_kept.
+// Whether the 3x3 activation kernels take the two-channel SWAR form for this layer (large
+// layers; SFC_ACT_PAIR=0/1 forces either).
+bool act_pair_wanted(const ConvGeom& g);
 cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep,
                               cudaStream_t st, bool pdl = false);
 // vq = q(kept V) for t < T, channels >= C zeroed (streaming; replaces launch_act_quant's

@@ -139,6 +139,26 @@ def test_swar_absmax_kernel_bit_exact(cuda, variant, case, monkeypatch):
     assert g["stats"]["vmax"] == r["report"]["vmax"]
 
 
+@pytest.mark.parametrize("qfuse", ["0", "1"])
+def test_padding_channels_never_count_as_saturations(cuda, qfuse, monkeypatch):
+    """Kept-V channels past C are not defined (the workspace is reused, not cleared): the
+    quantizers zero them before quantizing, so with the exact-fallback quantizer (bits 5 here:
+    no proven multiplier) a workspace full of garbage still reports 0 saturations and the
+    oracle's y."""
+    monkeypatch.setenv("SFC_QFUSE", qfuse)
+    rng = np.random.default_rng(5)
+    x = rng.integers(-128, 128, size=(2, 9, 15, 13), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(6, 9, 3, 3), dtype=np.int8)
+    layer = sc.SfcLayer("sfc6-6x6-3x3", torch.from_numpy(w).cuda(), 5)
+    ws = layer.workspace(2, 15, 13, 1)
+    ws.fill_(0x7F)
+    y = torch.empty((2, 6, 15, 13), dtype=torch.int32, device="cuda")
+    layer.forward(torch.from_numpy(x).cuda(), ws, 1, y_int32=y)
+    st = layer.stats(2, 15, 13, 1, ws)
+    assert not st["fast_quantizer_exact"] and st["saturations"] == 0
+    assert np.array_equal(y.cpu().numpy().astype(np.int64), ob.quantized_conv(x, w, "sfc6-6x6-3x3", 1, 5)["y_int"])
+
+
 @pytest.mark.parametrize("bits", [2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_bit_widths(cuda, variant, bits):
