@@ -228,6 +228,28 @@ int sfc_report_sq_err_f64(const double* d_out, const double* d_ref, int64_t n, d
 int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, int w, const double* d_weights,
                       int oc, int pad, int reduced, double* d_out, int64_t* counters, void* stream);
 
+/* ---- the general QuantConfig on a batch shard: the full batch's activation
+ *      scales from per-shard steps.  Layers from sfc_layer_create_ex with a non-default config
+ *      (int8-valued inputs), one workspace per shard.  Sequence per rank:
+ *        sfc_general_prepare       absmax keeps V; this shard's activation maxima -> *d_maxima
+ *                                  (count = 1 or F uint64: fp64 bit patterns of non-negative
+ *                                  values, so an integer all-reduce(MAX) is the exact global max)
+ *        all-reduce(MAX) of d_maxima
+ *        MseGrid only: sfc_general_mse_partial with d_err_in = the previous rank's d_err_out
+ *                                  (NULL on rank 0), sent on to the next rank: the reference's
+ *                                  one sequential fp64 sum per candidate (quant.cpp:19-30,
+ *                                  168-181) continued shard by shard in batch order; the last
+ *                                  rank's sums [count][101] are broadcast to every rank
+ *        sfc_general_conv          scales (MinMax from the maxima / the MseGrid pick over d_err),
+ *                                  quantize, contraction, fp64 epilogue -> out_f32 / out_f64 / i8
+ *      The result equals sfc_conv_forward on the whole batch bit for bit. */
+int sfc_general_prepare(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, void* d_workspace,
+                        size_t workspace_bytes, uint64_t** d_maxima, int* count, void* stream);
+int sfc_general_mse_partial(sfc_layer_t layer, int n, int h, int w, int pad, void* d_workspace,
+                            const double* d_err_in, double* d_err_out, void* stream);
+int sfc_general_conv(sfc_layer_t layer, int n, int h, int w, int pad, void* d_workspace, size_t workspace_bytes,
+                     const double* d_err, const sfc_outputs* outputs, void* stream);
+
 /* Profiling hook of the timeline build (libsfc_b200_tl.so, `make TIMELINE=1`): out[8][3] =
  * per kernel {first CTA entry, first CTA past its dependency wait, last CTA exit} in
  * %globaltimer ns (0 / UINT64_MAX when the kernel did not run); reset re-arms the stamps.

@@ -29,7 +29,7 @@ _i8p = ctypes.POINTER(ctypes.c_int8)
 class SfoConfig(ctypes.Structure):
     _fields_ = [("bits", ctypes.c_int), ("act_scope", ctypes.c_int), ("filter_scope", ctypes.c_int),
                 ("search", ctypes.c_int), ("threads", ctypes.c_int), ("want_report", ctypes.c_int),
-                ("vmax_override", ctypes.c_int64)]
+                ("vmax_override", ctypes.c_int64), ("act_scale_override", ctypes.POINTER(ctypes.c_double))]
 
 
 class SfoReport(ctypes.Structure):
@@ -130,8 +130,10 @@ def scale_mse_grid(vals, bits):
 
 def quantized_conv(x: np.ndarray, w: np.ndarray, spec_name: str, pad: int = 1, bits: int = 8,
                    act_scope: int = 0, filter_scope: int = 0, search: int = 0, threads: int | None = None,
-                   want=("out", "y_int"), report: bool = False, vmax_override: int = -1) -> dict:
-    """Run the C restatement.  x: int8 [B,C,H,W], w: int8 [OC,C,R,R]."""
+                   want=("out", "y_int"), report: bool = False, vmax_override: int = -1,
+                   act_scale_override=None) -> dict:
+    """Run the C restatement.  x: int8 [B,C,H,W], w: int8 [OC,C,R,R].  act_scale_override: the
+    activation scales (1 or F) to quantize with (a batch shard with the full batch's scales)."""
     lib = oracle_lib()
     x = np.ascontiguousarray(x, np.int8)
     w = np.ascontiguousarray(w, np.int8)
@@ -153,8 +155,9 @@ def quantized_conv(x: np.ndarray, w: np.ndarray, spec_name: str, pad: int = 1, b
     uq = np.empty((OC, C, F), np.int32) if "uq" in want else None
     act = np.empty(F, np.float64)
     fil = np.empty(OC * F, np.float64)
+    aso = None if act_scale_override is None else np.ascontiguousarray(act_scale_override, np.float64)
     cfg = SfoConfig(bits, act_scope, filter_scope, search, threads or os.cpu_count() or 1, int(report),
-                    int(vmax_override))
+                    int(vmax_override), None if aso is None else _ptr(aso, _f64p))
     rep = SfoReport()
     rc = lib.sfo_quantized_conv(_ptr(x, _i8p), B, C, H, W, _ptr(w, _i8p), OC, spec_name.encode(), pad,
                                 ctypes.byref(cfg), _ptr(out, _f64p), _ptr(y, _i64p), _ptr(pacc, _i64p),

@@ -583,6 +583,9 @@ int sfo_quantized_conv(const int8_t* x, int B, int C, int H, int W, const int8_t
         free(gall);
     }
 
+    if (cfg->act_scale_override)
+        for (int i = 0; i < n_act; ++i) act_scale[i] = cfg->act_scale_override[i];
+
     /* --- filter transform, scales and quantization (quant.cpp:183-229) --- */
     double* u = (double*)malloc(sizeof(double) * (size_t)OC * C * F);
     for (int oc = 0; oc < OC; ++oc)

@@ -41,6 +41,8 @@ typedef struct {
     int want_report;  /* 1: run the fp64 direct conv for mse / signal_energy / snr_db */
     int64_t vmax_override; /* >= 0: use this max|V| for the PerTensor MinMax scale instead of the
                               local one (a batch shard quantized with the global batch scale) */
+    const double* act_scale_override; /* non-NULL: the activation scales (1 or F) to quantize with,
+                                         any scope / search (a shard with the full batch's scales) */
 } sfo_config;
 
 typedef struct {

@@ -25,6 +25,7 @@ EXPORTED = (
     "sfc_act_transform", "sfc_conv_kept", "sfc_layer_create_ex", "sfc_layer_filter_scales_native",
     "sfc_conv_act_scales", "sfc_layer_create_f64", "sfc_conv_forward_f64", "sfc_direct_conv_f64",
     "sfc_report_sq_err_f64", "sfc_fast_conv_f64", "sfc_transform_filters_f64",
+    "sfc_general_prepare", "sfc_general_mse_partial", "sfc_general_conv",
 )
 
 
@@ -78,6 +79,9 @@ _SIGS = {
     "sfc_conv_int8": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
     "sfc_conv_int8_stages": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _sz, ctypes.POINTER(Outputs), ctypes.c_uint, _vp]),
     "sfc_conv_forward": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
+    "sfc_general_prepare": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _sz, ctypes.POINTER(_vp), ctypes.POINTER(_i), _vp]),
+    "sfc_general_mse_partial": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "sfc_general_conv": (_i, [_vp, _i, _i, _i, _i, _vp, _sz, _vp, ctypes.POINTER(Outputs), _vp]),
     "sfc_act_transform": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _sz, _vp]),
     "sfc_layer_create_ex": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _i, _vp, ctypes.POINTER(_vp)]),
     "sfc_layer_filter_scales_native": (_i, [_vp, _vp, _i64p]),

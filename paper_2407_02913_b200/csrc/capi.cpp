@@ -259,7 +259,83 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
 }
 }  // namespace
 
+namespace {
+// General QuantConfig (int8-valued inputs), in the steps a batch-sharded caller interleaves
+// with its exchanges: prepare (absmax keeps V; this shard's activation maxima -> ws), [all-
+// reduce(MAX) of the maxima; MseGrid: the rank-ordered chain of partial sums], conv (scales,
+// quantize, contraction, fp64 epilogue).  quant.cpp:163-278.
+void general_check(const sfc_layer* L, const sfc_outputs* o) {
+    if (!L->general) throw Unsupported("the default QuantConfig shards through sfc_act_transform / sfc_conv_kept");
+    if (o && (o->y_int32 || o->y_int64))
+        throw Unsupported("y_int is defined only for PerTensor activation + PerChannel filter MinMax scales");
+    if (L->act_scope == SFC_ACT_PER_FREQUENCY && L->F > 196) throw Unsupported("too many frequencies");
+}
+
+void general_prepare(const sfc_layer* L, const int8_t* d_x, const ConvGeom& g, const WsView& v, cudaStream_t st) {
+    ck(cudaMemsetAsync(v.vmax, 0, kWsMaxima + sizeof(unsigned long long) * L->F, st), "memset header");
+    ck(launch_act_absmax(L->variant, d_x, g, v.vmax, v.vkeep, st, false), "absmax launch");
+    ck(launch_act_maxima(v.vkeep, g, L->F, L->act_scope == SFC_ACT_PER_FREQUENCY, v.vmaxf, st), "maxima launch");
+}
+
+void general_conv(const sfc_layer* L, const ConvGeom& g, const WsView& v, const double* err, const sfc_outputs* o,
+                  cudaStream_t st) {
+    const bool pf = L->act_scope == SFC_ACT_PER_FREQUENCY;
+    ck(launch_act_pick(L->F, pf, v.vmaxf, L->bits, err, v.act_scale, st), "scale pick launch");
+    OutPtrs op{nullptr, nullptr, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
+    op.gen_act = v.act_scale, op.gen_per_freq = pf ? 1 : 0, op.gen_fil = L->d_fil;
+    auto quantize = [&](void* vq) {
+        ck(launch_act_quantize(v.vkeep, g, L->F, pf, v.act_scale, L->bits, vq, v.sat, st), "quantize launch");
+    };
+    if (L->bits > 8) return wide_tail(L, g, op, v.qp, quantize, st);
+    quantize(v.vq);
+    bool pdl = false;
+    gemm_output(L, g, v, 2, op, true, true, st, pdl, false);
+}
+}  // namespace
+
 extern "C" {
+
+int sfc_general_prepare(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int pad, void* ws, size_t ws_bytes,
+                        uint64_t** d_maxima, int* count, void* stream) {
+    return guarded([&] {
+        check_call(L, d_x, n, h, w, pad);
+        if (!ws) throw std::invalid_argument("null workspace");
+        general_check(L, nullptr);
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
+        const WsView v = carve(ws, g, L->F);
+        general_prepare(L, d_x, g, v, S(stream));
+        if (d_maxima) *d_maxima = reinterpret_cast<uint64_t*>(v.vmaxf);
+        if (count) *count = L->act_scope == SFC_ACT_PER_FREQUENCY ? L->F : 1;
+    });
+}
+
+int sfc_general_mse_partial(sfc_layer_t L, int n, int h, int w, int pad, void* ws, const double* d_err_in,
+                            double* d_err_out, void* stream) {
+    return guarded([&] {
+        if (!L || !ws || !d_err_out) throw std::invalid_argument("null argument");
+        general_check(L, nullptr);
+        if (L->search != SFC_SEARCH_MSE_GRID) throw std::invalid_argument("the layer's scale search is MinMax");
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        const WsView v = carve(ws, g, L->F);
+        ck(launch_act_mse(v.vkeep, g, L->F, L->act_scope == SFC_ACT_PER_FREQUENCY, v.vmaxf, L->bits, d_err_in,
+                          d_err_out, S(stream)),
+           "mse launch");
+    });
+}
+
+int sfc_general_conv(sfc_layer_t L, int n, int h, int w, int pad, void* ws, size_t ws_bytes, const double* d_err,
+                     const sfc_outputs* o, void* stream) {
+    return guarded([&] {
+        if (!L || !ws || !o) throw std::invalid_argument("null argument");
+        general_check(L, o);
+        if ((L->search == SFC_SEARCH_MSE_GRID) != (d_err != nullptr))
+            throw std::invalid_argument("d_err: the complete MseGrid sums for an MseGrid layer, NULL for MinMax");
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
+        general_conv(L, g, carve(ws, g, L->F), d_err, o, S(stream));
+    });
+}
 
 const char* sfc_last_error(void) { return g_err.c_str(); }
 int sfc_version(void) { return 1; }
@@ -500,23 +576,16 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
         WsView v = carve(ws, g, L->F);
         if (!o) throw std::invalid_argument("null outputs");
         if (L->general) {  // non-default QuantConfig: fp64 parity path (quant.cpp:163-278)
-            if (o->y_int32 || o->y_int64)
-                throw Unsupported("y_int is defined only for PerTensor activation + PerChannel filter MinMax scales");
-            if (L->act_scope == SFC_ACT_PER_FREQUENCY && L->F > 196) throw Unsupported("too many frequencies");
-            ck(cudaMemsetAsync(ws, 0, kWsMaxima + sizeof(unsigned long long) * L->F, S(stream)), "memset header");
-            ck(launch_act_absmax(L->variant, d_x, g, v.vmax, v.vkeep, S(stream), false), "absmax launch");
-            const bool pf = L->act_scope == SFC_ACT_PER_FREQUENCY;
-            OutPtrs op{nullptr, nullptr, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
-            op.gen_act = v.act_scale, op.gen_per_freq = pf ? 1 : 0, op.gen_fil = L->d_fil;
-            auto quantize = [&](void* vq) {
-                ck(launch_act_general(v.vkeep, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits, v.vmaxf,
-                                      v.act_scale, vq, v.sat, S(stream)),
-                   "general activation launch");
-            };
-            if (L->bits > 8) return wide_tail(L, g, op, v.qp, quantize, S(stream));
-            quantize(v.vq);
-            bool pdl = false;
-            gemm_output(L, g, v, 2, op, true, true, S(stream), pdl, false);
+            // the batch-sharded steps on the whole batch; the MseGrid sums use the (not yet
+            // written) vq region of the workspace as scratch
+            general_check(L, o);
+            general_prepare(L, d_x, g, v, S(stream));
+            double* err = reinterpret_cast<double*>(v.vq);
+            const bool mse = L->search == SFC_SEARCH_MSE_GRID;
+            if (mse) ck(launch_act_mse(v.vkeep, g, L->F, L->act_scope == SFC_ACT_PER_FREQUENCY, v.vmaxf, L->bits,
+                                       nullptr, err, S(stream)),
+                        "mse launch");
+            general_conv(L, g, v, mse ? err : nullptr, o, S(stream));
             return;
         }
         needs_y64(L, o);  // refuse before anything is launched
@@ -749,7 +818,7 @@ int sfc_conv_forward_f64(sfc_layer_t L, const double* d_x, int n, int h, int w, 
         op.gen_act = v.act_scale, op.gen_per_freq = pf ? 1 : 0, op.gen_fil = L->d_fil;
         auto quantize = [&](void* vq) {
             ck(launch_act_general_f64(Vd, g, L->F, pf, L->search == SFC_SEARCH_MSE_GRID, L->bits, v.vmaxf, v.act_scale,
-                                      vq, v.sat, S(stream)),
+                                      vq, v.sat, reinterpret_cast<double*>(v.vq), S(stream)),
                "general activation launch");
         };
         if (L->bits > 8) {

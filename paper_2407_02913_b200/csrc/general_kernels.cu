@@ -123,23 +123,23 @@ __global__ void __launch_bounds__(256) k_act_fmax(const TV* __restrict__ V, Conv
         atomicMax(&vmaxf[per_freq ? f : 0], (unsigned long long)__double_as_longlong(m));
 }
 
-// Activation scales from the maxima: MinMax, or MseGrid over the group's V in the
-// reference's order (quant.cpp:168-181: PerTensor = all of g.v in (tile, c, f) order,
-// PerFrequency = (tile, c) for one f).  One block of 4 warps per group; lane = candidate.
+// MseGrid over this shard's V for every candidate of every activation group, continuing the
+// reference's single sequential fp64 sum (quant.cpp:19-30) from err_in (the accumulators of
+// the shards before this one in batch order; nullptr = the start of the batch): the batch
+// split over ranks and chained rank by rank gives bitwise the full-batch sums.  Value order
+// as quant.cpp:168-181: PerTensor = all of g.v in (tile, c, f) order, PerFrequency = (tile,
+// c) for one f.  One block of 4 warps per group; lane = candidate (scales from the global
+// maxima).
 template <class TV>
-__global__ void __launch_bounds__(128) k_act_scales(const TV* __restrict__ V, ConvGeom g, int F, int per_freq,
-                                                    const unsigned long long* __restrict__ vmax, int mse, int bits,
-                                                    double* __restrict__ act_scale) {
+__global__ void __launch_bounds__(128) k_act_mse(const TV* __restrict__ V, ConvGeom g, int F, int per_freq,
+                                                 const unsigned long long* __restrict__ vmax, int bits,
+                                                 const double* __restrict__ err_in, double* __restrict__ err_out) {
     const int grp = blockIdx.x, cand = threadIdx.x;
+    if (cand >= kCands) return;
     const double qmax = double((1 << (bits - 1)) - 1), qmin = -qmax - 1.0;
     const double base = fmax(__longlong_as_double((long long)vmax[per_freq ? grp : 0]) / qmax, 1e-8);
-    __shared__ double s_err[kCands];
-    if (!mse) {
-        if (cand == 0) act_scale[grp] = base;
-        return;
-    }
-    const double s = grid_scale(base, cand < kCands ? cand : 0);
-    double err = 0.0;
+    const double s = grid_scale(base, cand);
+    double err = err_in ? err_in[grp * kCands + cand] : 0.0;
     const long long tc = (long long)g.T * g.C;
     if (per_freq) {
         const TV* Vf = V + (long long)grp * g.Tpad * g.Cpad;
@@ -154,14 +154,25 @@ __global__ void __launch_bounds__(128) k_act_scales(const TV* __restrict__ V, Co
                 err = __dadd_rn(err, mse_term(double(V[((long long)f * g.Tpad + t) * g.Cpad + c]), s, qmax, qmin));
         }
     }
-    if (cand < kCands) s_err[cand] = err;
-    __syncthreads();
-    if (cand == 0) {
-        double best = base, best_err = s_err[0];
-        for (int c = 1; c < kCands; ++c)
-            if (s_err[c] < best_err) best_err = s_err[c], best = grid_scale(base, c);
-        act_scale[grp] = best;
+    err_out[grp * kCands + cand] = err;
+}
+
+// Activation scales (quant.cpp:117-134): MinMax from the (global) maxima, or the MseGrid pick
+// over the complete sums (the MinMax scale unless a grid point is strictly better, first wins).
+__global__ void k_act_pick(int groups, int per_freq, const unsigned long long* __restrict__ vmax, int bits,
+                           const double* __restrict__ err, double* __restrict__ act_scale) {
+    const int grp = blockIdx.x * blockDim.x + threadIdx.x;
+    if (grp >= groups) return;
+    const double qmax = double((1 << (bits - 1)) - 1);
+    const double base = fmax(__longlong_as_double((long long)vmax[per_freq ? grp : 0]) / qmax, 1e-8);
+    if (!err) {
+        act_scale[grp] = base;
+        return;
     }
+    double best = base, best_err = err[grp * kCands];
+    for (int c = 1; c < kCands; ++c)
+        if (err[grp * kCands + c] < best_err) best_err = err[grp * kCands + c], best = grid_scale(base, c);
+    act_scale[grp] = best;
 }
 
 // vq[f][t][c] = quantize_value(V, sa(f)) (quant.cpp:242-250) for t < T, c < C (else 0);
@@ -356,13 +367,31 @@ cudaError_t fil_general(const TU* U, int OC, int IC, int F, int scope, int mse, 
 }
 
 template <class TV>
-cudaError_t act_general(const TV* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
-                        unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
-                        cudaStream_t st) {
+cudaError_t act_maxima(const TV* V, const ConvGeom& g, int F, int per_freq, unsigned long long* vmax,
+                       cudaStream_t st) {
     const long long n = (long long)g.T * g.C;
     const int bx = int((n + 255) / 256 < 64 ? (n + 255) / 256 : 64);
     k_act_fmax<TV><<<dim3(bx, F), 256, 0, st>>>(V, g, F, per_freq, vmax);
-    k_act_scales<TV><<<per_freq ? F : 1, 128, 0, st>>>(V, g, F, per_freq, vmax, mse, bits, act_scale);
+    return cudaGetLastError();
+}
+
+template <class TV>
+cudaError_t act_mse(const TV* V, const ConvGeom& g, int F, int per_freq, const unsigned long long* vmax, int bits,
+                    const double* err_in, double* err_out, cudaStream_t st) {
+    k_act_mse<TV><<<per_freq ? F : 1, 128, 0, st>>>(V, g, F, per_freq, vmax, bits, err_in, err_out);
+    return cudaGetLastError();
+}
+
+cudaError_t act_pick(int F, int per_freq, const unsigned long long* vmax, int bits, const double* err,
+                     double* act_scale, cudaStream_t st) {
+    const int groups = per_freq ? F : 1;
+    k_act_pick<<<(groups + 127) / 128, 128, 0, st>>>(groups, per_freq, vmax, bits, err, act_scale);
+    return cudaGetLastError();
+}
+
+template <class TV>
+cudaError_t act_quantize(const TV* V, const ConvGeom& g, int F, int per_freq, const double* act_scale, int bits,
+                         void* vqA, unsigned long long* sat, cudaStream_t st) {
     const long long nq = (long long)g.T * g.Cpad;
     const int bq = int((nq + 255) / 256 < 64 ? (nq + 255) / 256 : 64);
     if (bits > 8)
@@ -372,6 +401,17 @@ cudaError_t act_general(const TV* V, const ConvGeom& g, int F, int per_freq, int
         k_quant_general<TV, int8_t><<<dim3(bq, F), 256, 0, st>>>(V, g, F, per_freq, act_scale, bits,
                                                                  static_cast<int8_t*>(vqA), sat);
     return cudaGetLastError();
+}
+
+template <class TV>
+cudaError_t act_general(const TV* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
+                        unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
+                        double* err_tmp, cudaStream_t st) {
+    cudaError_t e = act_maxima(V, g, F, per_freq, vmax, st);
+    if (e == cudaSuccess && mse) e = act_mse(V, g, F, per_freq, vmax, bits, nullptr, err_tmp, st);
+    if (e == cudaSuccess) e = act_pick(F, per_freq, vmax, bits, mse ? err_tmp : nullptr, act_scale, st);
+    if (e == cudaSuccess) e = act_quantize(V, g, F, per_freq, act_scale, bits, vqA, sat, st);
+    return e;
 }
 }  // namespace
 
@@ -389,14 +429,34 @@ cudaError_t launch_fil_general_f64(const double* U, int OC, int IC, int F, int s
 
 cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
                                unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
-                               cudaStream_t st) {
-    return act_general(V, g, F, per_freq, mse, bits, vmax, act_scale, vqA, sat, st);
+                               double* err_tmp, cudaStream_t st) {
+    return act_general(V, g, F, per_freq, mse, bits, vmax, act_scale, vqA, sat, err_tmp, st);
 }
 
 cudaError_t launch_act_general_f64(const double* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
                                    unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
-                                   cudaStream_t st) {
-    return act_general(V, g, F, per_freq, mse, bits, vmax, act_scale, vqA, sat, st);
+                                   double* err_tmp, cudaStream_t st) {
+    return act_general(V, g, F, per_freq, mse, bits, vmax, act_scale, vqA, sat, err_tmp, st);
+}
+
+cudaError_t launch_act_maxima(const int16_t* V, const ConvGeom& g, int F, int per_freq, unsigned long long* vmax,
+                              cudaStream_t st) {
+    return act_maxima(V, g, F, per_freq, vmax, st);
+}
+
+cudaError_t launch_act_mse(const int16_t* V, const ConvGeom& g, int F, int per_freq, const unsigned long long* vmax,
+                           int bits, const double* err_in, double* err_out, cudaStream_t st) {
+    return act_mse(V, g, F, per_freq, vmax, bits, err_in, err_out, st);
+}
+
+cudaError_t launch_act_pick(int F, int per_freq, const unsigned long long* vmax, int bits, const double* err,
+                            double* act_scale, cudaStream_t st) {
+    return act_pick(F, per_freq, vmax, bits, err, act_scale, st);
+}
+
+cudaError_t launch_act_quantize(const int16_t* V, const ConvGeom& g, int F, int per_freq, const double* act_scale,
+                                int bits, void* vqA, unsigned long long* sat, cudaStream_t st) {
+    return act_quantize(V, g, F, per_freq, act_scale, bits, vqA, sat, st);
 }
 
 cudaError_t launch_act_f64(int variant, const double* x, const ConvGeom& g, double* Vd, cudaStream_t st) {

@@ -149,12 +149,23 @@ cudaError_t launch_fil_general(const int32_t* U, int OC, int IC, int F, int scop
 // MinMax / MseGrid scales act_scale[1 or F] and vq (exact fp64 quantizer, saturations counted).
 cudaError_t launch_act_general(const int16_t* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
                                unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
-                               cudaStream_t st);
+                               double* err_tmp, cudaStream_t st);
+// The same in steps, for the batch-sharded general path: local maxima (fp64 bit patterns,
+// 1 or F slots zeroed beforehand), the MseGrid partial sums continuing from err_in ([groups]
+// [101]; nullptr = batch start), the pick (err nullptr = MinMax), the quantize.
+cudaError_t launch_act_maxima(const int16_t* V, const ConvGeom& g, int F, int per_freq, unsigned long long* vmax,
+                              cudaStream_t st);
+cudaError_t launch_act_mse(const int16_t* V, const ConvGeom& g, int F, int per_freq, const unsigned long long* vmax,
+                           int bits, const double* err_in, double* err_out, cudaStream_t st);
+cudaError_t launch_act_pick(int F, int per_freq, const unsigned long long* vmax, int bits, const double* err,
+                            double* act_scale, cudaStream_t st);
+cudaError_t launch_act_quantize(const int16_t* V, const ConvGeom& g, int F, int per_freq, const double* act_scale,
+                                int bits, void* vqA, unsigned long long* sat, cudaStream_t st);
 // Real-valued (fp64) inputs and filters, the reference's own arithmetic order:
 // V [F][Tpad][Cpad] (gather_tiles), U [OC][IC][F] (transform_filters), direct conv.
 cudaError_t launch_act_general_f64(const double* V, const ConvGeom& g, int F, int per_freq, int mse, int bits,
                                    unsigned long long* vmax, double* act_scale, void* vqA, unsigned long long* sat,
-                                   cudaStream_t st);
+                                   double* err_tmp, cudaStream_t st);
 cudaError_t launch_fil_general_f64(const double* U, int OC, int IC, int F, int scope, int mse, int bits, int Cpad,
                                    int OCpad, double* scale_native, double* err_tmp, void* uqB, double* fil_full,
                                    unsigned long long* sat, cudaStream_t st);

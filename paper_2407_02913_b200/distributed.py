@@ -25,6 +25,10 @@ def shard_bounds(batch: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < rem else 0)
 
 
+def _global_rank(group, rank: int) -> int:
+    return rank if group is None else dist.get_global_rank(group, rank)
+
+
 class CudaEngine:
     """Adapter of sfconv.SfcLayer to the engine protocol used by ShardedConv."""
 
@@ -49,6 +53,25 @@ class CudaEngine:
     def conv(self, x, vmax, **outs):
         self.layer.conv_kept(tuple(x.shape), vmax, self._workspace(x), self.pad, **outs)
 
+    # -- general QuantConfig (per-frequency scopes, MseGrid): see ShardedConv.forward_general
+    @property
+    def mse(self) -> bool:
+        return self.layer.search == 1
+
+    def general_prepare(self, x):
+        return self.layer.general_prepare(x, self._workspace(x), self.pad)
+
+    def general_mse(self, x, err_in):
+        n, _, h, w = x.shape
+        groups = self.layer.spec.K ** 2 if self.layer.act_scope == 1 else 1
+        err_out = torch.empty((groups, 101), dtype=torch.float64, device=x.device)
+        self.layer.general_mse_partial(n, h, w, self.pad, self._workspace(x), err_in, err_out)
+        return err_out
+
+    def general_conv(self, x, err, **outs):
+        n, _, h, w = x.shape
+        self.layer.general_conv(n, h, w, self.pad, self._workspace(x), err, **outs)
+
 
 @dataclass
 class ShardedConv:
@@ -63,6 +86,35 @@ class ShardedConv:
             dist.all_reduce(vmax, op=dist.ReduceOp.MAX, group=self.group)
         self.engine.conv(x_local, vmax, **outs)
         return vmax
+
+    def forward_general(self, x_local, **outs):
+        """A non-default QuantConfig (PerFrequency scopes, MseGrid; quant.cpp:163-229): the
+        activation scales are functions of the whole batch.  Local maxima -> all-reduce(MAX)
+        (fp64 bit patterns, exact); for MseGrid each candidate's error is ONE sequential fp64
+        sum over the batch in tile order (quant.cpp:19-30), so the sums travel rank to rank in
+        batch order (each rank continues the previous rank's accumulators over its shard) and
+        the last rank's complete sums are broadcast; every rank then picks the same scales and
+        quantizes / contracts / transforms its shard.  Bitwise the full-batch result."""
+        maxima = self.engine.general_prepare(x_local)
+        multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
+        if multi:
+            dist.all_reduce(maxima, op=dist.ReduceOp.MAX, group=self.group)
+        err = None
+        if self.engine.mse:
+            err_in = None
+            if multi:
+                world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+                if rank > 0:
+                    err_in = torch.empty((maxima.numel(), 101), dtype=torch.float64, device=x_local.device)
+                    dist.recv(err_in, src=_global_rank(self.group, rank - 1), group=self.group)
+                err = self.engine.general_mse(x_local, err_in)
+                if rank < world - 1:
+                    dist.send(err, dst=_global_rank(self.group, rank + 1), group=self.group)
+                dist.broadcast(err, src=_global_rank(self.group, world - 1), group=self.group)
+            else:
+                err = self.engine.general_mse(x_local, None)
+        self.engine.general_conv(x_local, err, **outs)
+        return maxima
 
     @staticmethod
     def gather_to_rank0(t_local, batch: int, group=None):

@@ -350,6 +350,29 @@ class SfcLayer:
         check(lib().sfc_conv_forward_f64(self._h, _ptr(x), n, h, w, pad, _ptr(ws), ws.numel(), ctypes.byref(o),
                                          ctypes.c_void_p(_stream_ptr(stream))))
 
+    # -- the general QuantConfig on a batch shard (sfc_general_*: see include/sfc_b200.h)
+    def general_prepare(self, x: torch.Tensor, ws: torch.Tensor, pad: int, stream=None) -> torch.Tensor:
+        """absmax keeps V; returns this shard's activation maxima (int64 view of the fp64 bit
+        patterns in the workspace: an all-reduce(MAX) over ranks is the exact global max)."""
+        n, c, h, w = x.shape
+        if c != self.IC:
+            raise ValueError("input channel count does not match filters")
+        ptr, cnt = ctypes.c_void_p(), ctypes.c_int()
+        check(lib().sfc_general_prepare(self._h, _ptr(x), n, h, w, pad, _ptr(ws), ws.numel(), ctypes.byref(ptr),
+                                        ctypes.byref(cnt), ctypes.c_void_p(_stream_ptr(stream))))
+        return _wrap_device(ptr.value, (cnt.value,), torch.int64, self.device)
+
+    def general_mse_partial(self, n, h, w, pad, ws, err_in, err_out, stream=None):
+        """MseGrid sums [groups, 101] (fp64) continued over this shard from err_in (None: batch start)."""
+        check(lib().sfc_general_mse_partial(self._h, n, h, w, pad, _ptr(ws), _ptr(err_in), _ptr(err_out),
+                                            ctypes.c_void_p(_stream_ptr(stream))))
+
+    def general_conv(self, n, h, w, pad, ws, err=None, out_f32=None, out_f64=None, out_i8=None,
+                     requant_scale: float = 0.0, stream=None):
+        o = Outputs(None, None, _ptr(out_f32), _ptr(out_f64), _ptr(out_i8), float(requant_scale))
+        check(lib().sfc_general_conv(self._h, n, h, w, pad, _ptr(ws), ws.numel(), _ptr(err), ctypes.byref(o),
+                                     ctypes.c_void_p(_stream_ptr(stream))))
+
     def stats(self, n, h, w, pad, ws, stream=None) -> dict:
         s = np.zeros(6, np.int64)
         check(lib().sfc_conv_stats(self._h, n, h, w, pad, _ptr(ws), s.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
@@ -380,7 +403,7 @@ def _wrap_device(ptr: int, shape, dtype, device) -> torch.Tensor:
 
     class _Arr:
         __cuda_array_interface__ = {
-            "shape": (n,), "typestr": {1: "|i1", 4: "<i4"}[itemsize], "data": (ptr, False), "version": 3,
+            "shape": (n,), "typestr": {1: "|i1", 4: "<i4", 8: "<i8"}[itemsize], "data": (ptr, False), "version": 3,
             "strides": None,
         }
 

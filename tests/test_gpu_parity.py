@@ -483,6 +483,55 @@ def test_chunked_p_matches_whole(cuda, variant, budget_mb, monkeypatch):
     assert np.array_equal(chunked[0].numpy(), r["y_int"])
 
 
+GENERAL_SHARD_CFGS = [(8, 1, 0, 0), (8, 0, 2, 1), (6, 1, 1, 1), (12, 1, 2, 1), (8, 0, 1, 0)]
+
+
+@pytest.mark.parametrize("variant", ["sfc6-6x6-3x3", "sfc4-4x4-3x3", "sfc6-6x6-5x5"])
+@pytest.mark.parametrize("cfg", GENERAL_SHARD_CFGS, ids=[f"b{c[0]}a{c[1]}f{c[2]}s{c[3]}" for c in GENERAL_SHARD_CFGS])
+def test_general_quantconfig_shard_protocol(cuda, variant, cfg):
+    """The multi-GPU steps of a non-default QuantConfig (sfc_general_prepare / _mse_partial /
+    _conv, distributed.CudaEngine) run shard by shard on one device, exactly as the ranks run
+    them: maxima max-reduced, MseGrid sums chained in batch order.  Output, scales and counts
+    equal the whole-batch forward bit for bit."""
+    from paper_2407_02913_b200.distributed import CudaEngine, shard_bounds
+    bits, asc, fsc, srch = cfg
+    R = sc.catalog_algorithm(variant).R
+    rng = np.random.default_rng(sum(cfg) + R)
+    B, C, OC, H = 5, 6, 7, 12
+    x = rng.integers(-128, 128, size=(B, C, H, H), dtype=np.int8)
+    x[3:] //= 4
+    w = rng.integers(-127, 128, size=(OC, C, R, R), dtype=np.int8)
+    pad = R // 2
+    xt = torch.from_numpy(x).cuda()
+    layer = sc.SfcLayer(variant, torch.from_numpy(w).cuda(), bits, fsc, srch, act_scope=asc)
+    ws = layer.workspace(B, H, H, pad)
+    full = torch.empty((B, OC, H, H), dtype=torch.float64, device="cuda")
+    layer.forward(xt, ws, pad, out_f64=full)
+    full_scales = layer.act_scales(B, H, H, pad, ws)
+    full_stats = layer.stats(B, H, H, pad, ws)
+    world = 3
+    engines = [CudaEngine(layer, pad) for _ in range(world)]
+    shards = [xt[lo:hi] for lo, hi in (shard_bounds(B, r, world) for r in range(world))]
+    maxima = [e.general_prepare(xs) for e, xs in zip(engines, shards)]
+    glob = torch.stack(maxima).max(0).values  # the all-reduce(MAX)
+    for m in maxima:
+        m.copy_(glob)
+    err = None
+    if srch:
+        for e, xs in zip(engines, shards):  # rank order = batch order
+            err = e.general_mse(xs, err)
+    outs, sat = [], 0
+    for e, xs in zip(engines, shards):
+        o = torch.empty((xs.shape[0], OC, H, H), dtype=torch.float64, device="cuda")
+        e.general_conv(xs, err, out_f64=o)
+        outs.append(o)
+        n = xs.shape[0]
+        assert np.array_equal(layer.act_scales(n, H, H, pad, e._workspace(xs)), full_scales)
+        sat += layer.stats(n, H, H, pad, e._workspace(xs))["saturations"]
+    assert torch.equal(torch.cat(outs), full)
+    assert sat == full_stats["saturations"]
+
+
 # ------------------------------------------------------------------------------ 5x5 / 7x7 variants
 GOLD_R = np.load(os.path.join(HERE, "golden", "qconv_large_r.npz"))
 TAGS_R = sorted({k.split("/")[0] for k in GOLD_R.files})
