@@ -21,6 +21,8 @@ VARIANTS = ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]
 
 
 def stage_of(name):
+    if "k_act_pair<" in name:  # the two-channel SWAR form (large layers)
+        return "absmax" if re.search(r"k_act_pair<\d+, 0>", name) else "act_quant"
     if "k_act<" in name:
         return "absmax" if re.search(r"k_act<\d+, 0,", name) else "act_quant"
     for key, st in (("k_quant_kept", "quantize"), ("k_gemm", "gemm"), ("k_output", "output"),
