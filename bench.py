@@ -315,9 +315,9 @@ def run_b200(args, rank, world, local_rank):
     ms = float(t.item())
     step_ops = sum(wl.direct_equivalent_ops(c["L"]) for c in calls) * world
     value = step_ops / (ms / 1e3) / 1e12
-    # N=1: workspace reset, absmax (+V kept), quantize, gemm, output; N>1: the reset is a torch
-    # zero_() of vmax, not one of ours
-    launches_per_step = (5 if world == 1 else 4) * len(calls)
+    # N=1: workspace reset, absmax (+V kept), gemm (quantizing the kept V), output; N>1: the
+    # reset is a torch zero_() of vmax, not one of ours
+    launches_per_step = (4 if world == 1 else 3) * len(calls)
 
     # ---- end to end through the public API: pinned host input -> device -> outputs -> pinned host
     def e2e_step():
@@ -348,7 +348,9 @@ def run_b200(args, rank, world, local_rank):
     e2e_value = step_ops / (float(t.item()) / 1e3) / 1e12
 
     # ---- per-kernel live timing (same stream, CUDA events between the stage launches)
-    stage_names = ["absmax", "sat_reset", "quantize", "gemm", "output"]
+    # the forward's stages: absmax (V kept), the saturation reset, the GEMM that quantizes the
+    # kept V (TMA-staged) in its converter warps, the output transform
+    stage_names = ["absmax", "sat_reset", "gemm", "output"]
     stage_ms = {n: 0.0 for n in stage_names}
     per_call_stage = []
     L_ = lib()
@@ -358,7 +360,7 @@ def run_b200(args, rank, world, local_rank):
         acc = {n: 0.0 for n in stage_names}
         for _ in range(reps):
             flush.zero_()
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
             x, ws, pad = c["x"], c["ws"], c["L"].pad
             n, _, h, w_ = x.shape
             o = sc.Outputs(*(sc._ptr(c["outs"].get(k)) for k in ("y_int32", "y_int64", "out_f32", "out_f64", "out_i8")),
@@ -367,12 +369,12 @@ def run_b200(args, rank, world, local_rank):
             e[0].record(stream)
             c["layer"].transform(x, c["vmax"], ws, pad)  # absmax + V kept (as in forward)
             e[1].record(stream)
-            for si, mask in enumerate((1, 2 | 16, 4, 8)):  # 16: quantize the kept V
+            for si, mask in enumerate((1, 4 | 16, 8 | 16)):  # 16: the kept-V path (as in forward)
                 sc.check(L_.sfc_conv_int8_stages(c["layer"]._h, sc._ptr(x), n, h, w_, pad, sc._ptr(c["vmax"]),
                                                  sc._ptr(ws), ws.numel(), ctypes.byref(o), mask,
                                                  ctypes.c_void_p(stream.cuda_stream)))
                 e[2 + si].record(stream)
-            e[5].synchronize()
+            e[4].synchronize()
             for si, nme in enumerate(stage_names):
                 acc[nme] += e[si].elapsed_time(e[si + 1]) / reps
         per_call_stage.append(acc)
@@ -395,9 +397,9 @@ def run_b200(args, rank, world, local_rank):
                 alg_bytes += xb + 2 * F * T * L.cin  # read x, keep int16 V
             elif dom == "quantize":
                 alg_bytes += 3 * F * T * L.cin  # read int16 V, write int8 vq
-            elif dom == "gemm":
+            elif dom == "gemm":  # reads the kept int16 V and uq, writes P
                 alg_ops += 2 * F * T * L.cin * L.cout
-                alg_bytes += F * T * L.cin + F * L.cin * L.cout + 4 * F * T * L.cout
+                alg_bytes += 2 * F * T * L.cin + F * L.cin * L.cout + 4 * F * T * L.cout
             elif dom == "output":
                 alg_bytes += 4 * F * T * L.cout + outb
             else:

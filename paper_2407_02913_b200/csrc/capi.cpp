@@ -223,14 +223,14 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
         ck(cudaMemsetAsync(v.sat, 0, sizeof(unsigned long long), st), "memset sat");
         pdl = false;
     }
-    // Kept V is quantized inside the GEMM by converter warps (one launch and the vq round trip
-    // disappear) unless V is large and every A tile would be converted for several oc blocks:
-    // then the converters' DRAM-latency-bound V reads lose to the streaming quantizer (vq
-    // through HBM).  Measured: configs 1-4 faster fused, config 5 (V 236 MB, 2 oc blocks) not.
-    // SFC_QFUSE=0/1 forces either.
-    // (one oc block: every A tile is converted once; several: only if V is L2-sized)
-    bool qfuse = kept && (g.OCpad == g.BN || size_t(L->F) * g.Tpad * g.Cpad * 2 <= (size_t(64) << 20));
-    if (const char* q = std::getenv("SFC_QFUSE")) qfuse = kept && q[0] == '1';
+    // Kept V is quantized inside the GEMM by converter warps (the quantize launch and the vq
+    // round trip disappear).  Default: the producer TMA-loads each stage's V tile into shared
+    // memory next to A and B and the converters read it there (measured fastest on every
+    // BASELINE config: config 2 0.067 ms, config 5 0.382 vs 0.407 streaming, ResNet-18 1.106
+    // vs 1.187, VGG-16 15.38 vs 15.79).  SFC_QFUSE=0: streaming quantizer (vq through HBM);
+    // 1: converters loading V through registers; 2: the default.
+    bool qfuse = kept, qtma = kept;
+    if (const char* q = std::getenv("SFC_QFUSE")) qfuse = kept && (q[0] == '1' || q[0] == '2'), qtma = q[0] == '2';
     const bool chunked = p_chunk(g, L->F).n > 1;
     qfuse = qfuse && !chunked;  // the converter GEMM covers the whole tile range
     if (mask & SFC_STAGE_ACT) {
@@ -245,8 +245,9 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     const OutPtrs op{o->y_int32, o->y_int64, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
     if (qfuse) {
         if (mask & SFC_STAGE_GEMM) {
-            ck(launch_gemm_qfused(QFuse{v.vkeep, d_vmax, qparams_table(false), v.qp, v.sat, L->bits}, L->d_uq, v.P, g,
-                                  L->F, st, pdl),
+            const QFuse qf{v.vkeep, d_vmax, qparams_table(false), v.qp, v.sat, L->bits};
+            ck(qtma ? launch_gemm_qtma(qf, L->d_uq, v.P, g, L->F, st, pdl)
+                    : launch_gemm_qfused(qf, L->d_uq, v.P, g, L->F, st, pdl),
                "fused quantize + gemm launch");
             pdl = full_pdl;
         }

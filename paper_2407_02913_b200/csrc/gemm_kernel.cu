@@ -54,26 +54,34 @@ __device__ __forceinline__ QuantParams qparams_warp(int vmax, int bits, const Qu
 
 // QF = false: A = vq [F][Tpad][Cpad] int8 via TMA.  QF = true: A is produced by kConvWarps
 // converter warps from the kept int16 V: each thread owns 16-channel chunks of A rows,
-// loads them (2 x 16 B) before waiting for the stage to be free, quantizes, and stores the
-// 16 bytes at the chunk's swizzled position (128B swizzle: chunk j of row r at j ^ (r & 7);
-// 64B swizzle: j ^ ((r >> 1) & 3)), i.e. exactly the layout the TMA load would produce.
-template <int BN, int BK, int STAGES, bool QF>
+// quantizes them and stores the 16 bytes at the chunk's swizzled position (128B swizzle:
+// chunk j of row r at j ^ (r & 7); 64B swizzle: j ^ ((r >> 1) & 3)), i.e. exactly the
+// layout the TMA load would produce.  QT = false: the converters load their chunks from
+// global memory into registers (double-buffered); QT = true: the producer TMA-loads the
+// stage's V tile (128 rows x BK channels of int16, rows >= T and channels >= C zero-filled
+// by the tensor map) into a shared V stage next to A and B, and the converters read it
+// from there -- far more bytes in flight per SM than register staging allows.
+template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmP, int n_tb, int n_ob, int F, int nk, ConvGeom g, QFuse qf) {
+    static_assert(!QT || QF, "the TMA-staged V feeds the converters");
     constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
+    constexpr uint32_t kVStageBytes = kRowsPerTile * BK * 2;
     constexpr int kHalf = BN / 2;                     // columns per epilogue warp (two warps per lane quarter)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = sA + STAGES * kRowsPerTile * BK;
-    uint8_t* sE = sB + STAGES * BN * BK;              // [8 warps][kEpiBufs][32 rows x 128 B], 128B-swizzled
+    uint8_t* sV = sB + STAGES * BN * BK;              // QT: [STAGES][128 rows][BK] int16
+    uint8_t* sE = sV + (QT ? STAGES * kVStageBytes : 0);  // [8 warps][kEpiBufs][32 rows x 128 B], 128B-swizzled
     uint64_t* full = reinterpret_cast<uint64_t*>(sE + kEpiWarps * kEpiBufs * kEpiBoxBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* vfull = tempty + 2;                     // QT: V stage landed
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(vfull + (QT ? STAGES : 0));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int units = F * n_tb * n_ob;
@@ -88,10 +96,12 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], kEpiWarps);
         }
+        if (QT)
+            for (int s2 = 0; s2 < STAGES; ++s2) ptx::mbar_init(&vfull[s2], 1);
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        if (!QF) ptx::tma_prefetch(&tmA);
+        if (!QF || QT) ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB);
         ptx::tma_prefetch(&tmP);
     }
@@ -105,7 +115,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     if (warp == 0) {
         if (lane == 0) {
             // QF: B (the layer's filters) does not depend on the predecessor; the converters wait.
-            if (!QF) griddep_wait();  // vq written by the activation kernel
+            if (!QF || QT) griddep_wait();  // vq / V written by the activation kernel
             tl_mark(kTlGemm, 1);
             int stage = 0;
             uint32_t phase = 0;
@@ -115,6 +125,11 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (QF) {
                         ptx::mbar_expect_tx(&full[stage], uint32_t(BN * BK));
+                        if (QT) {
+                            ptx::mbar_expect_tx(&vfull[stage], kVStageBytes);
+                            ptx::tma_load_3d(sV + stage * kVStageBytes, &tmA, &vfull[stage], kc * BK,
+                                             tb * kRowsPerTile, f);
+                        }
                     } else {
                         ptx::mbar_expect_tx(&full[stage], kStageBytes);
                         ptx::tma_load_3d(sA + stage * kRowsPerTile * BK, &tmA, &full[stage], kc * BK, tb * kRowsPerTile, f);
@@ -187,6 +202,52 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             if (lane == 0) ptx::mbar_arrive(&tempty[ab]);
         }
         if (lane == 0) bulk_wait_all();
+    } else if (QF && QT) {
+        // Converters over the TMA-staged V: thread ct owns items i = ct + j * (32 * kConvWarps)
+        // of the stage's kRowsPerTile x (BK / 16) chunk grid; 32 B of V in, 16 B of A out.
+        constexpr int kCh = BK / 16, kItems = kRowsPerTile * kCh / (32 * kConvWarps);
+        const int ct = threadIdx.x - 32 * (2 + kEpiWarps);
+        griddep_wait();  // vmax comes from the activation pass
+        const QuantParams qp = qparams_warp(*qf.vmax, qf.bits, qf.qtab);
+        if (blockIdx.x == 0 && ct == 0) *qf.qp_out = qp;
+        const int npairs = ((units - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x)) * nk;
+        auto run = [&](auto quant) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int s2 = 0; s2 < npairs; ++s2) {
+                ptx::mbar_wait(&vfull[stage], phase);  // (the producer waited for the stage to be free)
+                const uint8_t* v_st = sV + stage * kVStageBytes;
+                uint8_t* a_st = sA + stage * kRowsPerTile * BK;
+#pragma unroll
+                for (int j = 0; j < kItems; ++j) {
+                    const int i = ct + j * (32 * kConvWarps);
+                    const int r = i / kCh, qc = i % kCh;
+                    const uint4* src = reinterpret_cast<const uint4*>(v_st + r * (BK * 2) + qc * 32);
+                    const uint4 a = src[0], b = src[1];
+                    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
+                        o[e >> 2] |= uint32_t(uint8_t(int8_t(quant(v)))) << (8 * (e & 3));
+                    }
+                    const int sw = BK == 128 ? (qc ^ (r & 7)) : (qc ^ ((r >> 1) & 3));
+                    *reinterpret_cast<uint4*>(a_st + r * BK + (sw << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+                }
+                fence_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full[stage]);
+                if (++stage == STAGES) stage = 0, phase ^= 1;
+            }
+        };
+        if (qp.exact) {
+            const int mul = int(qp.mul);
+            const long long half = 1ll << (qp.shift - 1);
+            const int shift = qp.shift;
+            run([=](int v) { return quant_fast(v, mul, half, shift); });
+        } else {  // (zero-filled padding quantizes to 0: no saturations from it)
+            run([&](int v) { return clamp_q(exact_q(v, qp.sa), qp.qmax, qf.sat); });
+        }
     } else if (QF) {
         // Converters: thread ct owns items i = ct + j * (32 * kConvWarps) of a stage's
         // kRowsPerTile x (BK / 16) chunk grid (row r = i / (BK / 16), chunk q = i % (BK / 16)).
@@ -306,11 +367,12 @@ int sm_count() {
     return n;
 }
 
-template <int BN, int BK, int STAGES, bool QF>
+template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const ConvGeom& g, int F,
                         const QFuse& qf, cudaStream_t st, bool pdl) {
-    const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256;
-    auto kern = k_gemm<BN, BK, STAGES, QF>;
+    const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + (QT ? size_t(STAGES) * kRowsPerTile * BK * 2 : 0) +
+                        size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256;
+    auto kern = k_gemm<BN, BK, STAGES, QF, QT>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -398,6 +460,35 @@ cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, c
 cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
                                bool pdl) {
     return gemm_dispatch<true>(nullptr, uqB, P, g, F, q, st, pdl);
+}
+
+cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
+                             bool pdl) {
+    // V [F][Tpad][Cpad] int16 seen as (C, T, F): channels >= C and rows >= T read as zero
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorInvalidValue;
+    CUtensorMap tv, tb, tp;
+    cuuint64_t dims[3] = {cuuint64_t(g.C), cuuint64_t(g.T), cuuint64_t(F)};
+    cuuint64_t strides[2] = {cuuint64_t(g.Cpad) * 2, cuuint64_t(g.Cpad) * g.Tpad * 2};
+    cuuint32_t box[3] = {cuuint32_t(g.BK), cuuint32_t(kRowsPerTile), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (fn(&tv, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<int16_t*>(q.v), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    if (!make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
+        !make_tmap_3d(&tp, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, g.Tpad, F, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+    // two stages: A + B + V stages and the epilogue boxes fill the 227 KB at BN = 256, BK = 128
+    if (g.BK == 128) {
+        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
+        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
+        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
+    }
+    if (g.BN == 64) return gemm_launch<64, 64, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
+    if (g.BN == 128) return gemm_launch<128, 64, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
+    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
 }
 
 SFC_TL_UNIT_READER(tl_read_gemm)

@@ -86,6 +86,9 @@ struct QFuse {
 };
 cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
                                bool pdl);
+// The same with the V tiles TMA-staged in shared memory (SFC_QFUSE=2).
+cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
+                             bool pdl);
 
 // Timeline stamps of the debug build ([8][3] per unit; cudaErrorNotSupported otherwise).
 cudaError_t tl_read_act(unsigned long long* out, bool reset);

@@ -414,11 +414,13 @@ def test_kept_and_recompute_paths_agree(cuda, variant, monkeypatch):
         layer = sc.SfcLayer(variant, w)
         ho = L.hw + 2 * L.pad - L.r + 1
         res = {}
-        for mode in ("forward", "kept", "kept-qfused", "recompute"):
+        for mode in ("forward", "kept", "kept-qfused", "kept-qtma", "recompute"):
             ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
             y = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int64, device="cuda")
             if mode == "kept-qfused":
                 monkeypatch.setenv("SFC_QFUSE", "1")
+            elif mode == "kept-qtma":
+                monkeypatch.setenv("SFC_QFUSE", "2")
             elif mode == "kept":
                 monkeypatch.setenv("SFC_QFUSE", "0")  # streaming quantizer materialises vq
             else:
