@@ -678,6 +678,8 @@ cudaError_t act_pair_launch(const int8_t* x, const ConvGeom& g, int* vmax, const
 template <int V, int MODE>
 cudaError_t act_launch(const int8_t* x, const ConvGeom& g, int* vmax, const int* vmax_in, int bits, QuantParams* qp,
                        int8_t* vqA, unsigned long long* sat, int16_t* vkeep, cudaStream_t st, bool pdl) {
+    if (act_reg_wanted(V, g))
+        return launch_act_reg(V, MODE, x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, st, pdl);
     if constexpr (V <= 2) {
         // the SWAR kernel has one thread per (tile, channel pair): it needs >= 32k of them to
         // fill the GPU (measured: config 5 absmax 0.121 -> 0.091 ms, ResNet-18 layers 0.435 ->

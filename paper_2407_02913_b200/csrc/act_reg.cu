@@ -1,0 +1,367 @@
+// Register-resident activation transform for the 3x3 SFC variants (sfc4-4x4, sfc6-6x6,
+// sfc6-7x7): V = B^T x B per (tile, channel) (gather_tiles, proj/src/quant.cpp:44-93), the
+// PerTensor max|V| (quant.cpp:168-172) and the exact activation quantizer
+// (quant.cpp:242-250).
+//
+// One CTA per (image, tile row, block of 2*PPW channels) covers the WHOLE tile row, so each
+// channel's window rows are one contiguous byte band of NCHW: it is staged raw, 16 bytes per
+// load (ld.global.nc.v4 of the 16-byte aligned chunks covering the band), into one shared
+// plane per channel (odd word stride; even channels first so lanes stepping channel pairs
+// hit distinct banks).  One thread then owns one tile and one channel pair (c, c+1) and
+// builds its window in the two-lane SWAR form P = x_c + 2^16 x_{c+1} straight from the raw
+// planes (three 32-bit shared loads + two funnel shifts per window row and channel, a byte
+// mask for the zero padding of quant.cpp:66-75, two byte permutes and an add per sample
+// pair).  The transforms are integer-linear and every intermediate stays in (-2^15, 2^15)
+// (|V| <= 4608), so one 32-bit add serves both channels.  The tile stays in registers: row
+// transforms into n x K values, column transforms into V, each value consumed where formed:
+//   MODE 0  max|V| only (unsigned 16x2 max/min of the biased words)
+//   MODE 2  max|V| and the kept V (int16x2 words, V[f][t][c])
+//   MODE 1  vq = q(V) with the verified quantizer of *vmax_in (two int8 per 16-bit store)
+// Lane = channel pair (PPW pairs per warp); the rest of the lane index and the warp index
+// select the tile column, so wide rows and narrow layers keep <= 10 warps per CTA.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "common.cuh"
+#include "sfc_kernels.hpp"
+#include "sfc_tables.cuh"
+#include "transforms.cuh"
+
+namespace sfcb200 {
+
+namespace {
+
+constexpr int kRowMaxWarps = 10;  // CTA size bound: 320 threads
+
+// Sign-extended byte q of w, and the same byte sign-extended into the upper half-word.
+// (prmt default mode: selector bit 3 replicates the sign of the selected byte)
+template <uint32_t sel>
+__device__ __forceinline__ int prmt0(uint32_t w) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(d) : "r"(w), "n"(sel));
+    return int(d);
+}
+template <int q>
+__device__ __forceinline__ int sx_lo(uint32_t w) {
+    return prmt0<q | ((q | 8) << 4) | ((q | 8) << 8) | ((q | 8) << 12)>(w);
+}
+template <int q>
+__device__ __forceinline__ int sx_hi(uint32_t w) {
+    return prmt0<4 | (4 << 4) | (q << 8) | ((q | 8) << 12)>(w);
+}
+
+// The reference quantizer with clamping (the rare case without a verified multiply-shift):
+// out of line, so the unrolled column loop stays small.
+__device__ __noinline__ int quant_slow(int v, double sa, int qmax, unsigned long long* sat) {
+    return clamp_q(exact_q(v, sa), qmax, sat);
+}
+
+}  // namespace
+
+// Shared words per channel plane: a 4-word guard (window columns left of the band), the band
+// (<= 15 bytes of chunk misalignment + n image rows) and a tail guard, rounded to odd.
+template <int V>
+__host__ __device__ inline int row_plane_words(int W) {
+    const int w = 4 + (48 + Tab<V>::n * W + 3) / 4;
+    return w | 1;
+}
+
+template <int V, int MODE, int PPW>
+__global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __restrict__ x, ConvGeom g, int plw,
+                                                              int* __restrict__ vmax, int16_t* __restrict__ vkeep,
+                                                              const int* __restrict__ vmax_in, int bits,
+                                                              QuantParams* __restrict__ qp_out,
+                                                              int8_t* __restrict__ vqA,
+                                                              unsigned long long* __restrict__ sat,
+                                                              const QuantParams* __restrict__ qtab) {
+    using T = Tab<V>;
+    constexpr int n = T::n, K = T::K, M = T::M, TPW = 32 / PPW, NCH = 2 * PPW;
+    constexpr int kTl = MODE == 1 ? kTlQuant : kTlAbsmax;
+    extern __shared__ __align__(16) uint32_t s_raw[];
+    tl_mark(kTl, 0);
+    if (MODE != 1) griddep_launch_dependents();
+
+    const int ti = blockIdx.x, b = blockIdx.y, c0 = blockIdx.z * NCH;
+    const int ih0 = ti * M - g.pad;
+    const int r_lo = max(ih0, 0), nr = min(ih0 + n, g.H) - r_lo;
+    const size_t HW = size_t(g.H) * g.W;
+    const int8_t* xb = x + (size_t(b) * g.C + c0) * HW + size_t(r_lo) * g.W;  // band of channel c0
+    const uintptr_t xlo = reinterpret_cast<uintptr_t>(x), xhi = xlo + size_t(g.B) * g.C * HW;
+    const int band = nr * g.W;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    auto plane = [&](int ch) { return ((ch & 1) * PPW + (ch >> 1)) * plw + 4; };
+
+    // ---- stage: per channel, the 16-byte chunks covering its band; lanes = chunks of a
+    // channel (LPC lanes per channel, a power of two >= the chunk count, capped at 32)
+    {
+        const int cq = (15 + band + 15) >> 4;  // chunk bound over every misalignment
+        int lg = 0;
+        while ((1 << lg) < cq && lg < 5) ++lg;
+        const int lpc = 1 << lg, cpw = 32 >> lg;  // lanes per channel, channels per warp pass
+        const int qq = (cq + lpc - 1) >> lg;        // chunk passes per channel
+        const int items = ((NCH + nwarps * cpw - 1) / (nwarps * cpw)) * qq;  // (channel pass, chunk pass)
+        constexpr int kB = 8;                       // loads in flight per thread
+        for (int j0 = 0; j0 < items; j0 += kB) {
+            uint4 v[kB];
+            uint32_t* d[kB];
+#pragma unroll
+            for (int jj = 0; jj < kB; ++jj) {
+                const int j = j0 + jj, jc = j / qq, jq = j - jc * qq;
+                const int ch = (wid + jc * nwarps) * cpw + (lane >> lg);
+                const int q = (lane & (lpc - 1)) + jq * lpc;
+                d[jj] = nullptr;
+                v[jj] = make_uint4(0, 0, 0, 0);
+                if (j >= items || ch >= NCH || c0 + ch >= g.C) continue;
+                const uintptr_t start = reinterpret_cast<uintptr_t>(xb + size_t(ch) * HW);
+                const uintptr_t a16 = start & ~uintptr_t(15);
+                if (q >= int((start - a16 + band + 15) >> 4)) continue;
+                const uintptr_t ad = a16 + 16 * uintptr_t(q);
+                d[jj] = s_raw + plane(ch) + 4 * q;
+                if (ad >= xlo && ad + 16 <= xhi) {
+                    v[jj] = __ldg(reinterpret_cast<const uint4*>(ad));
+                } else {  // the chunk straddles an end of x: only its bytes inside x
+                    uint32_t w[4] = {0, 0, 0, 0};
+                    for (int e = 0; e < 16; ++e)
+                        if (ad + e >= xlo && ad + e < xhi)
+                            w[e >> 2] |= uint32_t(*reinterpret_cast<const uint8_t*>(ad + e)) << (8 * (e & 3));
+                    v[jj] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < kB; ++jj)
+                if (d[jj]) d[jj][0] = v[jj].x, d[jj][1] = v[jj].y, d[jj][2] = v[jj].z, d[jj][3] = v[jj].w;
+        }
+    }
+    __syncthreads();
+
+    const int p = lane % PPW, tj = wid * TPW + lane / PPW;
+    const int c = c0 + 2 * p;
+    const bool active = tj < g.tw && c < g.C;
+    const int t = (b * g.th + ti) * g.tw + tj;
+
+    // ---- the window from the raw planes, SWAR-paired, zero padding by byte masks; then the
+    // vertical pass y[k][s] = sum_r BT[k][r] x[r][s] (the horizontal pass below then forms
+    // V[k][0..K) in frequency order f = k*K + l, so stores walk f with one pointer stride)
+    int y[K][n];
+    if (active) {
+        int xw[n][n];
+        const int wc0 = tj * M - g.pad;  // image column of window column 0
+        uint32_t mk[3] = {0, 0, 0};      // byte s of the window valid <=> 0 <= wc0 + s < W
+#pragma unroll
+        for (int s = 0; s < n; ++s)
+            if (unsigned(wc0 + s) < unsigned(g.W)) mk[s >> 2] |= 0xffu << (8 * (s & 3));
+        const bool ok1 = c + 1 < g.C;
+        const uint32_t* pe = s_raw + plane(2 * p);
+        const uint32_t* po = s_raw + plane(2 * p + 1);
+        const int me = int(reinterpret_cast<uintptr_t>(xb + size_t(2 * p) * HW) & 15) + wc0;
+        const int mo = int(reinterpret_cast<uintptr_t>(xb + size_t(2 * p + 1) * HW) & 15) + wc0;
+        constexpr int NW4 = (n + 3) / 4;  // window words per row
+#pragma unroll
+        for (int r = 0; r < n; ++r) {
+            const int ir = ih0 + r - r_lo;  // row within the band
+            uint32_t we[NW4], wo[NW4];
+            if (ir >= 0 && ir < nr) {  // CTA-uniform
+                auto row = [&](const uint32_t* pl, int off, uint32_t (&o)[NW4]) {
+                    const int wi = off >> 2, sh = (off & 3) * 8;
+                    uint32_t src[NW4 + 1];
+#pragma unroll
+                    for (int j = 0; j <= NW4; ++j) src[j] = pl[wi + j];
+#pragma unroll
+                    for (int j = 0; j < NW4; ++j) o[j] = __funnelshift_r(src[j], src[j + 1], sh) & mk[j];
+                };
+                row(pe, me + ir * g.W, we);
+                row(po, mo + ir * g.W, wo);
+                if (!ok1) {
+#pragma unroll
+                    for (int j = 0; j < NW4; ++j) wo[j] = 0;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < NW4; ++j) we[j] = wo[j] = 0;
+            }
+#pragma unroll
+            for (int s = 0; s < n; ++s) {
+                switch (s & 3) {
+                    case 0: xw[r][s] = sx_lo<0>(we[s >> 2]) + sx_hi<0>(wo[s >> 2]); break;
+                    case 1: xw[r][s] = sx_lo<1>(we[s >> 2]) + sx_hi<1>(wo[s >> 2]); break;
+                    case 2: xw[r][s] = sx_lo<2>(we[s >> 2]) + sx_hi<2>(wo[s >> 2]); break;
+                    default: xw[r][s] = sx_lo<3>(we[s >> 2]) + sx_hi<3>(wo[s >> 2]); break;
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < n; ++s) {
+            int col[n], yk[K];
+#pragma unroll
+            for (int r = 0; r < n; ++r) col[r] = xw[r][s];
+            fwd1d<V>(col, yk);
+#pragma unroll
+            for (int k = 0; k < K; ++k) y[k][s] = yk[k];
+        }
+    }
+
+    if constexpr (MODE == 1) {
+        griddep_wait();  // the absmax pre-pass (and any multi-GPU MAX exchange) is complete
+        tl_mark(kTl, 1);
+        const QuantParams qp = qparams_for(*vmax_in, bits, qtab);  // (block-uniform call)
+        if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *qp_out = qp;
+        griddep_launch_dependents();
+        if (!active) return;
+        // ---- columns, quantized: vq[f][t][c, c+1], one 16-bit store per pair
+        const size_t fstride = size_t(g.Tpad) * g.Cpad / 2;  // 16-bit units between frequency planes
+        int16_t* vq = reinterpret_cast<int16_t*>(vqA + size_t(t) * g.Cpad + c);
+        // qlo(lo), qhi(v - lo): the high lane is quantized as hi * 2^16 (same quotient with the
+        // multiplier's shift and rounding term scaled by 2^16), saving its unpack
+        auto rows = [&](auto qlo, auto qhi) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                int v[K];
+                fwd1d<V>(y[k], v);
+#pragma unroll
+                for (int l = 0; l < K; ++l) {
+                    const int lo = int(int16_t(v[l]));
+                    *vq = int16_t((qlo(lo) & 0xff) | (qhi(v[l] - lo) << 8));
+                    vq += fstride;  // f = k * K + l: next frequency plane
+                }
+            }
+        };
+        if (qp.exact) {  // uniform over the grid: no per-value branch
+            const int mul = int(qp.mul);
+            const long long half = 1ll << (qp.shift - 1), half16 = half << 16;
+            const int shift = qp.shift, shift16 = qp.shift + 16;
+            rows([=](int v) { return quant_fast(v, mul, half, shift); },
+                 [=](int v) { return quant_fast(v, mul, half16, shift16); });
+        } else {
+            const double sa = qp.sa;
+            const int qmax = qp.qmax;
+            rows([=](int v) { return quant_slow(v, sa, qmax, sat); },
+                 [=](int v) { return quant_slow(v >> 16, sa, qmax, sat); });
+        }
+        tl_mark(kTl, 2);
+    } else {
+        // ---- horizontal pass: V[k][l] = sum_s BT[l][s] y[k][s]; max/min over the int16x2 words,
+        // biased (+2^15 per lane) so unsigned 16x2 max/min order both lanes
+        uint32_t mx = 0u, mn = 0xffffffffu;
+        if (active) {
+            const size_t fstride = size_t(g.Tpad) * g.Cpad / 2;  // words between frequency planes
+            int* vk = MODE == 2 ? reinterpret_cast<int*>(vkeep + size_t(t) * g.Cpad + c) : nullptr;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                int v[K];
+                fwd1d<V>(y[k], v);
+#pragma unroll
+                for (int l = 0; l < K; ++l) {
+                    const uint32_t u = uint32_t(v[l]) + 0x80008000u;  // lane j -> V_j + 2^15 (mod 2^16)
+                    mx = __vmaxu2(mx, u);
+                    mn = __vminu2(mn, u);
+                    if constexpr (MODE == 2) {
+                        *vk = int(u ^ 0x80008000u);
+                        vk += fstride;  // f = k * K + l
+                    }
+                }
+            }
+        }
+        int local = 0;
+        if (active) {
+            const int hi_max = int(mx >> 16) - 0x8000, lo_max = int(mx & 0xffff) - 0x8000;
+            const int hi_min = int(mn >> 16) - 0x8000, lo_min = int(mn & 0xffff) - 0x8000;
+            local = max(max(hi_max, lo_max), -min(hi_min, lo_min));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+        griddep_wait();  // under PDL: *vmax has been zeroed by the predecessor
+        tl_mark(kTl, 1);
+        if (lane == 0 && local > 0) atomicMax(vmax, local);
+        tl_mark(kTl, 2);
+    }
+}
+
+// ============================================================================ host
+namespace {
+// Pairs per warp: the largest of 32, 16, ... that is <= the layer's pairs (rounded up to a
+// power of two) and keeps the whole tile row within kRowMaxWarps warps.
+int row_ppw(const ConvGeom& g) {
+    int ppw = 32;
+    const int pairs = (g.C + 1) / 2;
+    while (ppw > 1 && ppw / 2 >= pairs) ppw /= 2;
+    while (ppw > 1 && (g.tw + 32 / ppw - 1) / (32 / ppw) > kRowMaxWarps) ppw /= 2;
+    return ppw;
+}
+
+template <int V, int MODE, int PPW>
+cudaError_t row_launch(const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep, const int* vmax_in, int bits,
+                       QuantParams* qp, int8_t* vqA, unsigned long long* sat, const QuantParams* qtab,
+                       cudaStream_t st, bool pdl) {
+    constexpr int TPW = 32 / PPW;
+    const int nw = (g.tw + TPW - 1) / TPW;
+    const int plw = row_plane_words<V>(g.W);
+    const size_t smem = size_t(2 * PPW) * plw * 4;
+    const long gz = (g.C + 2 * PPW - 1) / (2 * PPW);
+    if (nw > kRowMaxWarps || g.th > 0x7fffffff || g.B > 65535 || gz > 65535 || smem > 200 * 1024)
+        return cudaErrorInvalidConfiguration;
+    auto kern = k_act_row<V, MODE, PPW>;
+    static size_t attr_bytes = 0;
+    if (smem > 48 * 1024 && smem > attr_bytes) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        attr_bytes = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(g.th), unsigned(g.B), unsigned(gz));
+    cfg.blockDim = dim3(32 * nw);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, x, g, plw, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab);
+}
+
+template <int V, int MODE>
+cudaError_t row_dispatch(const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep, const int* vmax_in, int bits,
+                         QuantParams* qp, int8_t* vqA, unsigned long long* sat, const QuantParams* qtab,
+                         cudaStream_t st, bool pdl) {
+    switch (row_ppw(g)) {
+        case 32: return row_launch<V, MODE, 32>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
+        case 16: return row_launch<V, MODE, 16>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
+        case 8: return row_launch<V, MODE, 8>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
+        case 4: return row_launch<V, MODE, 4>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
+        case 2: return row_launch<V, MODE, 2>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
+        default: return row_launch<V, MODE, 1>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
+    }
+}
+}  // namespace
+
+bool act_reg_wanted(int variant, const ConvGeom& g) {
+    if (variant > 2 || g.pad > 8) return false;  // (the plane guards cover windows from column -8)
+    const char* force = std::getenv("SFC_ACT_REG");  // "0": the shared-memory kernels (A/B knob)
+    if (force && force[0] == '0') return false;
+    const int ppw = row_ppw(g);
+    const int nw = (g.tw + 32 / ppw - 1) / (32 / ppw);
+    const size_t smem = size_t(2 * ppw) * (variant == 0   ? row_plane_words<0>(g.W)
+                                           : variant == 1 ? row_plane_words<1>(g.W)
+                                                          : row_plane_words<2>(g.W)) * 4;
+    return nw <= kRowMaxWarps && smem <= 200 * 1024;
+}
+
+cudaError_t launch_act_reg(int variant, int mode, const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep,
+                           const int* vmax_in, int bits, QuantParams* qp, int8_t* vqA, unsigned long long* sat,
+                           cudaStream_t st, bool pdl) {
+    const QuantParams* qtab = mode == 1 ? qparams_table(false) : nullptr;
+#define SFC_ROW_MODES(VV)                                                                                         \
+    if (mode == 1) return row_dispatch<VV, 1>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);     \
+    if (vkeep) return row_dispatch<VV, 2>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);         \
+    return row_dispatch<VV, 0>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
+    switch (variant) {
+        case 0: { SFC_ROW_MODES(0) }
+        case 1: { SFC_ROW_MODES(1) }
+        case 2: { SFC_ROW_MODES(2) }
+        default: return cudaErrorInvalidValue;
+    }
+#undef SFC_ROW_MODES
+}
+
+}  // namespace sfcb200

@@ -63,6 +63,13 @@ cudaError_t launch_filter_prepare(int variant, const int8_t* w, int OC, int IC, 
 // Whether the 3x3 activation kernels take the two-channel SWAR form for this layer (large
 // layers; SFC_ACT_PAIR=0/1 forces either).
 bool act_pair_wanted(const ConvGeom& g);
+// Register-resident SWAR transform (3x3 variants, act_reg.cu): mode 1 quantizes into vqA,
+// otherwise max|V| (+ the kept V when vkeep).  act_reg_wanted: variant supported and not
+// disabled (SFC_ACT_REG=0).
+bool act_reg_wanted(int variant, const ConvGeom& g);
+cudaError_t launch_act_reg(int variant, int mode, const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep,
+                           const int* vmax_in, int bits, QuantParams* qp, int8_t* vqA, unsigned long long* sat,
+                           cudaStream_t st, bool pdl);
 cudaError_t launch_act_absmax(int variant, const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep,
                               cudaStream_t st, bool pdl = false);
 // vq = q(kept V) for t < T, channels >= C zeroed (streaming; replaces launch_act_quant's
