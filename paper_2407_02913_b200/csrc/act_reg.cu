@@ -57,6 +57,15 @@ __device__ __noinline__ int quant_slow(int v, double sa, int qmax, unsigned long
     return clamp_q(exact_q(v, sa), qmax, sat);
 }
 
+// A 16-byte chunk that straddles an end of x: only its bytes inside [xlo, xhi), zeros elsewhere.
+__device__ __noinline__ uint4 chunk_clipped(uintptr_t ad, uintptr_t xlo, uintptr_t xhi) {
+    uint32_t w[4] = {0, 0, 0, 0};
+    for (int e = 0; e < 16; ++e)
+        if (ad + e >= xlo && ad + e < xhi)
+            w[e >> 2] |= uint32_t(*reinterpret_cast<const uint8_t*>(ad + e)) << (8 * (e & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 }  // namespace
 
 // Shared words per channel plane: a 4-word guard (window columns left of the band), the band
@@ -92,45 +101,45 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __r
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     auto plane = [&](int ch) { return ((ch & 1) * PPW + (ch >> 1)) * plw + 4; };
 
-    // ---- stage: per channel, the 16-byte chunks covering its band; lanes = chunks of a
-    // channel (LPC lanes per channel, a power of two >= the chunk count, capped at 32)
+    // ---- stage: per channel, the 16-byte chunks covering its band.  Lanes = chunks of one
+    // channel (lpc lanes per channel, a power of two >= the chunk count, capped at 32), a
+    // warp pass covers cpw channels; kB passes' loads are in flight before any is stored.
     {
+        const int nchv = min(NCH, g.C - c0);
         const int cq = (15 + band + 15) >> 4;  // chunk bound over every misalignment
         int lg = 0;
         while ((1 << lg) < cq && lg < 5) ++lg;
-        const int lpc = 1 << lg, cpw = 32 >> lg;  // lanes per channel, channels per warp pass
-        const int qq = (cq + lpc - 1) >> lg;        // chunk passes per channel
-        const int items = ((NCH + nwarps * cpw - 1) / (nwarps * cpw)) * qq;  // (channel pass, chunk pass)
-        constexpr int kB = 8;                       // loads in flight per thread
-        for (int j0 = 0; j0 < items; j0 += kB) {
-            uint4 v[kB];
-            uint32_t* d[kB];
+        const int lpc = 1 << lg, cpw = 32 >> lg;
+        const int qq = (cq + lpc - 1) >> lg;      // chunk passes per channel (1 unless band > 482 B)
+        const int ch0 = wid * cpw + (lane >> lg), chstep = nwarps * cpw;
+        const uintptr_t xb_u = reinterpret_cast<uintptr_t>(xb);
+        // the CTA's chunks all lie inside x unless it holds the first or last bytes of x
+        const bool inside = (xb_u & ~uintptr_t(15)) >= xlo &&
+                            ((xb_u + size_t(nchv - 1) * HW + band + 15) & ~uintptr_t(15)) <= xhi;
+        constexpr int kB = 8;
+        for (int jq = 0; jq < qq; ++jq) {
+            const int q = (lane & (lpc - 1)) + jq * lpc;
+            for (int chb = ch0; chb < nchv; chb += kB * chstep) {
+                uint4 v[kB];
+                uint32_t* d[kB];
 #pragma unroll
-            for (int jj = 0; jj < kB; ++jj) {
-                const int j = j0 + jj, jc = j / qq, jq = j - jc * qq;
-                const int ch = (wid + jc * nwarps) * cpw + (lane >> lg);
-                const int q = (lane & (lpc - 1)) + jq * lpc;
-                d[jj] = nullptr;
-                v[jj] = make_uint4(0, 0, 0, 0);
-                if (j >= items || ch >= NCH || c0 + ch >= g.C) continue;
-                const uintptr_t start = reinterpret_cast<uintptr_t>(xb + size_t(ch) * HW);
-                const uintptr_t a16 = start & ~uintptr_t(15);
-                if (q >= int((start - a16 + band + 15) >> 4)) continue;
-                const uintptr_t ad = a16 + 16 * uintptr_t(q);
-                d[jj] = s_raw + plane(ch) + 4 * q;
-                if (ad >= xlo && ad + 16 <= xhi) {
-                    v[jj] = __ldg(reinterpret_cast<const uint4*>(ad));
-                } else {  // the chunk straddles an end of x: only its bytes inside x
-                    uint32_t w[4] = {0, 0, 0, 0};
-                    for (int e = 0; e < 16; ++e)
-                        if (ad + e >= xlo && ad + e < xhi)
-                            w[e >> 2] |= uint32_t(*reinterpret_cast<const uint8_t*>(ad + e)) << (8 * (e & 3));
-                    v[jj] = make_uint4(w[0], w[1], w[2], w[3]);
+                for (int jj = 0; jj < kB; ++jj) {
+                    const int ch = chb + jj * chstep;
+                    const uintptr_t start = xb_u + size_t(ch) * HW;
+                    const uintptr_t ad = (start & ~uintptr_t(15)) + 16 * uintptr_t(q);
+                    d[jj] = (ch < nchv && ad < start + band) ? s_raw + plane(ch) + 4 * q : nullptr;
+                    v[jj] = make_uint4(0, 0, 0, 0);
+                    if (!d[jj]) continue;
+                    if (inside || (ad >= xlo && ad + 16 <= xhi)) {
+                        v[jj] = __ldg(reinterpret_cast<const uint4*>(ad));
+                    } else {
+                        v[jj] = chunk_clipped(ad, xlo, xhi);
+                    }
                 }
-            }
 #pragma unroll
-            for (int jj = 0; jj < kB; ++jj)
-                if (d[jj]) d[jj][0] = v[jj].x, d[jj][1] = v[jj].y, d[jj][2] = v[jj].z, d[jj][3] = v[jj].w;
+                for (int jj = 0; jj < kB; ++jj)
+                    if (d[jj]) d[jj][0] = v[jj].x, d[jj][1] = v[jj].y, d[jj][2] = v[jj].z, d[jj][3] = v[jj].w;
+            }
         }
     }
     __syncthreads();
@@ -147,10 +156,14 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __r
     if (active) {
         int xw[n][n];
         const int wc0 = tj * M - g.pad;  // image column of window column 0
-        uint32_t mk[3] = {0, 0, 0};      // byte s of the window valid <=> 0 <= wc0 + s < W
+        // byte s of the window valid <=> 0 <= wc0 + s < W: bytes [slo, shi) of a 12-byte mask
+        const int slo = max(0, -wc0), shi = min(n, g.W - wc0);
+        uint32_t mk[3];
 #pragma unroll
-        for (int s = 0; s < n; ++s)
-            if (unsigned(wc0 + s) < unsigned(g.W)) mk[s >> 2] |= 0xffu << (8 * (s & 3));
+        for (int j = 0; j < 3; ++j) {
+            const int lo = min(max(slo - 4 * j, 0), 4), hi = min(max(shi - 4 * j, 0), 4);
+            mk[j] = (hi >= 4 ? 0xffffffffu : (1u << (8 * hi)) - 1u) & ~(lo >= 4 ? 0xffffffffu : (1u << (8 * lo)) - 1u);
+        }
         const bool ok1 = c + 1 < g.C;
         const uint32_t* pe = s_raw + plane(2 * p);
         const uint32_t* po = s_raw + plane(2 * p + 1);
@@ -250,15 +263,23 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __r
             for (int k = 0; k < K; ++k) {
                 int v[K];
                 fwd1d<V>(y[k], v);
+                uint32_t u[K];
 #pragma unroll
                 for (int l = 0; l < K; ++l) {
-                    const uint32_t u = uint32_t(v[l]) + 0x80008000u;  // lane j -> V_j + 2^15 (mod 2^16)
-                    mx = __vmaxu2(mx, u);
-                    mn = __vminu2(mn, u);
+                    u[l] = uint32_t(v[l]) + 0x80008000u;  // lane j -> V_j + 2^15 (mod 2^16)
                     if constexpr (MODE == 2) {
-                        *vk = int(u ^ 0x80008000u);
+                        *vk = int(u[l] ^ 0x80008000u);
                         vk += fstride;  // f = k * K + l
                     }
+                }
+#pragma unroll
+                for (int l = 0; l + 1 < K; l += 2) {  // three-input SIMD max/min
+                    mx = __vimax3_u16x2(mx, u[l], u[l + 1]);
+                    mn = __vimin3_u16x2(mn, u[l], u[l + 1]);
+                }
+                if constexpr (K % 2) {
+                    mx = __vmaxu2(mx, u[K - 1]);
+                    mn = __vminu2(mn, u[K - 1]);
                 }
             }
         }
@@ -363,5 +384,7 @@ cudaError_t launch_act_reg(int variant, int mode, const int8_t* x, const ConvGeo
     }
 #undef SFC_ROW_MODES
 }
+
+SFC_TL_UNIT_READER(tl_read_reg)
 
 }  // namespace sfcb200

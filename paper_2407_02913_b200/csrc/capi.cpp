@@ -940,16 +940,16 @@ int sfc_debug_timeline(uint64_t* out, int reset) {
     return guarded([&] {
         if (!out) throw std::invalid_argument("null argument");
         ck(cudaDeviceSynchronize(), "sync");
-        unsigned long long part[4][kTlCount][3];
-        cudaError_t (*readers[4])(unsigned long long*, bool) = {tl_read_aux, tl_read_act, tl_read_gemm, tl_read_out};
-        for (int u = 0; u < 4; ++u) {
+        unsigned long long part[5][kTlCount][3];
+        cudaError_t (*readers[5])(unsigned long long*, bool) = {tl_read_aux, tl_read_act, tl_read_reg, tl_read_gemm, tl_read_out};
+        for (int u = 0; u < 5; ++u) {
             const cudaError_t e = readers[u](&part[u][0][0], reset != 0);
             if (e == cudaErrorNotSupported) throw Unsupported("not the timeline build (make TIMELINE=1)");
             ck(e, "timeline read");
         }
         for (int k = 0; k < kTlCount; ++k) {
             unsigned long long a = ~0ull, b = ~0ull, c = 0;
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 5; ++u) {
                 a = std::min(a, part[u][k][0]);
                 b = std::min(b, part[u][k][1]);
                 c = std::max(c, part[u][k][2]);

@@ -99,6 +99,7 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
 
 // Timeline stamps of the debug build ([8][3] per unit; cudaErrorNotSupported otherwise).
 cudaError_t tl_read_act(unsigned long long* out, bool reset);
+cudaError_t tl_read_reg(unsigned long long* out, bool reset);
 cudaError_t tl_read_gemm(unsigned long long* out, bool reset);
 cudaError_t tl_read_out(unsigned long long* out, bool reset);
 cudaError_t tl_read_aux(unsigned long long* out, bool reset);
