@@ -315,9 +315,11 @@ def run_b200(args, rank, world, local_rank):
     ms = float(t.item())
     step_ops = sum(wl.direct_equivalent_ops(c["L"]) for c in calls) * world
     value = step_ops / (ms / 1e3) / 1e12
-    # N=1: workspace reset, absmax (+V kept), gemm (quantizing the kept V), output; N>1: the
-    # reset is a torch zero_() of vmax, not one of ours
-    launches_per_step = (4 if world == 1 else 3) * len(calls)
+    # N=1: workspace reset, absmax (+V kept), [quantizing transform,] gemm, output (per the
+    # call's schedule); N>1: the reset is a torch zero_() of vmax, not one of ours
+    launches_per_step = sum(
+        (5 if c["layer"].schedule(*c["x"].shape[:1], *c["x"].shape[2:], c["L"].pad)["recompute"] else 4)
+        if world == 1 else 3 for c in calls)
 
     # ---- end to end through the public API: pinned host input -> device -> outputs -> pinned host
     def e2e_step():
@@ -347,10 +349,11 @@ def run_b200(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = step_ops / (float(t.item()) / 1e3) / 1e12
 
-    # ---- per-kernel live timing (same stream, CUDA events between the stage launches)
-    # the forward's stages: absmax (V kept), the saturation reset, the GEMM that quantizes the
-    # kept V (TMA-staged) in its converter warps, the output transform
-    stage_names = ["absmax", "sat_reset", "gemm", "output"]
+    # ---- per-kernel live timing (same stream, CUDA events between the stage launches), in
+    # the schedule forward() picks per call (sfc_conv_schedule): kept V = absmax (+V kept),
+    # the saturation reset, the GEMM quantizing the kept V in its converter warps, the output
+    # transform; recompute = absmax, reset, quantizing transform -> vq, TMA-fed GEMM, output
+    stage_names = ["absmax", "sat_reset", "quantize", "gemm", "output"]
     stage_ms = {n: 0.0 for n in stage_names}
     per_call_stage = []
     L_ = lib()
@@ -358,25 +361,33 @@ def run_b200(args, rank, world, local_rank):
     reps = max(3, args.steps // 2)
     for c in calls:
         acc = {n: 0.0 for n in stage_names}
+        x, ws, pad = c["x"], c["ws"], c["L"].pad
+        n, _, h, w_ = x.shape
+        rec = c["layer"].schedule(n, h, w_, pad)["recompute"] if world == 1 else False
+        c["recompute"] = rec
+        masks = ((1, "sat_reset"), (2, "quantize"), (4, "gemm"), (8, "output")) if rec else \
+            ((1, "sat_reset"), (4 | 16, "gemm"), (8 | 16, "output"))  # 16: the kept-V path
         for _ in range(reps):
             flush.zero_()
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-            x, ws, pad = c["x"], c["ws"], c["L"].pad
-            n, _, h, w_ = x.shape
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(len(masks) + 2)]
             o = sc.Outputs(*(sc._ptr(c["outs"].get(k)) for k in ("y_int32", "y_int64", "out_f32", "out_f64", "out_i8")),
                            c["rq"])
             c["vmax"].zero_()
             e[0].record(stream)
-            c["layer"].transform(x, c["vmax"], ws, pad)  # absmax + V kept (as in forward)
+            if rec:
+                c["layer"].absmax(x, c["vmax"], pad)  # absmax only (as in forward)
+            else:
+                c["layer"].transform(x, c["vmax"], ws, pad)  # absmax + V kept (as in forward)
             e[1].record(stream)
-            for si, mask in enumerate((1, 4 | 16, 8 | 16)):  # 16: the kept-V path (as in forward)
+            for si, (mask, _) in enumerate(masks):
                 sc.check(L_.sfc_conv_int8_stages(c["layer"]._h, sc._ptr(x), n, h, w_, pad, sc._ptr(c["vmax"]),
                                                  sc._ptr(ws), ws.numel(), ctypes.byref(o), mask,
                                                  ctypes.c_void_p(stream.cuda_stream)))
                 e[2 + si].record(stream)
-            e[4].synchronize()
-            for si, nme in enumerate(stage_names):
-                acc[nme] += e[si].elapsed_time(e[si + 1]) / reps
+            e[-1].synchronize()
+            acc["absmax"] += e[0].elapsed_time(e[1]) / reps
+            for si, (_, nme) in enumerate(masks):
+                acc[nme] += e[1 + si].elapsed_time(e[2 + si]) / reps
         per_call_stage.append(acc)
         for k in stage_names:
             stage_ms[k] += acc[k]
@@ -393,13 +404,14 @@ def run_b200(args, rank, world, local_rank):
             T, _, ho = wl.tile_grid(L, sp.M)
             xb = L.batch * L.cin * L.hw * L.hw
             outb = sum(t.numel() * t.element_size() for t in c["outs"].values())
+            rec = c["recompute"]
             if dom == "absmax":
-                alg_bytes += xb + 2 * F * T * L.cin  # read x, keep int16 V
+                alg_bytes += xb + (0 if rec else 2 * F * T * L.cin)  # read x (+ keep int16 V)
             elif dom == "quantize":
-                alg_bytes += 3 * F * T * L.cin  # read int16 V, write int8 vq
-            elif dom == "gemm":  # reads the kept int16 V and uq, writes P
+                alg_bytes += xb + F * T * L.cin  # read x, write int8 vq
+            elif dom == "gemm":  # reads vq (int8) or the kept V (int16) and uq, writes P
                 alg_ops += 2 * F * T * L.cin * L.cout
-                alg_bytes += 2 * F * T * L.cin + F * L.cin * L.cout + 4 * F * T * L.cout
+                alg_bytes += (1 if rec else 2) * F * T * L.cin + F * L.cin * L.cout + 4 * F * T * L.cout
             elif dom == "output":
                 alg_bytes += 4 * F * T * L.cout + outb
             else:

@@ -171,6 +171,14 @@ int sfc_conv_stats(sfc_layer_t layer, int n, int h, int w, int pad, const void* 
  * geom[6] = {T, Tpad, Cpad, OCpad, th, tw}. */
 int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_workspace, int8_t** d_vq,
                    int32_t** d_pacc, int64_t* geom);
+/* The schedule sfc_conv_forward picks for this layer and geometry (either may be NULL):
+ *   *recompute  0: the absmax pass keeps V and the GEMM quantizes it (sfc_act_transform +
+ *                  sfc_conv_kept); 1: absmax only, then a quantizing transform writes vq
+ *                  (sfc_act_absmax + sfc_conv_int8).  Both are bit-identical.
+ *   *p_layout   layout of the pacc view: 0 = [F][Tpad][OCpad] (default), 1 =
+ *               [Tpad][OCpad/32][F][32], 2 = [Tpad][F][OCpad] (SFC_P_BLOCKED=1/2: the register
+ *               output transform reads a tile's frequencies as one run). */
+int sfc_conv_schedule(sfc_layer_t layer, int n, int h, int w, int pad, int* recompute, int* p_layout);
 
 /* Exact int8 direct correlation (int32 accumulate), the report baseline
  * of quantized_fast_conv2d (quant.cpp:282) and direct_conv2d (conv.cpp:320-350). */

@@ -20,7 +20,7 @@ EXPORTED = (
     "sfc_last_error", "sfc_version", "sfc_catalog_json", "sfc_plan_create", "sfc_plan_destroy", "sfc_plan_dims",
     "sfc_plan_matrices", "sfc_layer_create", "sfc_layer_destroy", "sfc_layer_filter_scales",
     "sfc_layer_saturations", "sfc_layer_uq", "sfc_conv_workspace_size", "sfc_act_absmax", "sfc_conv_int8",
-    "sfc_conv_int8_stages", "sfc_conv_forward", "sfc_conv_stats", "sfc_conv_views", "sfc_direct_conv_int8", "sfc_frequency_energy_int8",
+    "sfc_conv_int8_stages", "sfc_conv_forward", "sfc_conv_stats", "sfc_conv_views", "sfc_conv_schedule", "sfc_direct_conv_int8", "sfc_frequency_energy_int8",
     "sfc_transform_filters_int8", "sfc_debug_quantizer", "sfc_report_sq_err", "sfc_debug_timeline",
     "sfc_act_transform", "sfc_conv_kept", "sfc_layer_create_ex", "sfc_layer_filter_scales_native",
     "sfc_conv_act_scales", "sfc_layer_create_f64", "sfc_conv_forward_f64", "sfc_direct_conv_f64",
@@ -94,6 +94,7 @@ _SIGS = {
     "sfc_conv_kept": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
     "sfc_conv_stats": (_i, [_vp, _i, _i, _i, _i, _vp, _i64p, _vp]),
     "sfc_conv_views": (_i, [_vp, _i, _i, _i, _i, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64p]),
+    "sfc_conv_schedule": (_i, [_vp, _i, _i, _i, _i, ctypes.POINTER(_i)]),
     "sfc_direct_conv_int8": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp]),
     "sfc_frequency_energy_int8": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "sfc_transform_filters_int8": (_i, [_vp, _vp, _i, _i, _vp, _vp]),

@@ -51,6 +51,13 @@ __device__ __forceinline__ int sx_hi(uint32_t w) {
     return prmt0<4 | (4 << 4) | (q << 8) | ((q | 8) << 12)>(w);
 }
 
+// mad.hi.s32: hi32(v * mul) + c, then an arithmetic shift (see the S >= 33 quantizer below)
+__device__ __forceinline__ int quant_hi32(int v, int mul, int c, int sh) {
+    int r;
+    asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(mul), "r"(c));
+    return r >> sh;
+}
+
 // The reference quantizer with clamping (the rare case without a verified multiply-shift):
 // out of line, so the unrolled column loop stays small.
 __device__ __noinline__ int quant_slow(int v, double sa, int qmax, unsigned long long* sat) {
@@ -234,12 +241,19 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __r
 #pragma unroll
                 for (int l = 0; l < K; ++l) {
                     const int lo = int(int16_t(v[l]));
-                    *vq = int16_t((qlo(lo) & 0xff) | (qhi(v[l] - lo) << 8));
+                    *vq = int16_t(__byte_perm(uint32_t(qlo(lo)), uint32_t(qhi(v[l] - lo)), 0x0040));
                     vq += fstride;  // f = k * K + l: next frequency plane
                 }
             }
         };
-        if (qp.exact) {  // uniform over the grid: no per-value branch
+        if (qp.exact && qp.shift >= 33) {
+            // q = floor((v*mul + 2^(S-1)) / 2^S) = (hi32(v*mul) + 2^(S-33)) >> (S-32) for S >= 33
+            // (the dropped low word only adds a fraction below one unit of the numerator):
+            // one mad.hi and one shift; the high lane (hi * 2^16) with S + 16.
+            const int mul = int(qp.mul), c = 1 << (qp.shift - 33), sh = qp.shift - 32;
+            const int c16 = 1 << (qp.shift - 17), sh16 = qp.shift - 16;
+            rows([=](int v) { return quant_hi32(v, mul, c, sh); }, [=](int v) { return quant_hi32(v, mul, c16, sh16); });
+        } else if (qp.exact) {  // uniform over the grid: no per-value branch
             const int mul = int(qp.mul);
             const long long half = 1ll << (qp.shift - 1), half16 = half << 16;
             const int shift = qp.shift, shift16 = qp.shift + 16;

@@ -172,6 +172,22 @@ void gemm_output(const sfc_layer* L, const ConvGeom& g, const WsView& v, int mod
     }
 }
 
+// The blocked P layout (ConvGeom::pblk) feeds the register output transform: the exact
+// int32 / int64 modes of the 3x3 variants, P not chunked.  SFC_P_BLOCKED=0 keeps
+// [F][Tpad][OCpad] and the TMA-slice output kernel (A/B knob).
+int p_blocked(const sfc_layer* L, const ConvGeom& g) {
+    static const char* force = std::getenv("SFC_P_BLOCKED");
+    if (!(!L->general && L->variant <= 2 && p_chunk(g, L->F).n == 1 && g.OCpad % 32 == 0)) return 0;
+    return force ? std::atoi(force) : 0;  // default [F][Tpad][OCpad]: measured best on configs 2 and 5
+}
+
+// sfc_conv_forward's schedule (see there): recompute V when the GEMM has several output-
+// channel blocks.  SFC_FORWARD_RECOMPUTE=0/1 forces one (A/B knob).
+bool forward_recomputes(const ConvGeom& g) {
+    if (const char* e = std::getenv("SFC_FORWARD_RECOMPUTE")) return e[0] == '1';
+    return g.OCpad > g.BN;
+}
+
 void check_call(const sfc_layer* L, const void* x, int n, int h, int w, int pad) {
     if (!L) throw std::invalid_argument("null layer");
     if (!x) throw std::invalid_argument("null input");  // (the kept-V entry points pass the workspace)
@@ -211,7 +227,8 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
         throw Unsupported("layers with a non-default QuantConfig run through sfc_conv_forward only (single GPU)");
     check_call(L, kept ? ws : static_cast<const void*>(d_x), n, h, w, pad);
     if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
-    const ConvGeom g = geom_of(L, n, h, w, pad);
+    ConvGeom g = geom_of(L, n, h, w, pad);
+    g.pblk = p_blocked(L, g);
     if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
     const bool need64 = needs_y64(L, o);
     WsView v = carve(ws, g, L->F);
@@ -592,12 +609,14 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
         needs_y64(L, o);  // refuse before anything is launched
         unsigned mask = SFC_STAGE_ALL & ~SFC_STAGE_QPARAMS;
         if (const char* dbg = std::getenv("SFC_DEBUG_FORWARD_MASK")) mask = unsigned(std::atoi(dbg));  // profiling only
-        // The absmax pass keeps V and the quantizer streams it (or runs inside the GEMM).
-        // Recomputing V from x in a quantizing transform instead (no int16 V round trip) was
-        // measured slower even with the SWAR kernels (config 5 0.390 vs 0.385 ms, ResNet-18
-        // 1.30 vs 1.19, VGG-16 18.3 vs 15.8); SFC_FORWARD_RECOMPUTE=1 selects it.
-        bool recompute = false;
-        if (const char* e = std::getenv("SFC_FORWARD_RECOMPUTE")) recompute = e[0] == '1';
+        // Two schedules, bit-identical.  Kept V: the absmax pass keeps V (int16) and the GEMM's
+        // converter warps quantize it into the A tiles.  Recompute: absmax only, then a
+        // quantizing transform writes vq (int8) for a TMA-fed GEMM.  The converters quantize
+        // every A tile once per output-channel block, so with several blocks (OCpad > BN) the
+        // recompute schedule wins (config 5: 0.331 vs 0.359 ms); with one block the kept V
+        // saves the second pass over x (ResNet-18 layer 0: 0.127 vs 0.150 ms, VGG-16 layer 2:
+        // 1.31 vs 1.49 ms).  forward_recomputes() decides; sfc_conv_schedule reports it.
+        const bool recompute = forward_recomputes(g);
         // vmax and the saturation counter share the first 16 bytes of the workspace
         ck(launch_zero_words(reinterpret_cast<uint32_t*>(v.vmax), 4, S(stream)), "workspace reset launch");
         ck(launch_act_absmax(L->variant, d_x, g, v.vmax, recompute ? nullptr : v.vkeep, S(stream), true),
@@ -663,6 +682,16 @@ int sfc_conv_views(sfc_layer_t L, int n, int h, int w, int pad, void* ws, int8_t
         if (geom) {
             geom[0] = g.T, geom[1] = g.Tpad, geom[2] = g.Cpad, geom[3] = g.OCpad, geom[4] = g.th, geom[5] = g.tw;
         }
+    });
+}
+
+int sfc_conv_schedule(sfc_layer_t L, int n, int h, int w, int pad, int* recompute, int* p_layout) {
+    return guarded([&] {
+        if (!L) throw std::invalid_argument("null argument");
+        check_call(L, L, n, h, w, pad);
+        const ConvGeom g = geom_of(L, n, h, w, pad);
+        if (recompute) *recompute = forward_recomputes(g) ? 1 : 0;
+        if (p_layout) *p_layout = p_blocked(L, g);
     });
 }
 

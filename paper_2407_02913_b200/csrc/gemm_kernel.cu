@@ -29,6 +29,13 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
         "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -43,6 +50,20 @@ constexpr int kEpiBufs = 2;                  // TMA-store staging boxes per epil
 constexpr int kEpiBoxBytes = 32 * 32 * 4;    // 32 rows x 32 int32 (one 128B-swizzle box)
 template <bool QF>
 constexpr int gemm_threads() { return 64 + 32 * kEpiWarps + (QF ? 32 * kConvWarps : 0); }
+
+// Work unit -> (oc block, tile block, frequency).  [F][Tpad][OCpad] P: oc block fastest, so
+// co-resident CTAs share a frequency's A tile in L2.  Blocked P ([Tpad][OCpad/32][F][32]):
+// frequency fastest, so co-resident CTAs write neighbouring 128-byte pieces of the same
+// (tile, 32-channel) runs and the line write-backs keep DRAM page locality.
+__device__ __forceinline__ void unit_of(int u, int n_ob, int n_tb, int F, int pblk, int& ob, int& tb, int& f) {
+    if (pblk == 1) {
+        f = u % F;
+        const int r = u / F;
+        ob = r % n_ob, tb = r / n_ob;
+    } else {
+        ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
+    }
+}
 
 // Quantizer parameters for a subset of warps (no CTA-wide barrier): table or warp derivation.
 __device__ __forceinline__ QuantParams qparams_warp(int vmax, int bits, const QuantParams* __restrict__ tab) {
@@ -120,7 +141,8 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
-                const int ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
+                int ob, tb, f;
+                unit_of(u, n_ob, n_tb, F, g.pblk, ob, tb, f);
                 for (int kc = 0; kc < nk; ++kc) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (QF) {
@@ -172,7 +194,8 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         int buf = 0;
         int i = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-            const int ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
+            int ob, tb, f;
+            unit_of(u, n_ob, n_tb, F, g.pblk, ob, tb, f);
             const int ab = i & 1;
             ptx::mbar_wait(&tfull[ab], (i >> 1) & 1);
             ptx::tc_fence_after();
@@ -192,7 +215,13 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_3d(&tmP, myE + buf * kEpiBoxBytes, ob * BN + c, tb * kRowsPerTile + q * 32, f);
+                    if (g.pblk == 2)  // [Tpad][F][OCpad]: coordinates (oc, f, t)
+                        tma_store_3d(&tmP, myE + buf * kEpiBoxBytes, ob * BN + c, f, tb * kRowsPerTile + q * 32);
+                    else if (g.pblk)  // [Tpad][OCpad/32][F][32]: coordinates (oc within group, f, group, t)
+                        tma_store_4d(&tmP, myE + buf * kEpiBoxBytes, 0, f, (ob * BN + c) >> 5,
+                                     tb * kRowsPerTile + q * 32);
+                    else
+                        tma_store_3d(&tmP, myE + buf * kEpiBoxBytes, ob * BN + c, tb * kRowsPerTile + q * 32, f);
                     bulk_commit();
                 }
                 buf = (buf + 1) % kEpiBufs;
@@ -261,7 +290,8 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         const int npairs = ((units - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x)) * nk;
         auto load = [&](int s, uint4 (&va)[kItems], uint4 (&vb)[kItems]) {
             const int u = int(blockIdx.x) + (s / nk) * int(gridDim.x), kc = s % nk;
-            const int tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
+            int ob, tb, f;
+            unit_of(u, n_ob, n_tb, F, g.pblk, ob, tb, f);
 #pragma unroll
             for (int j = 0; j < kItems; ++j) {
                 const int i = ct + j * (32 * kConvWarps);
@@ -356,6 +386,35 @@ bool make_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void*
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The GEMM's P map: [F][Tpad][OCpad] int32 boxes of 32 x 32 (rows x oc), or the blocked
+// layout [Tpad][OCpad/32][F][32] as a 4-D map (32 oc, F, OCpad/32, Tpad) with box (32, 1, 1, 32)
+// -- the same 32 x 128-byte shared box, 128B-swizzled.
+bool make_p_map(CUtensorMap* m, int32_t* P, const ConvGeom& g, int F, int rows) {
+    if (!g.pblk)
+        return make_tmap_3d(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, rows, F, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (g.pblk == 2) {  // [Tpad][F][OCpad] as (OCpad, F, Tpad), box (32, 1, 32)
+        auto fn = encode_fn();
+        if (!fn) return false;
+        cuuint64_t dims[3] = {cuuint64_t(g.OCpad), cuuint64_t(F), cuuint64_t(rows)};
+        cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * 4, cuuint64_t(g.OCpad) * F * 4};
+        cuuint32_t box[3] = {32, 1, 32};
+        cuuint32_t estr[3] = {1, 1, 1};
+        return fn(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t ng = cuuint64_t(g.OCpad / 32);
+    cuuint64_t dims[4] = {32, cuuint64_t(F), ng, cuuint64_t(rows)};
+    cuuint64_t strides[3] = {128, cuuint64_t(F) * 128, ng * F * 128};
+    cuuint32_t box[4] = {32, 1, 1, 32};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int sm_count() {
     static int n = 0;
     if (!n) {
@@ -418,8 +477,7 @@ cudaError_t gemm_dispatch(const int8_t* vqA, const int8_t* uqB, int32_t* P, cons
     if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, QF ? static_cast<const void*>(uqB) : vqA, g.Cpad,
                       QF ? g.OCpad : g.Tpad, F, g.BK, QF ? g.BN : kRowsPerTile, sw) ||
         !make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
-        !make_tmap_3d(&tp, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, g.Tpad, F, 32, 32,
-                      CU_TENSOR_MAP_SWIZZLE_128B))
+        !make_p_map(&tp, P, g, F, g.Tpad))
         return cudaErrorInvalidValue;
     const int nk = g.Cpad / g.BK;
     if (g.BK == 128)
@@ -478,7 +536,7 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
         return cudaErrorInvalidValue;
     const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     if (!make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
-        !make_tmap_3d(&tp, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, g.Tpad, F, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+        !make_p_map(&tp, P, g, F, g.Tpad))
         return cudaErrorInvalidValue;
     // two stages: A + B + V stages and the epilogue boxes fill the 227 KB at BN = 256, BK = 128
     if (g.BK == 128) {

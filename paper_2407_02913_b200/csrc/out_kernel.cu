@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -231,6 +232,119 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     tl_mark(kTlOutput, 2);
 }
 
+// ---------------------------------------------------------------------------------------
+// Register-resident output transform for the exact integer modes (MODE 0 int32 y, MODE 1
+// int64 y) of the 3x3 variants, over the blocked P layout [Tpad][OCpad/32][F][32] the GEMM
+// writes for it.  A CTA covers TB tile columns of one image tile row and 32 output channels;
+// thread (tile tj, lane oc) loads its K^2 values of P straight from global memory -- one
+// base pointer, the frequency in the immediate offset, a warp reading one contiguous
+// 128*F-byte run (streamed, evict-first) -- runs both scheduled inverse passes in registers
+//   Q[k][t2]   = sum_l P[k*K + l] A[l][t2]
+//   y[t1][t2]  = sum_k A[k][t1] Q[k][t2]
+// and parks y in shared memory only for the coalesced row-segment stores (stage C of
+// k_output).  No TMA round trip, no shared-memory P slice: small CTAs, many resident.
+constexpr int kRegTB = 4;
+template <bool Y64>
+constexpr int reg_tb() { return Y64 ? 2 : kRegTB; }  // (int64 y: half the tiles, same shared bytes)
+
+template <int V, bool Y64>
+__global__ void __launch_bounds__(32 * reg_tb<Y64>()) k_output_reg(const int32_t* __restrict__ P, ConvGeom g,
+                                                            const QuantParams* __restrict__ qpp,
+                                                            const double* __restrict__ sf, OutPtrs o) {
+    using T = Tab<V>;
+    constexpr int TB = reg_tb<Y64>();
+    constexpr int K = T::K, M = T::M, YS = (M * TB) | 1, NT = 32 * TB;
+    using acc_t = typename std::conditional<Y64, long long, int>::type;
+    __shared__ acc_t s_y[M * kOcc * YS];  // rows r = (t1, oc) of YS
+    __shared__ double s_scale[kOcc];
+    __shared__ float s_scalef[kOcc];
+    const int oc0 = blockIdx.x * kOcc, tc = blockIdx.y, row = blockIdx.z;
+    const int lane = threadIdx.x & 31, tjl = threadIdx.x >> 5;
+    tl_mark(kTlOutput, 0);
+    const int arow = g.row0 + row;
+    const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
+    const int noc = min(kOcc, g.OC - oc0);
+    const int ntb = min(TB, g.tw - tc * TB);
+    griddep_wait();  // P complete
+    tl_mark(kTlOutput, 1);
+    griddep_launch_dependents();
+    if (threadIdx.x < kOcc && int(threadIdx.x) < noc) {
+        const double sc = (qpp->sa * sf[oc0 + threadIdx.x]) / double(T::DEN * T::DEN);
+        s_scale[threadIdx.x] = sc;
+        s_scalef[threadIdx.x] = float(sc);
+    }
+    if (tjl < ntb) {
+        const size_t t = size_t(row * g.tw + tc * TB + tjl);
+        // pblk 1: [Tpad][OCpad/32][F][32] (frequency stride 32); 2: [Tpad][F][OCpad] (stride OCpad)
+        const int fst = g.pblk == 1 ? kOcc : g.OCpad;
+        const int32_t* pp = g.pblk == 1 ? P + (t * (g.OCpad / kOcc) + blockIdx.x) * (T::F * kOcc) + lane
+                                        : P + t * T::F * g.OCpad + oc0 + lane;
+        acc_t q[K][M];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            acc_t pr[K], qt[M];
+#pragma unroll
+            for (int l = 0; l < K; ++l) pr[l] = acc_t(__ldcs(pp + (k * K + l) * fst));  // f = k * K + l
+            inv1d<V>(pr, qt);
+#pragma unroll
+            for (int t2 = 0; t2 < M; ++t2) q[k][t2] = qt[t2];
+        }
+#pragma unroll
+        for (int t2 = 0; t2 < M; ++t2) {
+            acc_t qc[K], yt[M];
+#pragma unroll
+            for (int k = 0; k < K; ++k) qc[k] = q[k][t2];
+            inv1d<V>(qc, yt);
+#pragma unroll
+            for (int t1 = 0; t1 < M; ++t1) s_y[(t1 * kOcc + lane) * YS + tjl * M + t2] = yt[t1];
+        }
+    }
+    __syncthreads();
+
+    // stage C (as k_output): thread t keeps column c = t % ncol and walks rows r = (t1, oc)
+    const int WO = g.WO;
+    const int col0 = tc * TB * M;
+    const int ncol = min(ntb * M, WO - col0);  // <= TB * M <= 28
+    const int hrows = min(M, g.HO - ti * M);
+    const int plane = g.HO * WO;
+    const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
+    const unsigned nmag = c_magic32[ncol];
+    const int r0 = ncol == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
+    const int c = int(threadIdx.x) - r0 * ncol;
+    const int rstep = ncol == 1 ? NT : int(__umulhi(unsigned(NT), nmag));
+    const double rq = o.requant;
+    auto emit = [&](auto mask_c) {
+        constexpr int MK = decltype(mask_c)::value;
+        if (r0 >= rstep) return;
+        for (int r = r0; r < M * kOcc; r += rstep) {
+            const int oc = r % kOcc, t1 = r / kOcc;
+            if (oc >= noc || t1 >= hrows) continue;
+            const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
+            const acc_t y = s_y[r * YS + c];
+            if constexpr ((MK & 1) != 0) o.y32[x] = int(y);
+            if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y);
+            if constexpr ((MK & 4) != 0)
+                o.f32[x] = Y64 ? float(double(y) * s_scale[oc]) : __int2float_rn(int(y)) * s_scalef[oc];
+            if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * s_scale[oc];
+            if constexpr ((MK & 16) != 0) o.i8[x] = int8_t(fmin(fmax(rint(double(y) * s_scale[oc] * rq), 0.0), 127.0));
+        }
+    };
+    const int mask = (o.y32 ? 1 : 0) | (o.y64 ? 2 : 0) | (o.f32 ? 4 : 0) | (o.f64 ? 8 : 0) | (o.i8 ? 16 : 0);
+    switch (mask) {
+#define SFC_EMIT_CASE(m) \
+    case m: emit(std::integral_constant<int, m>{}); break;
+        SFC_EMIT_CASE(1) SFC_EMIT_CASE(2) SFC_EMIT_CASE(3) SFC_EMIT_CASE(4) SFC_EMIT_CASE(5) SFC_EMIT_CASE(6)
+        SFC_EMIT_CASE(7) SFC_EMIT_CASE(8) SFC_EMIT_CASE(9) SFC_EMIT_CASE(10) SFC_EMIT_CASE(11) SFC_EMIT_CASE(12)
+        SFC_EMIT_CASE(13) SFC_EMIT_CASE(14) SFC_EMIT_CASE(15) SFC_EMIT_CASE(16) SFC_EMIT_CASE(17) SFC_EMIT_CASE(18)
+        SFC_EMIT_CASE(19) SFC_EMIT_CASE(20) SFC_EMIT_CASE(21) SFC_EMIT_CASE(22) SFC_EMIT_CASE(23) SFC_EMIT_CASE(24)
+        SFC_EMIT_CASE(25) SFC_EMIT_CASE(26) SFC_EMIT_CASE(27) SFC_EMIT_CASE(28) SFC_EMIT_CASE(29) SFC_EMIT_CASE(30)
+        SFC_EMIT_CASE(31)
+#undef SFC_EMIT_CASE
+        default: break;
+    }
+    tl_mark(kTlOutput, 2);
+}
+
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -280,9 +394,38 @@ cudaError_t out_launch(const void* P, const ConvGeom& g, const QuantParams* qp, 
     return cudaLaunchKernelEx(&cfg, kern, tm, g, qp, sf, o);
 }
 
+template <int V, bool Y64>
+cudaError_t out_reg_launch(const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
+                           const OutPtrs& o, cudaStream_t st, bool pdl) {
+    const long rows = g.nrows;
+    constexpr int TB = reg_tb<Y64>();
+    if (rows > 65535 || (g.tw + TB - 1) / TB > 65535) return cudaErrorInvalidConfiguration;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((g.OC + kOcc - 1) / kOcc), unsigned((g.tw + TB - 1) / TB), unsigned(rows));
+    cfg.blockDim = dim3(32 * TB);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_output_reg<V, Y64>, static_cast<const int32_t*>(P), g, qp, sf, o);
+}
+
+bool out_reg_wanted(int variant, int mode, const OutPtrs& o) {  // (given the blocked P layout)
+    (void)o;
+    return variant <= 2 && mode <= 1;
+}
+
 template <int V>
 cudaError_t out_by_width(int mode, const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
                          const OutPtrs& o, cudaStream_t st, bool pdl) {
+    if constexpr (V <= 2) {
+        if (g.pblk && out_reg_wanted(V, mode, o))
+            return mode == 0 ? out_reg_launch<V, false>(P, g, qp, sf, o, st, pdl)
+                             : out_reg_launch<V, true>(P, g, qp, sf, o, st, pdl);
+    }
+    if (g.pblk) return cudaErrorInvalidValue;  // only the register kernel reads the blocked layout
     return mode == 0 ? out_launch<V, 0>(P, g, qp, sf, o, st, pdl)
          : mode == 1 ? out_launch<V, 1>(P, g, qp, sf, o, st, pdl)
          : mode == 2 ? out_launch<V, 2>(P, g, qp, sf, o, st, pdl)

@@ -19,6 +19,10 @@ struct ConvGeom {
     // output-transform launches over a chunk of image tile rows (P chunked, see PChunk):
     // rows [row0, row0 + nrows) of the B * th rows; geom_init sets the whole range
     int row0, nrows;
+    // P layout: 0 = [F][Tpad][OCpad]; 1 = blocked [Tpad][OCpad/32][F][32] (the default exact
+    // path: a (tile, 32-channel) group's K^2 values are one contiguous 128*F-byte run for the
+    // register output transform).  geom_init sets 0; run_conv decides (p_blocked).
+    int pblk;
 };
 
 // P chunking (opt-in: SFC_PCHUNK_MB = budget in MB; unset or 0 = never chunk).  P (4 B per

@@ -380,6 +380,12 @@ class SfcLayer:
         return dict(act_scale=float(s[0:1].view(np.float64)[0]), vmax=int(s[1]), saturations=int(s[2]),
                     fast_quantizer_exact=bool(s[3]), values_quantized=int(s[4]), tiles=int(s[5]))
 
+    def schedule(self, n, h, w, pad) -> dict:
+        """The schedule forward() picks (sfc_conv_schedule): recompute (bool), p_layout (int)."""
+        r, pl = ctypes.c_int(), ctypes.c_int()
+        check(lib().sfc_conv_schedule(self._h, n, h, w, pad, ctypes.byref(r), ctypes.byref(pl)))
+        return {"recompute": bool(r.value), "p_layout": pl.value}
+
     def views(self, n, h, w, pad, ws):
         """(vq int8 [F, T, IC], pacc int32 [F, T, OC]) views of the workspace after conv();
         pacc is None when the layer's P is chunked (never materialised whole)."""
@@ -392,6 +398,14 @@ class SfcLayer:
         vqt = _wrap_device(vq.value, (F, Tpad, Cpad), torch.int8, self.device)[:, :T, : self.IC]
         if not pa.value:
             return vqt, None
+        blocked = ctypes.c_int()
+        check(lib().sfc_conv_schedule(self._h, n, h, w, pad, None, ctypes.byref(blocked)))
+        if blocked.value == 1:  # [Tpad][OCpad/32][F][32] -> [F][Tpad][OCpad] (a copy)
+            pb = _wrap_device(pa.value, (Tpad, OCpad // 32, F, 32), torch.int32, self.device)
+            return vqt, pb.permute(2, 0, 1, 3).reshape(F, Tpad, OCpad)[:, :T, : self.OC]
+        if blocked.value == 2:  # [Tpad][F][OCpad] -> [F][Tpad][OCpad] (a view)
+            pb = _wrap_device(pa.value, (Tpad, F, OCpad), torch.int32, self.device)
+            return vqt, pb.permute(1, 0, 2)[:, :T, : self.OC]
         pat = _wrap_device(pa.value, (F, Tpad, OCpad), torch.int32, self.device)[:, :T, : self.OC]
         return vqt, pat
 
