@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -345,6 +346,205 @@ __global__ void __launch_bounds__(32 * reg_tb<Y64>()) k_output_reg(const int32_t
     tl_mark(kTlOutput, 2);
 }
 
+// ---------------------------------------------------------------------------------------
+// Persistent output transform for the exact integer modes of the 3x3 variants over the
+// [F][Tpad][OCpad] P layout.  Blocks as k_output (oc block of 32, TB tile columns of one
+// image tile row); one thread per (tile, oc) pair.  Per block: wait for the block's P slice
+// (one 3-D TMA load), stage A reads the pair's K^2 values from the slice straight into
+// registers (lanes = oc: conflict-free) and applies the first inverse pass; one barrier frees
+// the slice and the NEXT block's TMA load is issued at once, so it lands while this block
+// runs stage B (second inverse pass, y parked in shared memory) and stage C (coalesced
+// row-segment stores).  The transforms never round-trip through shared memory.
+template <int V>
+struct PersSmem {
+    static constexpr int TB = out_tb<V>();
+    static constexpr int YS = ((Tab<V>::M * TB + 1) & ~1) | 2;  // = 2 (mod 4): 8-byte aligned rows
+    static constexpr size_t slice = size_t(Tab<V>::F) * TB * kOcc * 4;
+    template <bool Y64>
+    static constexpr size_t y_bytes() { return size_t(Tab<V>::M) * kOcc * YS * (Y64 ? 8 : 4); }
+    template <bool Y64>
+    static constexpr size_t bytes() { return ((slice + 127) & ~size_t(127)) + y_bytes<Y64>() + 16; }
+};
+
+template <int V, bool Y64>
+__global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_constant__ CUtensorMap tmP, ConvGeom g,
+                                                                  const QuantParams* __restrict__ qpp,
+                                                                  const double* __restrict__ sf, OutPtrs o, int n_ob,
+                                                                  int n_tc, int nblk) {
+    using T = Tab<V>;
+    using PS = PersSmem<V>;
+    constexpr int K = T::K, M = T::M, TB = PS::TB, NT = 32 * TB, YS = PS::YS;
+    using acc_t = typename std::conditional<Y64, long long, int>::type;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int32_t* sp = reinterpret_cast<const int32_t*>(smem);  // [F][TB][kOcc]
+    acc_t* s_y = reinterpret_cast<acc_t*>(smem + ((PS::slice + 127) & ~size_t(127)));  // rows (t1, oc) of YS
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + ((PS::slice + 127) & ~size_t(127)) + PS::template y_bytes<Y64>());
+    __shared__ double s_scale[kOcc];
+    __shared__ float s_scalef[kOcc];
+    const int lane = threadIdx.x & 31, tjl = threadIdx.x >> 5;
+    tl_mark(kTlOutput, 0);
+    auto issue = [&](int blk) {  // thread 0: the block's P slice
+        const int ob = blk % n_ob, r = blk / n_ob, tc = r % n_tc, row = r / n_tc;
+        ptx::mbar_expect_tx(full, uint32_t(PS::slice));
+        ptx::tma_load_3d(smem, &tmP, full, ob * kOcc, row * g.tw + tc * TB, 0);
+    };
+    if (threadIdx.x == 0) {
+        ptx::tma_prefetch(&tmP);
+        ptx::mbar_init(full, 1);
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    griddep_wait();  // P complete
+    tl_mark(kTlOutput, 1);
+    griddep_launch_dependents();
+    if (threadIdx.x == 0 && int(blockIdx.x) < nblk) issue(blockIdx.x);
+    const double sa = qpp->sa;
+    const double rq = o.requant;
+    const int WO = g.WO, plane = g.HO * WO;
+    const int mask = (o.y32 ? 1 : 0) | (o.y64 ? 2 : 0) | (o.f32 ? 4 : 0) | (o.f64 ? 8 : 0) | (o.i8 ? 16 : 0);
+    uint32_t phase = 0;
+    for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int ob = blk % n_ob, rr = blk / n_ob, tc = rr % n_tc, row = rr / n_tc;
+        const int oc0 = ob * kOcc;
+        const int arow = g.row0 + row;
+        const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
+        const int noc = min(kOcc, g.OC - oc0);
+        const int ntb = min(TB, g.tw - tc * TB);
+        const bool act = tjl < ntb;
+        ptx::mbar_wait(full, phase);
+        phase ^= 1;
+        // stage A: Q[k][t2] = sum_l P[k*K + l] A[l][t2], P straight from the slice
+        acc_t q[K][M];
+        if (act) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                acc_t pr[K], qt[M];
+#pragma unroll
+                for (int l = 0; l < K; ++l) pr[l] = acc_t(sp[((k * K + l) * TB + tjl) * kOcc + lane]);
+                inv1d<V>(pr, qt);
+#pragma unroll
+                for (int t2 = 0; t2 < M; ++t2) q[k][t2] = qt[t2];
+            }
+        }
+        __syncthreads();  // slice consumed; the previous block's stage C is done with s_y / s_scale
+        if (threadIdx.x == 0 && blk + int(gridDim.x) < nblk) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async write
+            issue(blk + gridDim.x);
+        }
+        if (threadIdx.x < kOcc && int(threadIdx.x) < noc) {
+            const double sc = (sa * sf[oc0 + threadIdx.x]) / double(T::DEN * T::DEN);
+            s_scale[threadIdx.x] = sc;
+            s_scalef[threadIdx.x] = float(sc);
+        }
+        // stage B: y[t1][t2] = sum_k A[k][t1] Q[k][t2] -> s_y
+        if (act) {
+#pragma unroll
+            for (int t2 = 0; t2 < M; ++t2) {
+                acc_t qc[K], yt[M];
+#pragma unroll
+                for (int k = 0; k < K; ++k) qc[k] = q[k][t2];
+                inv1d<V>(qc, yt);
+#pragma unroll
+                for (int t1 = 0; t1 < M; ++t1) s_y[(t1 * kOcc + lane) * YS + tjl * M + t2] = yt[t1];
+            }
+        }
+        __syncthreads();
+        // stage C: row segments r = (t1, oc) of ncol columns.  Even WO: thread t keeps the
+        // column pair 2cp (cp = t % npair) and walks rows r = t / npair, + NT / npair, ...
+        // (8-byte loads and stores: output offsets are even); odd WO: single columns.
+        const int col0 = tc * TB * M;
+        const int ncol = min(ntb * M, WO - col0);  // <= TB * M <= 32
+        const int hrows = min(M, g.HO - ti * M);
+        const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
+        const bool pairs = (WO & 1) == 0 && o.pairs;
+        const int nit = pairs ? (ncol + 1) >> 1 : ncol;  // items per row
+        const unsigned nmag = c_magic32[nit];
+        const int r0 = nit == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
+        const int ci = int(threadIdx.x) - r0 * nit;
+        const int rstep = nit == 1 ? NT : int(__umulhi(unsigned(NT), nmag));
+        const double* scl = s_scale;
+        const float* sclf = s_scalef;
+        auto emit = [&](auto mask_c) {
+            constexpr int MK = decltype(mask_c)::value;
+            if (r0 >= rstep) return;
+            if (pairs) {
+                const int c = 2 * ci;
+                const bool two = c + 1 < ncol;
+                for (int r = r0; r < M * kOcc; r += rstep) {
+                    const int oc = r & (kOcc - 1), t1 = r >> 5;
+                    if (oc >= noc || t1 >= hrows) continue;
+                    const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
+                    acc_t y0, y1;
+                    if constexpr (Y64) {
+                        y0 = s_y[r * YS + c], y1 = s_y[r * YS + c + 1];
+                    } else {
+                        const int2 v = *reinterpret_cast<const int2*>(s_y + r * YS + c);
+                        y0 = v.x, y1 = v.y;
+                    }
+                    if (two) {
+                        if constexpr ((MK & 1) != 0) *reinterpret_cast<int2*>(o.y32 + x) = make_int2(int(y0), int(y1));
+                        if constexpr ((MK & 2) != 0) {
+                            o.y64[x] = int64_t(y0);
+                            o.y64[x + 1] = int64_t(y1);
+                        }
+                        if constexpr ((MK & 4) != 0) {
+                            const float2 f = Y64 ? make_float2(float(double(y0) * scl[oc]), float(double(y1) * scl[oc]))
+                                                 : make_float2(__int2float_rn(int(y0)) * sclf[oc],
+                                                               __int2float_rn(int(y1)) * sclf[oc]);
+                            *reinterpret_cast<float2*>(o.f32 + x) = f;
+                        }
+                        if constexpr ((MK & 8) != 0) {
+                            o.f64[x] = double(y0) * scl[oc];
+                            o.f64[x + 1] = double(y1) * scl[oc];
+                        }
+                        if constexpr ((MK & 16) != 0) {
+                            const int q0 = int(fmin(fmax(rint(double(y0) * scl[oc] * rq), 0.0), 127.0));
+                            const int q1 = int(fmin(fmax(rint(double(y1) * scl[oc] * rq), 0.0), 127.0));
+                            *reinterpret_cast<int16_t*>(o.i8 + x) = int16_t(q0 | (q1 << 8));
+                        }
+                    } else {
+                        if constexpr ((MK & 1) != 0) o.y32[x] = int(y0);
+                        if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y0);
+                        if constexpr ((MK & 4) != 0)
+                            o.f32[x] = Y64 ? float(double(y0) * scl[oc]) : __int2float_rn(int(y0)) * sclf[oc];
+                        if constexpr ((MK & 8) != 0) o.f64[x] = double(y0) * scl[oc];
+                        if constexpr ((MK & 16) != 0)
+                            o.i8[x] = int8_t(fmin(fmax(rint(double(y0) * scl[oc] * rq), 0.0), 127.0));
+                    }
+                }
+            } else {
+                const int c = ci;
+                for (int r = r0; r < M * kOcc; r += rstep) {
+                    const int oc = r & (kOcc - 1), t1 = r >> 5;
+                    if (oc >= noc || t1 >= hrows) continue;
+                    const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
+                    const acc_t y = s_y[r * YS + c];
+                    if constexpr ((MK & 1) != 0) o.y32[x] = int(y);
+                    if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y);
+                    if constexpr ((MK & 4) != 0)
+                        o.f32[x] = Y64 ? float(double(y) * scl[oc]) : __int2float_rn(int(y)) * sclf[oc];
+                    if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * scl[oc];
+                    if constexpr ((MK & 16) != 0)
+                        o.i8[x] = int8_t(fmin(fmax(rint(double(y) * scl[oc] * rq), 0.0), 127.0));
+                }
+            }
+        };
+        switch (mask) {
+#define SFC_EMIT_CASE(m) \
+    case m: emit(std::integral_constant<int, m>{}); break;
+            SFC_EMIT_CASE(1) SFC_EMIT_CASE(2) SFC_EMIT_CASE(3) SFC_EMIT_CASE(4) SFC_EMIT_CASE(5) SFC_EMIT_CASE(6)
+            SFC_EMIT_CASE(7) SFC_EMIT_CASE(8) SFC_EMIT_CASE(9) SFC_EMIT_CASE(10) SFC_EMIT_CASE(11) SFC_EMIT_CASE(12)
+            SFC_EMIT_CASE(13) SFC_EMIT_CASE(14) SFC_EMIT_CASE(15) SFC_EMIT_CASE(16) SFC_EMIT_CASE(17)
+            SFC_EMIT_CASE(18) SFC_EMIT_CASE(19) SFC_EMIT_CASE(20) SFC_EMIT_CASE(21) SFC_EMIT_CASE(22)
+            SFC_EMIT_CASE(23) SFC_EMIT_CASE(24) SFC_EMIT_CASE(25) SFC_EMIT_CASE(26) SFC_EMIT_CASE(27)
+            SFC_EMIT_CASE(28) SFC_EMIT_CASE(29) SFC_EMIT_CASE(30) SFC_EMIT_CASE(31)
+#undef SFC_EMIT_CASE
+            default: break;
+        }
+    }
+    tl_mark(kTlOutput, 2);
+}
+
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -412,6 +612,65 @@ cudaError_t out_reg_launch(const void* P, const ConvGeom& g, const QuantParams* 
     return cudaLaunchKernelEx(&cfg, k_output_reg<V, Y64>, static_cast<const int32_t*>(P), g, qp, sf, o);
 }
 
+int sm_count_out() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int V, bool Y64>
+cudaError_t out_pers_launch(const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
+                            const OutPtrs& o, cudaStream_t st, bool pdl) {
+    using PS = PersSmem<V>;
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorInvalidValue;
+    CUtensorMap tm;
+    cuuint64_t dims[3] = {cuuint64_t(g.OCpad), cuuint64_t(g.Tpad), cuuint64_t(Tab<V>::F)};
+    cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * 4, cuuint64_t(g.OCpad) * g.Tpad * 4};
+    cuuint32_t box[3] = {kOcc, PS::TB, Tab<V>::F};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(P), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    constexpr size_t smem = PS::template bytes<Y64>();
+    auto kern = k_output_pers<V, Y64>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int n_ob = (g.OC + kOcc - 1) / kOcc, n_tc = (g.tw + PS::TB - 1) / PS::TB;
+    const long nblk = long(n_ob) * n_tc * g.nrows;
+    if (nblk > 0x7fffffffL) return cudaErrorInvalidConfiguration;
+    int per_sm = int((220 * 1024) / (smem + 1024));
+    per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+    const long grid = std::min<long>(nblk, long(sm_count_out()) * per_sm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(32 * PS::TB);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr2[1];
+    attr2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr2[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr2;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, tm, g, qp, sf, o, n_ob, n_tc, int(nblk));
+}
+
+bool out_pers_wanted(int variant, int mode, const ConvGeom& g, const OutPtrs& o) {
+    if (variant > 2 || mode > 1 || o.p_discard || g.pblk) return false;
+    const char* force = std::getenv("SFC_OUT_PERS");  // "0": the one-block-per-CTA kernel (A/B knob)
+    return !force || force[0] != '0';
+}
+
 bool out_reg_wanted(int variant, int mode, const OutPtrs& o) {  // (given the blocked P layout)
     (void)o;
     return variant <= 2 && mode <= 1;
@@ -421,6 +680,16 @@ template <int V>
 cudaError_t out_by_width(int mode, const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
                          const OutPtrs& o, cudaStream_t st, bool pdl) {
     if constexpr (V <= 2) {
+        if (out_pers_wanted(V, mode, g, o)) {
+            OutPtrs op = o;
+            static const char* pe = std::getenv("SFC_OUT_PAIRS");  // "0": single columns (A/B knob)
+            // (the int8 requant output measured slower with paired 2-byte stores: VGG-16 layer 2
+            // 0.87 vs 0.58 ms; int32 / fp32 faster: config 5 0.110 vs 0.114, ResNet-18 layer 0
+            // 0.051 vs 0.055 ms)
+            op.pairs = !(pe && pe[0] == '0') && !o.i8;
+            return mode == 0 ? out_pers_launch<V, false>(P, g, qp, sf, op, st, pdl)
+                             : out_pers_launch<V, true>(P, g, qp, sf, op, st, pdl);
+        }
         if (g.pblk && out_reg_wanted(V, mode, o))
             return mode == 0 ? out_reg_launch<V, false>(P, g, qp, sf, o, st, pdl)
                              : out_reg_launch<V, true>(P, g, qp, sf, o, st, pdl);

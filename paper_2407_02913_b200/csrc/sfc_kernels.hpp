@@ -127,6 +127,7 @@ struct OutPtrs {
     const double* gen_act = nullptr;
     int gen_per_freq = 0;
     const double* gen_fil = nullptr;  // [OC][F]
+    int pairs = 1;  // the persistent output kernel may store column pairs (8-byte stores)
     // when set (the P chunk buffer): every block discards the P lines it consumed from L2
     // (discard.global.L2), so chunked P is never written back to HBM
     const void* p_discard = nullptr;
