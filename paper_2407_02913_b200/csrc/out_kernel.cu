@@ -666,7 +666,14 @@ cudaError_t out_pers_launch(const void* P, const ConvGeom& g, const QuantParams*
 }
 
 bool out_pers_wanted(int variant, int mode, const ConvGeom& g, const OutPtrs& o) {
-    if (variant > 2 || mode > 1 || o.p_discard || g.pblk) return false;
+    // (int8 requant outputs: the one-block kernel measured faster on every ResNet-18 / VGG-16
+    // layer, e.g. VGG-16 14.5 vs 15.5 ms; int32 / fp32 outputs: config 5 0.110 vs 0.119 ms)
+    if (variant > 2 || mode > 1 || o.p_discard || g.pblk || o.i8) return false;
+    // small layers (config 2: 320 blocks) keep the 512-thread one-block CTAs: a persistent CTA
+    // of 64-192 threads has the longer per-block latency chain
+    const int tb = variant == 0 ? out_tb<0>() : variant == 1 ? out_tb<1>() : out_tb<2>();
+    const long nblk = long((g.OC + kOcc - 1) / kOcc) * ((g.tw + tb - 1) / tb) * g.nrows;
+    if (nblk < 8L * sm_count_out()) return false;
     const char* force = std::getenv("SFC_OUT_PERS");  // "0": the one-block-per-CTA kernel (A/B knob)
     return !force || force[0] != '0';
 }
@@ -683,10 +690,7 @@ cudaError_t out_by_width(int mode, const void* P, const ConvGeom& g, const Quant
         if (out_pers_wanted(V, mode, g, o)) {
             OutPtrs op = o;
             static const char* pe = std::getenv("SFC_OUT_PAIRS");  // "0": single columns (A/B knob)
-            // (the int8 requant output measured slower with paired 2-byte stores: VGG-16 layer 2
-            // 0.87 vs 0.58 ms; int32 / fp32 faster: config 5 0.110 vs 0.114, ResNet-18 layer 0
-            // 0.051 vs 0.055 ms)
-            op.pairs = !(pe && pe[0] == '0') && !o.i8;
+            op.pairs = !(pe && pe[0] == '0');  // (config 5 0.110 vs 0.114 ms single columns)
             return mode == 0 ? out_pers_launch<V, false>(P, g, qp, sf, op, st, pdl)
                              : out_pers_launch<V, true>(P, g, qp, sf, op, st, pdl);
         }
