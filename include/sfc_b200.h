@@ -177,7 +177,9 @@ int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_work
  *                  (sfc_act_absmax + sfc_conv_int8).  Both are bit-identical.
  *   *p_layout   layout of the pacc view: 0 = [F][Tpad][OCpad] (default), 1 =
  *               [Tpad][OCpad/32][F][32], 2 = [Tpad][F][OCpad] (SFC_P_BLOCKED=1/2: the register
- *               output transform reads a tile's frequencies as one run). */
+ *               output transform reads a tile's frequencies as one run), 3 = no P: Cin <= 4
+ *               layers contract with dp4a inside the output transform, and the vq view is
+ *               compact [F][T][4] (SFC_SMALLC=0 keeps the tensor-core GEMM). */
 int sfc_conv_schedule(sfc_layer_t layer, int n, int h, int w, int pad, int* recompute, int* p_layout);
 
 /* Exact int8 direct correlation (int32 accumulate), the report baseline

@@ -181,11 +181,22 @@ int p_blocked(const sfc_layer* L, const ConvGeom& g) {
     return force ? std::atoi(force) : 0;  // default [F][Tpad][OCpad]: measured best on configs 2 and 5
 }
 
+// Layers with Cin <= 4 (3x3 variants, exact int32 y, whole P): the dp4a contraction fused
+// with the output transform replaces the GEMM and P (launch_output_smallc); vq is written
+// compact [F][T][4].  SFC_SMALLC=0 keeps the tensor-core GEMM (A/B knob, read per call).
+bool small_c(const sfc_layer* L, const ConvGeom& g) {
+    if (L->general || L->variant > 2 || g.C > 4 || p_chunk(g, L->F).n > 1) return false;
+    if (L->max_a_col_l1 * double(L->max_a_col_l1) * L->IC * 127.0 * 127.0 >= 2147483647.0) return false;
+    const char* e = std::getenv("SFC_SMALLC");
+    return !(e && e[0] == '0');
+}
+
 // sfc_conv_forward's schedule (see there): recompute V when the GEMM has several output-
-// channel blocks.  SFC_FORWARD_RECOMPUTE=0/1 forces one (A/B knob).
-bool forward_recomputes(const ConvGeom& g) {
+// channel blocks or the layer takes the small-channel path.  SFC_FORWARD_RECOMPUTE=0/1 forces
+// one (A/B knob).
+bool forward_recomputes(const sfc_layer* L, const ConvGeom& g) {
     if (const char* e = std::getenv("SFC_FORWARD_RECOMPUTE")) return e[0] == '1';
-    return g.OCpad > g.BN;
+    return g.OCpad > g.BN || small_c(L, g);
 }
 
 void check_call(const sfc_layer* L, const void* x, int n, int h, int w, int pad) {
@@ -250,6 +261,18 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     if (const char* q = std::getenv("SFC_QFUSE")) qfuse = kept && (q[0] == '1' || q[0] == '2'), qtma = q[0] == '2';
     const bool chunked = p_chunk(g, L->F).n > 1;
     qfuse = qfuse && !chunked;  // the converter GEMM covers the whole tile range
+    if (!kept && !need64 && small_c(L, g)) {  // quantizing transform -> compact vq, fused dp4a epilogue
+        ConvGeom gq = g;
+        gq.Cpad = 4, gq.Tpad = g.T;  // vq [F][T][4]
+        if (mask & SFC_STAGE_ACT) {
+            ck(launch_act_quant(L->variant, d_x, gq, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "act launch");
+            pdl = full_pdl;
+        }
+        const OutPtrs op{o->y_int32, o->y_int64, o->out_f32, o->out_f64, o->out_i8, o->requant_scale};
+        if (mask & SFC_STAGE_OUTPUT)
+            ck(launch_output_smallc(L->variant, v.vq, L->d_uq, g, v.qp, L->d_sf, op, st, pdl), "output launch");
+        return;
+    }
     if (mask & SFC_STAGE_ACT) {
         if (!kept) {
             ck(launch_act_quant(L->variant, d_x, g, d_vmax, L->bits, v.qp, v.vq, v.sat, st, pdl), "act launch");
@@ -616,7 +639,7 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
         // recompute schedule wins (config 5: 0.331 vs 0.359 ms); with one block the kept V
         // saves the second pass over x (ResNet-18 layer 0: 0.127 vs 0.150 ms, VGG-16 layer 2:
         // 1.31 vs 1.49 ms).  forward_recomputes() decides; sfc_conv_schedule reports it.
-        const bool recompute = forward_recomputes(g);
+        const bool recompute = forward_recomputes(L, g);
         // vmax and the saturation counter share the first 16 bytes of the workspace
         ck(launch_zero_words(reinterpret_cast<uint32_t*>(v.vmax), 4, S(stream)), "workspace reset launch");
         ck(launch_act_absmax(L->variant, d_x, g, v.vmax, recompute ? nullptr : v.vkeep, S(stream), true),
@@ -678,7 +701,7 @@ int sfc_conv_views(sfc_layer_t L, int n, int h, int w, int pad, void* ws, int8_t
         const ConvGeom g = geom_of(L, n, h, w, pad);
         WsView v = carve(ws, g, L->F);
         if (d_vq) *d_vq = v.vq;
-        if (d_pacc) *d_pacc = p_chunk(g, L->F).n > 1 ? nullptr : v.P;
+        if (d_pacc) *d_pacc = p_chunk(g, L->F).n > 1 || small_c(L, g) ? nullptr : v.P;
         if (geom) {
             geom[0] = g.T, geom[1] = g.Tpad, geom[2] = g.Cpad, geom[3] = g.OCpad, geom[4] = g.th, geom[5] = g.tw;
         }
@@ -690,8 +713,8 @@ int sfc_conv_schedule(sfc_layer_t L, int n, int h, int w, int pad, int* recomput
         if (!L) throw std::invalid_argument("null argument");
         check_call(L, L, n, h, w, pad);
         const ConvGeom g = geom_of(L, n, h, w, pad);
-        if (recompute) *recompute = forward_recomputes(g) ? 1 : 0;
-        if (p_layout) *p_layout = p_blocked(L, g);
+        if (recompute) *recompute = forward_recomputes(L, g) ? 1 : 0;
+        if (p_layout) *p_layout = small_c(L, g) ? 3 : p_blocked(L, g);
     });
 }
 

@@ -545,6 +545,103 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
     tl_mark(kTlOutput, 2);
 }
 
+// ---------------------------------------------------------------------------------------
+// Layers with at most 4 input channels (VGG-16's first layer, Cin = 3): the per-frequency
+// contraction has K <= 4, so the tensor-core GEMM would spend its time writing P (4 B per
+// (frequency, tile, oc); 4.7 GB on VGG-16 layer 0) for three multiply-adds per value.
+// Here the contraction is one dp4a per (frequency, tile, oc) -- vq as one int8x4 word per
+// (frequency, tile) (compact [F][T][4], written by the quantizing transform), the block's
+// uq words [F][32] in shared memory -- fused with both inverse passes in registers and the
+// coalesced row-segment stores of k_output.  P is never materialised; y is the same exact
+// int32 (the contraction is the same integer sum).
+constexpr int kSmallTB = 4;
+
+template <int V>
+__global__ void __launch_bounds__(32 * kSmallTB) k_output_smallc(const int32_t* __restrict__ vq4,
+                                                                 const int8_t* __restrict__ uq, ConvGeom g,
+                                                                 const QuantParams* __restrict__ qpp,
+                                                                 const double* __restrict__ sf, OutPtrs o) {
+    using T = Tab<V>;
+    constexpr int K = T::K, M = T::M, F = T::F, TB = kSmallTB, NT = 32 * TB, YS = (M * TB) | 1;
+    __shared__ int s_u[F * kOcc];      // uq words of this block's 32 output channels
+    __shared__ int s_y[M * kOcc * YS];  // rows r = (t1, oc) of YS
+    __shared__ double s_scale[kOcc];
+    __shared__ float s_scalef[kOcc];
+    const int oc0 = blockIdx.x * kOcc, tc = blockIdx.y, row = blockIdx.z;
+    const int lane = threadIdx.x & 31, tjl = threadIdx.x >> 5;
+    tl_mark(kTlOutput, 0);
+    for (int i = threadIdx.x; i < F * kOcc; i += NT) {  // the layer's filters: before the wait
+        const int f = i >> 5, oc = i & (kOcc - 1);
+        s_u[i] = oc0 + oc < g.OCpad ? *reinterpret_cast<const int*>(uq + (size_t(f) * g.OCpad + oc0 + oc) * g.Cpad)
+                                    : 0;
+    }
+    const int arow = g.row0 + row;
+    const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
+    const int noc = min(kOcc, g.OC - oc0);
+    const int ntb = min(TB, g.tw - tc * TB);
+    griddep_wait();  // vq and the activation scale complete
+    tl_mark(kTlOutput, 1);
+    griddep_launch_dependents();
+    if (threadIdx.x < kOcc && int(threadIdx.x) < noc) {  // (the same fp32 / fp64 epilogue as k_output)
+        const double sc = (qpp->sa * sf[oc0 + threadIdx.x]) / double(T::DEN * T::DEN);
+        s_scale[threadIdx.x] = sc;
+        s_scalef[threadIdx.x] = float(sc);
+    }
+    __syncthreads();
+    if (tjl < ntb) {
+        const int32_t* vt = vq4 + (row * g.tw + tc * TB + tjl);  // + f * T
+        int q[K][M];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            int pr[K], qt[M];
+#pragma unroll
+            for (int l = 0; l < K; ++l) {
+                const int f = k * K + l;
+                pr[l] = __dp4a(__ldg(vt + size_t(f) * g.T), s_u[f * kOcc + lane], 0);
+            }
+            inv1d<V>(pr, qt);
+#pragma unroll
+            for (int t2 = 0; t2 < M; ++t2) q[k][t2] = qt[t2];
+        }
+#pragma unroll
+        for (int t2 = 0; t2 < M; ++t2) {
+            int qc[K], yt[M];
+#pragma unroll
+            for (int k = 0; k < K; ++k) qc[k] = q[k][t2];
+            inv1d<V>(qc, yt);
+#pragma unroll
+            for (int t1 = 0; t1 < M; ++t1) s_y[(t1 * kOcc + lane) * YS + tjl * M + t2] = yt[t1];
+        }
+    }
+    __syncthreads();
+    // stage C (as k_output): thread t keeps column c = t % ncol and walks rows r = (t1, oc)
+    const int WO = g.WO;
+    const int col0 = tc * TB * M;
+    const int ncol = min(ntb * M, WO - col0);
+    const int hrows = min(M, g.HO - ti * M);
+    const int plane = g.HO * WO;
+    const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
+    const unsigned nmag = c_magic32[ncol];
+    const int r0 = ncol == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
+    const int c = int(threadIdx.x) - r0 * ncol;
+    const int rstep = ncol == 1 ? NT : int(__umulhi(unsigned(NT), nmag));
+    const double rq = o.requant;
+    if (r0 < rstep) {
+        for (int r = r0; r < M * kOcc; r += rstep) {
+            const int oc = r & (kOcc - 1), t1 = r >> 5;
+            if (oc >= noc || t1 >= hrows) continue;
+            const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
+            const int y = s_y[r * YS + c];
+            if (o.y32) o.y32[x] = y;
+            if (o.y64) o.y64[x] = int64_t(y);
+            if (o.f32) o.f32[x] = __int2float_rn(y) * s_scalef[oc];
+            if (o.f64) o.f64[x] = double(y) * s_scale[oc];
+            if (o.i8) o.i8[x] = int8_t(fmin(fmax(rint(double(y) * s_scale[oc] * rq), 0.0), 127.0));
+        }
+    }
+    tl_mark(kTlOutput, 2);
+}
+
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -715,6 +812,28 @@ cudaError_t launch_output(int variant, int mode, const void* P, const ConvGeom& 
         case 2: return out_by_width<2>(mode, P, g, qp, sf, o, st, pdl);
         case 3: return out_by_width<3>(mode, P, g, qp, sf, o, st, pdl);
         default: return out_by_width<4>(mode, P, g, qp, sf, o, st, pdl);
+    }
+}
+
+cudaError_t launch_output_smallc(int variant, const int8_t* vq4, const int8_t* uq, const ConvGeom& g,
+                                 const QuantParams* qp, const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl) {
+    if (g.nrows > 65535 || (g.tw + kSmallTB - 1) / kSmallTB > 65535 || g.Cpad % 4) return cudaErrorInvalidConfiguration;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((g.OC + kOcc - 1) / kOcc), unsigned((g.tw + kSmallTB - 1) / kSmallTB),
+                       unsigned(g.nrows));
+    cfg.blockDim = dim3(32 * kSmallTB);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    const int32_t* v = reinterpret_cast<const int32_t*>(vq4);
+    switch (variant) {
+        case 0: return cudaLaunchKernelEx(&cfg, k_output_smallc<0>, v, uq, g, qp, sf, o);
+        case 1: return cudaLaunchKernelEx(&cfg, k_output_smallc<1>, v, uq, g, qp, sf, o);
+        case 2: return cudaLaunchKernelEx(&cfg, k_output_smallc<2>, v, uq, g, qp, sf, o);
+        default: return cudaErrorInvalidValue;
     }
 }
 

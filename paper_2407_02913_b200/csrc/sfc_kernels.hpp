@@ -134,6 +134,10 @@ struct OutPtrs {
 };
 // mode 0: exact int32 y, 1: exact int64 y, 2: general QuantConfig (fp64, no y_int),
 // 3: fp64 P [F][Tpad][OCpad] of the float path (no dequantisation)
+// Cin <= 4, exact int32 y: dp4a contraction fused with the output transform (no P);
+// vq4 = compact [F][T][4] int8 from the quantizing transform.
+cudaError_t launch_output_smallc(int variant, const int8_t* vq4, const int8_t* uq, const ConvGeom& g,
+                                 const QuantParams* qp, const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
 cudaError_t launch_output(int variant, int mode, const void* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
 // report sums: `sums` holds 2 + 2 * kSqErrBlocks doubles (result in [0..1], block partials after)

@@ -395,11 +395,13 @@ class SfcLayer:
                                    geom.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
         T, Tpad, Cpad, OCpad = (int(v) for v in geom[:4])
         F = self.spec.K ** 2
+        blocked = ctypes.c_int()
+        check(lib().sfc_conv_schedule(self._h, n, h, w, pad, None, ctypes.byref(blocked)))
+        if blocked.value == 3:  # Cin <= 4: vq compact [F][T][4], P never materialised
+            return _wrap_device(vq.value, (F, T, 4), torch.int8, self.device)[:, :, : self.IC], None
         vqt = _wrap_device(vq.value, (F, Tpad, Cpad), torch.int8, self.device)[:, :T, : self.IC]
         if not pa.value:
             return vqt, None
-        blocked = ctypes.c_int()
-        check(lib().sfc_conv_schedule(self._h, n, h, w, pad, None, ctypes.byref(blocked)))
         if blocked.value == 1:  # [Tpad][OCpad/32][F][32] -> [F][Tpad][OCpad] (a copy)
             pb = _wrap_device(pa.value, (Tpad, OCpad // 32, F, 32), torch.int32, self.device)
             return vqt, pb.permute(2, 0, 1, 3).reshape(F, Tpad, OCpad)[:, :T, : self.OC]
