@@ -355,6 +355,104 @@ __global__ void __launch_bounds__(32 * reg_tb<Y64>()) k_output_reg(const int32_t
 // the slice and the NEXT block's TMA load is issued at once, so it lands while this block
 // runs stage B (second inverse pass, y parked in shared memory) and stage C (coalesced
 // row-segment stores).  The transforms never round-trip through shared memory.
+// Stage C of the register output kernels: the block's row segments r = (t1, oc) of ncol
+// columns from s_y (rows of ys), all requested outputs (compile-time mask MK).  Even WO:
+// thread t keeps the column pair 2cp (cp = t % npair) and walks rows r = t / npair,
+// + nt / npair, ... (8-byte loads and stores: output offsets are even); odd WO (or pairs
+// off): single columns.
+template <int MK, bool Y64, int M, class acc_t>
+__device__ __forceinline__ void emit_rows(const acc_t* __restrict__ s_y, int ys, int nt, int noc, int hrows,
+                                          size_t base0, int plane, int WO, int ncol, bool pairs,
+                                          const double* __restrict__ scl, const float* __restrict__ sclf, double rq,
+                                          const OutPtrs& o) {
+    const int nit = pairs ? (ncol + 1) >> 1 : ncol;  // items per row
+    const unsigned nmag = c_magic32[nit];
+    const int r0 = nit == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
+    const int ci = int(threadIdx.x) - r0 * nit;
+    const int rstep = nit == 1 ? nt : int(__umulhi(unsigned(nt), nmag));
+    if (r0 >= rstep) return;
+    if (pairs) {
+        const int c = 2 * ci;
+        const bool two = c + 1 < ncol;
+        for (int r = r0; r < M * kOcc; r += rstep) {
+            const int oc = r & (kOcc - 1), t1 = r >> 5;
+            if (oc >= noc || t1 >= hrows) continue;
+            const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
+            acc_t y0, y1;
+            if constexpr (Y64) {
+                y0 = s_y[r * ys + c], y1 = s_y[r * ys + c + 1];
+            } else {
+                const int2 v = *reinterpret_cast<const int2*>(s_y + r * ys + c);
+                y0 = v.x, y1 = v.y;
+            }
+            if (two) {
+                if constexpr ((MK & 1) != 0) *reinterpret_cast<int2*>(o.y32 + x) = make_int2(int(y0), int(y1));
+                if constexpr ((MK & 2) != 0) {
+                    o.y64[x] = int64_t(y0);
+                    o.y64[x + 1] = int64_t(y1);
+                }
+                if constexpr ((MK & 4) != 0) {
+                    const float2 f = Y64 ? make_float2(float(double(y0) * scl[oc]), float(double(y1) * scl[oc]))
+                                         : make_float2(__int2float_rn(int(y0)) * sclf[oc],
+                                                       __int2float_rn(int(y1)) * sclf[oc]);
+                    *reinterpret_cast<float2*>(o.f32 + x) = f;
+                }
+                if constexpr ((MK & 8) != 0) {
+                    o.f64[x] = double(y0) * scl[oc];
+                    o.f64[x + 1] = double(y1) * scl[oc];
+                }
+                if constexpr ((MK & 16) != 0) {
+                    const int q0 = int(fmin(fmax(rint(double(y0) * scl[oc] * rq), 0.0), 127.0));
+                    const int q1 = int(fmin(fmax(rint(double(y1) * scl[oc] * rq), 0.0), 127.0));
+                    *reinterpret_cast<int16_t*>(o.i8 + x) = int16_t(q0 | (q1 << 8));
+                }
+            } else {
+                if constexpr ((MK & 1) != 0) o.y32[x] = int(y0);
+                if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y0);
+                if constexpr ((MK & 4) != 0)
+                    o.f32[x] = Y64 ? float(double(y0) * scl[oc]) : __int2float_rn(int(y0)) * sclf[oc];
+                if constexpr ((MK & 8) != 0) o.f64[x] = double(y0) * scl[oc];
+                if constexpr ((MK & 16) != 0) o.i8[x] = int8_t(fmin(fmax(rint(double(y0) * scl[oc] * rq), 0.0), 127.0));
+            }
+        }
+    } else {
+        const int c = ci;
+        for (int r = r0; r < M * kOcc; r += rstep) {
+            const int oc = r & (kOcc - 1), t1 = r >> 5;
+            if (oc >= noc || t1 >= hrows) continue;
+            const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
+            const acc_t y = s_y[r * ys + c];
+            if constexpr ((MK & 1) != 0) o.y32[x] = int(y);
+            if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y);
+            if constexpr ((MK & 4) != 0) o.f32[x] = Y64 ? float(double(y) * scl[oc]) : __int2float_rn(int(y)) * sclf[oc];
+            if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * scl[oc];
+            if constexpr ((MK & 16) != 0) o.i8[x] = int8_t(fmin(fmax(rint(double(y) * scl[oc] * rq), 0.0), 127.0));
+        }
+    }
+}
+
+// Runtime output mask -> emit_rows<MK>.
+template <bool Y64, int M, class acc_t>
+__device__ __forceinline__ void emit_rows_any(int mask, const acc_t* __restrict__ s_y, int ys, int nt, int noc,
+                                              int hrows, size_t base0, int plane, int WO, int ncol, bool pairs,
+                                              const double* __restrict__ scl, const float* __restrict__ sclf,
+                                              double rq, const OutPtrs& o) {
+    switch (mask) {
+#define SFC_EMIT_CASE(m)                                                                                      \
+    case m:                                                                                                   \
+        emit_rows<m, Y64, M>(s_y, ys, nt, noc, hrows, base0, plane, WO, ncol, pairs, scl, sclf, rq, o); \
+        break;
+        SFC_EMIT_CASE(1) SFC_EMIT_CASE(2) SFC_EMIT_CASE(3) SFC_EMIT_CASE(4) SFC_EMIT_CASE(5) SFC_EMIT_CASE(6)
+        SFC_EMIT_CASE(7) SFC_EMIT_CASE(8) SFC_EMIT_CASE(9) SFC_EMIT_CASE(10) SFC_EMIT_CASE(11) SFC_EMIT_CASE(12)
+        SFC_EMIT_CASE(13) SFC_EMIT_CASE(14) SFC_EMIT_CASE(15) SFC_EMIT_CASE(16) SFC_EMIT_CASE(17) SFC_EMIT_CASE(18)
+        SFC_EMIT_CASE(19) SFC_EMIT_CASE(20) SFC_EMIT_CASE(21) SFC_EMIT_CASE(22) SFC_EMIT_CASE(23) SFC_EMIT_CASE(24)
+        SFC_EMIT_CASE(25) SFC_EMIT_CASE(26) SFC_EMIT_CASE(27) SFC_EMIT_CASE(28) SFC_EMIT_CASE(29) SFC_EMIT_CASE(30)
+        SFC_EMIT_CASE(31)
+#undef SFC_EMIT_CASE
+        default: break;
+    }
+}
+
 template <int V>
 struct PersSmem {
     static constexpr int TB = out_tb<V>();
@@ -449,98 +547,13 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
             }
         }
         __syncthreads();
-        // stage C: row segments r = (t1, oc) of ncol columns.  Even WO: thread t keeps the
-        // column pair 2cp (cp = t % npair) and walks rows r = t / npair, + NT / npair, ...
-        // (8-byte loads and stores: output offsets are even); odd WO: single columns.
+        // stage C: coalesced row segments (emit_rows)
         const int col0 = tc * TB * M;
         const int ncol = min(ntb * M, WO - col0);  // <= TB * M <= 32
         const int hrows = min(M, g.HO - ti * M);
         const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
-        const bool pairs = (WO & 1) == 0 && o.pairs;
-        const int nit = pairs ? (ncol + 1) >> 1 : ncol;  // items per row
-        const unsigned nmag = c_magic32[nit];
-        const int r0 = nit == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
-        const int ci = int(threadIdx.x) - r0 * nit;
-        const int rstep = nit == 1 ? NT : int(__umulhi(unsigned(NT), nmag));
-        const double* scl = s_scale;
-        const float* sclf = s_scalef;
-        auto emit = [&](auto mask_c) {
-            constexpr int MK = decltype(mask_c)::value;
-            if (r0 >= rstep) return;
-            if (pairs) {
-                const int c = 2 * ci;
-                const bool two = c + 1 < ncol;
-                for (int r = r0; r < M * kOcc; r += rstep) {
-                    const int oc = r & (kOcc - 1), t1 = r >> 5;
-                    if (oc >= noc || t1 >= hrows) continue;
-                    const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
-                    acc_t y0, y1;
-                    if constexpr (Y64) {
-                        y0 = s_y[r * YS + c], y1 = s_y[r * YS + c + 1];
-                    } else {
-                        const int2 v = *reinterpret_cast<const int2*>(s_y + r * YS + c);
-                        y0 = v.x, y1 = v.y;
-                    }
-                    if (two) {
-                        if constexpr ((MK & 1) != 0) *reinterpret_cast<int2*>(o.y32 + x) = make_int2(int(y0), int(y1));
-                        if constexpr ((MK & 2) != 0) {
-                            o.y64[x] = int64_t(y0);
-                            o.y64[x + 1] = int64_t(y1);
-                        }
-                        if constexpr ((MK & 4) != 0) {
-                            const float2 f = Y64 ? make_float2(float(double(y0) * scl[oc]), float(double(y1) * scl[oc]))
-                                                 : make_float2(__int2float_rn(int(y0)) * sclf[oc],
-                                                               __int2float_rn(int(y1)) * sclf[oc]);
-                            *reinterpret_cast<float2*>(o.f32 + x) = f;
-                        }
-                        if constexpr ((MK & 8) != 0) {
-                            o.f64[x] = double(y0) * scl[oc];
-                            o.f64[x + 1] = double(y1) * scl[oc];
-                        }
-                        if constexpr ((MK & 16) != 0) {
-                            const int q0 = int(fmin(fmax(rint(double(y0) * scl[oc] * rq), 0.0), 127.0));
-                            const int q1 = int(fmin(fmax(rint(double(y1) * scl[oc] * rq), 0.0), 127.0));
-                            *reinterpret_cast<int16_t*>(o.i8 + x) = int16_t(q0 | (q1 << 8));
-                        }
-                    } else {
-                        if constexpr ((MK & 1) != 0) o.y32[x] = int(y0);
-                        if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y0);
-                        if constexpr ((MK & 4) != 0)
-                            o.f32[x] = Y64 ? float(double(y0) * scl[oc]) : __int2float_rn(int(y0)) * sclf[oc];
-                        if constexpr ((MK & 8) != 0) o.f64[x] = double(y0) * scl[oc];
-                        if constexpr ((MK & 16) != 0)
-                            o.i8[x] = int8_t(fmin(fmax(rint(double(y0) * scl[oc] * rq), 0.0), 127.0));
-                    }
-                }
-            } else {
-                const int c = ci;
-                for (int r = r0; r < M * kOcc; r += rstep) {
-                    const int oc = r & (kOcc - 1), t1 = r >> 5;
-                    if (oc >= noc || t1 >= hrows) continue;
-                    const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
-                    const acc_t y = s_y[r * YS + c];
-                    if constexpr ((MK & 1) != 0) o.y32[x] = int(y);
-                    if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y);
-                    if constexpr ((MK & 4) != 0)
-                        o.f32[x] = Y64 ? float(double(y) * scl[oc]) : __int2float_rn(int(y)) * sclf[oc];
-                    if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * scl[oc];
-                    if constexpr ((MK & 16) != 0)
-                        o.i8[x] = int8_t(fmin(fmax(rint(double(y) * scl[oc] * rq), 0.0), 127.0));
-                }
-            }
-        };
-        switch (mask) {
-#define SFC_EMIT_CASE(m) \
-    case m: emit(std::integral_constant<int, m>{}); break;
-            SFC_EMIT_CASE(1) SFC_EMIT_CASE(2) SFC_EMIT_CASE(3) SFC_EMIT_CASE(4) SFC_EMIT_CASE(5) SFC_EMIT_CASE(6)
-            SFC_EMIT_CASE(7) SFC_EMIT_CASE(8) SFC_EMIT_CASE(9) SFC_EMIT_CASE(10) SFC_EMIT_CASE(11) SFC_EMIT_CASE(12)
-            SFC_EMIT_CASE(13) SFC_EMIT_CASE(14) SFC_EMIT_CASE(15) SFC_EMIT_CASE(16) SFC_EMIT_CASE(17)
-            SFC_EMIT_CASE(18) SFC_EMIT_CASE(19) SFC_EMIT_CASE(20) SFC_EMIT_CASE(21) SFC_EMIT_CASE(22)
-            SFC_EMIT_CASE(23) SFC_EMIT_CASE(24) SFC_EMIT_CASE(25) SFC_EMIT_CASE(26) SFC_EMIT_CASE(27)
-            SFC_EMIT_CASE(28) SFC_EMIT_CASE(29) SFC_EMIT_CASE(30) SFC_EMIT_CASE(31)
-#undef SFC_EMIT_CASE
-            default: break;
-        }
+        emit_rows_any<Y64, M>(mask, s_y, YS, NT, noc, hrows, base0, plane, WO, ncol, (WO & 1) == 0 && o.pairs, s_scale,
+                              s_scalef, rq, o);
     }
     tl_mark(kTlOutput, 2);
 }
@@ -556,18 +569,25 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
 // int32 (the contraction is the same integer sum).
 constexpr int kSmallTB = 4;
 
+// Persistent over tile blocks: a CTA keeps one oc block (its uq words staged once) and walks
+// blocks (tc, row) = blockIdx.y, + gridDim.y, ...; per block the TB tiles' vq words [F][TB]
+// are staged in shared memory (16-byte runs of the compact layout), then each thread forms
+// its K^2 products with dp4a from two broadcast-free shared loads.
 template <int V>
 __global__ void __launch_bounds__(32 * kSmallTB) k_output_smallc(const int32_t* __restrict__ vq4,
                                                                  const int8_t* __restrict__ uq, ConvGeom g,
                                                                  const QuantParams* __restrict__ qpp,
-                                                                 const double* __restrict__ sf, OutPtrs o) {
+                                                                 const double* __restrict__ sf, OutPtrs o, int n_tc,
+                                                                 int nblk) {
     using T = Tab<V>;
-    constexpr int K = T::K, M = T::M, F = T::F, TB = kSmallTB, NT = 32 * TB, YS = (M * TB) | 1;
-    __shared__ int s_u[F * kOcc];      // uq words of this block's 32 output channels
+    constexpr int K = T::K, M = T::M, F = T::F, TB = kSmallTB, NT = 32 * TB;
+    constexpr int YS = ((M * TB + 1) & ~1) | 2;  // = 2 (mod 4): 8-byte aligned rows for the paired stores
+    __shared__ int s_u[F * kOcc];      // uq words of this CTA's 32 output channels
+    __shared__ int s_v[F * TB];        // vq words of the block's tiles
     __shared__ int s_y[M * kOcc * YS];  // rows r = (t1, oc) of YS
     __shared__ double s_scale[kOcc];
     __shared__ float s_scalef[kOcc];
-    const int oc0 = blockIdx.x * kOcc, tc = blockIdx.y, row = blockIdx.z;
+    const int oc0 = blockIdx.x * kOcc;
     const int lane = threadIdx.x & 31, tjl = threadIdx.x >> 5;
     tl_mark(kTlOutput, 0);
     for (int i = threadIdx.x; i < F * kOcc; i += NT) {  // the layer's filters: before the wait
@@ -575,10 +595,7 @@ __global__ void __launch_bounds__(32 * kSmallTB) k_output_smallc(const int32_t* 
         s_u[i] = oc0 + oc < g.OCpad ? *reinterpret_cast<const int*>(uq + (size_t(f) * g.OCpad + oc0 + oc) * g.Cpad)
                                     : 0;
     }
-    const int arow = g.row0 + row;
-    const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
     const int noc = min(kOcc, g.OC - oc0);
-    const int ntb = min(TB, g.tw - tc * TB);
     griddep_wait();  // vq and the activation scale complete
     tl_mark(kTlOutput, 1);
     griddep_launch_dependents();
@@ -587,57 +604,61 @@ __global__ void __launch_bounds__(32 * kSmallTB) k_output_smallc(const int32_t* 
         s_scale[threadIdx.x] = sc;
         s_scalef[threadIdx.x] = float(sc);
     }
-    __syncthreads();
-    if (tjl < ntb) {
-        const int32_t* vt = vq4 + (row * g.tw + tc * TB + tjl);  // + f * T
-        int q[K][M];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            int pr[K], qt[M];
-#pragma unroll
-            for (int l = 0; l < K; ++l) {
-                const int f = k * K + l;
-                pr[l] = __dp4a(__ldg(vt + size_t(f) * g.T), s_u[f * kOcc + lane], 0);
-            }
-            inv1d<V>(pr, qt);
-#pragma unroll
-            for (int t2 = 0; t2 < M; ++t2) q[k][t2] = qt[t2];
-        }
-#pragma unroll
-        for (int t2 = 0; t2 < M; ++t2) {
-            int qc[K], yt[M];
-#pragma unroll
-            for (int k = 0; k < K; ++k) qc[k] = q[k][t2];
-            inv1d<V>(qc, yt);
-#pragma unroll
-            for (int t1 = 0; t1 < M; ++t1) s_y[(t1 * kOcc + lane) * YS + tjl * M + t2] = yt[t1];
-        }
-    }
-    __syncthreads();
-    // stage C (as k_output): thread t keeps column c = t % ncol and walks rows r = (t1, oc)
-    const int WO = g.WO;
-    const int col0 = tc * TB * M;
-    const int ncol = min(ntb * M, WO - col0);
-    const int hrows = min(M, g.HO - ti * M);
-    const int plane = g.HO * WO;
-    const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
-    const unsigned nmag = c_magic32[ncol];
-    const int r0 = ncol == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
-    const int c = int(threadIdx.x) - r0 * ncol;
-    const int rstep = ncol == 1 ? NT : int(__umulhi(unsigned(NT), nmag));
+    const int WO = g.WO, plane = g.HO * WO;
     const double rq = o.requant;
-    if (r0 < rstep) {
-        for (int r = r0; r < M * kOcc; r += rstep) {
-            const int oc = r & (kOcc - 1), t1 = r >> 5;
-            if (oc >= noc || t1 >= hrows) continue;
-            const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
-            const int y = s_y[r * YS + c];
-            if (o.y32) o.y32[x] = y;
-            if (o.y64) o.y64[x] = int64_t(y);
-            if (o.f32) o.f32[x] = __int2float_rn(y) * s_scalef[oc];
-            if (o.f64) o.f64[x] = double(y) * s_scale[oc];
-            if (o.i8) o.i8[x] = int8_t(fmin(fmax(rint(double(y) * s_scale[oc] * rq), 0.0), 127.0));
+    const int mask = (o.y32 ? 1 : 0) | (o.y64 ? 2 : 0) | (o.f32 ? 4 : 0) | (o.f64 ? 8 : 0) | (o.i8 ? 16 : 0);
+    for (int blk = blockIdx.y; blk < nblk; blk += gridDim.y) {
+        const int tc = blk % n_tc, row = blk / n_tc;
+        const int arow = g.row0 + row;
+        const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
+        const int ntb = min(TB, g.tw - tc * TB);
+        const int t0 = row * g.tw + tc * TB;
+        __syncthreads();  // the previous block is done with s_v and s_y
+        {
+            constexpr int kPer = (F * TB + NT - 1) / NT;  // every load in flight before the stores
+            int v[kPer];
+#pragma unroll
+            for (int jj = 0; jj < kPer; ++jj) {
+                const int i = int(threadIdx.x) + jj * NT, f = i / TB, j = i - f * TB;
+                v[jj] = i < F * TB && j < ntb ? __ldg(vq4 + size_t(f) * g.T + t0 + j) : 0;
+            }
+#pragma unroll
+            for (int jj = 0; jj < kPer; ++jj)
+                if (int(threadIdx.x) + jj * NT < F * TB) s_v[threadIdx.x + jj * NT] = v[jj];
         }
+        __syncthreads();
+        if (tjl < ntb) {
+            int q[K][M];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                int pr[K], qt[M];
+#pragma unroll
+                for (int l = 0; l < K; ++l) {
+                    const int f = k * K + l;
+                    pr[l] = __dp4a(s_v[f * TB + tjl], s_u[f * kOcc + lane], 0);
+                }
+                inv1d<V>(pr, qt);
+#pragma unroll
+                for (int t2 = 0; t2 < M; ++t2) q[k][t2] = qt[t2];
+            }
+#pragma unroll
+            for (int t2 = 0; t2 < M; ++t2) {
+                int qc[K], yt[M];
+#pragma unroll
+                for (int k = 0; k < K; ++k) qc[k] = q[k][t2];
+                inv1d<V>(qc, yt);
+#pragma unroll
+                for (int t1 = 0; t1 < M; ++t1) s_y[(t1 * kOcc + lane) * YS + tjl * M + t2] = yt[t1];
+            }
+        }
+        __syncthreads();
+        // stage C: coalesced row segments (emit_rows)
+        const int col0 = tc * TB * M;
+        const int ncol = min(ntb * M, WO - col0);
+        const int hrows = min(M, g.HO - ti * M);
+        const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
+        emit_rows_any<false, M>(mask, s_y, YS, NT, noc, hrows, base0, plane, WO, ncol, (WO & 1) == 0 && !o.i8, s_scale,
+                                s_scalef, rq, o);
     }
     tl_mark(kTlOutput, 2);
 }
@@ -817,10 +838,13 @@ cudaError_t launch_output(int variant, int mode, const void* P, const ConvGeom& 
 
 cudaError_t launch_output_smallc(int variant, const int8_t* vq4, const int8_t* uq, const ConvGeom& g,
                                  const QuantParams* qp, const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl) {
-    if (g.nrows > 65535 || (g.tw + kSmallTB - 1) / kSmallTB > 65535 || g.Cpad % 4) return cudaErrorInvalidConfiguration;
+    const int n_ob = (g.OC + kOcc - 1) / kOcc, n_tc = (g.tw + kSmallTB - 1) / kSmallTB;
+    const long nblk = long(n_tc) * g.nrows;
+    if (nblk > 0x7fffffffL || n_ob > 65535 || g.Cpad % 4) return cudaErrorInvalidConfiguration;
+    // ~6 CTAs of 4 warps per SM (shared memory ~34 KB each), split over the oc blocks
+    const long want = (long(sm_count_out()) * 6 + n_ob - 1) / n_ob;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned((g.OC + kOcc - 1) / kOcc), unsigned((g.tw + kSmallTB - 1) / kSmallTB),
-                       unsigned(g.nrows));
+    cfg.gridDim = dim3(unsigned(n_ob), unsigned(std::min<long>(std::min<long>(nblk, want), 65535)));
     cfg.blockDim = dim3(32 * kSmallTB);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -830,9 +854,9 @@ cudaError_t launch_output_smallc(int variant, const int8_t* vq4, const int8_t* u
     cfg.numAttrs = pdl ? 1 : 0;
     const int32_t* v = reinterpret_cast<const int32_t*>(vq4);
     switch (variant) {
-        case 0: return cudaLaunchKernelEx(&cfg, k_output_smallc<0>, v, uq, g, qp, sf, o);
-        case 1: return cudaLaunchKernelEx(&cfg, k_output_smallc<1>, v, uq, g, qp, sf, o);
-        case 2: return cudaLaunchKernelEx(&cfg, k_output_smallc<2>, v, uq, g, qp, sf, o);
+        case 0: return cudaLaunchKernelEx(&cfg, k_output_smallc<0>, v, uq, g, qp, sf, o, n_tc, int(nblk));
+        case 1: return cudaLaunchKernelEx(&cfg, k_output_smallc<1>, v, uq, g, qp, sf, o, n_tc, int(nblk));
+        case 2: return cudaLaunchKernelEx(&cfg, k_output_smallc<2>, v, uq, g, qp, sf, o, n_tc, int(nblk));
         default: return cudaErrorInvalidValue;
     }
 }
