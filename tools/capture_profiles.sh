@@ -8,9 +8,11 @@ python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/prof/bench_p
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/prof/launches_w2.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/prof/ncu_launches.log 2>&1
 for w in 2 5; do
+  # stage kernels per forward matched by the regex: kept-V schedule (w2) 3, recompute (w5) 4
+  n=$([ $w = 5 ] && echo 4 || echo 3)
   for v in sfc4-4x4-3x3 sfc6-6x6-3x3 sfc6-7x7-3x3; do
     python tools/prof_once.py --workload $w --variant $v --iters 2 > /dev/null 2>&1 || continue
-    ncu --set full --import-source on --clock-control none -k regex:"k_act|k_quant|k_gemm|k_output" -s 4 -c 4 \
+    ncu --set full --import-source on --clock-control none -k regex:"k_act|k_quant|k_gemm|k_output" -s $n -c $n \
         -o gpurun_out/prof/full_w${w}_${v} python tools/prof_once.py --workload $w --variant $v --iters 2 \
         > gpurun_out/prof/ncu_full_w${w}_${v}.log 2>&1
   done

@@ -21,6 +21,8 @@ VARIANTS = ["sfc4-4x4-3x3", "sfc6-6x6-3x3", "sfc6-7x7-3x3"]
 
 
 def stage_of(name):
+    if "k_act_row<" in name:  # register-resident SWAR transform: MODE 0/2 absmax (+kept V), 1 quantize
+        return "quantize" if re.search(r"k_act_row<\d+, 1,", name) else "absmax"
     if "k_act_pair<" in name:  # the two-channel SWAR form (large layers)
         return "absmax" if re.search(r"k_act_pair<\d+, 0>", name) else "act_quant"
     if "k_act<" in name:
@@ -43,7 +45,9 @@ for r in rows[1:]:
     k = re.sub(r"<(\d+), (\d+), \d+>", r"<\1, \2, CC>", k)
     tot[k] += float(r[iv]) / 1e3
     cnt[k] += 1
-ours = {k: v for k, v in tot.items() if k.split("<")[0] in ("k_zero_words", "k_act", "k_quant_kept", "k_gemm", "k_output")}
+ours = {k: v for k, v in tot.items() if k.split("<")[0] in ("k_zero_words", "k_act", "k_act_row", "k_act_pair",
+                                                           "k_quant_kept", "k_gemm", "k_output", "k_output_pers",
+                                                           "k_output_smallc", "k_output_reg")}
 s_all = sum(ours.values())
 with open(os.path.join(dst, f"{tag}_launches_w2.txt"), "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum --clock-control none of\n"
