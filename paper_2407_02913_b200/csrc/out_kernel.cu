@@ -786,7 +786,9 @@ cudaError_t out_pers_launch(const void* P, const ConvGeom& g, const QuantParams*
 bool out_pers_wanted(int variant, int mode, const ConvGeom& g, const OutPtrs& o) {
     // (int8 requant outputs: the one-block kernel measured faster on every ResNet-18 / VGG-16
     // layer, e.g. VGG-16 14.5 vs 15.5 ms; int32 / fp32 outputs: config 5 0.110 vs 0.119 ms)
-    if (variant > 2 || mode > 1 || o.p_discard || g.pblk || o.i8) return false;
+    // (and y32 / fp32 on narrower layers: VGG-16 layer 5 (256 channels) 0.438 vs 0.359 ms, layer 1
+    // (64 channels) 1.85 vs 1.16 ms -- the 96-thread persistent CTAs keep too little in flight)
+    if (variant > 2 || mode > 1 || o.p_discard || g.pblk || o.i8 || g.OC < 512) return false;
     // small layers (config 2: 320 blocks) keep the 512-thread one-block CTAs: a persistent CTA
     // of 64-192 threads has the longer per-block latency chain
     const int tb = variant == 0 ? out_tb<0>() : variant == 1 ? out_tb<1>() : out_tb<2>();
