@@ -175,11 +175,11 @@ int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_work
  *   *recompute  0: the absmax pass keeps V and the GEMM quantizes it (sfc_act_transform +
  *                  sfc_conv_kept); 1: absmax only, then a quantizing transform writes vq
  *                  (sfc_act_absmax + sfc_conv_int8).  Both are bit-identical.
- *   *p_layout   layout of the pacc view: 0 = [F][Tpad][OCpad] (default), 1 =
- *               [Tpad][OCpad/32][F][32], 2 = [Tpad][F][OCpad] (SFC_P_BLOCKED=1/2: the register
- *               output transform reads a tile's frequencies as one run), 3 = no P: Cin <= 4
- *               layers contract with dp4a inside the output transform, and the vq view is
- *               compact [F][T][4] (SFC_SMALLC=0 keeps the tensor-core GEMM). */
+ *   *p_layout   storage of pacc in the workspace: 0 = int32 [F][Tpad][OCpad]; 1 = 24-bit
+ *               planar [F][Tpad] rows of 3*OCpad bytes (OCpad int16 low halves, then OCpad
+ *               int8 high bytes; exact as qmax^2 * Cin < 2^23; SFC_P24=0 keeps int32);
+ *               3 = no P: Cin <= 4 layers contract with dp4a inside the output transform and
+ *               the vq view is compact [F][T][4] (SFC_SMALLC=0 keeps the tensor-core GEMM). */
 int sfc_conv_schedule(sfc_layer_t layer, int n, int h, int w, int pad, int* recompute, int* p_layout);
 
 /* Exact int8 direct correlation (int32 accumulate), the report baseline

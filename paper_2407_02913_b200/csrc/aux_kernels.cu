@@ -231,7 +231,7 @@ void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, in
     g.th_magic = g.th == 1 ? 0u : 0xffffffffu / unsigned(g.th) + 1u;
     g.row0 = 0;
     g.nrows = B * g.th;
-    g.pblk = 0;
+    g.p24 = 0;
 }
 
 PChunk p_chunk(const ConvGeom& g, int F) {

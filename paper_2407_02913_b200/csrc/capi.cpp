@@ -172,13 +172,16 @@ void gemm_output(const sfc_layer* L, const ConvGeom& g, const WsView& v, int mod
     }
 }
 
-// The blocked P layout (ConvGeom::pblk) feeds the register output transform: the exact
-// int32 / int64 modes of the 3x3 variants, P not chunked.  SFC_P_BLOCKED=0 keeps
-// [F][Tpad][OCpad] and the TMA-slice output kernel (A/B knob).
-int p_blocked(const sfc_layer* L, const ConvGeom& g) {
-    static const char* force = std::getenv("SFC_P_BLOCKED");
-    if (!(!L->general && L->variant <= 2 && p_chunk(g, L->F).n == 1 && g.OCpad % 32 == 0)) return 0;
-    return force ? std::atoi(force) : 0;  // default [F][Tpad][OCpad]: measured best on configs 2 and 5
+// 24-bit planar P (ConvGeom::p24): exact while qmax^2 * Cin < 2^23 (|vq|, |uq| <= qmax under
+// MinMax), for the exact int32 / int64 outputs of the 3x3 variants with P whole; the P
+// round trip (GEMM epilogue writes, output transform reads) shrinks by a quarter.
+// SFC_P24=0 keeps int32 P (A/B knob).
+bool p24_wanted(const sfc_layer* L, const ConvGeom& g) {
+    const char* e = std::getenv("SFC_P24");
+    if (e && e[0] == '0') return false;
+    if (L->general || L->variant > 2 || p_chunk(g, L->F).n > 1) return false;
+    const double qmax = double((1 << (L->bits - 1)) - 1);
+    return qmax * qmax * double(L->IC) < 8388608.0;
 }
 
 // Layers with Cin <= 4 (3x3 variants, exact int32 y, whole P): the dp4a contraction fused
@@ -239,7 +242,7 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     check_call(L, kept ? ws : static_cast<const void*>(d_x), n, h, w, pad);
     if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
     ConvGeom g = geom_of(L, n, h, w, pad);
-    g.pblk = p_blocked(L, g);
+    g.p24 = p24_wanted(L, g) ? 1 : 0;
     if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
     const bool need64 = needs_y64(L, o);
     WsView v = carve(ws, g, L->F);
@@ -714,7 +717,7 @@ int sfc_conv_schedule(sfc_layer_t L, int n, int h, int w, int pad, int* recomput
         check_call(L, L, n, h, w, pad);
         const ConvGeom g = geom_of(L, n, h, w, pad);
         if (recompute) *recompute = forward_recomputes(L, g) ? 1 : 0;
-        if (p_layout) *p_layout = small_c(L, g) ? 3 : p_blocked(L, g);
+        if (p_layout) *p_layout = small_c(L, g) ? 3 : (p24_wanted(L, g) ? 1 : 0);
     });
 }
 

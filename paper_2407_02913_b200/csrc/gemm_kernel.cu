@@ -29,13 +29,6 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
         "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-            reinterpret_cast<uint64_t>(map)),
-        "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-        : "memory");
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -51,18 +44,10 @@ constexpr int kEpiBoxBytes = 32 * 32 * 4;    // 32 rows x 32 int32 (one 128B-swi
 template <bool QF>
 constexpr int gemm_threads() { return 64 + 32 * kEpiWarps + (QF ? 32 * kConvWarps : 0); }
 
-// Work unit -> (oc block, tile block, frequency).  [F][Tpad][OCpad] P: oc block fastest, so
-// co-resident CTAs share a frequency's A tile in L2.  Blocked P ([Tpad][OCpad/32][F][32]):
-// frequency fastest, so co-resident CTAs write neighbouring 128-byte pieces of the same
-// (tile, 32-channel) runs and the line write-backs keep DRAM page locality.
-__device__ __forceinline__ void unit_of(int u, int n_ob, int n_tb, int F, int pblk, int& ob, int& tb, int& f) {
-    if (pblk == 1) {
-        f = u % F;
-        const int r = u / F;
-        ob = r % n_ob, tb = r / n_ob;
-    } else {
-        ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
-    }
+// Work unit -> (oc block, tile block, frequency): oc block fastest, so co-resident CTAs share
+// a frequency's A tile in L2.
+__device__ __forceinline__ void unit_of(int u, int n_ob, int n_tb, int& ob, int& tb, int& f) {
+    ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
 }
 
 // Quantizer parameters for a subset of warps (no CTA-wide barrier): table or warp derivation.
@@ -85,7 +70,8 @@ __device__ __forceinline__ QuantParams qparams_warp(int vmax, int bits, const Qu
 template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmP, int n_tb, int n_ob, int F, int nk, ConvGeom g, QFuse qf) {
+           const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2, int n_tb, int n_ob,
+           int F, int nk, ConvGeom g, QFuse qf) {
     static_assert(!QT || QF, "the TMA-staged V feeds the converters");
     constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
@@ -125,6 +111,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         if (!QF || QT) ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB);
         ptx::tma_prefetch(&tmP);
+        if (g.p24) ptx::tma_prefetch(&tmP2);
     }
     if (warp == 1) ptx::tmem_alloc(tmem_holder, kTmemCols);
     ptx::tc_fence_before();
@@ -142,7 +129,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 int ob, tb, f;
-                unit_of(u, n_ob, n_tb, F, g.pblk, ob, tb, f);
+                unit_of(u, n_ob, n_tb, ob, tb, f);
                 for (int kc = 0; kc < nk; ++kc) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (QF) {
@@ -195,7 +182,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         int i = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
             int ob, tb, f;
-            unit_of(u, n_ob, n_tb, F, g.pblk, ob, tb, f);
+            unit_of(u, n_ob, n_tb, ob, tb, f);
             const int ab = i & 1;
             ptx::mbar_wait(&tfull[ab], (i >> 1) & 1);
             ptx::tc_fence_after();
@@ -206,22 +193,46 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 ptx::tmem_wait_ld();
                 if (lane == 0) bulk_wait_read<kEpiBufs - 1>();  // this buffer's previous store has read smem
                 __syncwarp();
-                // row `lane` of a 32 x 32 int32 box, 16-byte chunk j stored at j ^ (lane & 7) (128B swizzle)
-                uint8_t* row = myE + buf * kEpiBoxBytes + lane * 128;
+                uint8_t* box = myE + buf * kEpiBoxBytes;
+                if (g.p24) {
+                    // 24-bit planar P: row `lane` of a 32 x 64 B box of int16 low halves (64B
+                    // swizzle: chunk j at j ^ ((lane >> 1) & 3)) and of a 32 x 32 B box of int8
+                    // high bytes (32B swizzle: chunk j at j ^ ((lane >> 2) & 1))
+                    uint32_t lo[16], hi[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    *reinterpret_cast<int4*>(row + ((j ^ (lane & 7)) << 4)) =
-                        make_int4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+                    for (int j = 0; j < 16; ++j) lo[j] = __byte_perm(uint32_t(r[2 * j]), uint32_t(r[2 * j + 1]), 0x5410);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        hi[j] = __byte_perm(__byte_perm(uint32_t(r[4 * j]), uint32_t(r[4 * j + 1]), 0x0062),
+                                            __byte_perm(uint32_t(r[4 * j + 2]), uint32_t(r[4 * j + 3]), 0x0062), 0x5410);
+                    uint8_t* rl = box + lane * 64;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        *reinterpret_cast<uint4*>(rl + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                            make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
+                    uint8_t* rh = box + 2048 + lane * 32;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        *reinterpret_cast<uint4*>(rh + ((j ^ ((lane >> 2) & 1)) << 4)) =
+                            make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
+                } else {
+                    // row `lane` of a 32 x 32 int32 box, 16-byte chunk j stored at j ^ (lane & 7) (128B swizzle)
+                    uint8_t* row = box + lane * 128;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<int4*>(row + ((j ^ (lane & 7)) << 4)) =
+                            make_int4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+                }
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    if (g.pblk == 2)  // [Tpad][F][OCpad]: coordinates (oc, f, t)
-                        tma_store_3d(&tmP, myE + buf * kEpiBoxBytes, ob * BN + c, f, tb * kRowsPerTile + q * 32);
-                    else if (g.pblk)  // [Tpad][OCpad/32][F][32]: coordinates (oc within group, f, group, t)
-                        tma_store_4d(&tmP, myE + buf * kEpiBoxBytes, 0, f, (ob * BN + c) >> 5,
-                                     tb * kRowsPerTile + q * 32);
-                    else
-                        tma_store_3d(&tmP, myE + buf * kEpiBoxBytes, ob * BN + c, tb * kRowsPerTile + q * 32, f);
+                    const int t0 = tb * kRowsPerTile + q * 32, o0 = ob * BN + c;
+                    if (g.p24) {  // byte coordinates: low halves at 2*oc, high bytes at oc (second map)
+                        tma_store_3d(&tmP, box, 2 * o0, t0, f);
+                        tma_store_3d(&tmP2, box + 2048, o0, t0, f);
+                    } else {
+                        tma_store_3d(&tmP, box, o0, t0, f);
+                    }
                     bulk_commit();
                 }
                 buf = (buf + 1) % kEpiBufs;
@@ -291,7 +302,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         auto load = [&](int s, uint4 (&va)[kItems], uint4 (&vb)[kItems]) {
             const int u = int(blockIdx.x) + (s / nk) * int(gridDim.x), kc = s % nk;
             int ob, tb, f;
-            unit_of(u, n_ob, n_tb, F, g.pblk, ob, tb, f);
+            unit_of(u, n_ob, n_tb, ob, tb, f);
 #pragma unroll
             for (int j = 0; j < kItems; ++j) {
                 const int i = ct + j * (32 * kConvWarps);
@@ -386,32 +397,29 @@ bool make_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void*
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// The GEMM's P map: [F][Tpad][OCpad] int32 boxes of 32 x 32 (rows x oc), or the blocked
-// layout [Tpad][OCpad/32][F][32] as a 4-D map (32 oc, F, OCpad/32, Tpad) with box (32, 1, 1, 32)
-// -- the same 32 x 128-byte shared box, 128B-swizzled.
-bool make_p_map(CUtensorMap* m, int32_t* P, const ConvGeom& g, int F, int rows) {
-    if (!g.pblk)
+// The GEMM's P maps: int32 [F][Tpad][OCpad] boxes of 32 x 32 (rows x oc), 128B-swizzled; or
+// 24-bit planar rows of 3*OCpad bytes: the low-half map (2*OCpad bytes, box 64 B x 32 rows,
+// 64B swizzle) and the high-byte map (OCpad bytes from byte 2*OCpad, box 32 B x 32, 32B
+// swizzle).
+bool make_p_maps(CUtensorMap* m, CUtensorMap* m2, int32_t* P, const ConvGeom& g, int F, int rows) {
+    if (!g.p24) {
+        *m2 = CUtensorMap{};
         return make_tmap_3d(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, rows, F, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (g.pblk == 2) {  // [Tpad][F][OCpad] as (OCpad, F, Tpad), box (32, 1, 32)
-        auto fn = encode_fn();
-        if (!fn) return false;
-        cuuint64_t dims[3] = {cuuint64_t(g.OCpad), cuuint64_t(F), cuuint64_t(rows)};
-        cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * 4, cuuint64_t(g.OCpad) * F * 4};
-        cuuint32_t box[3] = {32, 1, 32};
-        cuuint32_t estr[3] = {1, 1, 1};
-        return fn(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
     auto fn = encode_fn();
     if (!fn) return false;
-    const cuuint64_t ng = cuuint64_t(g.OCpad / 32);
-    cuuint64_t dims[4] = {32, cuuint64_t(F), ng, cuuint64_t(rows)};
-    cuuint64_t strides[3] = {128, cuuint64_t(F) * 128, ng * F * 128};
-    cuuint32_t box[4] = {32, 1, 1, 32};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    const cuuint64_t rb = cuuint64_t(g.OCpad) * 3;  // row bytes
+    cuuint64_t dlo[3] = {cuuint64_t(g.OCpad) * 2, cuuint64_t(rows), cuuint64_t(F)};
+    cuuint64_t dhi[3] = {cuuint64_t(g.OCpad), cuuint64_t(rows), cuuint64_t(F)};
+    cuuint64_t strides[2] = {rb, rb * rows};
+    cuuint32_t blo[3] = {64, 32, 1}, bhi[3] = {32, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    uint8_t* base = reinterpret_cast<uint8_t*>(P);
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dlo, strides, blo, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+               CUDA_SUCCESS &&
+           fn(m2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base + 2 * size_t(g.OCpad), dhi, strides, bhi, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -427,8 +435,8 @@ int sm_count() {
 }
 
 template <int BN, int BK, int STAGES, bool QF, bool QT = false>
-cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const ConvGeom& g, int F,
-                        const QFuse& qf, cudaStream_t st, bool pdl) {
+cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
+                        const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl) {
     const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + (QT ? size_t(STAGES) * kRowsPerTile * BK * 2 : 0) +
                         size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256;
     auto kern = k_gemm<BN, BK, STAGES, QF, QT>;
@@ -457,33 +465,33 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, a, b, p, n_tb, n_ob, F, g.Cpad / BK, g, qf);
+    return cudaLaunchKernelEx(&cfg, kern, a, b, p, p2, n_tb, n_ob, F, g.Cpad / BK, g, qf);
 }
 
 template <int BK, int STAGES, bool QF>
-cudaError_t gemm_by_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const ConvGeom& g, int F,
-                       const QFuse& qf, cudaStream_t st, bool pdl) {
-    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, g, F, qf, st, pdl);
-    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, g, F, qf, st, pdl);
-    return gemm_launch<256, BK, STAGES, QF>(a, b, p, g, F, qf, st, pdl);
+cudaError_t gemm_by_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
+                       const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl) {
+    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
+    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
+    return gemm_launch<256, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
 }
 
 template <bool QF>
 cudaError_t gemm_dispatch(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, const QFuse& qf,
                           cudaStream_t st, bool pdl) {
-    CUtensorMap ta, tb, tp;
+    CUtensorMap ta, tb, tp, tp2;
     const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     // (QF: the A map is unused; it is built over the filters only to keep one kernel signature)
     if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, QF ? static_cast<const void*>(uqB) : vqA, g.Cpad,
                       QF ? g.OCpad : g.Tpad, F, g.BK, QF ? g.BN : kRowsPerTile, sw) ||
         !make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
-        !make_p_map(&tp, P, g, F, g.Tpad))
+        !make_p_maps(&tp, &tp2, P, g, F, g.Tpad))
         return cudaErrorInvalidValue;
     const int nk = g.Cpad / g.BK;
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, g, F, qf, st, pdl)
-                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, g, F, qf, st, pdl);
-    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, g, F, qf, st, pdl) : gemm_by_bn<64, 4, QF>(ta, tb, tp, g, F, qf, st, pdl);
+        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl)
+                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl);
+    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl) : gemm_by_bn<64, 4, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl);
 }
 }  // namespace
 
@@ -496,7 +504,7 @@ cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, c
                              int tcpad, cudaStream_t st, bool pdl) {
     // A: rows [t0, t0 + tcpad) of every frequency plane of vq (rows past the planes' Tpad
     // read as zeros); P: a buffer of tcpad rows per frequency
-    CUtensorMap ta, tb, tp;
+    CUtensorMap ta, tb, tp, tp2{};
     const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     const int arows = tcpad < g.Tpad - t0 ? tcpad : g.Tpad - t0;
     if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, vqA + size_t(t0) * g.Cpad, g.Cpad, arows, F, g.BK,
@@ -509,10 +517,10 @@ cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, c
     const int nk = g.Cpad / g.BK;
     const QFuse none{};
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, gc, F, none, st, pdl)
-                       : gemm_by_bn<128, 3, false>(ta, tb, tp, gc, F, none, st, pdl);
-    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, gc, F, none, st, pdl)
-                   : gemm_by_bn<64, 4, false>(ta, tb, tp, gc, F, none, st, pdl);
+        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl)
+                       : gemm_by_bn<128, 3, false>(ta, tb, tp, tp2, gc, F, none, st, pdl);
+    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl)
+                   : gemm_by_bn<64, 4, false>(ta, tb, tp, tp2, gc, F, none, st, pdl);
 }
 
 cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
@@ -525,7 +533,7 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
     // V [F][Tpad][Cpad] int16 seen as (C, T, F): channels >= C and rows >= T read as zero
     auto fn = encode_fn();
     if (!fn) return cudaErrorInvalidValue;
-    CUtensorMap tv, tb, tp;
+    CUtensorMap tv, tb, tp, tp2;
     cuuint64_t dims[3] = {cuuint64_t(g.C), cuuint64_t(g.T), cuuint64_t(F)};
     cuuint64_t strides[2] = {cuuint64_t(g.Cpad) * 2, cuuint64_t(g.Cpad) * g.Tpad * 2};
     cuuint32_t box[3] = {cuuint32_t(g.BK), cuuint32_t(kRowsPerTile), 1};
@@ -536,17 +544,17 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
         return cudaErrorInvalidValue;
     const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     if (!make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
-        !make_p_map(&tp, P, g, F, g.Tpad))
+        !make_p_maps(&tp, &tp2, P, g, F, g.Tpad))
         return cudaErrorInvalidValue;
     // two stages: A + B + V stages and the epilogue boxes fill the 227 KB at BN = 256, BK = 128
     if (g.BK == 128) {
-        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
-        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
-        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
+        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
     }
-    if (g.BN == 64) return gemm_launch<64, 64, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
-    if (g.BN == 128) return gemm_launch<128, 64, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
-    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, g, F, q, st, pdl);
+    if (g.BN == 64) return gemm_launch<64, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+    if (g.BN == 128) return gemm_launch<128, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
 }
 
 SFC_TL_UNIT_READER(tl_read_gemm)

@@ -86,10 +86,10 @@ __constant__ unsigned c_magic32[33] = {  // 0xffffffff / d + 1 (exact for t < 2^
 // (oc, f) before the inverse transform, which then runs in fp64: quant.cpp:258-278),
 // 3: fp64 P of the float path (fast_conv2d, conv.cpp:495-510), no dequantisation,
 // 4: as 2 from an fp64 P (the exact-integer P of the 9-16 bit path, |P| < 2^53).
-template <int V, int MODE>
+template <int V, int MODE, bool P24 = false>
 __global__ void __launch_bounds__(kOutThreads, 2)
-    k_output(const __grid_constant__ CUtensorMap tmP, ConvGeom g, const QuantParams* __restrict__ qpp,
-             const double* __restrict__ sf, OutPtrs o) {
+    k_output(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2, ConvGeom g,
+             const QuantParams* __restrict__ qpp, const double* __restrict__ sf, OutPtrs o) {
     using T = Tab<V>;
     constexpr int K = T::K, M = T::M, TB = out_tbm<V, MODE>();
     constexpr bool Y64 = MODE == 1;
@@ -108,8 +108,12 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     // chunk-relative, the output position uses the absolute row g.row0 + row
     const int oc0 = blockIdx.x * kOcc, tc = blockIdx.y, row = blockIdx.z;
     tl_mark(kTlOutput, 0);
+    // 24-bit planar P: the slice's int16 low halves [F][TB][kOcc], then its int8 high bytes
+    const int16_t* sp_lo = reinterpret_cast<const int16_t*>(smem);
+    const int8_t* sp_hi = reinterpret_cast<const int8_t*>(smem + size_t(T::F) * TB * kOcc * 2);
     if (threadIdx.x == 0) {
         ptx::tma_prefetch(&tmP);
+        if (P24) ptx::tma_prefetch(&tmP2);
         ptx::mbar_init(full, 1);
         ptx::fence_mbar_init();
     }
@@ -118,8 +122,14 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     tl_mark(kTlOutput, 1);
     griddep_launch_dependents();
     if (threadIdx.x == 0) {
-        ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * sizeof(p_elem_t<MODE>)));
-        ptx::tma_load_3d(smem, &tmP, full, oc0, row * g.tw + tc * TB, 0);
+        if constexpr (P24) {
+            ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 3));
+            ptx::tma_load_3d(smem, &tmP, full, 2 * oc0, row * g.tw + tc * TB, 0);
+            ptx::tma_load_3d(smem + size_t(T::F) * TB * kOcc * 2, &tmP2, full, oc0, row * g.tw + tc * TB, 0);
+        } else {
+            ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * sizeof(p_elem_t<MODE>)));
+            ptx::tma_load_3d(smem, &tmP, full, oc0, row * g.tw + tc * TB, 0);
+        }
     }
     const int arow = g.row0 + row;
     const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
@@ -147,7 +157,13 @@ __global__ void __launch_bounds__(kOutThreads, 2)
         if (tj >= ntb) continue;
         acc_t pk[K], qt[M];
 #pragma unroll
-        for (int k = 0; k < K; ++k) pk[k] = sp[((k * K + l) * TB + tj) * kOcc + oc];
+        for (int k = 0; k < K; ++k) {
+            const int e = ((k * K + l) * TB + tj) * kOcc + oc;
+            if constexpr (P24)
+                pk[k] = acc_t((int(sp_hi[e]) << 16) | int(uint16_t(sp_lo[e])));
+            else
+                pk[k] = sp[e];
+        }
         if constexpr (MODE == 2 || MODE == 4) {  // pd[f] = double(pacc[f]) * sa(f) * fil(oc, f), left to right
             const int ocg = oc0 + oc < g.OC ? oc0 + oc : 0;
 #pragma unroll
@@ -230,119 +246,6 @@ __global__ void __launch_bounds__(kOutThreads, 2)
         default: break;
     }
     __syncthreads();
-    tl_mark(kTlOutput, 2);
-}
-
-// ---------------------------------------------------------------------------------------
-// Register-resident output transform for the exact integer modes (MODE 0 int32 y, MODE 1
-// int64 y) of the 3x3 variants, over the blocked P layout [Tpad][OCpad/32][F][32] the GEMM
-// writes for it.  A CTA covers TB tile columns of one image tile row and 32 output channels;
-// thread (tile tj, lane oc) loads its K^2 values of P straight from global memory -- one
-// base pointer, the frequency in the immediate offset, a warp reading one contiguous
-// 128*F-byte run (streamed, evict-first) -- runs both scheduled inverse passes in registers
-//   Q[k][t2]   = sum_l P[k*K + l] A[l][t2]
-//   y[t1][t2]  = sum_k A[k][t1] Q[k][t2]
-// and parks y in shared memory only for the coalesced row-segment stores (stage C of
-// k_output).  No TMA round trip, no shared-memory P slice: small CTAs, many resident.
-constexpr int kRegTB = 4;
-template <bool Y64>
-constexpr int reg_tb() { return Y64 ? 2 : kRegTB; }  // (int64 y: half the tiles, same shared bytes)
-
-template <int V, bool Y64>
-__global__ void __launch_bounds__(32 * reg_tb<Y64>()) k_output_reg(const int32_t* __restrict__ P, ConvGeom g,
-                                                            const QuantParams* __restrict__ qpp,
-                                                            const double* __restrict__ sf, OutPtrs o) {
-    using T = Tab<V>;
-    constexpr int TB = reg_tb<Y64>();
-    constexpr int K = T::K, M = T::M, YS = (M * TB) | 1, NT = 32 * TB;
-    using acc_t = typename std::conditional<Y64, long long, int>::type;
-    __shared__ acc_t s_y[M * kOcc * YS];  // rows r = (t1, oc) of YS
-    __shared__ double s_scale[kOcc];
-    __shared__ float s_scalef[kOcc];
-    const int oc0 = blockIdx.x * kOcc, tc = blockIdx.y, row = blockIdx.z;
-    const int lane = threadIdx.x & 31, tjl = threadIdx.x >> 5;
-    tl_mark(kTlOutput, 0);
-    const int arow = g.row0 + row;
-    const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
-    const int noc = min(kOcc, g.OC - oc0);
-    const int ntb = min(TB, g.tw - tc * TB);
-    griddep_wait();  // P complete
-    tl_mark(kTlOutput, 1);
-    griddep_launch_dependents();
-    if (threadIdx.x < kOcc && int(threadIdx.x) < noc) {
-        const double sc = (qpp->sa * sf[oc0 + threadIdx.x]) / double(T::DEN * T::DEN);
-        s_scale[threadIdx.x] = sc;
-        s_scalef[threadIdx.x] = float(sc);
-    }
-    if (tjl < ntb) {
-        const size_t t = size_t(row * g.tw + tc * TB + tjl);
-        // pblk 1: [Tpad][OCpad/32][F][32] (frequency stride 32); 2: [Tpad][F][OCpad] (stride OCpad)
-        const int fst = g.pblk == 1 ? kOcc : g.OCpad;
-        const int32_t* pp = g.pblk == 1 ? P + (t * (g.OCpad / kOcc) + blockIdx.x) * (T::F * kOcc) + lane
-                                        : P + t * T::F * g.OCpad + oc0 + lane;
-        acc_t q[K][M];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            acc_t pr[K], qt[M];
-#pragma unroll
-            for (int l = 0; l < K; ++l) pr[l] = acc_t(__ldcs(pp + (k * K + l) * fst));  // f = k * K + l
-            inv1d<V>(pr, qt);
-#pragma unroll
-            for (int t2 = 0; t2 < M; ++t2) q[k][t2] = qt[t2];
-        }
-#pragma unroll
-        for (int t2 = 0; t2 < M; ++t2) {
-            acc_t qc[K], yt[M];
-#pragma unroll
-            for (int k = 0; k < K; ++k) qc[k] = q[k][t2];
-            inv1d<V>(qc, yt);
-#pragma unroll
-            for (int t1 = 0; t1 < M; ++t1) s_y[(t1 * kOcc + lane) * YS + tjl * M + t2] = yt[t1];
-        }
-    }
-    __syncthreads();
-
-    // stage C (as k_output): thread t keeps column c = t % ncol and walks rows r = (t1, oc)
-    const int WO = g.WO;
-    const int col0 = tc * TB * M;
-    const int ncol = min(ntb * M, WO - col0);  // <= TB * M <= 28
-    const int hrows = min(M, g.HO - ti * M);
-    const int plane = g.HO * WO;
-    const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
-    const unsigned nmag = c_magic32[ncol];
-    const int r0 = ncol == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
-    const int c = int(threadIdx.x) - r0 * ncol;
-    const int rstep = ncol == 1 ? NT : int(__umulhi(unsigned(NT), nmag));
-    const double rq = o.requant;
-    auto emit = [&](auto mask_c) {
-        constexpr int MK = decltype(mask_c)::value;
-        if (r0 >= rstep) return;
-        for (int r = r0; r < M * kOcc; r += rstep) {
-            const int oc = r % kOcc, t1 = r / kOcc;
-            if (oc >= noc || t1 >= hrows) continue;
-            const size_t x = base0 + unsigned(oc * plane + t1 * WO + c);
-            const acc_t y = s_y[r * YS + c];
-            if constexpr ((MK & 1) != 0) o.y32[x] = int(y);
-            if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y);
-            if constexpr ((MK & 4) != 0)
-                o.f32[x] = Y64 ? float(double(y) * s_scale[oc]) : __int2float_rn(int(y)) * s_scalef[oc];
-            if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * s_scale[oc];
-            if constexpr ((MK & 16) != 0) o.i8[x] = int8_t(fmin(fmax(rint(double(y) * s_scale[oc] * rq), 0.0), 127.0));
-        }
-    };
-    const int mask = (o.y32 ? 1 : 0) | (o.y64 ? 2 : 0) | (o.f32 ? 4 : 0) | (o.f64 ? 8 : 0) | (o.i8 ? 16 : 0);
-    switch (mask) {
-#define SFC_EMIT_CASE(m) \
-    case m: emit(std::integral_constant<int, m>{}); break;
-        SFC_EMIT_CASE(1) SFC_EMIT_CASE(2) SFC_EMIT_CASE(3) SFC_EMIT_CASE(4) SFC_EMIT_CASE(5) SFC_EMIT_CASE(6)
-        SFC_EMIT_CASE(7) SFC_EMIT_CASE(8) SFC_EMIT_CASE(9) SFC_EMIT_CASE(10) SFC_EMIT_CASE(11) SFC_EMIT_CASE(12)
-        SFC_EMIT_CASE(13) SFC_EMIT_CASE(14) SFC_EMIT_CASE(15) SFC_EMIT_CASE(16) SFC_EMIT_CASE(17) SFC_EMIT_CASE(18)
-        SFC_EMIT_CASE(19) SFC_EMIT_CASE(20) SFC_EMIT_CASE(21) SFC_EMIT_CASE(22) SFC_EMIT_CASE(23) SFC_EMIT_CASE(24)
-        SFC_EMIT_CASE(25) SFC_EMIT_CASE(26) SFC_EMIT_CASE(27) SFC_EMIT_CASE(28) SFC_EMIT_CASE(29) SFC_EMIT_CASE(30)
-        SFC_EMIT_CASE(31)
-#undef SFC_EMIT_CASE
-        default: break;
-    }
     tl_mark(kTlOutput, 2);
 }
 
@@ -464,8 +367,9 @@ struct PersSmem {
     static constexpr size_t bytes() { return ((slice + 127) & ~size_t(127)) + y_bytes<Y64>() + 16; }
 };
 
-template <int V, bool Y64>
-__global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_constant__ CUtensorMap tmP, ConvGeom g,
+template <int V, bool Y64, bool P24>
+__global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_constant__ CUtensorMap tmP,
+                                                                  const __grid_constant__ CUtensorMap tmP2, ConvGeom g,
                                                                   const QuantParams* __restrict__ qpp,
                                                                   const double* __restrict__ sf, OutPtrs o, int n_ob,
                                                                   int n_tc, int nblk) {
@@ -481,13 +385,22 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
     __shared__ float s_scalef[kOcc];
     const int lane = threadIdx.x & 31, tjl = threadIdx.x >> 5;
     tl_mark(kTlOutput, 0);
+    const int16_t* sp_lo = reinterpret_cast<const int16_t*>(smem);  // P24: [F][TB][kOcc] low halves,
+    const int8_t* sp_hi = reinterpret_cast<const int8_t*>(smem + size_t(T::F) * TB * kOcc * 2);  // then high bytes
     auto issue = [&](int blk) {  // thread 0: the block's P slice
         const int ob = blk % n_ob, r = blk / n_ob, tc = r % n_tc, row = r / n_tc;
-        ptx::mbar_expect_tx(full, uint32_t(PS::slice));
-        ptx::tma_load_3d(smem, &tmP, full, ob * kOcc, row * g.tw + tc * TB, 0);
+        if constexpr (P24) {
+            ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 3));
+            ptx::tma_load_3d(smem, &tmP, full, 2 * ob * kOcc, row * g.tw + tc * TB, 0);
+            ptx::tma_load_3d(smem + size_t(T::F) * TB * kOcc * 2, &tmP2, full, ob * kOcc, row * g.tw + tc * TB, 0);
+        } else {
+            ptx::mbar_expect_tx(full, uint32_t(PS::slice));
+            ptx::tma_load_3d(smem, &tmP, full, ob * kOcc, row * g.tw + tc * TB, 0);
+        }
     };
     if (threadIdx.x == 0) {
         ptx::tma_prefetch(&tmP);
+        if (P24) ptx::tma_prefetch(&tmP2);
         ptx::mbar_init(full, 1);
         ptx::fence_mbar_init();
     }
@@ -518,7 +431,13 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
             for (int k = 0; k < K; ++k) {
                 acc_t pr[K], qt[M];
 #pragma unroll
-                for (int l = 0; l < K; ++l) pr[l] = acc_t(sp[((k * K + l) * TB + tjl) * kOcc + lane]);
+                for (int l = 0; l < K; ++l) {
+                    const int e = ((k * K + l) * TB + tjl) * kOcc + lane;
+                    if constexpr (P24)
+                        pr[l] = acc_t((int(sp_hi[e]) << 16) | int(uint16_t(sp_lo[e])));
+                    else
+                        pr[l] = acc_t(sp[e]);
+                }
                 inv1d<V>(pr, qt);
 #pragma unroll
                 for (int t2 = 0; t2 < M; ++t2) q[k][t2] = qt[t2];
@@ -676,25 +595,48 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+// The output kernels' P slice maps: int32 / fp64 (box kOcc x TB x F), or the two planes of
+// the 24-bit layout (low halves: box 2*kOcc bytes x TB x F; high bytes: kOcc x TB x F).
+bool make_slice_maps(CUtensorMap* tm, CUtensorMap* tm2, const void* P, const ConvGeom& g, int F, int TB, bool f64) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (g.p24) {
+        const cuuint64_t rb = cuuint64_t(g.OCpad) * 3;
+        cuuint64_t dlo[3] = {cuuint64_t(g.OCpad) * 2, cuuint64_t(g.Tpad), cuuint64_t(F)};
+        cuuint64_t dhi[3] = {cuuint64_t(g.OCpad), cuuint64_t(g.Tpad), cuuint64_t(F)};
+        cuuint64_t strides[2] = {rb, rb * g.Tpad};
+        cuuint32_t blo[3] = {2 * kOcc, cuuint32_t(TB), cuuint32_t(F)}, bhi[3] = {kOcc, cuuint32_t(TB), cuuint32_t(F)};
+        uint8_t* base = static_cast<uint8_t*>(const_cast<void*>(P));
+        return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dlo, strides, blo, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                   CUDA_SUCCESS &&
+               fn(tm2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base + 2 * size_t(g.OCpad), dhi, strides, bhi, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    const cuuint64_t es = f64 ? 8 : 4;
+    cuuint64_t dims[3] = {cuuint64_t(g.OCpad), cuuint64_t(g.Tpad), cuuint64_t(F)};
+    cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * es, cuuint64_t(g.OCpad) * g.Tpad * es};
+    cuuint32_t box[3] = {kOcc, cuuint32_t(TB), cuuint32_t(F)};
+    *tm2 = CUtensorMap{};
+    return fn(tm, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(P), dims,
+              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int V, int MODE>
 cudaError_t out_launch(const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf, const OutPtrs& o,
                        cudaStream_t st, bool pdl) {
     constexpr int TB = out_tbm<V, MODE>();
-    constexpr cuuint64_t es = sizeof(p_elem_t<MODE>);
-    auto fn = encode_fn();
-    if (!fn) return cudaErrorInvalidValue;
-    CUtensorMap tm;
-    cuuint64_t dims[3] = {cuuint64_t(g.OCpad), cuuint64_t(g.Tpad), cuuint64_t(Tab<V>::F)};
-    cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * es, cuuint64_t(g.OCpad) * g.Tpad * es};
-    cuuint32_t box[3] = {kOcc, TB, Tab<V>::F};
-    cuuint32_t estr[3] = {1, 1, 1};
-    if (fn(&tm, MODE >= 3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(P),
-           dims, strides, box, estr,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorInvalidValue;
+    if (g.p24 && MODE > 1) return cudaErrorInvalidValue;
+    CUtensorMap tm, tm2;
+    if (!make_slice_maps(&tm, &tm2, P, g, Tab<V>::F, TB, MODE >= 3)) return cudaErrorInvalidValue;
     const size_t smem = out_smem<V, MODE>().bytes;
-    auto kern = k_output<V, MODE>;
+    auto kern = k_output<V, MODE, false>;
+    if constexpr (MODE <= 1) {
+        if (g.p24) kern = k_output<V, MODE, true>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     const long rows = g.nrows;
@@ -709,25 +651,7 @@ cudaError_t out_launch(const void* P, const ConvGeom& g, const QuantParams* qp, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, tm, g, qp, sf, o);
-}
-
-template <int V, bool Y64>
-cudaError_t out_reg_launch(const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
-                           const OutPtrs& o, cudaStream_t st, bool pdl) {
-    const long rows = g.nrows;
-    constexpr int TB = reg_tb<Y64>();
-    if (rows > 65535 || (g.tw + TB - 1) / TB > 65535) return cudaErrorInvalidConfiguration;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned((g.OC + kOcc - 1) / kOcc), unsigned((g.tw + TB - 1) / TB), unsigned(rows));
-    cfg.blockDim = dim3(32 * TB);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_output_reg<V, Y64>, static_cast<const int32_t*>(P), g, qp, sf, o);
+    return cudaLaunchKernelEx(&cfg, kern, tm, tm2, g, qp, sf, o);
 }
 
 int sm_count_out() {
@@ -745,25 +669,12 @@ template <int V, bool Y64>
 cudaError_t out_pers_launch(const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
                             const OutPtrs& o, cudaStream_t st, bool pdl) {
     using PS = PersSmem<V>;
-    auto fn = encode_fn();
-    if (!fn) return cudaErrorInvalidValue;
-    CUtensorMap tm;
-    cuuint64_t dims[3] = {cuuint64_t(g.OCpad), cuuint64_t(g.Tpad), cuuint64_t(Tab<V>::F)};
-    cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * 4, cuuint64_t(g.OCpad) * g.Tpad * 4};
-    cuuint32_t box[3] = {kOcc, PS::TB, Tab<V>::F};
-    cuuint32_t estr[3] = {1, 1, 1};
-    if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(P), dims, strides, box, estr,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorInvalidValue;
+    CUtensorMap tm, tm2;
+    if (!make_slice_maps(&tm, &tm2, P, g, Tab<V>::F, PS::TB, false)) return cudaErrorInvalidValue;
     constexpr size_t smem = PS::template bytes<Y64>();
-    auto kern = k_output_pers<V, Y64>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    auto kern = g.p24 ? k_output_pers<V, Y64, true> : k_output_pers<V, Y64, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
     const int n_ob = (g.OC + kOcc - 1) / kOcc, n_tc = (g.tw + PS::TB - 1) / PS::TB;
     const long nblk = long(n_ob) * n_tc * g.nrows;
     if (nblk > 0x7fffffffL) return cudaErrorInvalidConfiguration;
@@ -780,7 +691,7 @@ cudaError_t out_pers_launch(const void* P, const ConvGeom& g, const QuantParams*
     attr2[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr2;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, tm, g, qp, sf, o, n_ob, n_tc, int(nblk));
+    return cudaLaunchKernelEx(&cfg, kern, tm, tm2, g, qp, sf, o, n_ob, n_tc, int(nblk));
 }
 
 bool out_pers_wanted(int variant, int mode, const ConvGeom& g, const OutPtrs& o) {
@@ -788,7 +699,7 @@ bool out_pers_wanted(int variant, int mode, const ConvGeom& g, const OutPtrs& o)
     // layer, e.g. VGG-16 14.5 vs 15.5 ms; int32 / fp32 outputs: config 5 0.110 vs 0.119 ms)
     // (and y32 / fp32 on narrower layers: VGG-16 layer 5 (256 channels) 0.438 vs 0.359 ms, layer 1
     // (64 channels) 1.85 vs 1.16 ms -- the 96-thread persistent CTAs keep too little in flight)
-    if (variant > 2 || mode > 1 || o.p_discard || g.pblk || o.i8 || g.OC < 512) return false;
+    if (variant > 2 || mode > 1 || o.p_discard || o.i8 || g.OC < 512) return false;
     // small layers (config 2: 320 blocks) keep the 512-thread one-block CTAs: a persistent CTA
     // of 64-192 threads has the longer per-block latency chain
     const int tb = variant == 0 ? out_tb<0>() : variant == 1 ? out_tb<1>() : out_tb<2>();
@@ -796,11 +707,6 @@ bool out_pers_wanted(int variant, int mode, const ConvGeom& g, const OutPtrs& o)
     if (nblk < 8L * sm_count_out()) return false;
     const char* force = std::getenv("SFC_OUT_PERS");  // "0": the one-block-per-CTA kernel (A/B knob)
     return !force || force[0] != '0';
-}
-
-bool out_reg_wanted(int variant, int mode, const OutPtrs& o) {  // (given the blocked P layout)
-    (void)o;
-    return variant <= 2 && mode <= 1;
 }
 
 template <int V>
@@ -814,11 +720,7 @@ cudaError_t out_by_width(int mode, const void* P, const ConvGeom& g, const Quant
             return mode == 0 ? out_pers_launch<V, false>(P, g, qp, sf, op, st, pdl)
                              : out_pers_launch<V, true>(P, g, qp, sf, op, st, pdl);
         }
-        if (g.pblk && out_reg_wanted(V, mode, o))
-            return mode == 0 ? out_reg_launch<V, false>(P, g, qp, sf, o, st, pdl)
-                             : out_reg_launch<V, true>(P, g, qp, sf, o, st, pdl);
     }
-    if (g.pblk) return cudaErrorInvalidValue;  // only the register kernel reads the blocked layout
     return mode == 0 ? out_launch<V, 0>(P, g, qp, sf, o, st, pdl)
          : mode == 1 ? out_launch<V, 1>(P, g, qp, sf, o, st, pdl)
          : mode == 2 ? out_launch<V, 2>(P, g, qp, sf, o, st, pdl)

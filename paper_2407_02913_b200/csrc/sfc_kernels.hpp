@@ -19,10 +19,10 @@ struct ConvGeom {
     // output-transform launches over a chunk of image tile rows (P chunked, see PChunk):
     // rows [row0, row0 + nrows) of the B * th rows; geom_init sets the whole range
     int row0, nrows;
-    // P layout: 0 = [F][Tpad][OCpad]; 1 = blocked [Tpad][OCpad/32][F][32] (the default exact
-    // path: a (tile, 32-channel) group's K^2 values are one contiguous 128*F-byte run for the
-    // register output transform).  geom_init sets 0; run_conv decides (p_blocked).
-    int pblk;
+    // P storage: 0 = int32 [F][Tpad][OCpad]; 1 = 24-bit planar [F][Tpad] rows of 3*OCpad bytes:
+    // OCpad int16 low halves, then OCpad int8 high bytes (exact when |P| < 2^23, i.e.
+    // qmax^2 * Cin < 2^23).  geom_init sets 0; run_conv decides (p24_wanted).
+    int p24;
 };
 
 // P chunking (opt-in: SFC_PCHUNK_MB = budget in MB; unset or 0 = never chunk).  P (4 B per

@@ -402,12 +402,11 @@ class SfcLayer:
         vqt = _wrap_device(vq.value, (F, Tpad, Cpad), torch.int8, self.device)[:, :T, : self.IC]
         if not pa.value:
             return vqt, None
-        if blocked.value == 1:  # [Tpad][OCpad/32][F][32] -> [F][Tpad][OCpad] (a copy)
-            pb = _wrap_device(pa.value, (Tpad, OCpad // 32, F, 32), torch.int32, self.device)
-            return vqt, pb.permute(2, 0, 1, 3).reshape(F, Tpad, OCpad)[:, :T, : self.OC]
-        if blocked.value == 2:  # [Tpad][F][OCpad] -> [F][Tpad][OCpad] (a view)
-            pb = _wrap_device(pa.value, (Tpad, F, OCpad), torch.int32, self.device)
-            return vqt, pb.permute(1, 0, 2)[:, :T, : self.OC]
+        if blocked.value == 1:  # 24-bit planar rows: OCpad int16 low halves, OCpad int8 high bytes (a copy)
+            raw = _wrap_device(pa.value, (F, Tpad, 3 * OCpad), torch.uint8, self.device)
+            lo = raw[:, :, : 2 * OCpad].contiguous().view(torch.int16).to(torch.int32) & 0xFFFF
+            hi = raw[:, :, 2 * OCpad:].contiguous().view(torch.int8).to(torch.int32)
+            return vqt, (lo | (hi << 16))[:, :T, : self.OC]
         pat = _wrap_device(pa.value, (F, Tpad, OCpad), torch.int32, self.device)[:, :T, : self.OC]
         return vqt, pat
 
