@@ -30,6 +30,13 @@
 
 namespace sfcb200 {
 
+// clamp(rint(v), 0, 127) as int8: cvt.rni.s32.f64 (round-to-nearest-even like rint, saturating
+// beyond int32, which the clamp maps to the same 0 / 127) and an integer clamp -- bit-identical
+// to fmin(fmax(rint(v), 0.0), 127.0) for every non-NaN v, in three instructions.
+__device__ __forceinline__ int8_t requant_i8(double v) {
+    return int8_t(min(max(__double2int_rn(v), 0), 127));
+}
+
 namespace {
 constexpr int kOcc = 32;  // output channels per block (128-byte TMA rows)
 constexpr int kOutThreads = 512;
@@ -222,13 +229,13 @@ __global__ void __launch_bounds__(kOutThreads, 2)
                 const double out = double(y) / double(T::DEN * T::DEN);
                 if constexpr ((MK & 4) != 0) o.f32[x] = float(out);
                 if constexpr ((MK & 8) != 0) o.f64[x] = out;
-                if constexpr ((MK & 16) != 0) o.i8[x] = int8_t(fmin(fmax(rint(out * rq), 0.0), 127.0));
+                if constexpr ((MK & 16) != 0) o.i8[x] = requant_i8(out * rq);
             } else {
                 if constexpr ((MK & 4) != 0)
                     o.f32[x] = Y64 ? float(double(y) * s_scale[oc]) : __int2float_rn(int(y)) * s_scalef[oc];
                 if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * s_scale[oc];
                 if constexpr ((MK & 16) != 0)
-                    o.i8[x] = int8_t(fmin(fmax(rint(double(y) * s_scale[oc] * rq), 0.0), 127.0));
+                    o.i8[x] = requant_i8(double(y) * s_scale[oc] * rq);
             }
         }
     };
@@ -305,8 +312,8 @@ __device__ __forceinline__ void emit_rows(const acc_t* __restrict__ s_y, int ys,
                     o.f64[x + 1] = double(y1) * scl[oc];
                 }
                 if constexpr ((MK & 16) != 0) {
-                    const int q0 = int(fmin(fmax(rint(double(y0) * scl[oc] * rq), 0.0), 127.0));
-                    const int q1 = int(fmin(fmax(rint(double(y1) * scl[oc] * rq), 0.0), 127.0));
+                    const int q0 = int(requant_i8(double(y0) * scl[oc] * rq));
+                    const int q1 = int(requant_i8(double(y1) * scl[oc] * rq));
                     *reinterpret_cast<int16_t*>(o.i8 + x) = int16_t(q0 | (q1 << 8));
                 }
             } else {
@@ -315,7 +322,7 @@ __device__ __forceinline__ void emit_rows(const acc_t* __restrict__ s_y, int ys,
                 if constexpr ((MK & 4) != 0)
                     o.f32[x] = Y64 ? float(double(y0) * scl[oc]) : __int2float_rn(int(y0)) * sclf[oc];
                 if constexpr ((MK & 8) != 0) o.f64[x] = double(y0) * scl[oc];
-                if constexpr ((MK & 16) != 0) o.i8[x] = int8_t(fmin(fmax(rint(double(y0) * scl[oc] * rq), 0.0), 127.0));
+                if constexpr ((MK & 16) != 0) o.i8[x] = requant_i8(double(y0) * scl[oc] * rq);
             }
         }
     } else {
@@ -329,7 +336,7 @@ __device__ __forceinline__ void emit_rows(const acc_t* __restrict__ s_y, int ys,
             if constexpr ((MK & 2) != 0) o.y64[x] = int64_t(y);
             if constexpr ((MK & 4) != 0) o.f32[x] = Y64 ? float(double(y) * scl[oc]) : __int2float_rn(int(y)) * sclf[oc];
             if constexpr ((MK & 8) != 0) o.f64[x] = double(y) * scl[oc];
-            if constexpr ((MK & 16) != 0) o.i8[x] = int8_t(fmin(fmax(rint(double(y) * scl[oc] * rq), 0.0), 127.0));
+            if constexpr ((MK & 16) != 0) o.i8[x] = requant_i8(double(y) * scl[oc] * rq);
         }
     }
 }

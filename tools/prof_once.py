@@ -10,6 +10,7 @@ ap.add_argument("--workload", type=int, default=2)
 ap.add_argument("--layer", type=int, default=0)
 ap.add_argument("--variant", default="sfc6-6x6-3x3")
 ap.add_argument("--iters", type=int, default=4)
+ap.add_argument("--i8", action="store_true", help="int8 requant output only (configs 3/4)")
 a = ap.parse_args()
 work = wl.WORKLOADS[a.workload]
 L = work.layers[a.layer]
@@ -20,6 +21,8 @@ ho = L.hw + 2 * L.pad - L.r + 1
 ws = layer.workspace(L.batch, L.hw, L.hw, L.pad)
 out = torch.empty((L.batch, L.cout, ho, ho), dtype=torch.float32, device="cuda")
 kw = dict(y_int32=torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int32, device="cuda"), out_f32=out)
+if a.i8:
+    kw = dict(out_i8=torch.empty((L.batch, L.cout, ho, ho), dtype=torch.int8, device="cuda"), requant_scale=0.004)
 try:
     layer.forward(x, ws, L.pad, **kw)
 except sc.SfcUnsupported if hasattr(sc, "SfcUnsupported") else Exception:
