@@ -82,9 +82,24 @@ __host__ __device__ inline int row_plane_words(int W) {
     const int w = 4 + (48 + Tab<V>::n * W + 3) / 4;
     return w | 1;
 }
+// RS: row pitch (words) for a chunk of tc tile columns: misalignment + window extent +
+// funnel overrun; the plane holds n rows plus the guards, rounded to odd.
+template <int V>
+__host__ __device__ inline int row_seg_pitch(int tc) {
+    return (15 + (tc - 1) * Tab<V>::M + Tab<V>::n + 12 + 3) / 4 + 1;
+}
+template <int V>
+__host__ __device__ inline int row_seg_plane_words(int tc) {
+    return (4 + Tab<V>::n * row_seg_pitch<V>(tc) + 4) | 1;
+}
 
-template <int V, int MODE, int PPW>
+// RS = true (rows wider than kRowMaxWarps warps of tiles at 32 pairs per warp): a CTA covers a
+// chunk of tc tile columns and stages one segment per (channel, window row) -- the columns
+// its windows touch -- at row pitch rpw words inside the channel's plane; otherwise the CTA
+// covers the whole tile row and each channel's band is one contiguous segment.
+template <int V, int MODE, int PPW, bool RS>
 __global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __restrict__ x, ConvGeom g, int plw,
+                                                              int rpw, int tc,
                                                               int* __restrict__ vmax, int16_t* __restrict__ vkeep,
                                                               const int* __restrict__ vmax_in, int bits,
                                                               QuantParams* __restrict__ qp_out,
@@ -98,43 +113,51 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __r
     tl_mark(kTl, 0);
     if (MODE != 1) griddep_launch_dependents();
 
-    const int ti = blockIdx.x, b = blockIdx.y, c0 = blockIdx.z * NCH;
+    const int nchunk = RS ? (g.tw + tc - 1) / tc : 1;
+    const int ti = RS ? blockIdx.x / nchunk : blockIdx.x, b = blockIdx.y, c0 = blockIdx.z * NCH;
+    const int tj0 = RS ? (blockIdx.x - ti * nchunk) * tc : 0;
     const int ih0 = ti * M - g.pad;
     const int r_lo = max(ih0, 0), nr = min(ih0 + n, g.H) - r_lo;
     const size_t HW = size_t(g.H) * g.W;
     const int8_t* xb = x + (size_t(b) * g.C + c0) * HW + size_t(r_lo) * g.W;  // band of channel c0
     const uintptr_t xlo = reinterpret_cast<uintptr_t>(x), xhi = xlo + size_t(g.B) * g.C * HW;
-    const int band = nr * g.W;
+    // staged columns [cs, ce): RS the chunk's windows, else whole rows
+    const int cs = RS ? max(tj0 * M - g.pad, 0) : 0;
+    const int ce = RS ? min((min(tj0 + tc, g.tw) - 1) * M - g.pad + n, g.W) : g.W;
+    const int band = RS ? ce - cs : nr * g.W;  // bytes per segment
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     auto plane = [&](int ch) { return ((ch & 1) * PPW + (ch >> 1)) * plw + 4; };
 
-    // ---- stage: per channel, the 16-byte chunks covering its band.  Lanes = chunks of one
-    // channel (lpc lanes per channel, a power of two >= the chunk count, capped at 32), a
-    // warp pass covers cpw channels; kB passes' loads are in flight before any is stored.
+    // ---- stage: per segment (a channel's band, or RS one (channel, row) piece), the 16-byte
+    // chunks covering it.  Lanes = chunks of one segment (lpc lanes, a power of two >= the
+    // chunk count, capped at 32), a warp pass covers cpw segments; kB passes' loads are in
+    // flight before any is stored.
     {
         const int nchv = min(NCH, g.C - c0);
+        const int nseg = RS ? nchv * nr : nchv;
         const int cq = (15 + band + 15) >> 4;  // chunk bound over every misalignment
         int lg = 0;
         while ((1 << lg) < cq && lg < 5) ++lg;
         const int lpc = 1 << lg, cpw = 32 >> lg;
-        const int qq = (cq + lpc - 1) >> lg;      // chunk passes per channel (1 unless band > 482 B)
-        const int ch0 = wid * cpw + (lane >> lg), chstep = nwarps * cpw;
-        const uintptr_t xb_u = reinterpret_cast<uintptr_t>(xb);
+        const int qq = (cq + lpc - 1) >> lg;      // chunk passes per segment
+        const int sg0 = wid * cpw + (lane >> lg), sgstep = nwarps * cpw;
+        const uintptr_t xb_u = reinterpret_cast<uintptr_t>(xb) + cs;
         // the CTA's chunks all lie inside x unless it holds the first or last bytes of x
         const bool inside = (xb_u & ~uintptr_t(15)) >= xlo &&
-                            ((xb_u + size_t(nchv - 1) * HW + band + 15) & ~uintptr_t(15)) <= xhi;
+                            ((xb_u + size_t(nchv - 1) * HW + size_t(nr - 1) * g.W + band + 15) & ~uintptr_t(15)) <= xhi;
         constexpr int kB = 8;
         for (int jq = 0; jq < qq; ++jq) {
             const int q = (lane & (lpc - 1)) + jq * lpc;
-            for (int chb = ch0; chb < nchv; chb += kB * chstep) {
+            for (int sgb = sg0; sgb < nseg; sgb += kB * sgstep) {
                 uint4 v[kB];
                 uint32_t* d[kB];
 #pragma unroll
                 for (int jj = 0; jj < kB; ++jj) {
-                    const int ch = chb + jj * chstep;
-                    const uintptr_t start = xb_u + size_t(ch) * HW;
+                    const int sg = sgb + jj * sgstep;
+                    const int ch = RS ? sg / nr : sg, ir = RS ? sg - ch * nr : 0;
+                    const uintptr_t start = xb_u + size_t(ch) * HW + size_t(ir) * g.W;
                     const uintptr_t ad = (start & ~uintptr_t(15)) + 16 * uintptr_t(q);
-                    d[jj] = (ch < nchv && ad < start + band) ? s_raw + plane(ch) + 4 * q : nullptr;
+                    d[jj] = (sg < nseg && ad < start + band) ? s_raw + plane(ch) + ir * rpw + 4 * q : nullptr;
                     v[jj] = make_uint4(0, 0, 0, 0);
                     if (!d[jj]) continue;
                     if (inside || (ad >= xlo && ad + 16 <= xhi)) {
@@ -151,7 +174,7 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __r
     }
     __syncthreads();
 
-    const int p = lane % PPW, tj = wid * TPW + lane / PPW;
+    const int p = lane % PPW, tj = tj0 + wid * TPW + lane / PPW;
     const int c = c0 + 2 * p;
     const bool active = tj < g.tw && c < g.C;
     const int t = (b * g.th + ti) * g.tw + tj;
@@ -174,8 +197,15 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __r
         const bool ok1 = c + 1 < g.C;
         const uint32_t* pe = s_raw + plane(2 * p);
         const uint32_t* po = s_raw + plane(2 * p + 1);
-        const int me = int(reinterpret_cast<uintptr_t>(xb + size_t(2 * p) * HW) & 15) + wc0;
-        const int mo = int(reinterpret_cast<uintptr_t>(xb + size_t(2 * p + 1) * HW) & 15) + wc0;
+        // byte offset of window column 0 of window row ir in the plane: whole rows, the band's
+        // 16-byte misalignment + ir * W + wc0; RS, ir * rpw words + the row piece's own
+        // misalignment + (wc0 - cs)
+        const uintptr_t ae = reinterpret_cast<uintptr_t>(xb + size_t(2 * p) * HW) + cs;
+        const uintptr_t ao = reinterpret_cast<uintptr_t>(xb + size_t(2 * p + 1) * HW) + cs;
+        const int me = int(ae & 15) + wc0 - cs, mo = int(ao & 15) + wc0 - cs;
+        auto roff = [&](uintptr_t a, int m, int ir) {
+            return RS ? ir * rpw * 4 + int((a + size_t(ir) * g.W) & 15) + (wc0 - cs) : m + ir * g.W;
+        };
         constexpr int NW4 = (n + 3) / 4;  // window words per row
 #pragma unroll
         for (int r = 0; r < n; ++r) {
@@ -190,8 +220,8 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __r
 #pragma unroll
                     for (int j = 0; j < NW4; ++j) o[j] = __funnelshift_r(src[j], src[j + 1], sh) & mk[j];
                 };
-                row(pe, me + ir * g.W, we);
-                row(po, mo + ir * g.W, wo);
+                row(pe, roff(ae, me, ir), we);
+                row(po, roff(ao, mo, ir), wo);
                 if (!ok1) {
 #pragma unroll
                     for (int j = 0; j < NW4; ++j) wo[j] = 0;
@@ -324,18 +354,30 @@ int row_ppw(const ConvGeom& g) {
     return ppw;
 }
 
-template <int V, int MODE, int PPW>
+// Wide rows of wide layers (more tiles than kRowMaxWarps warps hold at 32 pairs, >= 64
+// channels): row-chunk CTAs at 32 pairs per warp instead of narrowing the pairs per warp.
+bool row_segmented(const ConvGeom& g) {
+    const char* e = std::getenv("SFC_ACT_ROWSEG");  // "0": whole-row CTAs only (A/B knob)
+    return !(e && e[0] == '0') && g.tw > kRowMaxWarps && g.C >= 64;
+}
+
+template <int V, int MODE, int PPW, bool RS = false>
 cudaError_t row_launch(const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep, const int* vmax_in, int bits,
                        QuantParams* qp, int8_t* vqA, unsigned long long* sat, const QuantParams* qtab,
                        cudaStream_t st, bool pdl) {
     constexpr int TPW = 32 / PPW;
-    const int nw = (g.tw + TPW - 1) / TPW;
-    const int plw = row_plane_words<V>(g.W);
+    // RS: chunks of kRowMaxWarps * TPW tile columns, balanced over the row
+    const int nchunk = RS ? (g.tw + kRowMaxWarps * TPW - 1) / (kRowMaxWarps * TPW) : 1;
+    const int tc = RS ? (g.tw + nchunk - 1) / nchunk : g.tw;
+    const int nw = (tc + TPW - 1) / TPW;
+    const int plw = RS ? row_seg_plane_words<V>(tc) : row_plane_words<V>(g.W);
+    const int rpw = RS ? row_seg_pitch<V>(tc) : 0;
     const size_t smem = size_t(2 * PPW) * plw * 4;
     const long gz = (g.C + 2 * PPW - 1) / (2 * PPW);
-    if (nw > kRowMaxWarps || g.th > 0x7fffffff || g.B > 65535 || gz > 65535 || smem > 200 * 1024)
+    const long gx = long(g.th) * nchunk;
+    if (nw > kRowMaxWarps || gx > 0x7fffffffL || g.B > 65535 || gz > 65535 || smem > 200 * 1024)
         return cudaErrorInvalidConfiguration;
-    auto kern = k_act_row<V, MODE, PPW>;
+    auto kern = k_act_row<V, MODE, PPW, RS>;
     static size_t attr_bytes = 0;
     if (smem > 48 * 1024 && smem > attr_bytes) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -343,7 +385,7 @@ cudaError_t row_launch(const int8_t* x, const ConvGeom& g, int* vmax, int16_t* v
         attr_bytes = smem;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(g.th), unsigned(g.B), unsigned(gz));
+    cfg.gridDim = dim3(unsigned(gx), unsigned(g.B), unsigned(gz));
     cfg.blockDim = dim3(32 * nw);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -352,13 +394,15 @@ cudaError_t row_launch(const int8_t* x, const ConvGeom& g, int* vmax, int16_t* v
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, x, g, plw, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab);
+    return cudaLaunchKernelEx(&cfg, kern, x, g, plw, rpw, tc, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab);
 }
 
 template <int V, int MODE>
 cudaError_t row_dispatch(const int8_t* x, const ConvGeom& g, int* vmax, int16_t* vkeep, const int* vmax_in, int bits,
                          QuantParams* qp, int8_t* vqA, unsigned long long* sat, const QuantParams* qtab,
                          cudaStream_t st, bool pdl) {
+    if (row_segmented(g))
+        return row_launch<V, MODE, 32, true>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
     switch (row_ppw(g)) {
         case 32: return row_launch<V, MODE, 32>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
         case 16: return row_launch<V, MODE, 16>(x, g, vmax, vkeep, vmax_in, bits, qp, vqA, sat, qtab, st, pdl);
@@ -374,6 +418,7 @@ bool act_reg_wanted(int variant, const ConvGeom& g) {
     if (variant > 2 || g.pad > 8) return false;  // (the plane guards cover windows from column -8)
     const char* force = std::getenv("SFC_ACT_REG");  // "0": the shared-memory kernels (A/B knob)
     if (force && force[0] == '0') return false;
+    if (row_segmented(g)) return true;
     const int ppw = row_ppw(g);
     const int nw = (g.tw + 32 / ppw - 1) / (32 / ppw);
     const size_t smem = size_t(2 * ppw) * (variant == 0   ? row_plane_words<0>(g.W)

@@ -108,6 +108,10 @@ CASES = [  # (B, C, OC, H, W, pad, lo)
     (1, 17, 257, 6, 6, 1, -128),
     (1, 1, 1, 1, 1, 1, -128),
     (1, 2, 2, 3, 3, 0, -128),
+    # wide rows (> 10 tiles, >= 64 channels): the row-chunk CTAs of the register transform
+    (1, 64, 16, 9, 130, 1, -128),
+    (2, 70, 8, 7, 100, 2, 0),
+    (1, 128, 12, 13, 71, 0, -128),
 ]
 
 
