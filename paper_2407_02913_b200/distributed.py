@@ -46,12 +46,25 @@ class CudaEngine:
             self._ws[key] = self.layer.workspace(n, h, w, self.pad)
         return self._ws[key]
 
+    def _recompute(self, x) -> bool:
+        """The single-GPU forward's schedule for this shard (sfc_conv_schedule): recompute V
+        from x after the exchange, or keep it from the absmax pass."""
+        n, _, h, w = x.shape
+        return self.layer.schedule(n, h, w, self.pad)["recompute"]
+
     def absmax(self, x, vmax):
-        """Local absmax; V is kept in the shard's workspace for conv()."""
-        self.layer.transform(x, vmax, self._workspace(x), self.pad)
+        """Local absmax; V is kept in the shard's workspace for conv() unless the schedule
+        recomputes it."""
+        if self._recompute(x):
+            self.layer.absmax(x, vmax, self.pad)
+        else:
+            self.layer.transform(x, vmax, self._workspace(x), self.pad)
 
     def conv(self, x, vmax, **outs):
-        self.layer.conv_kept(tuple(x.shape), vmax, self._workspace(x), self.pad, **outs)
+        if self._recompute(x):
+            self.layer.conv(x, vmax, self._workspace(x), self.pad, **outs)
+        else:
+            self.layer.conv_kept(tuple(x.shape), vmax, self._workspace(x), self.pad, **outs)
 
     # -- general QuantConfig (per-frequency scopes, MseGrid): see ShardedConv.forward_general
     @property
