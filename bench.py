@@ -264,7 +264,8 @@ def run_b200(args, rank, world, local_rank):
             calls.append(dict(L=L, v=v, layer=layer, ws=ws, x=x, x_host=x_host, outs=outs, host_outs=host_outs,
                               vmax=torch.zeros(1, dtype=torch.int32, device=dev), rq=float(rq[i]),
                               spec=layer.spec,
-                              sched_rec=layer.schedule(L.batch, L.hw, L.hw, L.pad)["recompute"]))
+                              sched_rec=layer.schedule(L.batch, L.hw, L.hw, L.pad)["recompute"],
+                              p_layout=layer.schedule(L.batch, L.hw, L.hw, L.pad)["p_layout"]))
             h2d_bytes += x_host.numel()
             d2h_bytes += sum(t.numel() * t.element_size() for t in host_outs.values())
     # inputs are shared between variants of one layer: H2D once per layer
@@ -412,15 +413,16 @@ def run_b200(args, rank, world, local_rank):
             xb = L.batch * L.cin * L.hw * L.hw
             outb = sum(t.numel() * t.element_size() for t in c["outs"].values())
             rec = c["recompute"]
+            pb = {0: 4, 1: 3, 3: 0}.get(c["p_layout"], 4)  # P bytes per value: int32, 24-bit planar, none
             if dom == "absmax":
                 alg_bytes += xb + (0 if rec else 2 * F * T * L.cin)  # read x (+ keep int16 V)
             elif dom == "quantize":
                 alg_bytes += xb + F * T * L.cin  # read x, write int8 vq
             elif dom == "gemm":  # reads vq (int8) or the kept V (int16) and uq, writes P
                 alg_ops += 2 * F * T * L.cin * L.cout
-                alg_bytes += (1 if rec else 2) * F * T * L.cin + F * L.cin * L.cout + 4 * F * T * L.cout
-            elif dom == "output":
-                alg_bytes += 4 * F * T * L.cout + outb
+                alg_bytes += (1 if rec else 2) * F * T * L.cin + F * L.cin * L.cout + pb * F * T * L.cout
+            elif dom == "output":  # P in (or, Cin <= 4, vq words and uq: the fused dp4a contraction)
+                alg_bytes += (pb * F * T * L.cout if pb else 4 * F * T + F * L.cout * 4) + outb
             else:
                 alg_bytes += 64
         kms = stage_ms[dom]
