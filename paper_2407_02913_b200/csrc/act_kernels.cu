@@ -205,6 +205,9 @@ __global__ void __launch_bounds__(kActThreads) k_act(const int8_t* __restrict__ 
     };
     if (MODE != 1) {
         column([](int v) { return v; });
+    } else if (qp.exact && qp.shift >= 33) {  // one mad.hi + shift per value (common.cuh)
+        const int mul = int(qp.mul), c = 1 << (qp.shift - 33), sh = qp.shift - 32;
+        column([=](int v) { return quant_hi32(v, mul, c, sh); });
     } else if (qp.exact) {  // uniform over the CTA: no per-value branch
         // mul < 2^31 (derive_qparams): one 32x32+64 -> 64 multiply-add and a funnel shift
         const int mul = int(qp.mul);
@@ -415,7 +418,10 @@ __global__ void __launch_bounds__(32 * kPairMaxTiles)
                 vq += fstride;  // next l
             }
         };
-        if (qp.exact) {  // uniform over the grid: no per-value branch
+        if (qp.exact && qp.shift >= 33) {  // one mad.hi + shift per value (common.cuh)
+            const int mul = int(qp.mul), c = 1 << (qp.shift - 33), sh = qp.shift - 32;
+            columns([=](int v) { return quant_hi32(v, mul, c, sh); });
+        } else if (qp.exact) {  // uniform over the grid: no per-value branch
             const int mul = int(qp.mul);
             const long long half = 1ll << (qp.shift - 1);
             const int shift = qp.shift;
@@ -526,7 +532,10 @@ __global__ void __launch_bounds__(kActThreads) k_quant_kept(const int16_t* __res
             }
         }
     };
-    if (qp.exact) {
+    if (qp.exact && qp.shift >= 33) {  // one mad.hi + shift per value (common.cuh)
+        const int mul = int(qp.mul), c = 1 << (qp.shift - 33), sh = qp.shift - 32;
+        run([=](int v) { return quant_hi32(v, mul, c, sh); });
+    } else if (qp.exact) {
         const int mul = int(qp.mul);
         const long long half = 1ll << (qp.shift - 1);
         const int shift = qp.shift;

@@ -51,13 +51,6 @@ __device__ __forceinline__ int sx_hi(uint32_t w) {
     return prmt0<4 | (4 << 4) | (q << 8) | ((q | 8) << 12)>(w);
 }
 
-// mad.hi.s32: hi32(v * mul) + c, then an arithmetic shift (see the S >= 33 quantizer below)
-__device__ __forceinline__ int quant_hi32(int v, int mul, int c, int sh) {
-    int r;
-    asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(mul), "r"(c));
-    return r >> sh;
-}
-
 // The reference quantizer with clamping (the rare case without a verified multiply-shift):
 // out of line, so the unrolled column loop stays small.
 __device__ __noinline__ int quant_slow(int v, double sa, int qmax, unsigned long long* sat) {

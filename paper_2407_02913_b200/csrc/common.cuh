@@ -71,6 +71,15 @@ __device__ __forceinline__ int quant_fast(int v, int mul, long long half, int sh
     return int(r >> shift);
 }
 
+// The same quotient for S >= 33: floor((v*mul + 2^(S-1)) / 2^S) = (hi32(v*mul) + 2^(S-33)) >>
+// (S-32) -- the dropped low word only adds a fraction below one unit of the numerator -- as one
+// mad.hi.s32 and one shift (c = 2^(S-33), sh = S-32).
+__device__ __forceinline__ int quant_hi32(int v, int mul, int c, int sh) {
+    int r;
+    asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(mul), "r"(c));
+    return r >> sh;
+}
+
 // Activation quantizer.  Fast path (qp.exact): one 32x32->64 multiply-add and a
 // shift, proven equal to exact_q for every |v| <= vmax by derive_qparams (so no
 // clamp can trigger).  Otherwise the per-element fp64 division with clamping.

@@ -280,7 +280,10 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 if (++stage == STAGES) stage = 0, phase ^= 1;
             }
         };
-        if (qp.exact) {
+        if (qp.exact && qp.shift >= 33) {  // one mad.hi + shift per value (common.cuh)
+            const int mul = int(qp.mul), c = 1 << (qp.shift - 33), sh = qp.shift - 32;
+            run([=](int v) { return quant_hi32(v, mul, c, sh); });
+        } else if (qp.exact) {
             const int mul = int(qp.mul);
             const long long half = 1ll << (qp.shift - 1);
             const int shift = qp.shift;
@@ -354,7 +357,10 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 for (int j = 0; j < kItems; ++j) ca[j] = na[j], cb[j] = nb[j];
             }
         };
-        if (qp.exact) {  // CTA-uniform: one specialised loop per quantizer path
+        if (qp.exact && qp.shift >= 33) {  // CTA-uniform: one specialised loop per quantizer path
+            const int mul = int(qp.mul), c = 1 << (qp.shift - 33), sh = qp.shift - 32;
+            run([=](int v) { return quant_hi32(v, mul, c, sh); });
+        } else if (qp.exact) {
             const int mul = int(qp.mul);
             const long long half = 1ll << (qp.shift - 1);
             const int shift = qp.shift;
