@@ -50,6 +50,16 @@ __device__ __forceinline__ void unit_of(int u, int n_ob, int n_tb, int& ob, int&
     ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
 }
 
+// Quantize the four int16 values of two int16x2 words (lanes: low then high half) and pack
+// the four int8 results into one word: sign-extended halves, two byte permutes to pack.
+template <class Q>
+__device__ __forceinline__ uint32_t pack_q4(uint32_t w0, uint32_t w1, Q&& quant) {
+    const int a0 = int(int16_t(w0)), a1 = int(w0) >> 16, b0 = int(int16_t(w1)), b1 = int(w1) >> 16;
+    const uint32_t lo = __byte_perm(uint32_t(quant(a0)), uint32_t(quant(a1)), 0x0040);
+    const uint32_t hi = __byte_perm(uint32_t(quant(b0)), uint32_t(quant(b1)), 0x0040);
+    return __byte_perm(lo, hi, 0x5410);
+}
+
 // Quantizer parameters for a subset of warps (no CTA-wide barrier): table or warp derivation.
 __device__ __forceinline__ QuantParams qparams_warp(int vmax, int bits, const QuantParams* __restrict__ tab) {
     if (tab && vmax >= 0 && vmax <= kQpTableMax && bits >= 2 && bits <= 8)
@@ -265,12 +275,10 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                     const uint4* src = reinterpret_cast<const uint4*>(v_st + r * (BK * 2) + qc * 32);
                     const uint4 a = src[0], b = src[1];
                     const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-                    uint32_t o[4] = {0, 0, 0, 0};
+                    uint32_t o[4];
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
-                        o[e >> 2] |= uint32_t(uint8_t(int8_t(quant(v)))) << (8 * (e & 3));
-                    }
+                    for (int e = 0; e < 4; ++e)  // two int16x2 words -> four int8 in one word
+                        o[e] = pack_q4(w[2 * e], w[2 * e + 1], quant);
                     const int sw = BK == 128 ? (qc ^ (r & 7)) : (qc ^ ((r >> 1) & 3));
                     *reinterpret_cast<uint4*>(a_st + r * BK + (sw << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
                 }
@@ -340,12 +348,9 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                         for (int e = 0; e < 16; ++e)
                             if (e >= valid) w[e >> 1] &= ~(0xffffu << (16 * (e & 1)));
                     }
-                    uint32_t o[4] = {0, 0, 0, 0};
+                    uint32_t o[4];  // (quant(0) == 0: no saturation from padding)
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {  // (quant(0) == 0: no saturation from padding)
-                        const int v = int(int16_t(w[e >> 1] >> (16 * (e & 1))));
-                        o[e >> 2] |= uint32_t(uint8_t(int8_t(quant(v)))) << (8 * (e & 3));
-                    }
+                    for (int e = 0; e < 4; ++e) o[e] = pack_q4(w[2 * e], w[2 * e + 1], quant);
                     const int sw = BK == 128 ? (qc ^ (r & 7)) : (qc ^ ((r >> 1) & 3));
                     *reinterpret_cast<uint4*>(a_st + r * BK + (sw << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
                 }
