@@ -330,15 +330,34 @@ def run_b200(args, rank, world, local_rank):
     launches_per_step = sum((5 if c["sched_rec"] else 4) - (0 if world == 1 else 1) for c in calls)
 
     # ---- end to end through the public API: pinned host input -> device -> outputs -> pinned host
+    # outputs go back on a copy stream as soon as their call is done, so the device-to-host
+    # transfer of call i overlaps the kernels of call i+1 (the step ends when the last copy has
+    # landed: the compute stream waits for the copy stream before the closing event)
+    # inputs come in on an upload stream, all enqueued at the start of the step; each call waits
+    # only for its own input (PCIe is full duplex: uploads overlap downloads and kernels)
+    copy_stream = torch.cuda.Stream(device=dev)
+    up_stream = torch.cuda.Stream(device=dev)
+
     def e2e_step():
-        done = set()
+        ready = {}
+        up_stream.wait_stream(stream)  # (the previous step's kernels are done with the inputs)
+        with torch.cuda.stream(up_stream):
+            for c in calls:
+                if id(c["x"]) not in ready:
+                    c["x"].copy_(c["x_host"], non_blocking=True)
+                    ready[id(c["x"])] = torch.cuda.Event()
+                    ready[id(c["x"])].record(up_stream)
         for c in calls:
-            if id(c["x"]) not in done:
-                c["x"].copy_(c["x_host"], non_blocking=True)
-                done.add(id(c["x"]))
+            stream.wait_event(ready[id(c["x"])])
             run_call(c)
-            for k, t_dev in c["outs"].items():
-                c["host_outs"][k].copy_(t_dev, non_blocking=True)
+            ev_done = torch.cuda.Event()
+            ev_done.record(stream)
+            copy_stream.wait_event(ev_done)
+            with torch.cuda.stream(copy_stream):
+                for k, t_dev in c["outs"].items():
+                    c["host_outs"][k].copy_(t_dev, non_blocking=True)
+                    t_dev.record_stream(copy_stream)
+        stream.wait_stream(copy_stream)
 
     for _ in range(2):
         e2e_step()
