@@ -720,3 +720,27 @@ def test_small_channel_fused_path(cuda, variant, case, monkeypatch):
     assert g0["pacc"] is not None
     for k in ("y", "f32", "i8"):
         assert np.array_equal(ga[k], gb[k]), k
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_p24_and_output_kernels_agree(cuda, variant, monkeypatch):
+    """24-bit planar P (default) vs int32 P (SFC_P24=0), and the persistent output kernel of
+    512-channel int32 / fp32 layers vs the one-block kernel (SFC_OUT_PERS=0): y, fp32 and pacc
+    bit for bit on a 512-channel layer and on a small ragged one."""
+    rng = np.random.default_rng(11)
+    for (B, C, OC, H, W, pad) in ((26, 64, 512, 14, 14, 1), (2, 40, 70, 11, 9, 1)):  # (26 images: >= 8 blocks per SM)
+        x = rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)
+        w = rng.integers(-127, 128, size=(OC, C, 3, 3), dtype=np.int8)
+        dev = torch.device("cuda", 0)
+        layer = sc.SfcLayer(variant, torch.from_numpy(w).to(dev))
+        assert layer.schedule(B, H, W, pad)["p_layout"] == 1
+        res = {}
+        for name, env in (("default", {}), ("p32", {"SFC_P24": "0"}), ("one-block", {"SFC_OUT_PERS": "0"})):
+            for k in ("SFC_P24", "SFC_OUT_PERS"):
+                monkeypatch.delenv(k, raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            res[name] = run_gpu(x, w, variant, pad, outs=("y", "f32"), views=True)
+        for name in ("p32", "one-block"):
+            for k in ("y", "f32", "pacc", "vq"):
+                assert np.array_equal(res["default"][k], res[name][k]), (name, k)
