@@ -327,7 +327,9 @@ def run_b200(args, rank, world, local_rank):
     value = step_ops / (ms / 1e3) / 1e12
     # N=1: workspace reset, absmax (+V kept), [quantizing transform,] gemm, output (per the
     # call's schedule); N>1: the reset is a torch zero_() of vmax, not one of ours
-    launches_per_step = sum((5 if c["sched_rec"] else 4) - (0 if world == 1 else 1) for c in calls)
+    # (the Cin <= 4 path has no GEMM launch: its contraction runs inside the output kernel)
+    launches_per_step = sum((5 if c["sched_rec"] else 4) - (0 if world == 1 else 1) - (1 if c["p_layout"] == 3 else 0)
+                            for c in calls)
 
     # ---- end to end through the public API: pinned host input -> device -> outputs -> pinned host
     # outputs go back on a copy stream as soon as their call is done, so the device-to-host
