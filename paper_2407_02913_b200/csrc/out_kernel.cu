@@ -702,18 +702,21 @@ cudaError_t out_pers_launch(const void* P, const ConvGeom& g, const QuantParams*
 }
 
 bool out_pers_wanted(int variant, int mode, const ConvGeom& g, const OutPtrs& o) {
-    // (int8 requant outputs: the one-block kernel measured faster on every ResNet-18 / VGG-16
-    // layer, e.g. VGG-16 14.5 vs 15.5 ms; int32 / fp32 outputs: config 5 0.110 vs 0.119 ms)
-    // (and y32 / fp32 on narrower layers: VGG-16 layer 5 (256 channels) 0.438 vs 0.359 ms, layer 1
-    // (64 channels) 1.85 vs 1.16 ms -- the 96-thread persistent CTAs keep too little in flight)
-    if (variant > 2 || mode > 1 || o.p_discard || o.i8 || g.OC < 512) return false;
+    // Measured (24-bit P): faster on every ResNet-18 / VGG-16 layer with int8 requant outputs
+    // (VGG-16 11.37 -> 10.57 ms, ResNet-18 1.021 -> 0.999 ms) and on 512-channel int32 / fp32
+    // layers (config 5); slower for wide int32 outputs on narrower layers (VGG-16 layer 1 y32
+    // 1.49 vs 1.22 ms), which keep the one-block kernel.
+    const char* fe = std::getenv("SFC_OUT_PERS");  // "0": never, "1": force (A/B knob)
+    if (variant > 2 || mode > 1 || o.p_discard) return false;
+    if (fe && fe[0] == '1') return true;
+    const bool wide_out = o.y32 || o.y64 || o.f32 || o.f64;
+    if (wide_out && g.OC < 512) return false;
     // small layers (config 2: 320 blocks) keep the 512-thread one-block CTAs: a persistent CTA
     // of 64-192 threads has the longer per-block latency chain
     const int tb = variant == 0 ? out_tb<0>() : variant == 1 ? out_tb<1>() : out_tb<2>();
     const long nblk = long((g.OC + kOcc - 1) / kOcc) * ((g.tw + tb - 1) / tb) * g.nrows;
     if (nblk < 8L * sm_count_out()) return false;
-    const char* force = std::getenv("SFC_OUT_PERS");  // "0": the one-block-per-CTA kernel (A/B knob)
-    return !force || force[0] != '0';
+    return !fe || fe[0] != '0';
 }
 
 template <int V>
