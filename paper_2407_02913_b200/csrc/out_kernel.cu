@@ -63,10 +63,10 @@ struct OutSmem {
     size_t p_bytes, q_off, bar_off, bytes;
 };
 
-template <int V, int MODE>
+template <int V, int MODE, int TBX = 0>
 __host__ __device__ inline OutSmem out_smem() {
     using T = Tab<V>;
-    constexpr int TB = out_tbm<V, MODE>();
+    constexpr int TB = TBX ? TBX : out_tbm<V, MODE>();
     const size_t es = MODE == 0 ? 4 : 8;
     OutSmem s;
     s.qstride = kOcc | 1;
@@ -93,17 +93,20 @@ __constant__ unsigned c_magic32[33] = {  // 0xffffffff / d + 1 (exact for t < 2^
 // (oc, f) before the inverse transform, which then runs in fp64: quant.cpp:258-278),
 // 3: fp64 P of the float path (fast_conv2d, conv.cpp:495-510), no dequantisation,
 // 4: as 2 from an fp64 P (the exact-integer P of the 9-16 bit path, |P| < 2^53).
-template <int V, int MODE, bool P24 = false>
-__global__ void __launch_bounds__(kOutThreads, 2)
+// TBX = 1 (small grids, config 2): one tile per block and 256 threads -- three times the
+// blocks with a third of the per-thread chain, all resident in one wave.
+template <int V, int MODE, bool P24 = false, int TBX = 0>
+__global__ void __launch_bounds__(TBX ? 256 : kOutThreads, 2)
     k_output(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2, ConvGeom g,
              const QuantParams* __restrict__ qpp, const double* __restrict__ sf, OutPtrs o) {
     using T = Tab<V>;
-    constexpr int K = T::K, M = T::M, TB = out_tbm<V, MODE>();
+    constexpr int K = T::K, M = T::M, TB = TBX ? TBX : out_tbm<V, MODE>();
+    constexpr int NTH = TBX ? 256 : kOutThreads;
     constexpr bool Y64 = MODE == 1;
     using acc_t =
         typename std::conditional<MODE >= 2, double, typename std::conditional<Y64, long long, int>::type>::type;
     extern __shared__ __align__(128) uint8_t smem[];
-    const OutSmem L = out_smem<V, MODE>();
+    const OutSmem L = out_smem<V, MODE, TBX>();
     const p_elem_t<MODE>* sp = reinterpret_cast<const p_elem_t<MODE>*>(smem);  // [F][TB][kOcc]
     acc_t* s_y = reinterpret_cast<acc_t*>(smem);                 // [M][kOcc] rows of ystride (after stage A)
     acc_t* s_q = reinterpret_cast<acc_t*>(smem + L.q_off);       // [TB][M][K] rows of qstride
@@ -117,7 +120,9 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     tl_mark(kTlOutput, 0);
     // 24-bit planar P: the slice's int16 low halves [F][TB][kOcc], then its int8 high bytes
     const int16_t* sp_lo = reinterpret_cast<const int16_t*>(smem);
-    const int8_t* sp_hi = reinterpret_cast<const int8_t*>(smem + size_t(T::F) * TB * kOcc * 2);
+    // (TMA destinations are 128-byte aligned: the high plane starts at the next 128-byte boundary)
+    constexpr size_t kHiOff = (size_t(T::F) * TB * kOcc * 2 + 127) & ~size_t(127);
+    const int8_t* sp_hi = reinterpret_cast<const int8_t*>(smem + kHiOff);
     if (threadIdx.x == 0) {
         ptx::tma_prefetch(&tmP);
         if (P24) ptx::tma_prefetch(&tmP2);
@@ -132,7 +137,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
         if constexpr (P24) {
             ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 3));
             ptx::tma_load_3d(smem, &tmP, full, 2 * oc0, row * g.tw + tc * TB, 0);
-            ptx::tma_load_3d(smem + size_t(T::F) * TB * kOcc * 2, &tmP2, full, oc0, row * g.tw + tc * TB, 0);
+            ptx::tma_load_3d(smem + kHiOff, &tmP2, full, oc0, row * g.tw + tc * TB, 0);
         } else {
             ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * sizeof(p_elem_t<MODE>)));
             ptx::tma_load_3d(smem, &tmP, full, oc0, row * g.tw + tc * TB, 0);
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     if (o.p_discard) {  // this block is the only reader of its rows' lines: drop them from L2 unwritten
         constexpr int kLines = int(kOcc * sizeof(p_elem_t<MODE>) / 128);
         const char* pb = static_cast<const char*>(o.p_discard);
-        for (int i = threadIdx.x; i < T::F * ntb * kLines; i += kOutThreads) {
+        for (int i = threadIdx.x; i < T::F * ntb * kLines; i += NTH) {
             const int l = i % kLines, j = (i / kLines) % ntb, f = i / (kLines * ntb);
             const size_t e = (size_t(f) * g.Tpad + size_t(row) * g.tw + tc * TB + j) * g.OCpad + oc0;
             asm volatile("discard.global.L2 [%0], 128;" ::"l"(pb + e * sizeof(p_elem_t<MODE>) + l * 128) : "memory");
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     }
 
     // stage A: items (tj, l, oc)
-    for (int it = threadIdx.x; it < TB * K * kOcc; it += kOutThreads) {
+    for (int it = threadIdx.x; it < TB * K * kOcc; it += NTH) {
         const int oc = it % kOcc, l = (it / kOcc) % K, tj = it / (kOcc * K);
         if (tj >= ntb) continue;
         acc_t pk[K], qt[M];
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     __syncthreads();
 
     // stage B: items (tj, t1, oc)
-    for (int it = threadIdx.x; it < TB * M * kOcc; it += kOutThreads) {
+    for (int it = threadIdx.x; it < TB * M * kOcc; it += NTH) {
         const int oc = it % kOcc, t1 = (it / kOcc) % M, tj = it / (kOcc * M);
         if (tj >= ntb) continue;
         acc_t qv[K], yt[M];
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     __syncthreads();
 
     // stage C: the block's output row segments r = (t1, oc), ncol columns each.  Thread t
-    // keeps column c = t % ncol and walks rows r = t / ncol, + kOutThreads / ncol, ...
+    // keeps column c = t % ncol and walks rows r = t / ncol, + NTH / ncol, ...
     // (consecutive threads -> consecutive columns of a row: coalesced row segments); the
     // divisions by ncol <= 32 are multiply-highs from a constant table.  The set of
     // requested outputs is a compile-time mask (one specialisation per combination).
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(kOutThreads, 2)
     const unsigned nmag = c_magic32[ncol];
     const int r0 = ncol == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
     const int c = int(threadIdx.x) - r0 * ncol;
-    const int rstep = ncol == 1 ? kOutThreads : int(__umulhi(unsigned(kOutThreads), nmag));
+    const int rstep = ncol == 1 ? NTH : int(__umulhi(unsigned(NTH), nmag));
     const double rq = o.requant;
     auto emit = [&](auto mask_c) {
         constexpr int MK = decltype(mask_c)::value;
@@ -393,13 +398,14 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
     const int lane = threadIdx.x & 31, tjl = threadIdx.x >> 5;
     tl_mark(kTlOutput, 0);
     const int16_t* sp_lo = reinterpret_cast<const int16_t*>(smem);  // P24: [F][TB][kOcc] low halves,
-    const int8_t* sp_hi = reinterpret_cast<const int8_t*>(smem + size_t(T::F) * TB * kOcc * 2);  // then high bytes
+    constexpr size_t kHiOff = (size_t(T::F) * TB * kOcc * 2 + 127) & ~size_t(127);  // (128-byte aligned TMA)
+    const int8_t* sp_hi = reinterpret_cast<const int8_t*>(smem + kHiOff);  // then high bytes
     auto issue = [&](int blk) {  // thread 0: the block's P slice
         const int ob = blk % n_ob, r = blk / n_ob, tc = r % n_tc, row = r / n_tc;
         if constexpr (P24) {
             ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 3));
             ptx::tma_load_3d(smem, &tmP, full, 2 * ob * kOcc, row * g.tw + tc * TB, 0);
-            ptx::tma_load_3d(smem + size_t(T::F) * TB * kOcc * 2, &tmP2, full, ob * kOcc, row * g.tw + tc * TB, 0);
+            ptx::tma_load_3d(smem + kHiOff, &tmP2, full, ob * kOcc, row * g.tw + tc * TB, 0);
         } else {
             ptx::mbar_expect_tx(full, uint32_t(PS::slice));
             ptx::tma_load_3d(smem, &tmP, full, ob * kOcc, row * g.tw + tc * TB, 0);
@@ -632,17 +638,24 @@ bool make_slice_maps(CUtensorMap* tm, CUtensorMap* tm2, const void* P, const Con
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int V, int MODE>
+template <int V, int MODE, int TBX = 0>
 cudaError_t out_launch(const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf, const OutPtrs& o,
                        cudaStream_t st, bool pdl) {
-    constexpr int TB = out_tbm<V, MODE>();
+    constexpr int TB = TBX ? TBX : out_tbm<V, MODE>();
+    if constexpr (TBX == 0 && MODE <= 1) {  // small grids: one-tile blocks (fit one wave)
+        const char* e = std::getenv("SFC_OUT_SMALL");
+        const long nblk = long((g.OC + kOcc - 1) / kOcc) * ((g.tw + TB - 1) / TB) * g.nrows;
+        const long nblk1 = long((g.OC + kOcc - 1) / kOcc) * g.tw * g.nrows;
+        if (!(e && e[0] == '0') && !o.p_discard && nblk < 3L * 148 && nblk1 <= 8L * 148)
+            return out_launch<V, MODE, 1>(P, g, qp, sf, o, st, pdl);
+    }
     if (g.p24 && MODE > 1) return cudaErrorInvalidValue;
     CUtensorMap tm, tm2;
     if (!make_slice_maps(&tm, &tm2, P, g, Tab<V>::F, TB, MODE >= 3)) return cudaErrorInvalidValue;
-    const size_t smem = out_smem<V, MODE>().bytes;
-    auto kern = k_output<V, MODE, false>;
+    const size_t smem = out_smem<V, MODE, TBX>().bytes;
+    auto kern = k_output<V, MODE, false, TBX>;
     if constexpr (MODE <= 1) {
-        if (g.p24) kern = k_output<V, MODE, true>;
+        if (g.p24) kern = k_output<V, MODE, true, TBX>;
     }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
@@ -650,7 +663,7 @@ cudaError_t out_launch(const void* P, const ConvGeom& g, const QuantParams* qp, 
     if (rows > 65535 || (g.tw + TB - 1) / TB > 65535) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned((g.OC + kOcc - 1) / kOcc), unsigned((g.tw + TB - 1) / TB), unsigned(rows));
-    cfg.blockDim = dim3(kOutThreads);
+    cfg.blockDim = dim3(TBX ? 256 : kOutThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
