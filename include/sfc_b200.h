@@ -18,7 +18,9 @@
  *    asynchronous unless documented as synchronous.
  *  - Tensors are row-major NCHW like sfconv::DenseTensor (tensor.hpp:11-31);
  *    activations and weights are int8 (the integer values the reference
- *    receives as doubles); weights are [OC][IC][3][3].
+ *    receives as doubles); weights are [OC][IC][R][R] with R the algorithm's
+ *    filter size (3 for the three 3x3 algorithms, 5 / 7 for sfc6-6x6-5x5 /
+ *    sfc6-4x4-7x7).
  *  - Plans and layers are immutable after creation and may be shared across
  *    host threads; all per-call state lives in the caller's workspace, so
  *    concurrent calls on distinct streams need distinct workspaces.
@@ -57,10 +59,14 @@ int sfc_version(void);
 /* ---- catalog: replaces catalog_algorithm / catalog_export_json / catalog_hash
  *      (include/sfconv/spec.hpp:76-79, src/catalog.cpp:275-287, 562-601) ----------- */
 
-/* JSON of the three 3x3 SFC algorithms in the reference export layout; hash = FNV-1a 64 of it. */
+/* JSON of the five catalogued SFC algorithms (sfc4-4x4-3x3, sfc6-6x6-3x3, sfc6-7x7-3x3,
+ * sfc6-6x6-5x5, sfc6-4x4-7x7) in the reference export layout; hash = FNV-1a 64 of it. */
 int sfc_catalog_json(char* buf, size_t cap, uint64_t* hash);
 /* Derive + exactness-gate + bind the compiled kernels for `name`
- * ("sfc4-4x4-3x3" | "sfc6-6x6-3x3" | "sfc6-7x7-3x3"). */
+ * ("sfc4-4x4-3x3" | "sfc6-6x6-3x3" | "sfc6-7x7-3x3" | "sfc6-6x6-5x5" | "sfc6-4x4-7x7").
+ * Every kernel serves all five; the register-resident transform (k_act_row), 24-bit P, the
+ * small-channel (Cin <= 4) fused path and the persistent output kernel are 3x3-only fast
+ * paths (the 5x5 / 7x7 algorithms take the shared-memory transforms and int32 P). */
 int sfc_plan_create(const char* name, sfc_plan_t* out);
 int sfc_plan_destroy(sfc_plan_t plan);
 /* dims[10] = {K, n_in, M, R, N, offset, a_denom, n_corrections, mults_full, mults_reduced} */
@@ -159,18 +165,18 @@ int sfc_conv_forward(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, 
  *                values_quantized, tiles}. */
 /* Activation scales of the last call: 1 (PerTensor) or K*K (PerFrequency) doubles in *count;
  * scales may be NULL to query the count.  Synchronous on `stream`. */
-int sfc_conv_act_scales(sfc_layer_t layer, int n, int h, int w, int pad, const void* d_workspace, double* scales,
-                        int64_t* count, void* stream);
-int sfc_conv_stats(sfc_layer_t layer, int n, int h, int w, int pad, const void* d_workspace, int64_t* stats,
-                   void* stream);
+int sfc_conv_act_scales(sfc_layer_t layer, int n, int h, int w, int pad, const void* d_workspace,
+                        size_t workspace_bytes, double* scales, int64_t* count, void* stream);
+int sfc_conv_stats(sfc_layer_t layer, int n, int h, int w, int pad, const void* d_workspace, size_t workspace_bytes,
+                   int64_t* stats, void* stream);
 /* Device views into the workspace after sfc_conv_int8:
  *   vq   int8  [F][Tpad][Cpad]   quantized transformed activations
  *   pacc int32 [F][Tpad][OCpad]  per-frequency channel contractions; NULL when P is
  *                                chunked (opt-in SFC_PCHUNK_MB budget exceeded: each chunk
  *                                is consumed from L2 and never materialised whole)
  * geom[6] = {T, Tpad, Cpad, OCpad, th, tw}. */
-int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_workspace, int8_t** d_vq,
-                   int32_t** d_pacc, int64_t* geom);
+int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_workspace, size_t workspace_bytes,
+                   int8_t** d_vq, int32_t** d_pacc, int64_t* geom);
 /* The schedule sfc_conv_forward picks for this layer and geometry (either may be NULL):
  *   *recompute  0: the absmax pass keeps V and the GEMM quantizes it (sfc_act_transform +
  *                  sfc_conv_kept); 1: absmax only, then a quantizing transform writes vq
@@ -256,7 +262,7 @@ int sfc_fast_conv_f64(sfc_plan_t plan, const double* d_x, int n, int c, int h, i
 int sfc_general_prepare(sfc_layer_t layer, const int8_t* d_x, int n, int h, int w, int pad, void* d_workspace,
                         size_t workspace_bytes, uint64_t** d_maxima, int* count, void* stream);
 int sfc_general_mse_partial(sfc_layer_t layer, int n, int h, int w, int pad, void* d_workspace,
-                            const double* d_err_in, double* d_err_out, void* stream);
+                            size_t workspace_bytes, const double* d_err_in, double* d_err_out, void* stream);
 int sfc_general_conv(sfc_layer_t layer, int n, int h, int w, int pad, void* d_workspace, size_t workspace_bytes,
                      const double* d_err, const sfc_outputs* outputs, void* stream);
 

@@ -80,20 +80,20 @@ _SIGS = {
     "sfc_conv_int8_stages": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _sz, ctypes.POINTER(Outputs), ctypes.c_uint, _vp]),
     "sfc_conv_forward": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
     "sfc_general_prepare": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _sz, ctypes.POINTER(_vp), ctypes.POINTER(_i), _vp]),
-    "sfc_general_mse_partial": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "sfc_general_mse_partial": (_i, [_vp, _i, _i, _i, _i, _vp, _sz, _vp, _vp, _vp]),
     "sfc_general_conv": (_i, [_vp, _i, _i, _i, _i, _vp, _sz, _vp, ctypes.POINTER(Outputs), _vp]),
     "sfc_act_transform": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _sz, _vp]),
     "sfc_layer_create_ex": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _i, _vp, ctypes.POINTER(_vp)]),
     "sfc_layer_filter_scales_native": (_i, [_vp, _vp, _i64p]),
-    "sfc_conv_act_scales": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _i64p, _vp]),
+    "sfc_conv_act_scales": (_i, [_vp, _i, _i, _i, _i, _vp, _sz, _vp, _i64p, _vp]),
     "sfc_layer_create_f64": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _i, _vp, ctypes.POINTER(_vp)]),
     "sfc_conv_forward_f64": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
     "sfc_direct_conv_f64": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp]),
     "sfc_report_sq_err_f64": (_i, [_vp, _vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _vp]),
     "sfc_fast_conv_f64": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _i64p, _vp]),
     "sfc_conv_kept": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _sz, ctypes.POINTER(Outputs), _vp]),
-    "sfc_conv_stats": (_i, [_vp, _i, _i, _i, _i, _vp, _i64p, _vp]),
-    "sfc_conv_views": (_i, [_vp, _i, _i, _i, _i, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64p]),
+    "sfc_conv_stats": (_i, [_vp, _i, _i, _i, _i, _vp, _sz, _i64p, _vp]),
+    "sfc_conv_views": (_i, [_vp, _i, _i, _i, _i, _vp, _sz, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64p]),
     "sfc_conv_schedule": (_i, [_vp, _i, _i, _i, _i, ctypes.POINTER(_i)]),
     "sfc_direct_conv_int8": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp]),
     "sfc_frequency_energy_int8": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp]),

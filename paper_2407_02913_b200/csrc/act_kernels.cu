@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "devcache.hpp"
 #include "sfc_kernels.hpp"
 #include "sfc_tables.cuh"
 #include "transforms.cuh"
@@ -600,12 +601,8 @@ cudaError_t act_launch_cc(const int8_t* x, const ConvGeom& g, int twc, int* vmax
                           bool pdl) {
     const size_t smem = act_smem<V, CC>(g.W, twc).bytes;
     auto kern = k_act<V, MODE, CC>;
-    static size_t attr_bytes = 0;  // per instantiation: raise the opt-in only when a layer needs more
-    if (smem > attr_bytes) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        attr_bytes = smem;
-    }
+    static SmemOptIn opt_in;  // per instantiation and device: raised only when a layer needs more
+    if (cudaError_t e = opt_in.ensure(kern, smem); e != cudaSuccess) return e;
     const long gx = long(g.th) * ((g.tw + twc - 1) / twc);
     if (gx > 0x7fffffffL || g.B > 65535 || (g.C + CC - 1) / CC > 65535) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
@@ -662,12 +659,8 @@ cudaError_t act_pair_launch(const int8_t* x, const ConvGeom& g, int* vmax, const
     while (twc > 1 && ctas(twc) < 2 * 148) twc = (twc + 1) / 2;
     const size_t smem = pair_smem<V>(g.W, twc).bytes;
     auto kern = k_act_pair<V, MODE>;
-    static size_t attr_bytes = 0;
-    if (smem > attr_bytes) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        attr_bytes = smem;
-    }
+    static SmemOptIn opt_in;
+    if (cudaError_t e = opt_in.ensure(kern, smem); e != cudaSuccess) return e;
     const long gx = long(g.th) * ((g.tw + twc - 1) / twc);
     if (gx > 0x7fffffffL || g.B > 65535 || blocks_c > 65535) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};

@@ -24,6 +24,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "devcache.hpp"
 #include "sfc_kernels.hpp"
 #include "sfc_tables.cuh"
 #include "transforms.cuh"
@@ -371,12 +372,9 @@ cudaError_t row_launch(const int8_t* x, const ConvGeom& g, int* vmax, int16_t* v
     if (nw > kRowMaxWarps || gx > 0x7fffffffL || g.B > 65535 || gz > 65535 || smem > 200 * 1024)
         return cudaErrorInvalidConfiguration;
     auto kern = k_act_row<V, MODE, PPW, RS>;
-    static size_t attr_bytes = 0;
-    if (smem > 48 * 1024 && smem > attr_bytes) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        attr_bytes = smem;
-    }
+    static SmemOptIn opt_in;
+    if (smem > 48 * 1024)
+        if (cudaError_t e = opt_in.ensure(kern, smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(gx), unsigned(g.B), unsigned(gz));
     cfg.blockDim = dim3(32 * nw);

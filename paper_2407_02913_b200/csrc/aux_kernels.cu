@@ -228,7 +228,6 @@ void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, in
     g.Cpad = (C + g.BK - 1) / g.BK * g.BK;
     g.BN = OC <= 64 ? 64 : (OC <= 128 ? 128 : 256);
     g.OCpad = (OC + g.BN - 1) / g.BN * g.BN;
-    g.th_magic = g.th == 1 ? 0u : 0xffffffffu / unsigned(g.th) + 1u;
     g.row0 = 0;
     g.nrows = B * g.th;
     g.p24 = 0;

@@ -209,12 +209,29 @@ void check_call(const sfc_layer* L, const void* x, int n, int h, int w, int pad)
     if (w > 16384 || h > 16384 || pad > 64) throw Unsupported("image sides above 16384 or padding above 64");
     if (h + 2 * pad - L->plan->R + 1 <= 0 || w + 2 * pad - L->plan->R + 1 <= 0)
         throw std::invalid_argument("filter larger than padded input");
+    // tile counts, padded rows and every per-tile buffer size are formed in int / size_t
+    // from these: refuse shapes whose tile count (rounded to the GEMM row block) or
+    // per-frequency operand rows would not fit a signed 32-bit index
+    const long long M = L->plan->M;
+    const long long th = (h + 2 * pad - L->plan->R + 1 + M - 1) / M, tw = (w + 2 * pad - L->plan->R + 1 + M - 1) / M;
+    const long long tiles = (long long)n * th * tw;
+    if (tiles + 128 > 0x7fffffffLL || (long long)n * L->IC * h * w > 0x7fffffffffffLL)
+        throw Unsupported("tile count above 2^31 - 128");
 }
 
 ConvGeom geom_of(const sfc_layer* L, int n, int h, int w, int pad) {
     ConvGeom g;
     geom_init(g, L->variant, n, L->IC, h, w, pad, L->OC);
     return g;
+}
+
+// The inspection / protocol entry points that only read a workspace a previous call filled:
+// the same shape checks as a launch, and the workspace must be large enough for the shape.
+WsView checked_carve(const sfc_layer* L, int n, int h, int w, int pad, void* ws, size_t ws_bytes) {
+    check_call(L, ws, n, h, w, pad);
+    const ConvGeom g = geom_of(L, n, h, w, pad);
+    if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
+    return carve(ws, g, L->F);
 }
 
 // |y| <= (max_t sum_k |A[k,t]|)^2 * IC * qmax^2 (MinMax never clips, so |vq|,|uq| <= qmax):
@@ -354,14 +371,14 @@ int sfc_general_prepare(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, i
     });
 }
 
-int sfc_general_mse_partial(sfc_layer_t L, int n, int h, int w, int pad, void* ws, const double* d_err_in,
-                            double* d_err_out, void* stream) {
+int sfc_general_mse_partial(sfc_layer_t L, int n, int h, int w, int pad, void* ws, size_t ws_bytes,
+                            const double* d_err_in, double* d_err_out, void* stream) {
     return guarded([&] {
-        if (!L || !ws || !d_err_out) throw std::invalid_argument("null argument");
+        if (!d_err_out) throw std::invalid_argument("null argument");
+        const WsView v = checked_carve(L, n, h, w, pad, ws, ws_bytes);
         general_check(L, nullptr);
         if (L->search != SFC_SEARCH_MSE_GRID) throw std::invalid_argument("the layer's scale search is MinMax");
         const ConvGeom g = geom_of(L, n, h, w, pad);
-        const WsView v = carve(ws, g, L->F);
         ck(launch_act_mse(v.vkeep, g, L->F, L->act_scope == SFC_ACT_PER_FREQUENCY, v.vmaxf, L->bits, d_err_in,
                           d_err_out, S(stream)),
            "mse launch");
@@ -652,11 +669,12 @@ int sfc_conv_forward(sfc_layer_t L, const int8_t* d_x, int n, int h, int w, int 
     });
 }
 
-int sfc_conv_stats(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, int64_t* stats, void* stream) {
+int sfc_conv_stats(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, size_t ws_bytes, int64_t* stats,
+                   void* stream) {
     return guarded([&] {
-        if (!L || !ws || !stats) throw std::invalid_argument("null argument");
+        if (!stats) throw std::invalid_argument("null argument");
+        WsView v = checked_carve(L, n, h, w, pad, const_cast<void*>(ws), ws_bytes);
         const ConvGeom g = geom_of(L, n, h, w, pad);
-        WsView v = carve(const_cast<void*>(ws), g, L->F);
         QuantParams qp;
         unsigned long long sat = 0;
         ck(cudaMemcpyAsync(&qp, v.qp, sizeof qp, cudaMemcpyDeviceToHost, S(stream)), "copy qp");
@@ -676,12 +694,11 @@ int sfc_conv_stats(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, 
     });
 }
 
-int sfc_conv_act_scales(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, double* scales, int64_t* count,
-                        void* stream) {
+int sfc_conv_act_scales(sfc_layer_t L, int n, int h, int w, int pad, const void* ws, size_t ws_bytes, double* scales,
+                        int64_t* count, void* stream) {
     return guarded([&] {
-        if (!L || !ws || !count) throw std::invalid_argument("null argument");
-        const ConvGeom g = geom_of(L, n, h, w, pad);
-        WsView v = carve(const_cast<void*>(ws), g, L->F);
+        if (!count) throw std::invalid_argument("null argument");
+        WsView v = checked_carve(L, n, h, w, pad, const_cast<void*>(ws), ws_bytes);
         *count = L->general && L->act_scope == SFC_ACT_PER_FREQUENCY ? L->F : 1;
         if (!scales) return;
         if (L->general) {
@@ -697,12 +714,11 @@ int sfc_conv_act_scales(sfc_layer_t L, int n, int h, int w, int pad, const void*
     });
 }
 
-int sfc_conv_views(sfc_layer_t L, int n, int h, int w, int pad, void* ws, int8_t** d_vq, int32_t** d_pacc,
-                   int64_t* geom) {
+int sfc_conv_views(sfc_layer_t L, int n, int h, int w, int pad, void* ws, size_t ws_bytes, int8_t** d_vq,
+                   int32_t** d_pacc, int64_t* geom) {
     return guarded([&] {
-        if (!L || !ws) throw std::invalid_argument("null argument");
+        WsView v = checked_carve(L, n, h, w, pad, ws, ws_bytes);
         const ConvGeom g = geom_of(L, n, h, w, pad);
-        WsView v = carve(ws, g, L->F);
         if (d_vq) *d_vq = v.vq;
         if (d_pacc) *d_pacc = p_chunk(g, L->F).n > 1 || small_c(L, g) ? nullptr : v.P;
         if (geom) {

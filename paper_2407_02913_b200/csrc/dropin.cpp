@@ -484,7 +484,7 @@ static QuantReport quantized_fast_conv2d_real(const DenseTensor& input, const De
     double sums[2] = {0.0, 0.0};
     check(sfc_report_sq_err_f64(out.p, ref.p, int64_t(n), sums, stream()));
     std::int64_t stats[6] = {};
-    check(sfc_conv_stats(layer, B, H, W, padding, ws.p, stats, stream()));
+    check(sfc_conv_stats(layer, B, H, W, padding, ws.p, ws_bytes, stats, stream()));
     std::int64_t fsat = 0;
     check(sfc_layer_saturations(layer, &fsat));
     ck(cudaMemcpyAsync(rep.output.data.data(), out.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream()),
@@ -535,7 +535,7 @@ QuantReport quantized_fast_conv2d(const DenseTensor& input, const DenseTensor& f
     double sums[2] = {0.0, 0.0};
     check(sfc_report_sq_err(out.p, ref.p, int64_t(n), sums, stream()));
     std::int64_t stats[6] = {};
-    check(sfc_conv_stats(layer, B, H, W, padding, ws.p, stats, stream()));
+    check(sfc_conv_stats(layer, B, H, W, padding, ws.p, ws_bytes, stats, stream()));
     std::int64_t fsat = 0;
     check(sfc_layer_saturations(layer, &fsat));
     ck(cudaMemcpyAsync(rep.output.data.data(), out.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream()),

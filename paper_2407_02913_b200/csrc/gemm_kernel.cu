@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "devcache.hpp"
 #include "sfc_kernels.hpp"
 
 namespace sfcb200 {
@@ -385,14 +386,15 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
 // ============================================================================ host
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    // process-wide driver entry point, resolved once (thread-safe static initialisation)
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         cudaDriverEntryPointQueryResult q;
         void* p = nullptr;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        return PFN_cuTensorMapEncodeTiled_v12000(nullptr);
+    }();
     return fn;
 }
 
@@ -434,16 +436,7 @@ bool make_p_maps(CUtensorMap* m, CUtensorMap* m2, int32_t* P, const ConvGeom& g,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+int sm_count() { return device_sm_count(); }
 
 template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
@@ -451,12 +444,8 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + (QT ? size_t(STAGES) * kRowsPerTile * BK * 2 : 0) +
                         size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256;
     auto kern = k_gemm<BN, BK, STAGES, QF, QT>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static SmemOptIn opt_in;
+    if (cudaError_t e = opt_in.ensure(kern, smem); e != cudaSuccess) return e;
     const int n_tb = g.Tpad / kRowsPerTile, n_ob = g.OCpad / BN;
     const int units = F * n_tb * n_ob;
     // CTAs per SM bounded by shared memory and by TMEM (2*BN columns each of 512).

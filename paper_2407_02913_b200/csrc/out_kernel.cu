@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "devcache.hpp"
 #include "sfc_kernels.hpp"
 #include "sfc_tables.cuh"
 #include "transforms.cuh"
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(TBX ? 256 : kOutThreads, 2)
         }
     }
     const int arow = g.row0 + row;
-    const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
+    const int b = arow / g.th, ti = arow - b * g.th;  // per block: exact for any row count
     const int noc = min(kOcc, g.OC - oc0);
     const int ntb = min(TB, g.tw - tc * TB);
     if (threadIdx.x < kOcc && int(threadIdx.x) < noc) {
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
         const int ob = blk % n_ob, rr = blk / n_ob, tc = rr % n_tc, row = rr / n_tc;
         const int oc0 = ob * kOcc;
         const int arow = g.row0 + row;
-        const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
+        const int b = arow / g.th, ti = arow - b * g.th;  // per block: exact for any row count
         const int noc = min(kOcc, g.OC - oc0);
         const int ntb = min(TB, g.tw - tc * TB);
         const bool act = tjl < ntb;
@@ -542,7 +543,7 @@ __global__ void __launch_bounds__(32 * kSmallTB) k_output_smallc(const int32_t* 
     for (int blk = blockIdx.y; blk < nblk; blk += gridDim.y) {
         const int tc = blk % n_tc, row = blk / n_tc;
         const int arow = g.row0 + row;
-        const int b = g.th == 1 ? arow : int(__umulhi(unsigned(arow), g.th_magic)), ti = arow - b * g.th;
+        const int b = arow / g.th, ti = arow - b * g.th;  // per block: exact for any row count
         const int ntb = min(TB, g.tw - tc * TB);
         const int t0 = row * g.tw + tc * TB;
         __syncthreads();  // the previous block is done with s_v and s_y
@@ -597,14 +598,15 @@ __global__ void __launch_bounds__(32 * kSmallTB) k_output_smallc(const int32_t* 
 
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    // process-wide driver entry point, resolved once (thread-safe static initialisation)
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         cudaDriverEntryPointQueryResult q;
         void* p = nullptr;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        return PFN_cuTensorMapEncodeTiled_v12000(nullptr);
+    }();
     return fn;
 }
 
@@ -674,16 +676,7 @@ cudaError_t out_launch(const void* P, const ConvGeom& g, const QuantParams* qp, 
     return cudaLaunchKernelEx(&cfg, kern, tm, tm2, g, qp, sf, o);
 }
 
-int sm_count_out() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+int sm_count_out() { return device_sm_count(); }
 
 template <int V, bool Y64>
 cudaError_t out_pers_launch(const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,

@@ -15,7 +15,6 @@ struct ConvGeom {
     int Cpad;   // input channels rounded up to the GEMM K chunk (BK)
     int BK;     // 64 or 128 bytes of K per pipeline stage
     int OC, OCpad, BN;
-    unsigned th_magic;  // r / th == umulhi(r, th_magic) for r < 2^16 (th == 1: 0, divide by identity)
     // output-transform launches over a chunk of image tile rows (P chunked, see PChunk):
     // rows [row0, row0 + nrows) of the B * th rows; geom_init sets the whole range
     int row0, nrows;

@@ -74,6 +74,10 @@ class CudaEngine:
     def general_prepare(self, x):
         return self.layer.general_prepare(x, self._workspace(x), self.pad)
 
+    def general_count(self) -> int:
+        """Number of activation maxima exchanged: K*K for PerFrequency, else 1."""
+        return self.layer.spec.K ** 2 if self.layer.act_scope == 1 else 1
+
     def general_mse(self, x, err_in):
         n, _, h, w = x.shape
         groups = self.layer.spec.K ** 2 if self.layer.act_scope == 1 else 1
@@ -92,12 +96,17 @@ class ShardedConv:
     group: object = None
 
     def forward(self, x_local, **outs):
-        """absmax on the local shard -> all-reduce(MAX) -> quantize/contract/transform locally."""
+        """absmax on the local shard -> all-reduce(MAX) -> quantize/contract/transform locally.
+        A rank whose shard is empty (batch < world) contributes a zero maximum and still joins
+        the exchange, so no rank waits on a collective another one never reaches."""
         vmax = self.engine.new_vmax(x_local.device)
-        self.engine.absmax(x_local, vmax)
+        empty = x_local.shape[0] == 0
+        if not empty:
+            self.engine.absmax(x_local, vmax)
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
             dist.all_reduce(vmax, op=dist.ReduceOp.MAX, group=self.group)
-        self.engine.conv(x_local, vmax, **outs)
+        if not empty:
+            self.engine.conv(x_local, vmax, **outs)
         return vmax
 
     def forward_general(self, x_local, **outs):
@@ -108,10 +117,16 @@ class ShardedConv:
         batch order (each rank continues the previous rank's accumulators over its shard) and
         the last rank's complete sums are broadcast; every rank then picks the same scales and
         quantizes / contracts / transforms its shard.  Bitwise the full-batch result."""
-        maxima = self.engine.general_prepare(x_local)
+        empty = x_local.shape[0] == 0  # batch < world: join every exchange with a neutral part
+        if empty:
+            maxima = torch.zeros(self.engine.general_count(), dtype=torch.int64, device=x_local.device)
+        else:
+            maxima = self.engine.general_prepare(x_local)
         multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
         if multi:
             dist.all_reduce(maxima, op=dist.ReduceOp.MAX, group=self.group)
+        elif empty:
+            raise ValueError("empty batch")
         err = None
         if self.engine.mse:
             err_in = None
@@ -120,13 +135,15 @@ class ShardedConv:
                 if rank > 0:
                     err_in = torch.empty((maxima.numel(), 101), dtype=torch.float64, device=x_local.device)
                     dist.recv(err_in, src=_global_rank(self.group, rank - 1), group=self.group)
-                err = self.engine.general_mse(x_local, err_in)
+                # an empty shard adds no terms: the running sums pass through unchanged
+                err = err_in if empty else self.engine.general_mse(x_local, err_in)
                 if rank < world - 1:
                     dist.send(err, dst=_global_rank(self.group, rank + 1), group=self.group)
                 dist.broadcast(err, src=_global_rank(self.group, world - 1), group=self.group)
             else:
                 err = self.engine.general_mse(x_local, None)
-        self.engine.general_conv(x_local, err, **outs)
+        if not empty:
+            self.engine.general_conv(x_local, err, **outs)
         return maxima
 
     @staticmethod

@@ -270,10 +270,10 @@ class SfcLayer:
     def act_scales(self, n, h, w, pad, ws, stream=None) -> np.ndarray:
         """Activation scales of the last call (1 or K*K)."""
         cnt = ctypes.c_int64()
-        check(lib().sfc_conv_act_scales(self._h, n, h, w, pad, _ptr(ws), None, ctypes.byref(cnt),
+        check(lib().sfc_conv_act_scales(self._h, n, h, w, pad, _ptr(ws), ws.numel(), None, ctypes.byref(cnt),
                                         ctypes.c_void_p(_stream_ptr(stream))))
         out = np.zeros(cnt.value, np.float64)
-        check(lib().sfc_conv_act_scales(self._h, n, h, w, pad, _ptr(ws), out.ctypes.data_as(
+        check(lib().sfc_conv_act_scales(self._h, n, h, w, pad, _ptr(ws), ws.numel(), out.ctypes.data_as(
             ctypes.POINTER(ctypes.c_double)), ctypes.byref(cnt), ctypes.c_void_p(_stream_ptr(stream))))
         return out
 
@@ -364,7 +364,7 @@ class SfcLayer:
 
     def general_mse_partial(self, n, h, w, pad, ws, err_in, err_out, stream=None):
         """MseGrid sums [groups, 101] (fp64) continued over this shard from err_in (None: batch start)."""
-        check(lib().sfc_general_mse_partial(self._h, n, h, w, pad, _ptr(ws), _ptr(err_in), _ptr(err_out),
+        check(lib().sfc_general_mse_partial(self._h, n, h, w, pad, _ptr(ws), ws.numel(), _ptr(err_in), _ptr(err_out),
                                             ctypes.c_void_p(_stream_ptr(stream))))
 
     def general_conv(self, n, h, w, pad, ws, err=None, out_f32=None, out_f64=None, out_i8=None,
@@ -375,7 +375,7 @@ class SfcLayer:
 
     def stats(self, n, h, w, pad, ws, stream=None) -> dict:
         s = np.zeros(6, np.int64)
-        check(lib().sfc_conv_stats(self._h, n, h, w, pad, _ptr(ws), s.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        check(lib().sfc_conv_stats(self._h, n, h, w, pad, _ptr(ws), ws.numel(), s.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                    ctypes.c_void_p(_stream_ptr(stream))))
         return dict(act_scale=float(s[0:1].view(np.float64)[0]), vmax=int(s[1]), saturations=int(s[2]),
                     fast_quantizer_exact=bool(s[3]), values_quantized=int(s[4]), tiles=int(s[5]))
@@ -391,7 +391,7 @@ class SfcLayer:
         pacc is None when the layer's P is chunked (never materialised whole)."""
         vq, pa = ctypes.c_void_p(), ctypes.c_void_p()
         geom = np.zeros(6, np.int64)
-        check(lib().sfc_conv_views(self._h, n, h, w, pad, _ptr(ws), ctypes.byref(vq), ctypes.byref(pa),
+        check(lib().sfc_conv_views(self._h, n, h, w, pad, _ptr(ws), ws.numel(), ctypes.byref(vq), ctypes.byref(pa),
                                    geom.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
         T, Tpad, Cpad, OCpad = (int(v) for v in geom[:4])
         F = self.spec.K ** 2

@@ -194,6 +194,9 @@ class _MaximaHook:
     def general_conv(self, x, err, **outs):
         return self.eng.general_conv(x, err, **outs)
 
+    def general_count(self):
+        return self.eng.sp["K"] ** 2 if self.eng.asc == 1 else 1
+
 
 def _general_worker(rank, world, port, x, w, spec, cfg, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -236,3 +239,49 @@ def test_sharded_general_quantconfig_equals_full_batch(cfg):
         p.join(timeout=60)
     assert np.array_equal(scales, full["act_scale"])
     assert np.array_equal(out, full["out"])
+
+
+def _empty_worker(rank, world, port, x, w, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = shard_bounds(x.shape[0], rank, world)
+        xl = torch.from_numpy(x[lo:hi].copy())
+        y = torch.empty((hi - lo, w.shape[0], x.shape[2], x.shape[3]), dtype=torch.int32)
+        vmax = ShardedConv(OracleEngine(w, "sfc6-6x6-3x3", 1)).forward(xl, y_int32=y)
+        full = ShardedConv.gather_to_rank0(y, x.shape[0])
+        eng = NumpyGeneralEngine(w, "sfc4-4x4-3x3", 1, 8, 1, 0, 1)
+        out = torch.empty((hi - lo, w.shape[0], x.shape[2], x.shape[3]), dtype=torch.float64)
+        ShardedConv(_MaximaHook(eng)).forward_general(xl, out_f64=out)
+        gen = ShardedConv.gather_to_rank0(out, x.shape[0])
+        if rank == 0:
+            q.put((int(vmax.item()), full.numpy(), eng.scales, gen.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_batch_smaller_than_world():
+    """batch 2 over 3 ranks: rank 2's shard is empty.  It joins the all-reduce with a zero
+    maximum (and passes the MseGrid sums through), so no rank blocks, and the gathered
+    results equal the full-batch oracle's (empty shards used to raise before the
+    collective and hang the other ranks)."""
+    from oracle import bindings as ob
+    rng = np.random.default_rng(5)
+    x = rng.integers(-128, 128, size=(2, 3, 7, 7), dtype=np.int8)
+    w = rng.integers(-127, 128, size=(2, 3, 3, 3), dtype=np.int8)
+    full = ob.quantized_conv(x, w, "sfc6-6x6-3x3", 1, want=("y_int",))
+    gen = ob.quantized_conv(x, w, "sfc4-4x4-3x3", 1, 8, 1, 0, 1, want=("out",))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_empty_worker, args=(r, 3, port, x, w, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    vmax, y, scales, out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert vmax == full["report"]["vmax"]
+    assert np.array_equal(y.astype(np.int64), full["y_int"])
+    assert np.array_equal(scales, gen["act_scale"])
+    assert np.array_equal(out, gen["out"])
