@@ -182,8 +182,8 @@ int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_work
  *                  sfc_conv_kept); 1: absmax only, then a quantizing transform writes vq
  *                  (sfc_act_absmax + sfc_conv_int8).  Both are bit-identical.
  *   *p_layout   storage of pacc in the workspace: 0 = int32 [F][Tpad][OCpad]; 1 = 24-bit
- *               planar [F][Tpad] rows of 3*OCpad bytes (OCpad int16 low halves, then OCpad
- *               int8 high bytes; exact as qmax^2 * Cin < 2^23; SFC_P24=0 keeps int32);
+ *               [F][Tpad] rows of 3*OCpad bytes (byte planes b0 | b1 | b2, P = b0 + 2^8 b1 +
+ *               2^16 b2 with b2 signed; exact as qmax^2 * Cin < 2^23; SFC_P24=0 keeps int32);
  *               3 = no P: Cin <= 4 layers contract with dp4a inside the output transform and
  *               the vq view is compact [F][T][4] (SFC_SMALLC=0 keeps the tensor-core GEMM). */
 int sfc_conv_schedule(sfc_layer_t layer, int n, int h, int w, int pad, int* recompute, int* p_layout);

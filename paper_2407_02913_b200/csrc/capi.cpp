@@ -2,6 +2,7 @@
 // numerical stage runs in the CUDA kernels of kernels.cu; there is no CPU
 // fallback -- a missing / failing device path returns SFC_ERR_CUDA.
 #include "../../include/sfc_b200.h"
+#include "devcache.hpp"
 
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
@@ -176,6 +177,29 @@ void gemm_output(const sfc_layer* L, const ConvGeom& g, const WsView& v, int mod
 // MinMax), for the exact int32 / int64 outputs of the 3x3 variants with P whole; the P
 // round trip (GEMM epilogue writes, output transform reads) shrinks by a quarter.
 // SFC_P24=0 keeps int32 P (A/B knob).
+bool p24_wanted(const sfc_layer* L, const ConvGeom& g);
+
+// |y| bound of the layer needs 64-bit accumulation (see needs_y64)
+bool y_bound_needs64(const sfc_layer* L) {
+    const double qmax = double((1 << (L->bits - 1)) - 1);
+    return double(L->max_a_col_l1) * double(L->max_a_col_l1) * L->IC * qmax * qmax >= 2147483647.0;
+}
+
+// P storage of a GEMM + output-transform call (ConvGeom::p24): 2 = unit-major 24-bit P for the
+// tensor-core output transform (out_mma.cu; 3x3 variants, int32-exact y, OC <= 1024), else
+// 1 = 24-bit rows for the CUDA-core output kernels, 0 = int32.  SFC_OUT_MMA=0 keeps layout 1
+// (A/B knob, read per call).
+int p_layout_of(const sfc_layer* L, const ConvGeom& g) {
+    if (!p24_wanted(L, g)) return 0;
+    const char* e = std::getenv("SFC_OUT_MMA");
+    if (e && e[0] == '0') return 1;
+    if (L->variant > 2 || y_bound_needs64(L) || g.OC > 1024) return 1;
+    // small grids (config 2: 200 units of 128 pairs) are latency-bound in the persistent
+    // tensor-core kernel; the one-block CUDA-core kernels cover them in one short wave
+    const long units = long((g.OC + kUnitOc - 1) / kUnitOc) * ((g.T + kUnitTiles - 1) / kUnitTiles);
+    return units < 2L * device_sm_count() ? 1 : 2;
+}
+
 bool p24_wanted(const sfc_layer* L, const ConvGeom& g) {
     const char* e = std::getenv("SFC_P24");
     if (e && e[0] == '0') return false;
@@ -259,7 +283,7 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     check_call(L, kept ? ws : static_cast<const void*>(d_x), n, h, w, pad);
     if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
     ConvGeom g = geom_of(L, n, h, w, pad);
-    g.p24 = p24_wanted(L, g) ? 1 : 0;
+    g.p24 = p_layout_of(L, g);
     if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
     const bool need64 = needs_y64(L, o);
     WsView v = carve(ws, g, L->F);
@@ -733,7 +757,7 @@ int sfc_conv_schedule(sfc_layer_t L, int n, int h, int w, int pad, int* recomput
         check_call(L, L, n, h, w, pad);
         const ConvGeom g = geom_of(L, n, h, w, pad);
         if (recompute) *recompute = forward_recomputes(L, g) ? 1 : 0;
-        if (p_layout) *p_layout = small_c(L, g) ? 3 : (p24_wanted(L, g) ? 1 : 0);
+        if (p_layout) *p_layout = small_c(L, g) ? 3 : p_layout_of(L, g);
     });
 }
 

@@ -188,4 +188,12 @@ __device__ __forceinline__ QuantParams derive_qparams_warp(int vmax, int bits) {
     return p;
 }
 
+// clamp(rint(v), 0, 127) as int8: cvt.rni.s32.f64 (round-to-nearest-even like rint, saturating
+// beyond int32, which the clamp maps to the same 0 / 127) and an integer clamp -- bit-identical
+// to fmin(fmax(rint(v), 0.0), 127.0) for every non-NaN v, in three instructions.
+__device__ __forceinline__ int8_t requant_i8(double v) {
+    return int8_t(min(max(__double2int_rn(v), 0), 127));
+}
+
+
 }  // namespace sfcb200

@@ -15,6 +15,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 #include "devcache.hpp"
@@ -28,6 +30,14 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
         "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
             reinterpret_cast<uint64_t>(map)),
         "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3,
+                                             int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -49,6 +59,12 @@ constexpr int gemm_threads() { return 64 + 32 * kEpiWarps + (QF ? 32 * kConvWarp
 // a frequency's A tile in L2.
 __device__ __forceinline__ void unit_of(int u, int n_ob, int n_tb, int& ob, int& tb, int& f) {
     ob = u % n_ob, tb = (u / n_ob) % n_tb, f = u / (n_ob * n_tb);
+}
+// Frequency before tile block (A/B knob SFC_GEMM_FMAJOR=1 with unit-major P; ob stays fastest,
+// so concurrent CTAs still share the A tile).
+__device__ __forceinline__ void unit_of(int u, int n_ob, int n_tb, int F, bool f_major, int& ob, int& tb, int& f) {
+    if (!f_major) return unit_of(u, n_ob, n_tb, ob, tb, f);
+    ob = u % n_ob, f = (u / n_ob) % F, tb = u / (n_ob * F);
 }
 
 // Quantize the four int16 values of two int16x2 words (lanes: low then high half) and pack
@@ -82,7 +98,7 @@ template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2, int n_tb, int n_ob,
-           int F, int nk, ConvGeom g, QFuse qf) {
+           int F, int nk, ConvGeom g, QFuse qf, uint8_t* __restrict__ pu) {
     static_assert(!QT || QF, "the TMA-staged V feeds the converters");
     constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
@@ -122,7 +138,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         if (!QF || QT) ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB);
         ptx::tma_prefetch(&tmP);
-        if (g.p24) ptx::tma_prefetch(&tmP2);
+        if (g.p24 >= 2) ptx::tma_prefetch(&tmP2);
     }
     if (warp == 1) ptx::tmem_alloc(tmem_holder, kTmemCols);
     ptx::tc_fence_before();
@@ -140,7 +156,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 int ob, tb, f;
-                unit_of(u, n_ob, n_tb, ob, tb, f);
+                unit_of(u, n_ob, n_tb, F, g.p24 == 2, ob, tb, f);
                 for (int kc = 0; kc < nk; ++kc) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (QF) {
@@ -193,7 +209,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         int i = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
             int ob, tb, f;
-            unit_of(u, n_ob, n_tb, ob, tb, f);
+            unit_of(u, n_ob, n_tb, F, g.p24 == 2, ob, tb, f);
             const int ab = i & 1;
             ptx::mbar_wait(&tfull[ab], (i >> 1) & 1);
             ptx::tc_fence_after();
@@ -205,27 +221,47 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 if (lane == 0) bulk_wait_read<kEpiBufs - 1>();  // this buffer's previous store has read smem
                 __syncwarp();
                 uint8_t* box = myE + buf * kEpiBoxBytes;
-                if (g.p24) {
-                    // 24-bit planar P: row `lane` of a 32 x 64 B box of int16 low halves (64B
-                    // swizzle: chunk j at j ^ ((lane >> 1) & 3)) and of a 32 x 32 B box of int8
-                    // high bytes (32B swizzle: chunk j at j ^ ((lane >> 2) & 1))
-                    uint32_t lo[16], hi[8];
+                if (g.p24 >= 2) {
+                    // unit-major 24-bit P (sfc_kernels.hpp pu_offset): this thread's tile t and 32
+                    // channels are one 32-byte piece of row f of each byte plane of unit
+                    // (oc block, t / 4), chunks 2 (t & 3) and 2 (t & 3) + 1 swizzled with f & 7;
+                    // the warp's 8 units x 128 B rows per plane are staged as [8][128 B] and
+                    // stored with one TMA box per plane (tmP2: the 5-D unit-major map)
+                    // (the staging box is 128B-swizzled by the store map: row r = lane / 4 of the box
+                    // holds global chunk c at c ^ r -- conflict-free 16-byte stores)
+                    const int sw = (f & 7) ^ (lane >> 2), c0 = 2 * (lane & 3);
+                    uint8_t* rb = box + (lane >> 2) * 128;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) lo[j] = __byte_perm(uint32_t(r[2 * j]), uint32_t(r[2 * j + 1]), 0x5410);
+                    for (int pl = 0; pl < 3; ++pl) {
+                        const uint32_t sel = pl == 0 ? 0x0040u : (pl == 1 ? 0x0051u : 0x0062u);
+                        uint32_t wv[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        hi[j] = __byte_perm(__byte_perm(uint32_t(r[4 * j]), uint32_t(r[4 * j + 1]), 0x0062),
-                                            __byte_perm(uint32_t(r[4 * j + 2]), uint32_t(r[4 * j + 3]), 0x0062), 0x5410);
-                    uint8_t* rl = box + lane * 64;
+                        for (int j = 0; j < 8; ++j)
+                            wv[j] = __byte_perm(__byte_perm(uint32_t(r[4 * j]), uint32_t(r[4 * j + 1]), sel),
+                                                __byte_perm(uint32_t(r[4 * j + 2]), uint32_t(r[4 * j + 3]), sel), 0x5410);
+                        *reinterpret_cast<uint4*>(rb + pl * 1024 + ((c0 ^ sw) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                        *reinterpret_cast<uint4*>(rb + pl * 1024 + (((c0 + 1) ^ sw) << 4)) =
+                            make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                    }
+                } else if (g.p24) {
+                    // 24-bit P as three byte planes (b0, b1 unsigned, b2 signed: P = b0 + 2^8 b1 +
+                    // 2^16 b2): row `lane` of three 32 x 32 B boxes (32B swizzle: chunk j at
+                    // j ^ ((lane >> 2) & 1)); the byte planes are the int8 operands of the
+                    // tensor-core output transform (out_mma.cu)
+                    uint8_t* rb = box + lane * 32;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        *reinterpret_cast<uint4*>(rl + ((j ^ ((lane >> 1) & 3)) << 4)) =
-                            make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
-                    uint8_t* rh = box + 2048 + lane * 32;
+                    for (int pl = 0; pl < 3; ++pl) {
+                        const uint32_t sel = pl == 0 ? 0x0040u : (pl == 1 ? 0x0051u : 0x0062u);
+                        uint32_t wv[8];
 #pragma unroll
-                    for (int j = 0; j < 2; ++j)
-                        *reinterpret_cast<uint4*>(rh + ((j ^ ((lane >> 2) & 1)) << 4)) =
-                            make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
+                        for (int j = 0; j < 8; ++j)
+                            wv[j] = __byte_perm(__byte_perm(uint32_t(r[4 * j]), uint32_t(r[4 * j + 1]), sel),
+                                                __byte_perm(uint32_t(r[4 * j + 2]), uint32_t(r[4 * j + 3]), sel), 0x5410);
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            *reinterpret_cast<uint4*>(rb + pl * 1024 + ((j ^ ((lane >> 2) & 1)) << 4)) =
+                                make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]);
+                    }
                 } else {
                     // row `lane` of a 32 x 32 int32 box, 16-byte chunk j stored at j ^ (lane & 7) (128B swizzle)
                     uint8_t* row = box + lane * 128;
@@ -238,9 +274,13 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 __syncwarp();
                 if (lane == 0) {
                     const int t0 = tb * kRowsPerTile + q * 32, o0 = ob * BN + c;
-                    if (g.p24) {  // byte coordinates: low halves at 2*oc, high bytes at oc (second map)
-                        tma_store_3d(&tmP, box, 2 * o0, t0, f);
-                        tma_store_3d(&tmP2, box + 2048, o0, t0, f);
+                    if (g.p24 >= 2) {  // (row, f, plane, tile group, oc block)
+                        const int t0u = (tb * kRowsPerTile + q * 32) / kUnitTiles, o0u = (ob * BN + c) / kUnitOc;
+#pragma unroll
+                        for (int pl = 0; pl < 3; ++pl) tma_store_5d(&tmP2, box + pl * 1024, 0, t0u, f, pl, o0u);
+                    } else if (g.p24) {  // byte coordinates: plane j of a P row starts at j * OCpad
+#pragma unroll
+                        for (int pl = 0; pl < 3; ++pl) tma_store_3d(&tmP, box + pl * 1024, pl * g.OCpad + o0, t0, f);
                     } else {
                         tma_store_3d(&tmP, box, o0, t0, f);
                     }
@@ -314,7 +354,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         auto load = [&](int s, uint4 (&va)[kItems], uint4 (&vb)[kItems]) {
             const int u = int(blockIdx.x) + (s / nk) * int(gridDim.x), kc = s % nk;
             int ob, tb, f;
-            unit_of(u, n_ob, n_tb, ob, tb, f);
+            unit_of(u, n_ob, n_tb, F, g.p24 == 2, ob, tb, f);
 #pragma unroll
             for (int j = 0; j < kItems; ++j) {
                 const int i = ct + j * (32 * kConvWarps);
@@ -411,36 +451,42 @@ bool make_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void*
 }
 
 // The GEMM's P maps: int32 [F][Tpad][OCpad] boxes of 32 x 32 (rows x oc), 128B-swizzled; or
-// 24-bit planar rows of 3*OCpad bytes: the low-half map (2*OCpad bytes, box 64 B x 32 rows,
-// 64B swizzle) and the high-byte map (OCpad bytes from byte 2*OCpad, box 32 B x 32, 32B
-// swizzle).
+// 24-bit P as rows of 3*OCpad bytes (byte planes b0 | b1 | b2 of OCpad bytes each): one byte
+// map, box 32 B x 32 rows, 32B swizzle, stored once per plane.
 bool make_p_maps(CUtensorMap* m, CUtensorMap* m2, int32_t* P, const ConvGeom& g, int F, int rows) {
-    if (!g.p24) {
-        *m2 = CUtensorMap{};
-        return make_tmap_3d(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, rows, F, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    *m2 = CUtensorMap{};
+    if (g.p24 == 2) {  // unit-major: box [8 tile groups][128 B] per (f, plane), 128B-swizzled staging
+        return make_pu_map(m2, P, g, F, 8, 1, true) &&
+               make_tmap_3d(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, P, uint64_t(g.OCpad) * 3, rows, F, 32, 32,
+                            CU_TENSOR_MAP_SWIZZLE_32B);
     }
-    auto fn = encode_fn();
-    if (!fn) return false;
-    const cuuint64_t rb = cuuint64_t(g.OCpad) * 3;  // row bytes
-    cuuint64_t dlo[3] = {cuuint64_t(g.OCpad) * 2, cuuint64_t(rows), cuuint64_t(F)};
-    cuuint64_t dhi[3] = {cuuint64_t(g.OCpad), cuuint64_t(rows), cuuint64_t(F)};
-    cuuint64_t strides[2] = {rb, rb * rows};
-    cuuint32_t blo[3] = {64, 32, 1}, bhi[3] = {32, 32, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    uint8_t* base = reinterpret_cast<uint8_t*>(P);
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dlo, strides, blo, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-               CUDA_SUCCESS &&
-           fn(m2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base + 2 * size_t(g.OCpad), dhi, strides, bhi, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    if (!g.p24)
+        return make_tmap_3d(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, P, g.OCpad, rows, F, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    return make_tmap_3d(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, P, uint64_t(g.OCpad) * 3, rows, F, 32, 32,
+                        CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
 int sm_count() { return device_sm_count(); }
+}  // namespace
+
+bool make_pu_map(CUtensorMap* m, void* P, const ConvGeom& g, int F, int box_tg, int box_f, bool swizzle128) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t ntg = cuuint64_t(g.Tpad) / kUnitTiles;
+    cuuint64_t dims[5] = {128, ntg, cuuint64_t(F), 3, cuuint64_t(g.OCpad) / kUnitOc};
+    cuuint64_t strides[4] = {128, ntg * 128, cuuint64_t(F) * ntg * 128, 3 * cuuint64_t(F) * ntg * 128};
+    cuuint32_t box[5] = {128, cuuint32_t(box_tg), cuuint32_t(box_f), 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
 
 template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
-                        const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl) {
+                        const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl, uint8_t* pu) {
     const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + (QT ? size_t(STAGES) * kRowsPerTile * BK * 2 : 0) +
                         size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256;
     auto kern = k_gemm<BN, BK, STAGES, QF, QT>;
@@ -465,15 +511,20 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, a, b, p, p2, n_tb, n_ob, F, g.Cpad / BK, g, qf);
+    ConvGeom gk = g;
+    if (g.p24 == 2) {  // unit-major P: tile-block-major unit order unless SFC_GEMM_FMAJOR=1 (A/B knob)
+        const char* e = std::getenv("SFC_GEMM_FMAJOR");
+        if (!(e && e[0] == '1')) gk.p24 = 3;  // (3: unit-major P, tile-block-major order)
+    }
+    return cudaLaunchKernelEx(&cfg, kern, a, b, p, p2, n_tb, n_ob, F, g.Cpad / BK, gk, qf, pu);
 }
 
 template <int BK, int STAGES, bool QF>
 cudaError_t gemm_by_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
-                       const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl) {
-    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
-    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
-    return gemm_launch<256, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
+                       const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl, uint8_t* pu) {
+    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, pu);
+    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, pu);
+    return gemm_launch<256, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, pu);
 }
 
 template <bool QF>
@@ -488,10 +539,12 @@ cudaError_t gemm_dispatch(const int8_t* vqA, const int8_t* uqB, int32_t* P, cons
         !make_p_maps(&tp, &tp2, P, g, F, g.Tpad))
         return cudaErrorInvalidValue;
     const int nk = g.Cpad / g.BK;
+    uint8_t* pu = reinterpret_cast<uint8_t*>(P);
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl)
-                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl);
-    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl) : gemm_by_bn<64, 4, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl);
+        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, pu)
+                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, pu);
+    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, pu)
+                   : gemm_by_bn<64, 4, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, pu);
 }
 }  // namespace
 
@@ -517,10 +570,10 @@ cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, c
     const int nk = g.Cpad / g.BK;
     const QFuse none{};
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl)
-                       : gemm_by_bn<128, 3, false>(ta, tb, tp, tp2, gc, F, none, st, pdl);
-    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl)
-                   : gemm_by_bn<64, 4, false>(ta, tb, tp, tp2, gc, F, none, st, pdl);
+        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, nullptr)
+                       : gemm_by_bn<128, 3, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, nullptr);
+    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, nullptr)
+                   : gemm_by_bn<64, 4, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, nullptr);
 }
 
 cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
@@ -548,13 +601,13 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
         return cudaErrorInvalidValue;
     // two stages: A + B + V stages and the epilogue boxes fill the 227 KB at BN = 256, BK = 128
     if (g.BK == 128) {
-        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
-        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
-        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
+        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
+        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
     }
-    if (g.BN == 64) return gemm_launch<64, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
-    if (g.BN == 128) return gemm_launch<128, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
-    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+    if (g.BN == 64) return gemm_launch<64, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
+    if (g.BN == 128) return gemm_launch<128, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
+    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
 }
 
 SFC_TL_UNIT_READER(tl_read_gemm)

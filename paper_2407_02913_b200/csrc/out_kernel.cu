@@ -31,11 +31,10 @@
 
 namespace sfcb200 {
 
-// clamp(rint(v), 0, 127) as int8: cvt.rni.s32.f64 (round-to-nearest-even like rint, saturating
-// beyond int32, which the clamp maps to the same 0 / 127) and an integer clamp -- bit-identical
-// to fmin(fmax(rint(v), 0.0), 127.0) for every non-NaN v, in three instructions.
-__device__ __forceinline__ int8_t requant_i8(double v) {
-    return int8_t(min(max(__double2int_rn(v), 0), 127));
+// One value of a 24-bit P slice held as three byte planes (b0, b1 unsigned, b2 signed) of
+// `pl` bytes each: P = b0 + 2^8 b1 + 2^16 b2.
+__device__ __forceinline__ int p24_value(const uint8_t* __restrict__ sp, size_t pl, int e) {
+    return (int(reinterpret_cast<const int8_t*>(sp + 2 * pl)[e]) << 16) | (int(sp[pl + e]) << 8) | int(sp[e]);
 }
 
 namespace {
@@ -119,14 +118,12 @@ __global__ void __launch_bounds__(TBX ? 256 : kOutThreads, 2)
     // chunk-relative, the output position uses the absolute row g.row0 + row
     const int oc0 = blockIdx.x * kOcc, tc = blockIdx.y, row = blockIdx.z;
     tl_mark(kTlOutput, 0);
-    // 24-bit planar P: the slice's int16 low halves [F][TB][kOcc], then its int8 high bytes
-    const int16_t* sp_lo = reinterpret_cast<const int16_t*>(smem);
-    // (TMA destinations are 128-byte aligned: the high plane starts at the next 128-byte boundary)
-    constexpr size_t kHiOff = (size_t(T::F) * TB * kOcc * 2 + 127) & ~size_t(127);
-    const int8_t* sp_hi = reinterpret_cast<const int8_t*>(smem + kHiOff);
+    // 24-bit P: the slice's byte planes b0, b1 (unsigned), b2 (signed), [F][TB][kOcc] each, at
+    // 128-byte aligned offsets (TMA destinations)
+    constexpr size_t kPl = (size_t(T::F) * TB * kOcc + 127) & ~size_t(127);
+    const uint8_t* sp_b = smem;
     if (threadIdx.x == 0) {
         ptx::tma_prefetch(&tmP);
-        if (P24) ptx::tma_prefetch(&tmP2);
         ptx::mbar_init(full, 1);
         ptx::fence_mbar_init();
     }
@@ -137,8 +134,9 @@ __global__ void __launch_bounds__(TBX ? 256 : kOutThreads, 2)
     if (threadIdx.x == 0) {
         if constexpr (P24) {
             ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 3));
-            ptx::tma_load_3d(smem, &tmP, full, 2 * oc0, row * g.tw + tc * TB, 0);
-            ptx::tma_load_3d(smem + kHiOff, &tmP2, full, oc0, row * g.tw + tc * TB, 0);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+                ptx::tma_load_3d(smem + pl * kPl, &tmP, full, pl * g.OCpad + oc0, row * g.tw + tc * TB, 0);
         } else {
             ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * sizeof(p_elem_t<MODE>)));
             ptx::tma_load_3d(smem, &tmP, full, oc0, row * g.tw + tc * TB, 0);
@@ -173,7 +171,7 @@ __global__ void __launch_bounds__(TBX ? 256 : kOutThreads, 2)
         for (int k = 0; k < K; ++k) {
             const int e = ((k * K + l) * TB + tj) * kOcc + oc;
             if constexpr (P24)
-                pk[k] = acc_t((int(sp_hi[e]) << 16) | int(uint16_t(sp_lo[e])));
+                pk[k] = acc_t(p24_value(sp_b, kPl, e));
             else
                 pk[k] = sp[e];
         }
@@ -398,15 +396,16 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
     __shared__ float s_scalef[kOcc];
     const int lane = threadIdx.x & 31, tjl = threadIdx.x >> 5;
     tl_mark(kTlOutput, 0);
-    const int16_t* sp_lo = reinterpret_cast<const int16_t*>(smem);  // P24: [F][TB][kOcc] low halves,
-    constexpr size_t kHiOff = (size_t(T::F) * TB * kOcc * 2 + 127) & ~size_t(127);  // (128-byte aligned TMA)
-    const int8_t* sp_hi = reinterpret_cast<const int8_t*>(smem + kHiOff);  // then high bytes
+    // P24: byte planes b0, b1, b2 of [F][TB][kOcc] at 128-byte aligned offsets (TMA destinations)
+    constexpr size_t kPl = (size_t(T::F) * TB * kOcc + 127) & ~size_t(127);
+    const uint8_t* sp_b = smem;
     auto issue = [&](int blk) {  // thread 0: the block's P slice
         const int ob = blk % n_ob, r = blk / n_ob, tc = r % n_tc, row = r / n_tc;
         if constexpr (P24) {
             ptx::mbar_expect_tx(full, uint32_t(size_t(T::F) * TB * kOcc * 3));
-            ptx::tma_load_3d(smem, &tmP, full, 2 * ob * kOcc, row * g.tw + tc * TB, 0);
-            ptx::tma_load_3d(smem + kHiOff, &tmP2, full, ob * kOcc, row * g.tw + tc * TB, 0);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+                ptx::tma_load_3d(smem + pl * kPl, &tmP, full, pl * g.OCpad + ob * kOcc, row * g.tw + tc * TB, 0);
         } else {
             ptx::mbar_expect_tx(full, uint32_t(PS::slice));
             ptx::tma_load_3d(smem, &tmP, full, ob * kOcc, row * g.tw + tc * TB, 0);
@@ -414,7 +413,6 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
     };
     if (threadIdx.x == 0) {
         ptx::tma_prefetch(&tmP);
-        if (P24) ptx::tma_prefetch(&tmP2);
         ptx::mbar_init(full, 1);
         ptx::fence_mbar_init();
     }
@@ -448,7 +446,7 @@ __global__ void __launch_bounds__(32 * out_tb<V>()) k_output_pers(const __grid_c
                 for (int l = 0; l < K; ++l) {
                     const int e = ((k * K + l) * TB + tjl) * kOcc + lane;
                     if constexpr (P24)
-                        pr[l] = acc_t((int(sp_hi[e]) << 16) | int(uint16_t(sp_lo[e])));
+                        pr[l] = acc_t(p24_value(sp_b, kPl, e));
                     else
                         pr[l] = acc_t(sp[e]);
                 }
@@ -610,23 +608,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// The output kernels' P slice maps: int32 / fp64 (box kOcc x TB x F), or the two planes of
-// the 24-bit layout (low halves: box 2*kOcc bytes x TB x F; high bytes: kOcc x TB x F).
+// The output kernels' P slice maps: int32 / fp64 (box kOcc x TB x F), or the byte rows of the
+// 24-bit layout (3*OCpad bytes: planes b0 | b1 | b2; box kOcc x TB x F, loaded once per plane).
 bool make_slice_maps(CUtensorMap* tm, CUtensorMap* tm2, const void* P, const ConvGeom& g, int F, int TB, bool f64) {
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint32_t estr[3] = {1, 1, 1};
+    *tm2 = CUtensorMap{};
     if (g.p24) {
         const cuuint64_t rb = cuuint64_t(g.OCpad) * 3;
-        cuuint64_t dlo[3] = {cuuint64_t(g.OCpad) * 2, cuuint64_t(g.Tpad), cuuint64_t(F)};
-        cuuint64_t dhi[3] = {cuuint64_t(g.OCpad), cuuint64_t(g.Tpad), cuuint64_t(F)};
+        cuuint64_t dims[3] = {rb, cuuint64_t(g.Tpad), cuuint64_t(F)};
         cuuint64_t strides[2] = {rb, rb * g.Tpad};
-        cuuint32_t blo[3] = {2 * kOcc, cuuint32_t(TB), cuuint32_t(F)}, bhi[3] = {kOcc, cuuint32_t(TB), cuuint32_t(F)};
-        uint8_t* base = static_cast<uint8_t*>(const_cast<void*>(P));
-        return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dlo, strides, blo, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-                   CUDA_SUCCESS &&
-               fn(tm2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base + 2 * size_t(g.OCpad), dhi, strides, bhi, estr,
+        cuuint32_t box[3] = {kOcc, cuuint32_t(TB), cuuint32_t(F)};
+        return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(P), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
@@ -634,7 +628,6 @@ bool make_slice_maps(CUtensorMap* tm, CUtensorMap* tm2, const void* P, const Con
     cuuint64_t dims[3] = {cuuint64_t(g.OCpad), cuuint64_t(g.Tpad), cuuint64_t(F)};
     cuuint64_t strides[2] = {cuuint64_t(g.OCpad) * es, cuuint64_t(g.OCpad) * g.Tpad * es};
     cuuint32_t box[3] = {kOcc, cuuint32_t(TB), cuuint32_t(F)};
-    *tm2 = CUtensorMap{};
     return fn(tm, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(P), dims,
               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -728,6 +721,10 @@ bool out_pers_wanted(int variant, int mode, const ConvGeom& g, const OutPtrs& o)
 template <int V>
 cudaError_t out_by_width(int mode, const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
                          const OutPtrs& o, cudaStream_t st, bool pdl) {
+    if (g.p24 == 2) {  // unit-major P: only the tensor-core output transform reads it
+        if (mode != 0) return cudaErrorInvalidValue;
+        return launch_output_mma(V, P, g, qp, sf, o, st, pdl);
+    }
     if constexpr (V <= 2) {
         if (out_pers_wanted(V, mode, g, o)) {
             OutPtrs op = o;

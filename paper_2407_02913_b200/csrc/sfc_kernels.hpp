@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace sfcb200 {
@@ -18,11 +19,25 @@ struct ConvGeom {
     // output-transform launches over a chunk of image tile rows (P chunked, see PChunk):
     // rows [row0, row0 + nrows) of the B * th rows; geom_init sets the whole range
     int row0, nrows;
-    // P storage: 0 = int32 [F][Tpad][OCpad]; 1 = 24-bit planar [F][Tpad] rows of 3*OCpad bytes:
-    // OCpad int16 low halves, then OCpad int8 high bytes (exact when |P| < 2^23, i.e.
-    // qmax^2 * Cin < 2^23).  geom_init sets 0; run_conv decides (p24_wanted).
+    // P storage: 0 = int32 [F][Tpad][OCpad]; 1 = 24-bit [F][Tpad] rows of 3*OCpad bytes: byte
+    // planes b0 | b1 | b2 of OCpad bytes, P = b0 + 2^8 b1 + 2^16 b2 (exact when |P| < 2^23, i.e.
+    // qmax^2 * Cin < 2^23).  2 = the same 24-bit values unit-major for the tensor-core output
+    // transform (pu_offset below).  geom_init sets 0; run_conv decides (p24_wanted).
     int p24;
 };
+
+// 24-bit P, unit-major (ConvGeom::p24 == 2): the A operands of the tensor-core output
+// transform (out_mma.cu), written pre-swizzled by the GEMM epilogue.  A unit is kUnitOc output
+// channels x kUnitTiles consecutive tiles = 128 MMA rows (row = tt * 32 + oc).  Storage
+// [OCpad / 32][3 byte planes][F][Tpad / 4][128 B]: byte plane b0, b1 (unsigned), b2 (signed)
+// (P = b0 + 2^8 b1 + 2^16 b2); the 128-byte row (f, unit) holds [tt][32 oc] with 16-byte chunk
+// c at c ^ (f & 7), the 128B-swizzle pattern of an MN-major tcgen05 operand.  The F rows of a
+// unit land in shared memory as that operand with one TMA box; the GEMM writes the rows of 8
+// consecutive units (1 KB contiguous) per box.
+constexpr int kUnitTiles = 4, kUnitOc = 32;
+__host__ __device__ inline size_t pu_offset(int ob, int tg, int plane, int f, int n_tg, int F) {
+    return (((size_t(ob) * 3 + plane) * F + f) * n_tg + tg) * 128;
+}
 
 // P chunking (opt-in: SFC_PCHUNK_MB = budget in MB; unset or 0 = never chunk).  P (4 B per
 // (frequency, tile, oc)) is the largest intermediate; when the whole of it exceeds the
@@ -137,6 +152,14 @@ struct OutPtrs {
 // vq4 = compact [F][T][4] int8 from the quantizing transform.
 cudaError_t launch_output_smallc(int variant, const int8_t* vq4, const int8_t* uq, const ConvGeom& g,
                                  const QuantParams* qp, const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
+// Tensor-core output transform over unit-major 24-bit P (g.p24 == 2; 3x3 variants, int32-exact
+// y, every output kind): cudaErrorNotSupported when not applicable.
+cudaError_t launch_output_mma(int variant, const void* P, const ConvGeom& g, const QuantParams* qp, const double* sf,
+                              const OutPtrs& o, cudaStream_t st, bool pdl);
+// The 5-D map over unit-major P: (128-byte row, tile group, f, plane, oc block), box rows x
+// tile groups x frequencies as given; swizzle as given (the data itself is pre-swizzled).
+bool make_pu_map(CUtensorMap* m, void* P, const ConvGeom& g, int F, int box_tg, int box_f, bool swizzle128);
+bool output_mma_supported(int variant, const ConvGeom& g, const OutPtrs& o);
 cudaError_t launch_output(int variant, int mode, const void* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
 // report sums: `sums` holds 2 + 2 * kSqErrBlocks doubles (result in [0..1], block partials after)

@@ -402,11 +402,22 @@ class SfcLayer:
         vqt = _wrap_device(vq.value, (F, Tpad, Cpad), torch.int8, self.device)[:, :T, : self.IC]
         if not pa.value:
             return vqt, None
-        if blocked.value == 1:  # 24-bit planar rows: OCpad int16 low halves, OCpad int8 high bytes (a copy)
+        if blocked.value == 2:  # unit-major 24-bit P (sfc_kernels.hpp pu_offset), pre-swizzled (a copy)
+            n_ob, n_tg = OCpad // 32, Tpad // 4
+            raw = _wrap_device(pa.value, (n_ob, 3, F, n_tg, 128), torch.uint8, self.device)
+            f = torch.arange(F, device=self.device)[:, None, None]
+            lb = torch.arange(128, device=self.device)[None, None, :]
+            src = ((((lb >> 4) ^ (f & 7)) << 4) | (lb & 15)).expand(n_ob, 3, F, n_tg, 128)
+            lg = torch.gather(raw, 4, src).to(torch.int32)  # [ob][plane][f][tg][tt * 32 + oc]
+            p = (lg[:, 0] & 0xFF) | ((lg[:, 1] & 0xFF) << 8) | (((lg[:, 2] & 0xFF) ^ 0x80) - 0x80) * 65536
+            p = p.view(n_ob, F, n_tg, 4, 32).permute(1, 2, 3, 0, 4).reshape(F, n_tg * 4, n_ob * 32)
+            return vqt, p[:, :T, : self.OC]
+        if blocked.value == 1:  # 24-bit rows of three byte planes b0 | b1 | b2 (a copy)
             raw = _wrap_device(pa.value, (F, Tpad, 3 * OCpad), torch.uint8, self.device)
-            lo = raw[:, :, : 2 * OCpad].contiguous().view(torch.int16).to(torch.int32) & 0xFFFF
-            hi = raw[:, :, 2 * OCpad:].contiguous().view(torch.int8).to(torch.int32)
-            return vqt, (lo | (hi << 16))[:, :T, : self.OC]
+            b0 = raw[:, :, :OCpad].to(torch.int32) & 0xFF  # (the wrapped view may be signed bytes)
+            b1 = raw[:, :, OCpad:2 * OCpad].to(torch.int32) & 0xFF
+            b2 = raw[:, :, 2 * OCpad:].contiguous().view(torch.int8).to(torch.int32)
+            return vqt, (b0 | (b1 << 8) | (b2 << 16))[:, :T, : self.OC]
         pat = _wrap_device(pa.value, (F, Tpad, OCpad), torch.int32, self.device)[:, :T, : self.OC]
         return vqt, pat
 

@@ -724,23 +724,29 @@ def test_small_channel_fused_path(cuda, variant, case, monkeypatch):
 
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_p24_and_output_kernels_agree(cuda, variant, monkeypatch):
-    """24-bit planar P (default) vs int32 P (SFC_P24=0), and the persistent output kernel of
-    512-channel int32 / fp32 layers vs the one-block kernel (SFC_OUT_PERS=0): y, fp32 and pacc
-    bit for bit on a 512-channel layer and on a small ragged one."""
+    """The output-transform paths agree bit for bit: unit-major 24-bit P with the tensor-core
+    output transform (default, out_mma.cu), 24-bit P rows with the CUDA-core kernels
+    (SFC_OUT_MMA=0: persistent kernel on 512-channel layers, one-block kernel with
+    SFC_OUT_PERS=0) and int32 P (SFC_P24=0): y, fp32, int8 requant and pacc on a 512-channel
+    layer, a 64-channel layer and a small ragged one."""
     rng = np.random.default_rng(11)
-    for (B, C, OC, H, W, pad) in ((26, 64, 512, 14, 14, 1), (2, 40, 70, 11, 9, 1)):  # (26 images: >= 8 blocks per SM)
+    for (B, C, OC, H, W, pad) in ((26, 64, 512, 14, 14, 1), (40, 64, 64, 30, 26, 1), (2, 40, 70, 11, 9, 1)):
         x = rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)
         w = rng.integers(-127, 128, size=(OC, C, 3, 3), dtype=np.int8)
         dev = torch.device("cuda", 0)
         layer = sc.SfcLayer(variant, torch.from_numpy(w).to(dev))
-        assert layer.schedule(B, H, W, pad)["p_layout"] == 1
+        for k in ("SFC_P24", "SFC_OUT_PERS", "SFC_OUT_MMA"):
+            monkeypatch.delenv(k, raising=False)
+        # (small grids keep the 24-bit rows and the one-block kernels)
+        assert layer.schedule(B, H, W, pad)["p_layout"] == (1 if B == 2 else 2)
         res = {}
-        for name, env in (("default", {}), ("p32", {"SFC_P24": "0"}), ("one-block", {"SFC_OUT_PERS": "0"})):
-            for k in ("SFC_P24", "SFC_OUT_PERS"):
+        for name, env in (("default", {}), ("rows", {"SFC_OUT_MMA": "0"}), ("p32", {"SFC_P24": "0"}),
+                          ("one-block", {"SFC_OUT_MMA": "0", "SFC_OUT_PERS": "0"})):
+            for k in ("SFC_P24", "SFC_OUT_PERS", "SFC_OUT_MMA"):
                 monkeypatch.delenv(k, raising=False)
             for k, v in env.items():
                 monkeypatch.setenv(k, v)
-            res[name] = run_gpu(x, w, variant, pad, outs=("y", "f32"), views=True)
-        for name in ("p32", "one-block"):
-            for k in ("y", "f32", "pacc", "vq"):
+            res[name] = run_gpu(x, w, variant, pad, outs=("y", "f32", "i8"), requant=0.003, views=True)
+        for name in ("rows", "p32", "one-block"):
+            for k in ("y", "f32", "i8", "pacc", "vq"):
                 assert np.array_equal(res["default"][k], res[name][k]), (name, k)

@@ -76,7 +76,8 @@ __global__ void k_ldtm2(int iters, long long* cyc, int* sink) {
     if (warp == 0) ptx::tmem_dealloc(base, 512);
 }
 
-__global__ void k_mma(int iters, int N, long long* cyc) {
+__global__ void k_mma(int iters, int N, long long* cyc, int mode) {
+    // mode 0: SS (A, B from shared memory); mode 1: A from TMEM (columns 256..), B from shared memory
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tbase;
     __shared__ __align__(8) uint64_t bar;
@@ -88,21 +89,29 @@ __global__ void k_mma(int iters, int N, long long* cyc) {
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    long long t0 = clock64();
     if (threadIdx.x == 32) {
         const uint32_t sa = ptx::smem_u32(smem), sb = ptx::smem_u32(smem + 32768);
         const uint32_t idesc = ptx::idesc_i8(128, N);
+        long long t0 = clock64();
         for (int i = 0; i < iters; ++i) {
             const int kk = i & 3;   // 4 K steps of 32 B within a 128B-swizzled row
-            ptx::mma_i8(tbase + uint32_t((i & 1) * 256), ptx::smem_desc_kmajor(sa + kk * 32, 128),
-                        ptx::smem_desc_kmajor(sb + kk * 32, 128), idesc, 1);
+            if (mode == 0) {
+                ptx::mma_i8(tbase + uint32_t((i & 1) * 256), ptx::smem_desc_kmajor(sa + kk * 32, 128),
+                            ptx::smem_desc_kmajor(sb + kk * 32, 128), idesc, 1);
+            } else {
+                const uint32_t ta = tbase + 256 + uint32_t(kk * 8);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tbase + uint32_t((i & 1) * 128)),
+                    "r"(ta), "l"(ptx::smem_desc_kmajor(sb + kk * 32, 128)), "r"(idesc)
+                    : "memory");
+            }
         }
         ptx::mma_commit(&bar);
         ptx::mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        cyc[blockIdx.x] = t1 - t0;
     }
-    __syncthreads();
-    long long t1 = clock64();
-    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc(tbase, 512);
@@ -154,17 +163,19 @@ int main() {
         printf("ldtm x32 x2-in-flight warps=%2d: %.1f B/cyc/SM\n", w, 4096.0 * w * iters / c);
     }
     CK(cudaFuncSetAttribute(k_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-    for (int n : {16, 32, 64, 128, 256}) {
+    for (int mode = 0; mode < 2; ++mode)
+    for (int n : {8, 16, 24, 32, 48, 64, 128, 256}) {
+        if (mode == 1 && n > 128) continue;
         const int it = 8192;
-        k_mma<<<G, 128, 65536>>>(it, n, dc);
+        k_mma<<<G, 128, 65536>>>(it, n, dc, mode);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
-        k_mma<<<G, 128, 65536>>>(it, n, dc);
+        k_mma<<<G, 128, 65536>>>(it, n, dc, mode);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpy(hc, dc, sizeof(hc), cudaMemcpyDeviceToHost));
         double c = avg(hc, G);
-        printf("tcgen05.mma i8 M=128 N=%3d: %.2f cyc/mma  %.0f MAC/cyc/SM\n", n, c / it, 128.0 * n * 32 * it / c);
+        printf("tcgen05.mma i8 %s M=128 N=%3d: %.2f cyc/mma  %.0f MAC/cyc/SM\n", mode ? "TS" : "SS", n, c / it, 128.0 * n * 32 * it / c);
     }
     for (int w : {4, 8, 16, 32}) {
         const int it = 2048;
