@@ -4,7 +4,6 @@
 #include "../../include/sfc_b200.h"
 #include "devcache.hpp"
 
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -85,22 +84,10 @@ struct Unsupported : std::length_error {
 
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
-// cuBLAS for the fp64 contractions (tcgen05 has no fp64 kind): one handle per host thread.
-cublasHandle_t cublas_on(cudaStream_t st) {
-    thread_local cublasHandle_t handle = nullptr;
-    if (!handle && cublasCreate(&handle) != CUBLAS_STATUS_SUCCESS) throw CudaFail("cublasCreate failed");
-    if (cublasSetStream(handle, st) != CUBLAS_STATUS_SUCCESS) throw CudaFail("cublasSetStream failed");
-    return handle;
-}
-
-// P_f[t][o] = sum_c V_f[t][c] U_f[o][c] for `batch` frequency slices (row-major), i.e. the
-// column-major P_f^T (OCpad x Tpad) = U_f (op T of the col-major view) x V_f^T.
+// P_f[t][o] = sum_c V_f[t][c] U_f[o][c] for `batch` frequency slices (row-major): the fp64
+// contractions tcgen05 has no kind for (f64_gemm.cu).
 void dgemm_freq(const double* U, const double* V, double* P, const ConvGeom& g, int batch, cudaStream_t st) {
-    const double one = 1.0, zero = 0.0;
-    if (cublasDgemmStridedBatched(cublas_on(st), CUBLAS_OP_T, CUBLAS_OP_N, g.OCpad, g.Tpad, g.Cpad, &one, U, g.Cpad,
-                                  (long long)g.OCpad * g.Cpad, V, g.Cpad, (long long)g.Tpad * g.Cpad, &zero, P, g.OCpad,
-                                  (long long)g.Tpad * g.OCpad, batch) != CUBLAS_STATUS_SUCCESS)
-        throw CudaFail("cublasDgemmStridedBatched failed");
+    ck(launch_dgemm_freq(U, V, P, g.Tpad, g.OCpad, g.Cpad, batch, st), "fp64 contraction launch");
 }
 
 // The wide (9-16 bit) tail of a general forward: vq as integer-valued doubles from the

@@ -160,6 +160,10 @@ cudaError_t launch_output_mma(int variant, const void* P, const ConvGeom& g, con
 // tile groups x frequencies as given; swizzle as given (the data itself is pre-swizzled).
 bool make_pu_map(CUtensorMap* m, void* P, const ConvGeom& g, int F, int box_tg, int box_f, bool swizzle128);
 bool output_mma_supported(int variant, const ConvGeom& g, const OutPtrs& o);
+// Batched fp64 NT contraction P_f = V_f U_f^T (f64_gemm.cu): the 9-16 bit exact-integer path
+// and the float fast_conv2d path.
+cudaError_t launch_dgemm_freq(const double* U, const double* V, double* P, int Tpad, int OCpad, int Cpad, int batch,
+                              cudaStream_t st);
 cudaError_t launch_output(int variant, int mode, const void* P, const ConvGeom& g, const QuantParams* qp,
                           const double* sf, const OutPtrs& o, cudaStream_t st, bool pdl);
 // report sums: `sums` holds 2 + 2 * kSqErrBlocks doubles (result in [0..1], block partials after)
