@@ -500,7 +500,11 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     per_sm = per_sm < 1 ? 1 : per_sm;
     per_sm = per_sm > 512 / kTmemCols ? 512 / kTmemCols : per_sm;
     per_sm = per_sm > 2 ? 2 : per_sm;
-    const int resident = sm_count() * per_sm;
+    int resident = sm_count() * per_sm;
+    if (const char* e = std::getenv("SFC_GEMM_GRID")) {  // experiment knob: cap the persistent grid
+        const int cap = std::atoi(e);
+        if (cap > 0 && cap < resident) resident = cap;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units < resident ? units : resident);
     cfg.blockDim = dim3(gemm_threads<QF>());

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "devcache.hpp"
@@ -310,8 +311,13 @@ cudaError_t om_launch(const void* P, const ConvGeom& g, const QuantParams* qp, c
     const int n_tg_used = (g.T + kUnitTiles - 1) / kUnitTiles;
     const long units = long(n_ob) * n_tg_used;
     if (units > 0x7fffffffL) return cudaErrorInvalidConfiguration;
+    long grid = std::min<long>(units, device_sm_count());
+    if (const char* e = std::getenv("SFC_OUT_GRID")) {  // experiment knob: cap the persistent grid
+        const long cap = std::atol(e);
+        if (cap > 0 && cap < grid) grid = cap;
+    }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(std::min<long>(units, device_sm_count())));
+    cfg.gridDim = dim3(unsigned(grid));
     cfg.blockDim = dim3(kOmThreads);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
