@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             int ob, tb, f;
             unit_of(u, n_ob, n_tb, F, g.p24 == 2, ob, tb, f);
             const int ab = i & 1;
-            ptx::mbar_wait(&tfull[ab], (i >> 1) & 1);
+            ptx::mbar_wait_sleep(&tfull[ab], (i >> 1) & 1);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = half * kHalf; c < (half + 1) * kHalf; c += 32) {
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int s2 = 0; s2 < npairs; ++s2) {
-                ptx::mbar_wait(&vfull[stage], phase);  // (the producer waited for the stage to be free)
+                ptx::mbar_wait_sleep(&vfull[stage], phase);  // (the producer waited for the stage to be free)
                 const uint8_t* v_st = sV + stage * kVStageBytes;
                 uint8_t* a_st = sA + stage * kRowsPerTile * BK;
 #pragma unroll
@@ -603,15 +603,18 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
     if (!make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
         !make_p_maps(&tp, &tp2, P, g, F, g.Tpad))
         return cudaErrorInvalidValue;
-    // two stages: A + B + V stages and the epilogue boxes fill the 227 KB at BN = 256, BK = 128
+    // stages: A + B + V per stage plus the 64 KB of epilogue boxes within 227 KB -- two at
+    // BK = 128, four at BK = 64 with BN <= 128 (the single-K-chunk
+    // 64-channel layers: more units' V tiles in flight to hide the load latency)
+    uint8_t* pu = reinterpret_cast<uint8_t*>(P);
     if (g.BK == 128) {
-        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
-        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
-        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
+        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
+        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
+        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
     }
-    if (g.BN == 64) return gemm_launch<64, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
-    if (g.BN == 128) return gemm_launch<128, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
-    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, reinterpret_cast<uint8_t*>(P));
+    if (g.BN == 64) return gemm_launch<64, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
+    if (g.BN == 128) return gemm_launch<128, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
+    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
 }
 
 SFC_TL_UNIT_READER(tl_read_gemm)
