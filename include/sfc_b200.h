@@ -171,7 +171,8 @@ int sfc_conv_stats(sfc_layer_t layer, int n, int h, int w, int pad, const void* 
                    int64_t* stats, void* stream);
 /* Device views into the workspace after sfc_conv_int8:
  *   vq   int8  [F][Tpad][Cpad]   quantized transformed activations
- *   pacc int32 [F][Tpad][OCpad]  per-frequency channel contractions; NULL when P is
+ *   pacc                         per-frequency channel contractions in the storage
+ *                                sfc_conv_schedule reports as p_layout; NULL when P is
  *                                chunked (opt-in SFC_PCHUNK_MB budget exceeded: each chunk
  *                                is consumed from L2 and never materialised whole)
  * geom[6] = {T, Tpad, Cpad, OCpad, th, tw}. */
@@ -184,8 +185,14 @@ int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_work
  *   *p_layout   storage of pacc in the workspace: 0 = int32 [F][Tpad][OCpad]; 1 = 24-bit
  *               [F][Tpad] rows of 3*OCpad bytes (byte planes b0 | b1 | b2, P = b0 + 2^8 b1 +
  *               2^16 b2 with b2 signed; exact as qmax^2 * Cin < 2^23; SFC_P24=0 keeps int32);
- *               3 = no P: Cin <= 4 layers contract with dp4a inside the output transform and
- *               the vq view is compact [F][T][4] (SFC_SMALLC=0 keeps the tensor-core GEMM). */
+ *               2 = the same 24-bit values unit-major for the tensor-core output transform
+ *               ([OCpad/32][3 planes][F][Tpad/4][128 B]: 32 channels x 4 tiles per 128-byte
+ *               row, 16-byte chunk c of row f at c ^ (f & 7); the default for the 3x3 variants
+ *               on grids of >= 2 units per SM, SFC_OUT_MMA=0 keeps layout 1); 3 = no P:
+ *               Cin <= 4 layers contract with dp4a inside the output transform and the vq
+ *               view is compact [F][T][4] (SFC_SMALLC=0 keeps the tensor-core GEMM).
+ *               sfc_conv_views returns the raw P storage in this layout (the Python
+ *               SfcLayer.views() decodes every layout to int32 [F][T][OC]). */
 int sfc_conv_schedule(sfc_layer_t layer, int n, int h, int w, int pad, int* recompute, int* p_layout);
 
 /* Exact int8 direct correlation (int32 accumulate), the report baseline
