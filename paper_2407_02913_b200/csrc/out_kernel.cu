@@ -367,6 +367,35 @@ __device__ __forceinline__ void emit_rows_any(int mask, const acc_t* __restrict_
     }
 }
 
+// int8-only stage C (the small-channel kernel's VGG-16 layer 0 output): thread t keeps the
+// column pair 2 (t % npair) and walks rows r = (t1, oc) = t / npair, + nt / npair, ...; two
+// values per 8-byte shared load and 2-byte store (even WO).
+template <int M>
+__device__ __forceinline__ void emit_rows_i8(const int* __restrict__ s_y, int ys, int nt, int noc, int hrows,
+                                             size_t base0, int plane, int WO, int ncol,
+                                             const double* __restrict__ scl, double rq, int8_t* __restrict__ out) {
+    const int npair = (ncol + 1) >> 1;
+    const unsigned nmag = c_magic32[npair];
+    const int r0 = npair == 1 ? int(threadIdx.x) : int(__umulhi(threadIdx.x, nmag));
+    const int c = 2 * (int(threadIdx.x) - r0 * npair);
+    const int rstep = npair == 1 ? nt : int(__umulhi(unsigned(nt), nmag));
+    if (r0 >= rstep) return;
+    const bool two = c + 1 < ncol, pair = two && (WO & 1) == 0;
+    for (int r = r0; r < M * kOcc; r += rstep) {
+        const int oc = r & (kOcc - 1), t1 = r >> 5;
+        if (oc >= noc || t1 >= hrows) continue;
+        const int2 v = *reinterpret_cast<const int2*>(s_y + r * ys + c);
+        const int qa = requant_i8(double(v.x) * scl[oc] * rq), qb = requant_i8(double(v.y) * scl[oc] * rq);
+        int8_t* d = out + base0 + unsigned(oc * plane + t1 * WO + c);
+        if (pair) {
+            *reinterpret_cast<uint16_t*>(d) = uint16_t((qa & 0xff) | ((qb & 0xff) << 8));
+        } else {
+            d[0] = int8_t(qa);
+            if (two) d[1] = int8_t(qb);
+        }
+    }
+}
+
 template <int V>
 struct PersSmem {
     static constexpr int TB = out_tb<V>();
@@ -588,6 +617,10 @@ __global__ void __launch_bounds__(32 * kSmallTB) k_output_smallc(const int32_t* 
         const int ncol = min(ntb * M, WO - col0);
         const int hrows = min(M, g.HO - ti * M);
         const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
+        if (mask == 16) {  // int8 only (configs 3-4): paired fp32 requant stores
+            emit_rows_i8<M>(s_y, YS, NT, noc, hrows, base0, plane, WO, ncol, s_scale, rq, o.i8);
+            continue;
+        }
         emit_rows_any<false, M>(mask, s_y, YS, NT, noc, hrows, base0, plane, WO, ncol, (WO & 1) == 0 && !o.i8, s_scale,
                                 s_scalef, rq, o);
     }
