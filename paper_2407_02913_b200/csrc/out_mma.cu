@@ -56,7 +56,7 @@ struct Om {
     static constexpr uint32_t STAGE = 3 * PLANE;
     static constexpr int STAGES = STAGE * 3 <= 150 * 1024 ? 3 : 2;  // bulk-copy pipeline depth
     static constexpr int ROW = kUnitTiles * M;         // staged columns per (oc, t1): 4 tiles x M
-    static constexpr int OCS = M * ROW + 1;            // staged words per output channel (odd stride)
+    static constexpr int OCS = M * ROW + 2;            // staged words per output channel, at most (see k_out_mma)
     static constexpr int TMEM_COLS = 6 * N <= 128 ? 128 : (6 * N <= 256 ? 256 : 512);
     static_assert(6 * N <= 512, "two buffers of three accumulators must fit TMEM");
     static constexpr size_t W_BYTES = size_t(KB) * N * 128;
@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(kOmThreads, 1)
         const int q = warp & 3, pp = (warp - 2) >> 2;    // lane quarter = tile of the unit, output part
         const int cnt = min(C::PART, C::MM - pp * C::PART);
         const double sa = qpp->sa, rq = o.requant;
+        // staged words per output channel: odd (conflict-free staging) for single columns, even
+        // for the 8-byte pair loads
+        constexpr int OCSK = (C::M % 2 == 0 && MK == 16) ? C::M * C::ROW + 2 : C::M * C::ROW + 1;
         for (int i = et; i < g.OC; i += 32 * kOmEpiWarps) {
             const double sc = (sa * sf[i]) / double(T::DEN * T::DEN);
             s_scale[i] = sc;
@@ -177,8 +180,13 @@ __global__ void __launch_bounds__(kOmThreads, 1)
         }
         const int WO = g.WO, HO = g.HO, plane = HO * WO;
         const int tiles_img = g.th * g.tw;
-        constexpr int NG = (32 * kOmEpiWarps) / C::ROW;  // channel groups of the store phase
-        const int x_col = et % C::ROW, x_grp = et / C::ROW, x_tt = x_col / C::M, x_t2 = x_col % C::M;
+        // column pairs (8-byte shared loads, 2-byte stores) for int8-only outputs of the even-M
+        // variants; single columns otherwise (measured: pairs help the int8 layers of configs
+        // 3-4, not the int32 outputs of config 5)
+        constexpr int PW = (C::M % 2 == 0 && MK == 16) ? 2 : 1;
+        constexpr int CPR = C::ROW / PW;                 // column items per staged row
+        constexpr int NG = (32 * kOmEpiWarps) / CPR;     // channel groups of the store phase
+        const int x_col = PW * (et % CPR), x_grp = et / CPR, x_tt = x_col / C::M, x_t2 = x_col % C::M;
         int rofs[C::M];  // row offsets t1 * WO
 #pragma unroll
         for (int t1 = 0; t1 < C::M; ++t1) rofs[t1] = t1 * WO;
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(kOmThreads, 1)
                 }
                 st[et] = ti;
             }
-            int* yr = sy + lane * C::OCS;
+            int* yr = sy + lane * OCSK;
 #pragma unroll
             for (int c = 0; c < C::NP; ++c)
                 if (c < cnt) {
@@ -228,64 +236,71 @@ __global__ void __launch_bounds__(kOmThreads, 1)
                     yr[t1 * C::ROW + q * C::M + t2] = int(y[c]);
                 }
             named_bar_epi();
-            // stores: thread et keeps column x = et % ROW of the unit's staged rows (tile x / M,
-            // column t2 = x % M of that tile) and walks output channels oc = et / ROW, + NG, ...,
-            // all M rows each (independent: predicated, not a loop exit); consecutive threads
-            // write consecutive columns of an output row
-            if (et < NG * C::ROW) {
+            // stores: thread et keeps a column pair (x, x + 1) = PW (et % (ROW / PW)) of the unit's
+            // staged rows (tile x / M, columns t2 (+1) of that tile; pairs for the even M of the
+            // 6x6 / 4x4 variants) and walks output channels oc = et / (ROW / PW), + NG, ..., all
+            // M rows each (predicated per row); consecutive threads write consecutive columns
+            if (et < NG * CPR) {
                 const TileInfo ti = st[x_tt];
                 const int noc = min(kUnitOc, g.OC - ob * kUnitOc);
-                if (x_t2 < ti.cols) {
+                const bool v0 = x_t2 < ti.cols, v1 = PW == 2 && x_t2 + 1 < ti.cols;
+                const bool pair = v1 && (WO % 2 == 0);  // even element offsets: 2 / 8-byte stores
+                if (v0) {
                     for (int oc = x_grp; oc < noc; oc += NG) {
                         const int ocg = ob * kUnitOc + oc;
                         const long long e0 = ti.base + x_t2 + (long long)oc * plane;
-                        const int* ys = sy + oc * C::OCS + x_col;
+                        const int* ys = sy + oc * OCSK + x_col;
                         double sc = 0.0;
                         float scf = 0.f;
                         if ((MK ? (MK & 24) : (o.f64 || o.i8)) != 0) sc = s_scale[ocg];
                         if ((MK ? (MK & 4) : (o.f32 != nullptr)) != 0) scf = s_scalef[ocg];
-                        int yv[C::M];
+                        int ya[C::M], yb[C::M];
 #pragma unroll
-                        for (int t1 = 0; t1 < C::M; ++t1) yv[t1] = ys[t1 * C::ROW];
-                        // conversions for every row, then one predicated store per row and output
-                        // (no per-row branch regions: the rows stay independent)
+                        for (int t1 = 0; t1 < C::M; ++t1) {
+                            if constexpr (PW == 2) {
+                                const int2 w = *reinterpret_cast<const int2*>(ys + t1 * C::ROW);
+                                ya[t1] = w.x, yb[t1] = w.y;
+                            } else {
+                                ya[t1] = ys[t1 * C::ROW], yb[t1] = 0;
+                            }
+                        }
 #pragma unroll
                         for (int t1 = 0; t1 < C::M; ++t1) {
                             const bool ok = t1 < ti.rows;
                             const long long e = e0 + rofs[t1];
-                            if ((MK ? (MK & 1) : (o.y32 != nullptr)) && ok) o.y32[e] = yv[t1];
-                            if ((MK ? (MK & 2) : (o.y64 != nullptr)) && ok) o.y64[e] = yv[t1];
+                            if ((MK ? (MK & 1) : (o.y32 != nullptr))) {
+                                if (ok && pair) *reinterpret_cast<int2*>(o.y32 + e) = make_int2(ya[t1], yb[t1]);
+                                else {
+                                    if (ok) o.y32[e] = ya[t1];
+                                    if (ok && v1) o.y32[e + 1] = yb[t1];
+                                }
+                            }
+                            if ((MK ? (MK & 2) : (o.y64 != nullptr))) {
+                                if (ok) o.y64[e] = ya[t1];
+                                if (ok && v1) o.y64[e + 1] = yb[t1];
+                            }
                             if ((MK ? (MK & 4) : (o.f32 != nullptr))) {
-                                const float v = __int2float_rn(yv[t1]) * scf;
-                                if (ok) o.f32[e] = v;
+                                const float fa = __int2float_rn(ya[t1]) * scf, fb = __int2float_rn(yb[t1]) * scf;
+                                if (ok && pair) *reinterpret_cast<float2*>(o.f32 + e) = make_float2(fa, fb);
+                                else {
+                                    if (ok) o.f32[e] = fa;
+                                    if (ok && v1) o.f32[e + 1] = fb;
+                                }
                             }
                             if ((MK ? (MK & 8) : (o.f64 != nullptr))) {
-                                const double v = double(yv[t1]) * sc;
-                                if (ok) o.f64[e] = v;
+                                if (ok) o.f64[e] = double(ya[t1]) * sc;
+                                if (ok && v1) o.f64[e + 1] = double(yb[t1]) * sc;
                             }
-                        }
-                        if ((MK ? (MK & 16) : (o.i8 != nullptr))) {
-                            // int8 requant clamp(rint(double(y) * sc * rq), 0, 127): t = float(y) * c32
-                            // (c32 = float(sc * rq)) is within 3 * 2^-24 |t| of the fp64 value (< 2.4e-5
-                            // wherever the clamp does not decide, |t| < 130), so rint(t) is exact unless t
-                            // lies within 1e-4 of a half-integer; such rows (~2e-4 of values) redo the fp64
-                            // formula -- once per warp, so the common path has no fp64 and no divergence.
-                            const float c32 = s_rq32[ocg];
-                            int qv[C::M];
-                            bool near = false;
-#pragma unroll
-                            for (int t1 = 0; t1 < C::M; ++t1) {
-                                const float t = __int2float_rn(yv[t1]) * c32;
-                                near |= fabsf(t - rintf(t)) > 0.4999f;
-                                qv[t1] = min(max(__float2int_rn(t), 0), 127);
+                            if ((MK ? (MK & 16) : (o.i8 != nullptr))) {
+                                const int qa = requant_i8(double(ya[t1]) * sc * rq);
+                                const int qb = requant_i8(double(yb[t1]) * sc * rq);
+                                int8_t* d = o.i8 + e;
+                                if (ok && pair) *reinterpret_cast<uint16_t*>(d) = uint16_t((qa & 0xff) | ((qb & 0xff) << 8));
+                                else {
+                                    if (ok) d[0] = int8_t(qa);
+                                    if (ok && v1) d[1] = int8_t(qb);
+                                }
                             }
-                            if (__any_sync(__activemask(), near)) {  // (each lane votes in its own group)
-#pragma unroll
-                                for (int t1 = 0; t1 < C::M; ++t1) qv[t1] = requant_i8(double(yv[t1]) * sc * rq);
-                            }
-#pragma unroll
-                            for (int t1 = 0; t1 < C::M; ++t1)
-                                if (t1 < ti.rows) o.i8[e0 + rofs[t1]] = int8_t(qv[t1]);
                         }
                     }
                 }
