@@ -86,8 +86,7 @@ __global__ void __launch_bounds__(kOmThreads, 1)
     int* s_y = reinterpret_cast<int*>(sW + C::W_BYTES);   // 2 x [32 oc][M rows][ROW] (row stride OCS per oc)
     double* s_scale = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(s_y) + 2 * C::Y_BYTES);
     float* s_scalef = reinterpret_cast<float*>(s_scale + kOmMaxOc);
-    float* s_rq32 = s_scalef + kOmMaxOc;
-    uint64_t* full = reinterpret_cast<uint64_t*>(s_rq32 + kOmMaxOc);
+    uint64_t* full = reinterpret_cast<uint64_t*>(s_scalef + kOmMaxOc);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
@@ -176,7 +175,6 @@ __global__ void __launch_bounds__(kOmThreads, 1)
             const double sc = (sa * sf[i]) / double(T::DEN * T::DEN);
             s_scale[i] = sc;
             s_scalef[i] = float(sc);
-            s_rq32[i] = float(sc * rq);
         }
         const int WO = g.WO, HO = g.HO, plane = HO * WO;
         const int tiles_img = g.th * g.tw;

@@ -750,3 +750,34 @@ def test_p24_and_output_kernels_agree(cuda, variant, monkeypatch):
         for name in ("rows", "p32", "one-block"):
             for k in ("y", "f32", "i8", "pacc", "vq"):
                 assert np.array_equal(res["default"][k], res[name][k]), (name, k)
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("outs", [("y32",), ("i8",), ("y32", "f32"), ("y64", "f64", "i8"), ("f32", "i8")],
+                         ids=lambda o: "+".join(o))
+def test_tensor_core_output_transform_every_output_set(cuda, variant, outs, monkeypatch):
+    """k_out_mma (unit-major P) against the CUDA-core output kernels (SFC_OUT_MMA=0) for every
+    output set it specialises or reads at run time, on shapes whose unit tiles cross image rows
+    (tw = 3, 5), leave partial output tiles (odd and even WO), and partial channel blocks
+    (OC = 70): every output bit for bit."""
+    rng = np.random.default_rng(21)
+    dev = torch.device("cuda", 0)
+    for (B, C, OC, H, W) in ((64, 48, 70, 17, 15), (80, 64, 96, 14, 20)):
+        x = torch.from_numpy(rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)).to(dev)
+        w = torch.from_numpy(rng.integers(-127, 128, size=(OC, C, 3, 3), dtype=np.int8)).to(dev)
+        layer = sc.SfcLayer(variant, w)
+        res = {}
+        for name, env in (("mma", {}), ("cuda-core", {"SFC_OUT_MMA": "0"})):
+            monkeypatch.delenv("SFC_OUT_MMA", raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            assert layer.schedule(B, H, W, 1)["p_layout"] == (2 if name == "mma" else 1)
+            ws = layer.workspace(B, H, W, 1)
+            kinds = {"y32": torch.int32, "y64": torch.int64, "f32": torch.float32, "f64": torch.float64,
+                     "i8": torch.int8}
+            t = {k: torch.full((B, OC, H, W), 77, dtype=kinds[k], device=dev) for k in outs}
+            layer.forward(x, ws, 1, y_int32=t.get("y32"), y_int64=t.get("y64"), out_f32=t.get("f32"),
+                          out_f64=t.get("f64"), out_i8=t.get("i8"), requant_scale=0.0021)
+            torch.cuda.synchronize()
+            res[name] = {k: v.cpu().numpy() for k, v in t.items()}
+        for k in outs:
+            assert np.array_equal(res["mma"][k], res["cuda-core"][k]), k
