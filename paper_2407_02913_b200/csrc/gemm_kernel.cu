@@ -67,6 +67,17 @@ __device__ __forceinline__ void unit_of(int u, int n_ob, int n_tb, int F, bool f
     ob = u % n_ob, f = (u / n_ob) % F, tb = u / (n_ob * F);
 }
 
+// Byte planes 0..2 of four int32 values (a, b, c, d): p_j = [a.b_j, b.b_j, c.b_j, d.b_j] -- a
+// 4x4 byte transpose restricted to three outputs, 7 byte permutes (instead of 9 per plane set).
+__device__ __forceinline__ void byte_planes3(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t& p0,
+                                             uint32_t& p1, uint32_t& p2) {
+    const uint32_t lo_ab = __byte_perm(a, b, 0x5140), lo_cd = __byte_perm(c, d, 0x5140);  // [x.b0 y.b0 x.b1 y.b1]
+    const uint32_t hi_ab = __byte_perm(a, b, 0x6262), hi_cd = __byte_perm(c, d, 0x6262);  // [x.b2 y.b2 ..]
+    p0 = __byte_perm(lo_ab, lo_cd, 0x5410);
+    p1 = __byte_perm(lo_ab, lo_cd, 0x7632);
+    p2 = __byte_perm(hi_ab, hi_cd, 0x5410);
+}
+
 // Quantize the four int16 values of two int16x2 words (lanes: low then high half) and pack
 // the four int8 results into one word: sign-extended halves, two byte permutes to pack.
 template <class Q>
@@ -158,7 +169,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 int ob, tb, f;
                 unit_of(u, n_ob, n_tb, F, g.p24 == 2, ob, tb, f);
                 for (int kc = 0; kc < nk; ++kc) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
                     if (QF) {
                         ptx::mbar_expect_tx(&full[stage], uint32_t(BN * BK));
                         if (QT) {
@@ -183,7 +194,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             int i = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
                 const int ab = i & 1;
-                ptx::mbar_wait(&tempty[ab], ((i >> 1) & 1) ^ 1);
+                ptx::mbar_wait_sleep(&tempty[ab], ((i >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + uint32_t(ab * BN);
                 for (int kc = 0; kc < nk; ++kc) {
@@ -231,17 +242,17 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                     // holds global chunk c at c ^ r -- conflict-free 16-byte stores)
                     const int sw = (f & 7) ^ (lane >> 2), c0 = 2 * (lane & 3);
                     uint8_t* rb = box + (lane >> 2) * 128;
+                    uint32_t wv[3][8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        byte_planes3(uint32_t(r[4 * j]), uint32_t(r[4 * j + 1]), uint32_t(r[4 * j + 2]),
+                                     uint32_t(r[4 * j + 3]), wv[0][j], wv[1][j], wv[2][j]);
 #pragma unroll
                     for (int pl = 0; pl < 3; ++pl) {
-                        const uint32_t sel = pl == 0 ? 0x0040u : (pl == 1 ? 0x0051u : 0x0062u);
-                        uint32_t wv[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            wv[j] = __byte_perm(__byte_perm(uint32_t(r[4 * j]), uint32_t(r[4 * j + 1]), sel),
-                                                __byte_perm(uint32_t(r[4 * j + 2]), uint32_t(r[4 * j + 3]), sel), 0x5410);
-                        *reinterpret_cast<uint4*>(rb + pl * 1024 + ((c0 ^ sw) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                        *reinterpret_cast<uint4*>(rb + pl * 1024 + ((c0 ^ sw) << 4)) =
+                            make_uint4(wv[pl][0], wv[pl][1], wv[pl][2], wv[pl][3]);
                         *reinterpret_cast<uint4*>(rb + pl * 1024 + (((c0 + 1) ^ sw) << 4)) =
-                            make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                            make_uint4(wv[pl][4], wv[pl][5], wv[pl][6], wv[pl][7]);
                     }
                 } else if (g.p24) {
                     // 24-bit P as three byte planes (b0, b1 unsigned, b2 signed: P = b0 + 2^8 b1 +
