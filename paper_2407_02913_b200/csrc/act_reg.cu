@@ -92,7 +92,7 @@ __host__ __device__ inline int row_seg_plane_words(int tc) {
 // its windows touch -- at row pitch rpw words inside the channel's plane; otherwise the CTA
 // covers the whole tile row and each channel's band is one contiguous segment.
 template <int V, int MODE, int PPW, bool RS>
-__global__ void __launch_bounds__(32 * kRowMaxWarps) k_act_row(const int8_t* __restrict__ x, ConvGeom g, int plw,
+__global__ void __launch_bounds__(32 * kRowMaxWarps, 2) k_act_row(const int8_t* __restrict__ x, ConvGeom g, int plw,
                                                               int rpw, int tc,
                                                               int* __restrict__ vmax, int16_t* __restrict__ vkeep,
                                                               const int* __restrict__ vmax_in, int bits,
