@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip the multi-GPU gather check")
+    ap.add_argument("--no-graph", action="store_true", help="time direct launches instead of a captured step graph")
     ap.add_argument("--measure-int8-peak", action="store_true")
     ap.add_argument("--stages", action="store_true", help="per-kernel stage timing (always on at N=1)")
     return ap.parse_args()
@@ -416,6 +417,24 @@ def run_b200(args, rank, world, local_rank):
         step()
     sync_all()
 
+    # One step's launches as a CUDA graph (single GPU): the same kernels with their programmatic
+    # dependent-launch edges, replayed without the per-launch host cost (ctypes, tensor-map
+    # encoding), which otherwise starves the GPU between the short kernels of small layers.
+    graph = None
+    if world == 1 and not args.no_graph:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):  # (captured on torch's side stream; replays on `stream`)
+                step()
+            sync_all()
+            for _ in range(2):
+                graph.replay()
+            sync_all()
+        except Exception as exc:  # capture unsupported here: time the launches directly
+            print(f"[bench] CUDA graph capture failed ({exc}); timing direct launches", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize()
+
     # ---- timed region (device time; L2 flushed between steps outside the events)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local_rank)
@@ -424,7 +443,10 @@ def run_b200(args, rank, world, local_rank):
         for s in range(args.steps):
             flush.zero_()
             ev[s][0].record(stream)
-            step()
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
             ev[s][1].record(stream)
         sync_all()
     ms_local = sum(a.elapsed_time(b) for a, b in ev) / args.steps
