@@ -140,6 +140,9 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) k_act_row(const int8_t* 
         const bool inside = (xb_u & ~uintptr_t(15)) >= xlo &&
                             ((xb_u + size_t(nchv - 1) * HW + size_t(nr - 1) * g.W + band + 15) & ~uintptr_t(15)) <= xhi;
         constexpr int kB = 8;
+        // sg / nr by a multiply-high (exact for sg < 2^16 and 2 <= nr <= 9 window rows; nr == 1
+        // separately): the staging loop's per-chunk integer division was a third of its instructions
+        const unsigned nr_mag = (RS && nr > 1) ? 0xffffffffu / unsigned(nr) + 1u : 0u;
         for (int jq = 0; jq < qq; ++jq) {
             const int q = (lane & (lpc - 1)) + jq * lpc;
             for (int sgb = sg0; sgb < nseg; sgb += kB * sgstep) {
@@ -148,7 +151,8 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) k_act_row(const int8_t* 
 #pragma unroll
                 for (int jj = 0; jj < kB; ++jj) {
                     const int sg = sgb + jj * sgstep;
-                    const int ch = RS ? sg / nr : sg, ir = RS ? sg - ch * nr : 0;
+                    const int ch = RS ? (nr == 1 ? sg : int(__umulhi(unsigned(sg), nr_mag))) : sg;
+                    const int ir = RS ? sg - ch * nr : 0;
                     const uintptr_t start = xb_u + size_t(ch) * HW + size_t(ir) * g.W;
                     const uintptr_t ad = (start & ~uintptr_t(15)) + 16 * uintptr_t(q);
                     d[jj] = (sg < nseg && ad < start + band) ? s_raw + plane(ch) + ir * rpw + 4 * q : nullptr;
