@@ -123,51 +123,54 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) k_act_row(const int8_t* 
     auto plane = [&](int ch) { return ((ch & 1) * PPW + (ch >> 1)) * plw + 4; };
 
     // ---- stage: per segment (a channel's band, or RS one (channel, row) piece), the 16-byte
-    // chunks covering it.  Lanes = chunks of one segment (lpc lanes, a power of two >= the
-    // chunk count, capped at 32), a warp pass covers cpw segments; kB passes' loads are in
-    // flight before any is stored.
+    // chunks covering it.  The CTA's threads walk the flat (segment, chunk) index, so
+    // consecutive lanes load consecutive chunks of a segment; kB chunks' loads are in flight
+    // before any is stored.  Destinations are word offsets into s_raw (shared stores, no
+    // generic pointers).
     {
         const int nchv = min(NCH, g.C - c0);
         const int nseg = RS ? nchv * nr : nchv;
         const int cq = (15 + band + 15) >> 4;  // chunk bound over every misalignment
-        int lg = 0;
-        while ((1 << lg) < cq && lg < 5) ++lg;
-        const int lpc = 1 << lg, cpw = 32 >> lg;
-        const int qq = (cq + lpc - 1) >> lg;      // chunk passes per segment
-        const int sg0 = wid * cpw + (lane >> lg), sgstep = nwarps * cpw;
+        const int total = nseg * cq;
         const uintptr_t xb_u = reinterpret_cast<uintptr_t>(xb) + cs;
         // the CTA's chunks all lie inside x unless it holds the first or last bytes of x
         const bool inside = (xb_u & ~uintptr_t(15)) >= xlo &&
                             ((xb_u + size_t(nchv - 1) * HW + size_t(nr - 1) * g.W + band + 15) & ~uintptr_t(15)) <= xhi;
         constexpr int kB = 8;
-        // sg / nr by a multiply-high (exact for sg < 2^16 and 2 <= nr <= 9 window rows; nr == 1
-        // separately): the staging loop's per-chunk integer division was a third of its instructions
+        // idx / cq and sg / nr by multiply-high: umulhi(i, floor(2^32 / d) + 1) == i / d while
+        // i * d < 2^32 (the magic's excess over 2^32 / d is below 1); d == 1 separately
+        const bool cq_fast = cq > 1 && (unsigned long long)total * unsigned(cq) < (1ull << 32);
+        const unsigned cq_mag = cq > 1 ? 0xffffffffu / unsigned(cq) + 1u : 0u;
         const unsigned nr_mag = (RS && nr > 1) ? 0xffffffffu / unsigned(nr) + 1u : 0u;
-        for (int jq = 0; jq < qq; ++jq) {
-            const int q = (lane & (lpc - 1)) + jq * lpc;
-            for (int sgb = sg0; sgb < nseg; sgb += kB * sgstep) {
-                uint4 v[kB];
-                uint32_t* d[kB];
+        const int nt = blockDim.x;
+        for (int i0 = threadIdx.x; i0 < total; i0 += kB * nt) {
+            uint4 v[kB];
+            int dst[kB];
 #pragma unroll
-                for (int jj = 0; jj < kB; ++jj) {
-                    const int sg = sgb + jj * sgstep;
-                    const int ch = RS ? (nr == 1 ? sg : int(__umulhi(unsigned(sg), nr_mag))) : sg;
-                    const int ir = RS ? sg - ch * nr : 0;
-                    const uintptr_t start = xb_u + size_t(ch) * HW + size_t(ir) * g.W;
-                    const uintptr_t ad = (start & ~uintptr_t(15)) + 16 * uintptr_t(q);
-                    d[jj] = (sg < nseg && ad < start + band) ? s_raw + plane(ch) + ir * rpw + 4 * q : nullptr;
-                    v[jj] = make_uint4(0, 0, 0, 0);
-                    if (!d[jj]) continue;
-                    if (inside || (ad >= xlo && ad + 16 <= xhi)) {
-                        v[jj] = __ldg(reinterpret_cast<const uint4*>(ad));
-                    } else {
-                        v[jj] = chunk_clipped(ad, xlo, xhi);
-                    }
+            for (int jj = 0; jj < kB; ++jj) {
+                const int idx = i0 + jj * nt;
+                const int sg = cq == 1 ? idx : (cq_fast ? int(__umulhi(unsigned(idx), cq_mag)) : idx / cq);
+                const int q = idx - sg * cq;
+                const int ch = RS ? (nr == 1 ? sg : int(__umulhi(unsigned(sg), nr_mag))) : sg;
+                const int ir = RS ? sg - ch * nr : 0;
+                const uintptr_t start = xb_u + size_t(ch) * HW + size_t(ir) * g.W;
+                const int mis = int(start & 15);
+                const uintptr_t ad = start - mis + 16 * q;
+                dst[jj] = (idx < total && 16 * q < mis + band) ? plane(ch) + ir * rpw + 4 * q : -1;
+                v[jj] = make_uint4(0, 0, 0, 0);
+                if (dst[jj] < 0) continue;
+                if (inside || (ad >= xlo && ad + 16 <= xhi)) {
+                    v[jj] = __ldg(reinterpret_cast<const uint4*>(ad));
+                } else {
+                    v[jj] = chunk_clipped(ad, xlo, xhi);
                 }
-#pragma unroll
-                for (int jj = 0; jj < kB; ++jj)
-                    if (d[jj]) d[jj][0] = v[jj].x, d[jj][1] = v[jj].y, d[jj][2] = v[jj].z, d[jj][3] = v[jj].w;
             }
+#pragma unroll
+            for (int jj = 0; jj < kB; ++jj)
+                if (dst[jj] >= 0) {
+                    uint32_t* d = s_raw + dst[jj];
+                    d[0] = v[jj].x, d[1] = v[jj].y, d[2] = v[jj].z, d[3] = v[jj].w;
+                }
         }
     }
     __syncthreads();

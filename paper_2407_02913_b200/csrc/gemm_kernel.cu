@@ -109,7 +109,7 @@ template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2, int n_tb, int n_ob,
-           int F, int nk, ConvGeom g, QFuse qf, uint8_t* __restrict__ pu) {
+           int F, int nk, ConvGeom g, QFuse qf) {
     static_assert(!QT || QF, "the TMA-staged V feeds the converters");
     constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
@@ -497,7 +497,7 @@ namespace {
 
 template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
-                        const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl, uint8_t* pu) {
+                        const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl) {
     const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + (QT ? size_t(STAGES) * kRowsPerTile * BK * 2 : 0) +
                         size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256;
     auto kern = k_gemm<BN, BK, STAGES, QF, QT>;
@@ -531,15 +531,15 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
         const char* e = std::getenv("SFC_GEMM_FMAJOR");
         if (!(e && e[0] == '1')) gk.p24 = 3;  // (3: unit-major P, tile-block-major order)
     }
-    return cudaLaunchKernelEx(&cfg, kern, a, b, p, p2, n_tb, n_ob, F, g.Cpad / BK, gk, qf, pu);
+    return cudaLaunchKernelEx(&cfg, kern, a, b, p, p2, n_tb, n_ob, F, g.Cpad / BK, gk, qf);
 }
 
 template <int BK, int STAGES, bool QF>
 cudaError_t gemm_by_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
-                       const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl, uint8_t* pu) {
-    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, pu);
-    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, pu);
-    return gemm_launch<256, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, pu);
+                       const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl) {
+    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
+    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
+    return gemm_launch<256, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
 }
 
 template <bool QF>
@@ -554,12 +554,11 @@ cudaError_t gemm_dispatch(const int8_t* vqA, const int8_t* uqB, int32_t* P, cons
         !make_p_maps(&tp, &tp2, P, g, F, g.Tpad))
         return cudaErrorInvalidValue;
     const int nk = g.Cpad / g.BK;
-    uint8_t* pu = reinterpret_cast<uint8_t*>(P);
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, pu)
-                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, pu);
-    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, pu)
-                   : gemm_by_bn<64, 4, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, pu);
+        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl)
+                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl);
+    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl)
+                   : gemm_by_bn<64, 4, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl);
 }
 }  // namespace
 
@@ -585,10 +584,10 @@ cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, c
     const int nk = g.Cpad / g.BK;
     const QFuse none{};
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, nullptr)
-                       : gemm_by_bn<128, 3, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, nullptr);
-    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, nullptr)
-                   : gemm_by_bn<64, 4, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, nullptr);
+        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl)
+                       : gemm_by_bn<128, 3, false>(ta, tb, tp, tp2, gc, F, none, st, pdl);
+    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl)
+                   : gemm_by_bn<64, 4, false>(ta, tb, tp, tp2, gc, F, none, st, pdl);
 }
 
 cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
@@ -617,15 +616,14 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
     // stages: A + B + V per stage plus the 64 KB of epilogue boxes within 227 KB -- two at
     // BK = 128, four at BK = 64 with BN <= 128 (the single-K-chunk
     // 64-channel layers: more units' V tiles in flight to hide the load latency)
-    uint8_t* pu = reinterpret_cast<uint8_t*>(P);
     if (g.BK == 128) {
-        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
-        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
-        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
+        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
     }
-    if (g.BN == 64) return gemm_launch<64, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
-    if (g.BN == 128) return gemm_launch<128, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
-    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, pu);
+    if (g.BN == 64) return gemm_launch<64, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+    if (g.BN == 128) return gemm_launch<128, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
 }
 
 SFC_TL_UNIT_READER(tl_read_gemm)
