@@ -8,11 +8,13 @@
 // load (ld.global.nc.v4 of the 16-byte aligned chunks covering the band), into one shared
 // plane per channel (odd word stride; even channels first so lanes stepping channel pairs
 // hit distinct banks).  One thread then owns one tile and one channel pair (c, c+1) and
-// builds its window in the two-lane SWAR form P = x_c + 2^16 x_{c+1} straight from the raw
-// planes (three 32-bit shared loads + two funnel shifts per window row and channel, a byte
-// mask for the zero padding of quant.cpp:66-75, two byte permutes and an add per sample
-// pair).  The transforms are integer-linear and every intermediate stays in (-2^15, 2^15)
-// (|V| <= 4608), so one 32-bit add serves both channels.  The tile stays in registers: row
+// builds its window in the two-lane SWAR form P = x'_c + 2^16 x'_{c+1} of the biased samples
+// x' = x + 128 straight from the raw planes (three 32-bit shared loads + two funnel shifts per
+// window row and channel, one LOP3 for the zero padding of quant.cpp:66-75 and the bias, one
+// byte permute and a mask per sample pair).  The transforms are integer-linear and every
+// intermediate stays in (-2^15, 2^15) (|V'| <= 9216), so one 32-bit add serves both channels;
+// the bias adds 128 * rowsum_k * rowsum_l per lane to frequency (k, l) (the DC frequency only),
+// removed together with the max/min lane bias in the horizontal pass.  The tile stays in registers: row
 // transforms into n x K values, column transforms into V, each value consumed where formed:
 //   MODE 0  max|V| only (unsigned 16x2 max/min of the biased words)
 //   MODE 2  max|V| and the kept V (int16x2 words, V[f][t][c])
@@ -34,23 +36,6 @@ namespace sfcb200 {
 namespace {
 
 constexpr int kRowMaxWarps = 10;  // CTA size bound: 320 threads
-
-// Sign-extended byte q of w, and the same byte sign-extended into the upper half-word.
-// (prmt default mode: selector bit 3 replicates the sign of the selected byte)
-template <uint32_t sel>
-__device__ __forceinline__ int prmt0(uint32_t w) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(d) : "r"(w), "n"(sel));
-    return int(d);
-}
-template <int q>
-__device__ __forceinline__ int sx_lo(uint32_t w) {
-    return prmt0<q | ((q | 8) << 4) | ((q | 8) << 8) | ((q | 8) << 12)>(w);
-}
-template <int q>
-__device__ __forceinline__ int sx_hi(uint32_t w) {
-    return prmt0<4 | (4 << 4) | (q << 8) | ((q | 8) << 12)>(w);
-}
 
 // The reference quantizer with clamping (the rare case without a verified multiply-shift):
 // out of line, so the unrolled column loop stays small.
@@ -103,6 +88,11 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) k_act_row(const int8_t* 
     using T = Tab<V>;
     constexpr int n = T::n, K = T::K, M = T::M, TPW = 32 / PPW, NCH = 2 * PPW;
     constexpr int kTl = MODE == 1 ? kTlQuant : kTlAbsmax;
+    // The window is transformed from the biased samples x + 128, so the transform of frequency
+    // (k, l) carries 128 * rowsum_k * rowsum_l extra per lane (rowsum = the response of BT row k
+    // to a constant; only the DC rows have one), removed in the horizontal pass.
+    constexpr uint32_t kBias8 = 0x80808080u;
+    auto in_corr = [](int k, int l) { return 128 * bt_rowsum<V>(k) * bt_rowsum<V>(l) * 0x10001; };
     extern __shared__ __align__(16) uint32_t s_raw[];
     tl_mark(kTl, 0);
     if (MODE != 1) griddep_launch_dependents();
@@ -119,7 +109,7 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) k_act_row(const int8_t* 
     const int cs = RS ? max(tj0 * M - g.pad, 0) : 0;
     const int ce = RS ? min((min(tj0 + tc, g.tw) - 1) * M - g.pad + n, g.W) : g.W;
     const int band = RS ? ce - cs : nr * g.W;  // bytes per segment
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     auto plane = [&](int ch) { return ((ch & 1) * PPW + (ch >> 1)) * plw + 4; };
 
     // ---- stage: per segment (a channel's band, or RS one (channel, row) piece), the 16-byte
@@ -213,31 +203,34 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) k_act_row(const int8_t* 
             const int ir = ih0 + r - r_lo;  // row within the band
             uint32_t we[NW4], wo[NW4];
             if (ir >= 0 && ir < nr) {  // CTA-uniform
+                // biased bytes x + 128 (x ^ 0x80), padding bytes 0x80 (x = 0): one LOP3
                 auto row = [&](const uint32_t* pl, int off, uint32_t (&o)[NW4]) {
                     const int wi = off >> 2, sh = (off & 3) * 8;
                     uint32_t src[NW4 + 1];
 #pragma unroll
                     for (int j = 0; j <= NW4; ++j) src[j] = pl[wi + j];
 #pragma unroll
-                    for (int j = 0; j < NW4; ++j) o[j] = __funnelshift_r(src[j], src[j + 1], sh) & mk[j];
+                    for (int j = 0; j < NW4; ++j) o[j] = (__funnelshift_r(src[j], src[j + 1], sh) & mk[j]) ^ kBias8;
                 };
                 row(pe, roff(ae, me, ir), we);
                 row(po, roff(ao, mo, ir), wo);
                 if (!ok1) {
 #pragma unroll
-                    for (int j = 0; j < NW4; ++j) wo[j] = 0;
+                    for (int j = 0; j < NW4; ++j) wo[j] = kBias8;
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < NW4; ++j) we[j] = wo[j] = 0;
+                for (int j = 0; j < NW4; ++j) we[j] = wo[j] = kBias8;
             }
+            // the biased samples are non-negative, so the SWAR word is the two bytes zero-
+            // extended into the half-words: one byte permute and one mask per sample pair
 #pragma unroll
             for (int s = 0; s < n; ++s) {
                 switch (s & 3) {
-                    case 0: xw[r][s] = sx_lo<0>(we[s >> 2]) + sx_hi<0>(wo[s >> 2]); break;
-                    case 1: xw[r][s] = sx_lo<1>(we[s >> 2]) + sx_hi<1>(wo[s >> 2]); break;
-                    case 2: xw[r][s] = sx_lo<2>(we[s >> 2]) + sx_hi<2>(wo[s >> 2]); break;
-                    default: xw[r][s] = sx_lo<3>(we[s >> 2]) + sx_hi<3>(wo[s >> 2]); break;
+                    case 0: xw[r][s] = int(__byte_perm(we[s >> 2], wo[s >> 2], 0x4400) & 0x00ff00ffu); break;
+                    case 1: xw[r][s] = int(__byte_perm(we[s >> 2], wo[s >> 2], 0x5511) & 0x00ff00ffu); break;
+                    case 2: xw[r][s] = int(__byte_perm(we[s >> 2], wo[s >> 2], 0x6622) & 0x00ff00ffu); break;
+                    default: xw[r][s] = int(__byte_perm(we[s >> 2], wo[s >> 2], 0x7733) & 0x00ff00ffu); break;
                 }
             }
         }
@@ -267,8 +260,10 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) k_act_row(const int8_t* 
         auto rows = [&](auto qlo, auto qhi) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                int v[K];
-                fwd1d<V>(y[k], v);
+                int v[K], cb[K];
+#pragma unroll
+                for (int l = 0; l < K; ++l) cb[l] = -in_corr(k, l);
+                fwd1d_bias<V>(y[k], v, cb);
 #pragma unroll
                 for (int l = 0; l < K; ++l) {
                     const int lo = int(int16_t(v[l]));
@@ -306,12 +301,14 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) k_act_row(const int8_t* 
             int* vk = MODE == 2 ? reinterpret_cast<int*>(vkeep + size_t(t) * g.Cpad + c) : nullptr;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                int v[K];
-                fwd1d<V>(y[k], v);
+                int v[K], cb[K];
+#pragma unroll
+                for (int l = 0; l < K; ++l) cb[l] = int(0x80008000u) - in_corr(k, l);
+                fwd1d_bias<V>(y[k], v, cb);
                 uint32_t u[K];
 #pragma unroll
                 for (int l = 0; l < K; ++l) {
-                    u[l] = uint32_t(v[l]) + 0x80008000u;  // lane j -> V_j + 2^15 (mod 2^16)
+                    u[l] = uint32_t(v[l]);  // lane j -> V_j + 2^15 (mod 2^16)
                     if constexpr (MODE == 2) {
                         *vk = int(u[l] ^ 0x80008000u);
                         vk += fstride;  // f = k * K + l

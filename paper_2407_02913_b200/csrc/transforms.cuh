@@ -100,6 +100,51 @@ __host__ __device__ __forceinline__ void fwd1d(const T (&x)[Tab<V>::n], T (&y)[T
     }
 }
 
+// Row sum of BT row k: the response of channel k to a constant input.
+template <int V>
+__host__ __device__ constexpr int bt_rowsum(int k) {
+    int r = 0;
+    for (int s = 0; s < Tab<V>::n; ++s) r += Tab<V>::bt(k, s);
+    return r;
+}
+
+// fwd1d plus a constant per channel, y[k] = sum_s BT[k][s] x[s] + C[k], in the same number of
+// additions as fwd1d where the constants fold into three-input adds (the register transform's
+// horizontal pass: the +2^15 lane bias of the max/min and the input-bias correction).
+template <int V, class T>
+__host__ __device__ __forceinline__ void fwd1d_bias(const T (&x)[Tab<V>::n], T (&y)[Tab<V>::K], const T (&C)[Tab<V>::K]) {
+    if constexpr (V == 1 || V == 2) {
+        const T a = x[1] + x[4], b = x[2] + x[5], c = x[3] + x[6];
+        const T d = x[1] - x[4], e = x[2] - x[5], f = x[3] - x[6];
+        y[0] = (a + b) + (c + C[0]);
+        y[1] = d + e + C[1];
+        y[2] = C[2] - e - f;
+        y[3] = y[1] + y[2] + (C[3] - C[1] - C[2]);
+        y[4] = a - c + C[4];
+        y[5] = c - b + C[5];
+        y[6] = y[4] + y[5] + (C[6] - C[4] - C[5]);
+        y[7] = (d + f + C[7]) - e;
+        y[8] = x[0] - x[6] + C[8];
+        y[9] = x[7] - x[1] + C[9];
+        if constexpr (V == 2) {
+            y[10] = x[7] - x[1] + C[10];
+            y[11] = x[8] - x[2] + C[11];
+        }
+    } else if constexpr (V == 0) {
+        const T s0 = x[1] + x[3], s1 = x[2] + x[4], a1 = x[1] - x[3], b1 = x[4] - x[2];
+        y[0] = s0 + s1 + C[0];
+        y[1] = s1 - s0 + C[1];
+        y[2] = a1 + b1 + C[2];
+        y[3] = b1 + C[3];
+        y[4] = a1 + C[4];
+        y[5] = x[0] - x[4] + C[5];
+        y[6] = x[5] - x[1] + C[6];
+    } else {
+        fwd1d_generic<V>(x, y);
+        for (int k = 0; k < Tab<V>::K; ++k) y[k] += C[k];
+    }
+}
+
 template <int V, class T>
 __host__ __device__ __forceinline__ void inv1d(const T (&p)[Tab<V>::K], T (&y)[Tab<V>::M]) {
     // Output t of the tile sits at cyclic position (t - offset) mod N with offset = 1,
