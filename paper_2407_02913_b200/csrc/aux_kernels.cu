@@ -231,6 +231,7 @@ void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, in
     g.row0 = 0;
     g.nrows = B * g.th;
     g.p24 = 0;
+    g.p2s = 0;
 }
 
 PChunk p_chunk(const ConvGeom& g, int F) {

@@ -187,6 +187,14 @@ int p_layout_of(const sfc_layer* L, const ConvGeom& g) {
     return units < 2L * device_sm_count() ? 1 : 2;
 }
 
+// Unit-major P stores plane 2 sparsely (sfc_kernels.hpp p2_flags_offset).  SFC_P2_DENSE=1
+// keeps every row of plane 2 (A/B knob, read per call; the Python views() reads it too).
+bool p2_sparse_wanted(const ConvGeom& g) {
+    if (g.p24 != 2) return false;
+    const char* e = std::getenv("SFC_P2_DENSE");
+    return !(e && e[0] == '1');
+}
+
 bool p24_wanted(const sfc_layer* L, const ConvGeom& g) {
     const char* e = std::getenv("SFC_P24");
     if (e && e[0] == '0') return false;
@@ -271,6 +279,7 @@ void run_conv(const sfc_layer* L, const int8_t* d_x, int n, int h, int w, int pa
     if (!d_vmax || !ws || !o) throw std::invalid_argument("null argument");
     ConvGeom g = geom_of(L, n, h, w, pad);
     g.p24 = p_layout_of(L, g);
+    g.p2s = p2_sparse_wanted(g) ? 1 : 0;
     if (ws_bytes < workspace_bytes(g, L->F)) throw std::invalid_argument("workspace too small");
     const bool need64 = needs_y64(L, o);
     WsView v = carve(ws, g, L->F);

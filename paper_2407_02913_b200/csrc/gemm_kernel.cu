@@ -22,6 +22,13 @@
 #include "devcache.hpp"
 #include "sfc_kernels.hpp"
 
+#ifdef GM_TRACE  // experiment build: clock stamps of CTA 0's first units per role, printed at exit
+#include <cstdio>
+#define GM_STAMP(role, unit, k) do { if (blockIdx.x == 0 && (unit) < 32) s_trace[((role) * 32 + (unit)) * 4 + (k)] = clock64(); } while (0)
+#else
+#define GM_STAMP(role, unit, k) do { } while (0)
+#endif
+
 namespace sfcb200 {
 
 namespace {
@@ -39,6 +46,11 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void*
             reinterpret_cast<uint64_t>(map)),
         "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
+}
+__device__ __forceinline__ void bulk_store_128(void* dst, const void* src) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;" ::"l"(reinterpret_cast<uint64_t>(dst)),
+                 "r"(ptx::smem_u32(src))
+                 : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
@@ -109,7 +121,7 @@ template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2, int n_tb, int n_ob,
-           int F, int nk, ConvGeom g, QFuse qf) {
+           int F, int nk, ConvGeom g, QFuse qf, uint8_t* __restrict__ p_raw) {
     static_assert(!QT || QF, "the TMA-staged V feeds the converters");
     constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
@@ -127,6 +139,10 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     uint64_t* tempty = tfull + 2;
     uint64_t* vfull = tempty + 2;                     // QT: V stage landed
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(vfull + (QT ? STAGES : 0));
+#ifdef GM_TRACE
+    long long* s_trace = reinterpret_cast<long long*>(tmem_holder + 2);
+    int tu = 0;
+#endif
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int units = F * n_tb * n_ob;
@@ -170,6 +186,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 unit_of(u, n_ob, n_tb, F, g.p24 == 2, ob, tb, f);
                 for (int kc = 0; kc < nk; ++kc) {
                     ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
+                    GM_STAMP(0, tu, 0);
                     if (QF) {
                         ptx::mbar_expect_tx(&full[stage], uint32_t(BN * BK));
                         if (QT) {
@@ -182,8 +199,12 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                         ptx::tma_load_3d(sA + stage * kRowsPerTile * BK, &tmA, &full[stage], kc * BK, tb * kRowsPerTile, f);
                     }
                     ptx::tma_load_3d(sB + stage * BN * BK, &tmB, &full[stage], kc * BK, ob * BN, f);
+                    GM_STAMP(0, tu, 1);
                     if (++stage == STAGES) stage = 0, phase ^= 1;
                 }
+#ifdef GM_TRACE
+                ++tu;
+#endif
             }
         }
     } else if (warp == 1) {
@@ -195,10 +216,12 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
                 const int ab = i & 1;
                 ptx::mbar_wait_sleep(&tempty[ab], ((i >> 1) & 1) ^ 1);
+                GM_STAMP(1, i, 0);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + uint32_t(ab * BN);
                 for (int kc = 0; kc < nk; ++kc) {
                     ptx::mbar_wait(&full[stage], phase);
+                    GM_STAMP(1, i, 1);
                     ptx::tc_fence_after();
                     const uint32_t a0 = ptx::smem_u32(sA + stage * kRowsPerTile * BK);
                     const uint32_t b0 = ptx::smem_u32(sB + stage * BN * BK);
@@ -210,6 +233,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                     if (++stage == STAGES) stage = 0, phase ^= 1;
                 }
                 ptx::mma_commit(&tfull[ab]);
+                GM_STAMP(1, i, 2);
             }
         }
     } else if (warp < 2 + kEpiWarps) {
@@ -223,15 +247,19 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             unit_of(u, n_ob, n_tb, F, g.p24 == 2, ob, tb, f);
             const int ab = i & 1;
             ptx::mbar_wait_sleep(&tfull[ab], (i >> 1) & 1);
+            if (warp == 2 && lane == 0) GM_STAMP(2, i, 0);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = half * kHalf; c < (half + 1) * kHalf; c += 32) {
                 int32_t r[32];
                 ptx::tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(ab * BN + c), r);
                 ptx::tmem_wait_ld();
+                if (warp == 2 && lane == 0) GM_STAMP(2, i, 1);
                 if (lane == 0) bulk_wait_read<kEpiBufs - 1>();  // this buffer's previous store has read smem
                 __syncwarp();
+                if (warp == 2 && lane == 0) GM_STAMP(2, i, 2);
                 uint8_t* box = myE + buf * kEpiBoxBytes;
+                uint32_t p2rows = 0;
                 if (g.p24 >= 2) {
                     // unit-major 24-bit P (sfc_kernels.hpp pu_offset): this thread's tile t and 32
                     // channels are one 32-byte piece of row f of each byte plane of unit
@@ -243,15 +271,31 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                     const int sw = (f & 7) ^ (lane >> 2), c0 = 2 * (lane & 3);
                     uint8_t* rb = box + (lane >> 2) * 128;
                     uint32_t wv[3][8];
+                    if (g.p2s) {  // sparse plane 2: P' = P + 2^15 keeps 16-bit values in planes 0 and 1
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) r[j] += 32768;
+                    }
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
                         byte_planes3(uint32_t(r[4 * j]), uint32_t(r[4 * j + 1]), uint32_t(r[4 * j + 2]),
                                      uint32_t(r[4 * j + 3]), wv[0][j], wv[1][j], wv[2][j]);
+                    // rows of plane 2 to store: all (dense), or the units (4 lanes each) holding a
+                    // value outside 16 bits
+                    p2rows = 0xffffffffu;
+                    if (g.p2s)
+                        p2rows = __ballot_sync(0xffffffffu, (wv[2][0] | wv[2][1] | wv[2][2] | wv[2][3] | wv[2][4] |
+                                                             wv[2][5] | wv[2][6] | wv[2][7]) != 0);
+                    p2rows = (p2rows | (p2rows >> 1) | (p2rows >> 2) | (p2rows >> 3)) & 0x11111111u;  // bit 4u: unit u
+                    // all eight units: the swizzled box and one TMA store; some: rows in their
+                    // global chunk order (c ^ (f & 7)) for one 128-byte bulk store each
+                    const int sw2 = p2rows == 0x11111111u ? sw : (f & 7);
 #pragma unroll
                     for (int pl = 0; pl < 3; ++pl) {
-                        *reinterpret_cast<uint4*>(rb + pl * 1024 + ((c0 ^ sw) << 4)) =
+                        if (pl == 2 && p2rows == 0) break;
+                        const int s2 = pl == 2 ? sw2 : sw;
+                        *reinterpret_cast<uint4*>(rb + pl * 1024 + ((c0 ^ s2) << 4)) =
                             make_uint4(wv[pl][0], wv[pl][1], wv[pl][2], wv[pl][3]);
-                        *reinterpret_cast<uint4*>(rb + pl * 1024 + (((c0 + 1) ^ sw) << 4)) =
+                        *reinterpret_cast<uint4*>(rb + pl * 1024 + (((c0 + 1) ^ s2) << 4)) =
                             make_uint4(wv[pl][4], wv[pl][5], wv[pl][6], wv[pl][7]);
                     }
                 } else if (g.p24) {
@@ -288,7 +332,22 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                     if (g.p24 >= 2) {  // (row, f, plane, tile group, oc block)
                         const int t0u = (tb * kRowsPerTile + q * 32) / kUnitTiles, o0u = (ob * BN + c) / kUnitOc;
 #pragma unroll
-                        for (int pl = 0; pl < 3; ++pl) tma_store_5d(&tmP2, box + pl * 1024, 0, t0u, f, pl, o0u);
+                        for (int pl = 0; pl < 2; ++pl) tma_store_5d(&tmP2, box + pl * 1024, 0, t0u, f, pl, o0u);
+                        if (p2rows == 0x11111111u) {
+                            tma_store_5d(&tmP2, box + 2 * 1024, 0, t0u, f, 2, o0u);
+                        } else if (p2rows) {
+                            for (int uu = 0; uu < 8; ++uu)
+                                if ((p2rows >> (4 * uu)) & 1u)
+                                    bulk_store_128(p_raw + pu_offset(o0u, t0u + uu, 2, f, g.Tpad / kUnitTiles, F),
+                                                   box + 2 * 1024 + uu * 128);
+                        }
+                        if (g.p2s) {  // one flag byte per (unit, f): [oc block][tile group / 8][F][8]
+                            unsigned long long fl = 0;
+#pragma unroll
+                            for (int uu = 0; uu < 8; ++uu) fl |= (unsigned long long)((p2rows >> (4 * uu)) & 1u) << (8 * uu);
+                            *reinterpret_cast<unsigned long long*>(p_raw + p2_flags_offset(F, g.Tpad, g.OCpad) +
+                                                                   p2_flag_index(o0u, t0u, f, g.Tpad, F)) = fl;
+                        }
                     } else if (g.p24) {  // byte coordinates: plane j of a P row starts at j * OCpad
 #pragma unroll
                         for (int pl = 0; pl < 3; ++pl) tma_store_3d(&tmP, box + pl * 1024, pl * g.OCpad + o0, t0, f);
@@ -302,6 +361,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[ab]);
+            if (warp == 2 && lane == 0) GM_STAMP(2, i, 3);
         }
         if (lane == 0) bulk_wait_all();
     } else if (QF && QT) {
@@ -318,6 +378,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             uint32_t phase = 0;
             for (int s2 = 0; s2 < npairs; ++s2) {
                 ptx::mbar_wait_sleep(&vfull[stage], phase);  // (the producer waited for the stage to be free)
+                if (ct == 0) GM_STAMP(3, s2, 0);
                 const uint8_t* v_st = sV + stage * kVStageBytes;
                 uint8_t* a_st = sA + stage * kRowsPerTile * BK;
 #pragma unroll
@@ -337,6 +398,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 fence_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&full[stage]);
+                if (ct == 0) GM_STAMP(3, s2, 1);
                 if (++stage == STAGES) stage = 0, phase ^= 1;
             }
         };
@@ -427,6 +489,18 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         }
     }
     __syncthreads();
+#ifdef GM_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0 && units > 40 * int(gridDim.x)) {
+        const long long t0 = s_trace[(0 * 32 + 8) * 4 + 0];
+        for (int u2 = 8; u2 < 28; ++u2)
+            printf("g%2d prod: free %6lld issued %6lld | conv: vfull %6lld done %6lld | mma: tempty %6lld full %6lld committed %6lld | epi: tfull %6lld ld %6lld bufready %6lld released %6lld\n",
+                   u2, s_trace[(0 * 32 + u2) * 4 + 0] - t0, s_trace[(0 * 32 + u2) * 4 + 1] - t0,
+                   s_trace[(3 * 32 + u2) * 4 + 0] - t0, s_trace[(3 * 32 + u2) * 4 + 1] - t0,
+                   s_trace[(1 * 32 + u2) * 4 + 0] - t0, s_trace[(1 * 32 + u2) * 4 + 1] - t0, s_trace[(1 * 32 + u2) * 4 + 2] - t0,
+                   s_trace[(2 * 32 + u2) * 4 + 0] - t0, s_trace[(2 * 32 + u2) * 4 + 1] - t0, s_trace[(2 * 32 + u2) * 4 + 2] - t0,
+                   s_trace[(2 * 32 + u2) * 4 + 3] - t0);
+    }
+#endif
     tl_mark(kTlGemm, 2);
     if (warp == 1) {
         ptx::tc_fence_after();
@@ -497,9 +571,13 @@ namespace {
 
 template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
-                        const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl) {
+                        const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl, void* p_raw) {
     const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + (QT ? size_t(STAGES) * kRowsPerTile * BK * 2 : 0) +
-                        size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256;
+                        size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256
+#ifdef GM_TRACE
+                        + 4200
+#endif
+        ;
     auto kern = k_gemm<BN, BK, STAGES, QF, QT>;
     static SmemOptIn opt_in;
     if (cudaError_t e = opt_in.ensure(kern, smem); e != cudaSuccess) return e;
@@ -531,15 +609,15 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
         const char* e = std::getenv("SFC_GEMM_FMAJOR");
         if (!(e && e[0] == '1')) gk.p24 = 3;  // (3: unit-major P, tile-block-major order)
     }
-    return cudaLaunchKernelEx(&cfg, kern, a, b, p, p2, n_tb, n_ob, F, g.Cpad / BK, gk, qf);
+    return cudaLaunchKernelEx(&cfg, kern, a, b, p, p2, n_tb, n_ob, F, g.Cpad / BK, gk, qf, static_cast<uint8_t*>(p_raw));
 }
 
 template <int BK, int STAGES, bool QF>
 cudaError_t gemm_by_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
-                       const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl) {
-    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
-    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
-    return gemm_launch<256, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl);
+                       const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl, void* p_raw) {
+    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, p_raw);
+    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, p_raw);
+    return gemm_launch<256, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, p_raw);
 }
 
 template <bool QF>
@@ -555,10 +633,10 @@ cudaError_t gemm_dispatch(const int8_t* vqA, const int8_t* uqB, int32_t* P, cons
         return cudaErrorInvalidValue;
     const int nk = g.Cpad / g.BK;
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl)
-                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl);
-    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl)
-                   : gemm_by_bn<64, 4, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl);
+        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, P)
+                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, P);
+    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, P)
+                   : gemm_by_bn<64, 4, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, P);
 }
 }  // namespace
 
@@ -584,10 +662,10 @@ cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, c
     const int nk = g.Cpad / g.BK;
     const QFuse none{};
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl)
-                       : gemm_by_bn<128, 3, false>(ta, tb, tp, tp2, gc, F, none, st, pdl);
-    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl)
-                   : gemm_by_bn<64, 4, false>(ta, tb, tp, tp2, gc, F, none, st, pdl);
+        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, P)
+                       : gemm_by_bn<128, 3, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, P);
+    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, P)
+                   : gemm_by_bn<64, 4, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, P);
 }
 
 cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
@@ -617,13 +695,13 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
     // BK = 128, four at BK = 64 with BN <= 128 (the single-K-chunk
     // 64-channel layers: more units' V tiles in flight to hide the load latency)
     if (g.BK == 128) {
-        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
-        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
-        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
+        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
+        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
     }
-    if (g.BN == 64) return gemm_launch<64, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
-    if (g.BN == 128) return gemm_launch<128, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
-    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl);
+    if (g.BN == 64) return gemm_launch<64, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
+    if (g.BN == 128) return gemm_launch<128, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
+    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
 }
 
 SFC_TL_UNIT_READER(tl_read_gemm)

@@ -42,6 +42,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 // As mbar_wait, but the waiting thread may be suspended (up to ~0.5 us per try) instead of
 // spinning: for warps whose waits are long, so their retries do not take issue slots.
+// As mbar_wait, but a failed try is followed by a sleep of up to NS nanoseconds before the next
+// one (the compiler emits NANOSLEEP.SYNCS): for warps whose waits are long, so their retries do
+// not take issue slots.  A sleeping warp wakes up to NS late -- waits on a pipeline's critical
+// ring use mbar_wait or a short NS.
+template <int NS = 500>
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     do {
@@ -50,7 +55,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(500)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(NS)
             : "memory");
     } while (!ok);
 }

@@ -24,6 +24,8 @@ struct ConvGeom {
     // qmax^2 * Cin < 2^23).  2 = the same 24-bit values unit-major for the tensor-core output
     // transform (pu_offset below).  geom_init sets 0; run_conv decides (p24_wanted).
     int p24;
+    // unit-major P with a sparse plane 2 (p2_flags_offset below); run_conv decides (p2_sparse_wanted)
+    int p2s;
 };
 
 // 24-bit P, unit-major (ConvGeom::p24 == 2): the A operands of the tensor-core output
@@ -33,8 +35,23 @@ struct ConvGeom {
 // (P = b0 + 2^8 b1 + 2^16 b2); the 128-byte row (f, unit) holds [tt][32 oc] with 16-byte chunk
 // c at c ^ (f & 7), the 128B-swizzle pattern of an MN-major tcgen05 operand.  The F rows of a
 // unit land in shared memory as that operand with one TMA box; the GEMM writes the rows of 8
-// consecutive units (1 KB contiguous) per box.
+// consecutive units (1 KB contiguous) per box.  (Measured: with each unit's rows contiguous
+// instead -- [oc block][tile group][plane][F] -- the output transform is no faster and the
+// GEMM's 128-byte writes 38 KB apart cost 0.1-0.7 ms per VGG-16 step.)
+//
+// Sparse plane 2 (ConvGeom::p2s): the GEMM stores P' = P + 2^15, so every value within 16 bits
+// has a zero third byte; row (f, unit) of plane 2 is written only when one of its 128 values
+// leaves that range, and a flag byte per (unit, f) says so: flags [OCpad / 32][Tpad / 32][F][8]
+// (8 consecutive tile groups per entry) after the three planes.  The output transform loads
+// the flagged rows, zero-fills the others, skips the all-zero K steps and subtracts the bias
+// 2^15 * sum_f W[o][f] per output.  Post-ReLU activations leave only the DC frequency outside
+// 16 bits, so about a third of the P traffic disappears; with every row flagged the layout
+// degenerates to the dense one plus the flags.
 constexpr int kUnitTiles = 4, kUnitOc = 32;
+__host__ __device__ inline size_t p2_flags_offset(int F, int Tpad, int OCpad) { return size_t(3) * F * Tpad * OCpad; }
+__host__ __device__ inline size_t p2_flag_index(int ob, int tg, int f, int Tpad, int F) {
+    return ((size_t(ob) * (Tpad / (8 * kUnitTiles)) + tg / 8) * F + f) * 8 + (tg & 7);
+}
 __host__ __device__ inline size_t pu_offset(int ob, int tg, int plane, int f, int n_tg, int F) {
     return (((size_t(ob) * 3 + plane) * F + f) * n_tg + tg) * 128;
 }

@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes
 import enum
 import math
+import os
 from dataclasses import dataclass, field
 from functools import lru_cache
 
@@ -409,7 +410,14 @@ class SfcLayer:
             lb = torch.arange(128, device=self.device)[None, None, :]
             src = ((((lb >> 4) ^ (f & 7)) << 4) | (lb & 15)).expand(n_ob, 3, F, n_tg, 128)
             lg = torch.gather(raw, 4, src).to(torch.int32)  # [ob][plane][f][tg][tt * 32 + oc]
-            p = (lg[:, 0] & 0xFF) | ((lg[:, 1] & 0xFF) << 8) | (((lg[:, 2] & 0xFF) ^ 0x80) - 0x80) * 65536
+            hi = (((lg[:, 2] & 0xFF) ^ 0x80) - 0x80) * 65536
+            p = (lg[:, 0] & 0xFF) | ((lg[:, 1] & 0xFF) << 8)
+            if os.environ.get("SFC_P2_DENSE", "0")[:1] == "1":
+                p = p | hi
+            else:  # sparse plane 2: P + 2^15 stored; rows of plane 2 exist where the flag byte is set
+                fl = _wrap_device(pa.value + 3 * F * Tpad * OCpad, (n_ob, n_tg // 8, F, 8), torch.uint8, self.device)
+                fl = fl.permute(0, 2, 1, 3).reshape(n_ob, F, n_tg, 1) != 0
+                p = p + torch.where(fl, hi, torch.zeros_like(hi)) - 32768
             p = p.view(n_ob, F, n_tg, 4, 32).permute(1, 2, 3, 0, 4).reshape(F, n_tg * 4, n_ob * 32)
             return vqt, p[:, :T, : self.OC]
         if blocked.value == 1:  # 24-bit rows of three byte planes b0 | b1 | b2 (a copy)
