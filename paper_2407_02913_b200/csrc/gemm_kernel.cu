@@ -66,6 +66,12 @@ constexpr int kEpiBufs = 2;                  // TMA-store staging boxes per epil
 constexpr int kEpiBoxBytes = 32 * 32 * 4;    // 32 rows x 32 int32 (one 128B-swizzle box)
 template <bool QF>
 constexpr int gemm_threads() { return 64 + 32 * kEpiWarps + (QF ? 32 * kConvWarps : 0); }
+// TMEM accumulator buffers: the epilogue warps take every unit in turn, so their per-unit latency
+// bounds the kernel; with more than two buffers the MMAs run ahead and the epilogue never waits
+// for them (BN = 64: 4 x 64 columns, still two CTAs per SM; the TMA-staged-V kernel is alone on
+// its SM and takes 512 columns at BN = 128).
+template <int BN, bool QT>
+constexpr int gemm_acc() { return BN == 64 ? 4 : (BN == 128 && QT ? 4 : 2); }
 
 // Work unit -> (oc block, tile block, frequency): oc block fastest, so co-resident CTAs share
 // a frequency's A tile in L2.
@@ -78,6 +84,32 @@ __device__ __forceinline__ void unit_of(int u, int n_ob, int n_tb, int F, bool f
     if (!f_major) return unit_of(u, n_ob, n_tb, ob, tb, f);
     ob = u % n_ob, f = (u / n_ob) % F, tb = u / (n_ob * F);
 }
+
+// The same unit sequence u = u0, u0 + stride, ... as mixed-radix digits (d0 fastest: the oc block; d1, d2 =
+// (tile block, f) or, f_major, (f, tile block)) advanced by addition with carries -- no division per unit.
+struct UnitWalk3 {
+    int d0, d1, d2, s0, s1, s2, r0, r1;
+    bool fm;
+    __device__ __forceinline__ UnitWalk3(int u0, int stride, int n_ob, int n_tb, int F, bool f_major) : fm(f_major) {
+        r0 = n_ob, r1 = f_major ? F : n_tb;
+        d0 = u0 % r0, d1 = (u0 / r0) % r1, d2 = u0 / (r0 * r1);
+        s0 = stride % r0, s1 = (stride / r0) % r1, s2 = stride / (r0 * r1);
+    }
+    __device__ __forceinline__ void get(int& ob, int& tb, int& f) const {
+        ob = d0;
+        if (fm) f = d1, tb = d2;
+        else tb = d1, f = d2;
+    }
+    __device__ __forceinline__ void next() {
+        d0 += s0;
+        int c = 0;
+        if (d0 >= r0) d0 -= r0, c = 1;
+        d1 += s1 + c;
+        c = 0;
+        if (d1 >= r1) d1 -= r1, c = 1;
+        d2 += s2 + c;
+    }
+};
 
 // Byte planes 0..2 of four int32 values (a, b, c, d): p_j = [a.b_j, b.b_j, c.b_j, d.b_j] -- a
 // 4x4 byte transpose restricted to three outputs, 7 byte permutes (instead of 9 per plane set).
@@ -120,10 +152,12 @@ __device__ __forceinline__ QuantParams qparams_warp(int vmax, int bits, const Qu
 template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2, int n_tb, int n_ob,
-           int F, int nk, ConvGeom g, QFuse qf, uint8_t* __restrict__ p_raw) {
+           const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2,
+           const __grid_constant__ CUtensorMap tmP3, int n_tb, int n_ob, int F, int nk, ConvGeom g, QFuse qf,
+           uint8_t* __restrict__ p_raw) {
     static_assert(!QT || QF, "the TMA-staged V feeds the converters");
-    constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
+    constexpr int kAcc = gemm_acc<BN, QT>();          // TMEM accumulator buffers
+    constexpr int kTmemCols = kAcc * BN <= 128 ? 128 : (kAcc * BN <= 256 ? 256 : 512);
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
     constexpr uint32_t kVStageBytes = kRowsPerTile * BK * 2;
     constexpr int kHalf = BN / 2;                     // columns per epilogue warp (two warps per lane quarter)
@@ -136,8 +170,8 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(sE + kEpiWarps * kEpiBufs * kEpiBoxBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint64_t* vfull = tempty + 2;                     // QT: V stage landed
+    uint64_t* tempty = tfull + kAcc;
+    uint64_t* vfull = tempty + kAcc;                  // QT: V stage landed
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(vfull + (QT ? STAGES : 0));
 #ifdef GM_TRACE
     long long* s_trace = reinterpret_cast<long long*>(tmem_holder + 2);
@@ -153,7 +187,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             ptx::mbar_init(&full[s], QF ? 1 + kConvWarps : 1);
             ptx::mbar_init(&empty[s], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kAcc; ++i) {
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], kEpiWarps);
         }
@@ -165,7 +199,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         if (!QF || QT) ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB);
         ptx::tma_prefetch(&tmP);
-        if (g.p24 >= 2) ptx::tma_prefetch(&tmP2);
+        if (g.p24 >= 2) ptx::tma_prefetch(&tmP2), ptx::tma_prefetch(&tmP3);
     }
     if (warp == 1) ptx::tmem_alloc(tmem_holder, kTmemCols);
     ptx::tc_fence_before();
@@ -181,11 +215,13 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             tl_mark(kTlGemm, 1);
             int stage = 0;
             uint32_t phase = 0;
+            UnitWalk3 uw(blockIdx.x, gridDim.x, n_ob, n_tb, F, g.p24 == 2);
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 int ob, tb, f;
-                unit_of(u, n_ob, n_tb, F, g.p24 == 2, ob, tb, f);
+                uw.get(ob, tb, f);
+                uw.next();
                 for (int kc = 0; kc < nk; ++kc) {
-                    ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
+                    ptx::mbar_wait_sleep<100>(&empty[stage], phase ^ 1);
                     GM_STAMP(0, tu, 0);
                     if (QF) {
                         ptx::mbar_expect_tx(&full[stage], uint32_t(BN * BK));
@@ -214,8 +250,8 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             uint32_t phase = 0;
             int i = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-                const int ab = i & 1;
-                ptx::mbar_wait_sleep(&tempty[ab], ((i >> 1) & 1) ^ 1);
+                const int ab = i % kAcc;
+                ptx::mbar_wait(&tempty[ab], ((i / kAcc) & 1) ^ 1);
                 GM_STAMP(1, i, 0);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + uint32_t(ab * BN);
@@ -242,11 +278,14 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
         uint8_t* myE = sE + (warp - 2) * kEpiBufs * kEpiBoxBytes;
         int buf = 0;
         int i = 0;
+        UnitWalk3 uw(blockIdx.x, gridDim.x, n_ob, n_tb, F, g.p24 == 2);
+        int ab = 0;
+        uint32_t aphase = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
             int ob, tb, f;
-            unit_of(u, n_ob, n_tb, F, g.p24 == 2, ob, tb, f);
-            const int ab = i & 1;
-            ptx::mbar_wait_sleep(&tfull[ab], (i >> 1) & 1);
+            uw.get(ob, tb, f);
+            uw.next();
+            ptx::mbar_wait_sleep<100>(&tfull[ab], aphase);
             if (warp == 2 && lane == 0) GM_STAMP(2, i, 0);
             ptx::tc_fence_after();
 #pragma unroll 1
@@ -327,26 +366,26 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
                 }
                 fence_async_smem();
                 __syncwarp();
+                if (g.p24 >= 2 && g.p2s && (lane & 3) == 0) {
+                    // one flag byte per (unit, f): [oc block][tile group / 8][F][8]; lane 4 uu owns unit uu
+                    const int t0u = (tb * kRowsPerTile + q * 32) / kUnitTiles, o0u = (ob * BN + c) / kUnitOc;
+                    p_raw[p2_flags_offset(F, g.Tpad, g.OCpad) + p2_flag_index(o0u, t0u, f, g.Tpad, F) + (lane >> 2)] =
+                        uint8_t((p2rows >> lane) & 1u);
+                }
                 if (lane == 0) {
                     const int t0 = tb * kRowsPerTile + q * 32, o0 = ob * BN + c;
                     if (g.p24 >= 2) {  // (row, f, plane, tile group, oc block)
                         const int t0u = (tb * kRowsPerTile + q * 32) / kUnitTiles, o0u = (ob * BN + c) / kUnitOc;
-#pragma unroll
-                        for (int pl = 0; pl < 2; ++pl) tma_store_5d(&tmP2, box + pl * 1024, 0, t0u, f, pl, o0u);
+                        // planes 0 and 1 as one box (the staging is [plane][8 units][128 B]): a TMA
+                        // store costs its issuing lane ~300 cycles
+                        tma_store_5d(&tmP2, box, 0, t0u, f, 0, o0u);
                         if (p2rows == 0x11111111u) {
-                            tma_store_5d(&tmP2, box + 2 * 1024, 0, t0u, f, 2, o0u);
+                            tma_store_5d(&tmP3, box + 2 * 1024, 0, t0u, f, 2, o0u);
                         } else if (p2rows) {
                             for (int uu = 0; uu < 8; ++uu)
                                 if ((p2rows >> (4 * uu)) & 1u)
                                     bulk_store_128(p_raw + pu_offset(o0u, t0u + uu, 2, f, g.Tpad / kUnitTiles, F),
                                                    box + 2 * 1024 + uu * 128);
-                        }
-                        if (g.p2s) {  // one flag byte per (unit, f): [oc block][tile group / 8][F][8]
-                            unsigned long long fl = 0;
-#pragma unroll
-                            for (int uu = 0; uu < 8; ++uu) fl |= (unsigned long long)((p2rows >> (4 * uu)) & 1u) << (8 * uu);
-                            *reinterpret_cast<unsigned long long*>(p_raw + p2_flags_offset(F, g.Tpad, g.OCpad) +
-                                                                   p2_flag_index(o0u, t0u, f, g.Tpad, F)) = fl;
                         }
                     } else if (g.p24) {  // byte coordinates: plane j of a P row starts at j * OCpad
 #pragma unroll
@@ -362,6 +401,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[ab]);
             if (warp == 2 && lane == 0) GM_STAMP(2, i, 3);
+            if (++ab == kAcc) ab = 0, aphase ^= 1;
         }
         if (lane == 0) bulk_wait_all();
     } else if (QF && QT) {
@@ -377,7 +417,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int s2 = 0; s2 < npairs; ++s2) {
-                ptx::mbar_wait_sleep(&vfull[stage], phase);  // (the producer waited for the stage to be free)
+                ptx::mbar_wait_sleep<100>(&vfull[stage], phase);  // (the producer waited for the stage to be free)
                 if (ct == 0) GM_STAMP(3, s2, 0);
                 const uint8_t* v_st = sV + stage * kVStageBytes;
                 uint8_t* a_st = sA + stage * kRowsPerTile * BK;
@@ -538,10 +578,11 @@ bool make_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void*
 // The GEMM's P maps: int32 [F][Tpad][OCpad] boxes of 32 x 32 (rows x oc), 128B-swizzled; or
 // 24-bit P as rows of 3*OCpad bytes (byte planes b0 | b1 | b2 of OCpad bytes each): one byte
 // map, box 32 B x 32 rows, 32B swizzle, stored once per plane.
-bool make_p_maps(CUtensorMap* m, CUtensorMap* m2, int32_t* P, const ConvGeom& g, int F, int rows) {
+bool make_p_maps(CUtensorMap* m, CUtensorMap* m2, CUtensorMap* m3, int32_t* P, const ConvGeom& g, int F, int rows) {
     *m2 = CUtensorMap{};
-    if (g.p24 == 2) {  // unit-major: box [8 tile groups][128 B] per (f, plane), 128B-swizzled staging
-        return make_pu_map(m2, P, g, F, 8, 1, true) &&
+    *m3 = CUtensorMap{};
+    if (g.p24 == 2) {  // unit-major: box [planes 0-1][8 tile groups][128 B] per f (and plane 2 alone), 128B-swizzled staging
+        return make_pu_map(m2, P, g, F, 8, 1, true, 2) && make_pu_map(m3, P, g, F, 8, 1, true) &&
                make_tmap_3d(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, P, uint64_t(g.OCpad) * 3, rows, F, 32, 32,
                             CU_TENSOR_MAP_SWIZZLE_32B);
     }
@@ -554,13 +595,14 @@ bool make_p_maps(CUtensorMap* m, CUtensorMap* m2, int32_t* P, const ConvGeom& g,
 int sm_count() { return device_sm_count(); }
 }  // namespace
 
-bool make_pu_map(CUtensorMap* m, void* P, const ConvGeom& g, int F, int box_tg, int box_f, bool swizzle128) {
+bool make_pu_map(CUtensorMap* m, void* P, const ConvGeom& g, int F, int box_tg, int box_f, bool swizzle128,
+                 int box_planes) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t ntg = cuuint64_t(g.Tpad) / kUnitTiles;
     cuuint64_t dims[5] = {128, ntg, cuuint64_t(F), 3, cuuint64_t(g.OCpad) / kUnitOc};
     cuuint64_t strides[4] = {128, ntg * 128, cuuint64_t(F) * ntg * 128, 3 * cuuint64_t(F) * ntg * 128};
-    cuuint32_t box[5] = {128, cuuint32_t(box_tg), cuuint32_t(box_f), 1, 1};
+    cuuint32_t box[5] = {128, cuuint32_t(box_tg), cuuint32_t(box_f), cuuint32_t(box_planes), 1};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
               swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -571,7 +613,8 @@ namespace {
 
 template <int BN, int BK, int STAGES, bool QF, bool QT = false>
 cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
-                        const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl, void* p_raw) {
+                        const CUtensorMap& p3, const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl,
+                        void* p_raw) {
     const size_t smem = size_t(STAGES) * (kRowsPerTile + BN) * BK + (QT ? size_t(STAGES) * kRowsPerTile * BK * 2 : 0) +
                         size_t(kEpiWarps) * kEpiBufs * kEpiBoxBytes + 1024 + 256
 #ifdef GM_TRACE
@@ -584,7 +627,8 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     const int n_tb = g.Tpad / kRowsPerTile, n_ob = g.OCpad / BN;
     const int units = F * n_tb * n_ob;
     // CTAs per SM bounded by shared memory and by TMEM (2*BN columns each of 512).
-    constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
+    constexpr int kAcc = gemm_acc<BN, QT>();
+    constexpr int kTmemCols = kAcc * BN <= 128 ? 128 : (kAcc * BN <= 256 ? 256 : 512);
     int per_sm = int((227 * 1024) / smem);
     per_sm = per_sm < 1 ? 1 : per_sm;
     per_sm = per_sm > 512 / kTmemCols ? 512 / kTmemCols : per_sm;
@@ -609,34 +653,35 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
         const char* e = std::getenv("SFC_GEMM_FMAJOR");
         if (!(e && e[0] == '1')) gk.p24 = 3;  // (3: unit-major P, tile-block-major order)
     }
-    return cudaLaunchKernelEx(&cfg, kern, a, b, p, p2, n_tb, n_ob, F, g.Cpad / BK, gk, qf, static_cast<uint8_t*>(p_raw));
+    return cudaLaunchKernelEx(&cfg, kern, a, b, p, p2, p3, n_tb, n_ob, F, g.Cpad / BK, gk, qf, static_cast<uint8_t*>(p_raw));
 }
 
 template <int BK, int STAGES, bool QF>
 cudaError_t gemm_by_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& p2,
-                       const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl, void* p_raw) {
-    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, p_raw);
-    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, p_raw);
-    return gemm_launch<256, BK, STAGES, QF>(a, b, p, p2, g, F, qf, st, pdl, p_raw);
+                       const CUtensorMap& p3, const ConvGeom& g, int F, const QFuse& qf, cudaStream_t st, bool pdl,
+                       void* p_raw) {
+    if (g.BN == 64) return gemm_launch<64, BK, STAGES, QF>(a, b, p, p2, p3, g, F, qf, st, pdl, p_raw);
+    if (g.BN == 128) return gemm_launch<128, BK, STAGES, QF>(a, b, p, p2, p3, g, F, qf, st, pdl, p_raw);
+    return gemm_launch<256, BK, STAGES, QF>(a, b, p, p2, p3, g, F, qf, st, pdl, p_raw);
 }
 
 template <bool QF>
 cudaError_t gemm_dispatch(const int8_t* vqA, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, const QFuse& qf,
                           cudaStream_t st, bool pdl) {
-    CUtensorMap ta, tb, tp, tp2;
+    CUtensorMap ta, tb, tp, tp2, tp3;
     const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     // (QF: the A map is unused; it is built over the filters only to keep one kernel signature)
     if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, QF ? static_cast<const void*>(uqB) : vqA, g.Cpad,
                       QF ? g.OCpad : g.Tpad, F, g.BK, QF ? g.BN : kRowsPerTile, sw) ||
         !make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
-        !make_p_maps(&tp, &tp2, P, g, F, g.Tpad))
+        !make_p_maps(&tp, &tp2, &tp3, P, g, F, g.Tpad))
         return cudaErrorInvalidValue;
     const int nk = g.Cpad / g.BK;
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, P)
-                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, P);
-    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, P)
-                   : gemm_by_bn<64, 4, QF>(ta, tb, tp, tp2, g, F, qf, st, pdl, P);
+        return nk <= 2 ? gemm_by_bn<128, 2, QF>(ta, tb, tp, tp2, tp3, g, F, qf, st, pdl, P)
+                       : gemm_by_bn<128, 3, QF>(ta, tb, tp, tp2, tp3, g, F, qf, st, pdl, P);
+    return nk <= 2 ? gemm_by_bn<64, 2, QF>(ta, tb, tp, tp2, tp3, g, F, qf, st, pdl, P)
+                   : gemm_by_bn<64, 4, QF>(ta, tb, tp, tp2, tp3, g, F, qf, st, pdl, P);
 }
 }  // namespace
 
@@ -649,7 +694,7 @@ cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, c
                              int tcpad, cudaStream_t st, bool pdl) {
     // A: rows [t0, t0 + tcpad) of every frequency plane of vq (rows past the planes' Tpad
     // read as zeros); P: a buffer of tcpad rows per frequency
-    CUtensorMap ta, tb, tp, tp2{};
+    CUtensorMap ta, tb, tp, tp2{}, tp3{};
     const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     const int arows = tcpad < g.Tpad - t0 ? tcpad : g.Tpad - t0;
     if (!make_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, vqA + size_t(t0) * g.Cpad, g.Cpad, arows, F, g.BK,
@@ -662,10 +707,10 @@ cudaError_t launch_gemm_rows(const int8_t* vqA, const int8_t* uqB, int32_t* P, c
     const int nk = g.Cpad / g.BK;
     const QFuse none{};
     if (g.BK == 128)
-        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, P)
-                       : gemm_by_bn<128, 3, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, P);
-    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, P)
-                   : gemm_by_bn<64, 4, false>(ta, tb, tp, tp2, gc, F, none, st, pdl, P);
+        return nk <= 2 ? gemm_by_bn<128, 2, false>(ta, tb, tp, tp2, tp3, gc, F, none, st, pdl, P)
+                       : gemm_by_bn<128, 3, false>(ta, tb, tp, tp2, tp3, gc, F, none, st, pdl, P);
+    return nk <= 2 ? gemm_by_bn<64, 2, false>(ta, tb, tp, tp2, tp3, gc, F, none, st, pdl, P)
+                   : gemm_by_bn<64, 4, false>(ta, tb, tp, tp2, tp3, gc, F, none, st, pdl, P);
 }
 
 cudaError_t launch_gemm_qfused(const QFuse& q, const int8_t* uqB, int32_t* P, const ConvGeom& g, int F, cudaStream_t st,
@@ -678,7 +723,7 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
     // V [F][Tpad][Cpad] int16 seen as (C, T, F): channels >= C and rows >= T read as zero
     auto fn = encode_fn();
     if (!fn) return cudaErrorInvalidValue;
-    CUtensorMap tv, tb, tp, tp2;
+    CUtensorMap tv, tb, tp, tp2, tp3;
     cuuint64_t dims[3] = {cuuint64_t(g.C), cuuint64_t(g.T), cuuint64_t(F)};
     cuuint64_t strides[2] = {cuuint64_t(g.Cpad) * 2, cuuint64_t(g.Cpad) * g.Tpad * 2};
     cuuint32_t box[3] = {cuuint32_t(g.BK), cuuint32_t(kRowsPerTile), 1};
@@ -689,19 +734,19 @@ cudaError_t launch_gemm_qtma(const QFuse& q, const int8_t* uqB, int32_t* P, cons
         return cudaErrorInvalidValue;
     const CUtensorMapSwizzle sw = g.BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     if (!make_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uqB, g.Cpad, g.OCpad, F, g.BK, g.BN, sw) ||
-        !make_p_maps(&tp, &tp2, P, g, F, g.Tpad))
+        !make_p_maps(&tp, &tp2, &tp3, P, g, F, g.Tpad))
         return cudaErrorInvalidValue;
     // stages: A + B + V per stage plus the 64 KB of epilogue boxes within 227 KB -- two at
     // BK = 128, four at BK = 64 with BN <= 128 (the single-K-chunk
     // 64-channel layers: more units' V tiles in flight to hide the load latency)
     if (g.BK == 128) {
-        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
-        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
-        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
+        if (g.BN == 64) return gemm_launch<64, 128, 2, true, true>(tv, tb, tp, tp2, tp3, g, F, q, st, pdl, P);
+        if (g.BN == 128) return gemm_launch<128, 128, 2, true, true>(tv, tb, tp, tp2, tp3, g, F, q, st, pdl, P);
+        return gemm_launch<256, 128, 2, true, true>(tv, tb, tp, tp2, tp3, g, F, q, st, pdl, P);
     }
-    if (g.BN == 64) return gemm_launch<64, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
-    if (g.BN == 128) return gemm_launch<128, 64, 4, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
-    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, g, F, q, st, pdl, P);
+    if (g.BN == 64) return gemm_launch<64, 64, 4, true, true>(tv, tb, tp, tp2, tp3, g, F, q, st, pdl, P);
+    if (g.BN == 128) return gemm_launch<128, 64, 4, true, true>(tv, tb, tp, tp2, tp3, g, F, q, st, pdl, P);
+    return gemm_launch<256, 64, 2, true, true>(tv, tb, tp, tp2, tp3, g, F, q, st, pdl, P);
 }
 
 SFC_TL_UNIT_READER(tl_read_gemm)

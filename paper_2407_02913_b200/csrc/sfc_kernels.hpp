@@ -175,7 +175,8 @@ cudaError_t launch_output_mma(int variant, const void* P, const ConvGeom& g, con
                               const OutPtrs& o, cudaStream_t st, bool pdl);
 // The 5-D map over unit-major P: (128-byte row, tile group, f, plane, oc block), box rows x
 // tile groups x frequencies as given; swizzle as given (the data itself is pre-swizzled).
-bool make_pu_map(CUtensorMap* m, void* P, const ConvGeom& g, int F, int box_tg, int box_f, bool swizzle128);
+bool make_pu_map(CUtensorMap* m, void* P, const ConvGeom& g, int F, int box_tg, int box_f, bool swizzle128,
+                 int box_planes = 1);
 bool output_mma_supported(int variant, const ConvGeom& g, const OutPtrs& o);
 // Batched fp64 NT contraction P_f = V_f U_f^T (f64_gemm.cu): the 9-16 bit exact-integer path
 // and the float fast_conv2d path.
