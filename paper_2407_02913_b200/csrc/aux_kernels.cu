@@ -227,6 +227,10 @@ void geom_init(ConvGeom& g, int variant, int B, int C, int H, int W, int pad, in
     g.BK = C > 64 ? 128 : 64;
     g.Cpad = (C + g.BK - 1) / g.BK * g.BK;
     g.BN = OC <= 64 ? 64 : (OC <= 128 ? 128 : 256);
+    if (const char* e = std::getenv("SFC_BN_MAX")) {  // experiment knob: cap the GEMM N tile (64 / 128)
+        const int cap = std::atoi(e);
+        if ((cap == 64 || cap == 128) && g.BN > cap && OC > 256) g.BN = cap;
+    }
     g.OCpad = (OC + g.BN - 1) / g.BN * g.BN;
     g.row0 = 0;
     g.nrows = B * g.th;

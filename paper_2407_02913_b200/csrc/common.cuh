@@ -195,5 +195,16 @@ __device__ __forceinline__ int8_t requant_i8(double v) {
     return int8_t(min(max(__double2int_rn(v), 0), 127));
 }
 
+// clamp(rint(y * sc * rq), 0, 127) with the conversions on the fp64 add pipe (the I2F / F2I
+// conversion units are a quarter of its rate): double(y) = (2^52 + 2^31 + y) - (2^52 + 2^31)
+// exactly, the products as in requant_i8(double(y) * sc * rq), and rint(t) as the low word of
+// t + 1.5 * 2^52 (round to nearest even at unit ulp) -- valid while |t| < 2^31, which the caller
+// guarantees with |sc * rq| < 1.
+__device__ __forceinline__ int requant_i8_small(int y, double sc, double rq) {
+    const double yd = __hiloint2double(0x43300000, y ^ int(0x80000000u)) - 4503601774854144.0;
+    const double t = yd * sc * rq;
+    return min(max(__double2loint(t + 6755399441055744.0), 0), 127);
+}
+
 
 }  // namespace sfcb200

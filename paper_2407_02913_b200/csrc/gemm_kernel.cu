@@ -70,8 +70,13 @@ constexpr int gemm_threads() { return 64 + 32 * kEpiWarps + (QF ? 32 * kConvWarp
 // bounds the kernel; with more than two buffers the MMAs run ahead and the epilogue never waits
 // for them (BN = 64: 4 x 64 columns, still two CTAs per SM; the TMA-staged-V kernel is alone on
 // its SM and takes 512 columns at BN = 128).
-template <int BN, bool QT>
-constexpr int gemm_acc() { return BN == 64 ? 4 : (BN == 128 && QT ? 4 : 2); }
+template <int BN, int BK, int STAGES, bool QT>
+constexpr int gemm_acc() {
+    // (a CTA whose shared memory leaves room for a second one on the SM shares the 512 columns with it)
+    const size_t smem = size_t(STAGES) * (128 + BN) * BK + (QT ? size_t(STAGES) * 128 * BK * 2 : 0) + 64 * 1024 + 1280;
+    const int share = 2 * smem <= 227 * 1024 ? 256 : 512;
+    return share / BN >= 4 ? 4 : (share / BN >= 2 ? share / BN : 2);
+}
 
 // Work unit -> (oc block, tile block, frequency): oc block fastest, so co-resident CTAs share
 // a frequency's A tile in L2.
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(gemm_threads<QF>(), 1)
            const __grid_constant__ CUtensorMap tmP3, int n_tb, int n_ob, int F, int nk, ConvGeom g, QFuse qf,
            uint8_t* __restrict__ p_raw) {
     static_assert(!QT || QF, "the TMA-staged V feeds the converters");
-    constexpr int kAcc = gemm_acc<BN, QT>();          // TMEM accumulator buffers
+    constexpr int kAcc = gemm_acc<BN, BK, STAGES, QT>();  // TMEM accumulator buffers
     constexpr int kTmemCols = kAcc * BN <= 128 ? 128 : (kAcc * BN <= 256 ? 256 : 512);
     constexpr uint32_t kStageBytes = (kRowsPerTile + BN) * BK;
     constexpr uint32_t kVStageBytes = kRowsPerTile * BK * 2;
@@ -627,7 +632,7 @@ cudaError_t gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     const int n_tb = g.Tpad / kRowsPerTile, n_ob = g.OCpad / BN;
     const int units = F * n_tb * n_ob;
     // CTAs per SM bounded by shared memory and by TMEM (2*BN columns each of 512).
-    constexpr int kAcc = gemm_acc<BN, QT>();
+    constexpr int kAcc = gemm_acc<BN, BK, STAGES, QT>();
     constexpr int kTmemCols = kAcc * BN <= 128 ? 128 : (kAcc * BN <= 256 ? 256 : 512);
     int per_sm = int((227 * 1024) / smem);
     per_sm = per_sm < 1 ? 1 : per_sm;

@@ -385,7 +385,13 @@ __device__ __forceinline__ void emit_rows_i8(const int* __restrict__ s_y, int ys
         const int oc = r & (kOcc - 1), t1 = r >> 5;
         if (oc >= noc || t1 >= hrows) continue;
         const int2 v = *reinterpret_cast<const int2*>(s_y + r * ys + c);
-        const int qa = requant_i8(double(v.x) * scl[oc] * rq), qb = requant_i8(double(v.y) * scl[oc] * rq);
+        const double sc = scl[oc];
+        int qa, qb;
+        if (fabs(sc * rq) < 1.0) {  // |y sc rq| < 2^31: the conversions on the fp64 add pipe (common.cuh)
+            qa = requant_i8_small(v.x, sc, rq), qb = requant_i8_small(v.y, sc, rq);
+        } else {
+            qa = requant_i8(double(v.x) * sc * rq), qb = requant_i8(double(v.y) * sc * rq);
+        }
         int8_t* d = out + base0 + unsigned(oc * plane + t1 * WO + c);
         if (pair) {
             *reinterpret_cast<uint16_t*>(d) = uint16_t((qa & 0xff) | ((qb & 0xff) << 8));

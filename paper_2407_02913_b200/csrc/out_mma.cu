@@ -116,17 +116,6 @@ struct UnitWalk {
     }
 };
 
-// clamp(rint(y * sc * rq), 0, 127) with the conversions on the fp64 add pipe (the I2F / F2I
-// conversion units are a quarter of its rate): double(y) = (2^52 + 2^31 + y) - (2^52 + 2^31)
-// exactly, the products as in requant_i8(double(y) * sc * rq), and rint(t) as the low word of
-// t + 1.5 * 2^52 (round to nearest even at unit ulp) -- valid while |t| < 2^31, which the caller
-// guarantees with |sc * rq| < 1.
-__device__ __forceinline__ int requant_i8_small(int y, double sc, double rq) {
-    const double yd = __hiloint2double(0x43300000, y ^ int(0x80000000u)) - 4503601774854144.0;
-    const double t = yd * sc * rq;
-    return min(max(__double2loint(t + 6755399441055744.0), 0), 127);
-}
-
 __device__ __forceinline__ void named_bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kOmBWarps) : "memory"); }
 
 // MK: compile-time output set (bits: 1 y32, 2 y64, 4 f32, 8 f64, 16 i8); 0 = read o at run time

@@ -781,3 +781,74 @@ def test_tensor_core_output_transform_every_output_set(cuda, variant, outs, monk
             res[name] = {k: v.cpu().numpy() for k, v in t.items()}
         for k in outs:
             assert np.array_equal(res["mma"][k], res["cuda-core"][k]), k
+
+
+def _p2_flag_fraction(layer, B, H, W, pad, ws):
+    """Fraction of (unit, f) rows of plane 2 the GEMM flagged (sparse plane 2 of unit-major P)."""
+    import ctypes
+    vq, pa = ctypes.c_void_p(), ctypes.c_void_p()
+    geom = np.zeros(6, np.int64)
+    sc.check(sc.lib().sfc_conv_views(layer._h, B, H, W, pad, sc._ptr(ws), ws.numel(), ctypes.byref(vq), ctypes.byref(pa),
+                                     geom.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+    T, Tpad, _, OCpad = (int(v) for v in geom[:4])
+    F = layer.spec.K ** 2
+    n_ob, n_tg = OCpad // 32, Tpad // 4
+    fl = sc._wrap_device(pa.value + 3 * F * Tpad * OCpad, (n_ob, n_tg // 8, F, 8), torch.uint8, ws.device)
+    return float((fl != 0).float().mean())
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("kind", ["relu-dc-only", "signed-mixed", "huge-all-flagged", "tiny-none"])
+def test_sparse_plane2_of_unit_major_p(cuda, variant, kind, monkeypatch):
+    """Sparse plane 2 (the GEMM stores P + 2^15 and writes a plane-2 row only when one of its
+    values leaves 16 bits): every flag regime -- post-ReLU inputs (the DC frequency only: rows
+    loaded one by one), signed inputs at 512 channels (many rows: the box + fix-up path),
+    large operands (most rows) and few channels (hardly any row) -- gives the
+    dense layout's (SFC_P2_DENSE=1) and the oracle's pacc / y_int / int8 / fp32 bit for bit."""
+    rng = np.random.default_rng({"relu-dc-only": 5, "signed-mixed": 6, "huge-all-flagged": 7, "tiny-none": 8}[kind])
+    if kind == "relu-dc-only":
+        B, C, OC, H, W = 40, 64, 64, 26, 22
+        x = rng.integers(0, 128, size=(B, C, H, W), dtype=np.int8)
+        w = np.clip(np.rint(rng.normal(0, 40, size=(OC, C, 3, 3))), -127, 127).astype(np.int8)
+    elif kind == "signed-mixed":
+        B, C, OC, H, W = 96, 512, 128, 14, 14
+        x = rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)
+        w = np.clip(np.rint(rng.normal(0, 30, size=(OC, C, 3, 3))), -127, 127).astype(np.int8)
+    elif kind == "huge-all-flagged":
+        B, C, OC, H, W = 96, 256, 128, 14, 14
+        x = np.full((B, C, H, W), 127, dtype=np.int8)
+        x[:, ::2] = -128
+        w = np.full((OC, C, 3, 3), 127, dtype=np.int8)
+        w[:, ::2] = -127
+        x[rng.random(x.shape) < 0.3] = 90
+    else:
+        B, C, OC, H, W = 40, 8, 64, 26, 22
+        x = rng.integers(-128, 128, size=(B, C, H, W), dtype=np.int8)
+        w = rng.integers(-2, 3, size=(OC, C, 3, 3)).astype(np.int8)
+    dev = torch.device("cuda", 0)
+    layer = sc.SfcLayer(variant, torch.from_numpy(w).to(dev))
+    monkeypatch.delenv("SFC_P2_DENSE", raising=False)
+    assert layer.schedule(B, H, W, 1)["p_layout"] == 2
+    res = {}
+    for name in ("sparse", "dense"):
+        if name == "dense":
+            monkeypatch.setenv("SFC_P2_DENSE", "1")
+        res[name] = run_gpu(x, w, variant, 1, outs=("y", "f32", "i8"), requant=0.0017, views=True)
+    monkeypatch.delenv("SFC_P2_DENSE")
+    for k in ("y", "f32", "i8", "pacc", "vq"):
+        assert np.array_equal(res["sparse"][k], res["dense"][k]), k
+    check_against_oracle(x, w, variant, 1, intermediates=True)
+    xt = torch.from_numpy(x).to(dev)
+    ws = layer.workspace(B, H, W, 1)
+    y = torch.empty((B, OC, H, W), dtype=torch.int32, device=dev)
+    layer.forward(xt, ws, 1, y_int32=y)
+    torch.cuda.synchronize()
+    frac = _p2_flag_fraction(layer, B, H, W, 1, ws)
+    if kind == "relu-dc-only":
+        assert 0.0 < frac < 0.08, frac
+    elif kind == "tiny-none":
+        assert frac < 0.01, frac
+    elif kind == "huge-all-flagged":
+        assert frac > 0.05, frac
+    else:
+        assert 0.02 < frac < 0.98, frac
