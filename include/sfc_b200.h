@@ -188,7 +188,12 @@ int sfc_conv_views(sfc_layer_t layer, int n, int h, int w, int pad, void* d_work
  *               2 = the same 24-bit values unit-major for the tensor-core output transform
  *               ([OCpad/32][3 planes][F][Tpad/4][128 B]: 32 channels x 4 tiles per 128-byte
  *               row, 16-byte chunk c of row f at c ^ (f & 7); the default for the 3x3 variants
- *               on grids of >= 2 units per SM, SFC_OUT_MMA=0 keeps layout 1); 3 = no P:
+ *               on grids of >= 2 units per SM, SFC_OUT_MMA=0 keeps layout 1).  Layout 2 holds
+ *               P + 2^15 and its plane 2 is sparse: row (f, unit) of plane 2 is written only
+ *               when one of its 128 values leaves 16 bits, and a flag byte per (unit, f) --
+ *               [OCpad/32][Tpad/32][F][8] at byte offset 3*F*Tpad*OCpad -- says so (unflagged
+ *               rows of plane 2 are undefined and stand for zeros; SFC_P2_DENSE=1 writes every
+ *               row); 3 = no P:
  *               Cin <= 4 layers contract with dp4a inside the output transform and the vq
  *               view is compact [F][T][4] (SFC_SMALLC=0 keeps the tensor-core GEMM).
  *               sfc_conv_views returns the raw P storage in this layout (the Python
