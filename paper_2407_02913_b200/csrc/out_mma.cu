@@ -200,6 +200,9 @@ __global__ void __launch_bounds__(kOmThreads, 1)
         constexpr int KS = C::KP / 32;
         constexpr int NPROD = C::STAGES % kOmProdWarps == 0 ? kOmProdWarps : 1;
         const int pm = warp;
+#ifdef OM_TRACE
+        tu = pm;
+#endif
         const int u0 = pm < NPROD ? int(blockIdx.x) + pm * int(gridDim.x) : units, ustep = NPROD * int(gridDim.x);
         if (lane == 0) ptx::tma_prefetch(&tmP);
         // the flag words (8 tile groups per (oc block, tile group / 8, f)) of the next FRING units
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(kOmThreads, 1)
             }
             ptx::mbar_wait(&empty[stage], phase ^ 1);
 #ifdef OM_TRACE
-            if (lane == 0 && pm == 0) OM_STAMP(0, tu, 0);
+            if (lane == 0) OM_STAMP(0, tu, 0);
 #endif
             uint8_t* dst = sA + size_t(stage) * C::STAGE;
             uint32_t kmask = 0;
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(kOmThreads, 1)
                 }
             }
 #ifdef OM_TRACE
-            if (lane == 0 && pm == 0) OM_STAMP(0, tu, 1);
+            if (lane == 0) OM_STAMP(0, tu, 1);
             tu += NPROD;
 #endif
             stage += NPROD;
@@ -346,16 +349,19 @@ __global__ void __launch_bounds__(kOmThreads, 1)
         for (int ks = 0; ks < C::KP / 32; ++ks)
             wd[ks] = ptx::smem_desc_kmajor(ptx::smem_u32(sW) + (ks / 4) * (C::N * 128) + (ks % 4) * 32, 128);
         const int m = warp - kOmProdWarps;
+#ifdef OM_TRACE
+        tu = m;
+#endif
         int stage = m % C::STAGES, ab = m % C::NACC;
         uint32_t phase = 0, aphase = 0;
         for (int u = blockIdx.x + m * gridDim.x; u < units; u += kOmMmaWarps * gridDim.x) {
             ptx::mbar_wait(&tempty[ab], aphase ^ 1);
 #ifdef OM_TRACE
-            if (lane == 0 && m == 0) OM_STAMP(1, tu, 0);
+            if (lane == 0) OM_STAMP(1, tu, 0);
 #endif
             ptx::mbar_wait(&full[stage], phase);
 #ifdef OM_TRACE
-            if (lane == 0 && m == 0) OM_STAMP(1, tu, 1);
+            if (lane == 0) OM_STAMP(1, tu, 1);
 #endif
             const uint32_t km = s_kmask[stage];  // plane-2 K steps to run (bit 0 always set)
             if (km >> 31) {  // fix-up: zero the plane-2 rows the GEMM did not write
@@ -388,7 +394,7 @@ __global__ void __launch_bounds__(kOmThreads, 1)
             }
             __syncwarp();
 #ifdef OM_TRACE
-            if (lane == 0 && m == 0) OM_STAMP(1, tu, 2);
+            if (lane == 0) OM_STAMP(1, tu, 2);
             tu += kOmMmaWarps;
 #endif
             stage += kOmMmaWarps;
