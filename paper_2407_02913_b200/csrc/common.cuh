@@ -202,8 +202,10 @@ __device__ __forceinline__ int8_t requant_i8(double v) {
 // guarantees with |sc * rq| < 1.
 __device__ __forceinline__ int requant_i8_small(int y, double sc, double rq) {
     const double yd = __hiloint2double(0x43300000, y ^ int(0x80000000u)) - 4503601774854144.0;
-    const double t = yd * sc * rq;
-    return min(max(__double2loint(t + 6755399441055744.0), 0), 127);
+    // (explicitly rounded products and sum: a fused t * rq + 1.5 * 2^52 would round the exact product,
+    // not t, to an integer -- a different result when t lands exactly on a half-integer)
+    const double t = __dmul_rn(__dmul_rn(yd, sc), rq);
+    return __vimin_s32_relu(__double2loint(__dadd_rn(t, 6755399441055744.0)), 127);  // max(min(r, 127), 0)
 }
 
 

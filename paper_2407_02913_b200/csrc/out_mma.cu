@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(kOmThreads, 1)
                                         const int qa = requant_i8_small(ya[t1], sc, rq);
                                         if constexpr (PW == 2) {
                                             const int qb = requant_i8_small(yb[t1], sc, rq);
-                                            *reinterpret_cast<uint16_t*>(d + rofs[t1]) = uint16_t(qa | (qb << 8));
+                                            *reinterpret_cast<uint16_t*>(d + rofs[t1]) = uint16_t(__byte_perm(uint32_t(qa), uint32_t(qb), 0x0040));
                                         } else {
                                             d[rofs[t1]] = int8_t(qa);
                                         }
