@@ -623,7 +623,34 @@ __global__ void __launch_bounds__(32 * kSmallTB) k_output_smallc(const int32_t* 
         const int ncol = min(ntb * M, WO - col0);
         const int hrows = min(M, g.HO - ti * M);
         const size_t base0 = (size_t(b) * g.OC + oc0) * size_t(plane) + size_t(ti) * M * WO + col0;
-        if (mask == 16) {  // int8 only (configs 3-4): paired fp32 requant stores
+        if (mask == 16) {  // int8 only (configs 3-4)
+            if (ntb == TB && hrows == M && ncol == TB * M && noc == kOcc && (WO & 1) == 0 && M % 2 == 0) {
+                // whole block (TB full tiles x M rows x 32 channels): thread items (oc, column pair) walk
+                // the M rows with the scale, the base pointer and the row stride hoisted -- no predicates
+                constexpr int NP2 = TB * M / 2;  // column pairs per staged row
+                for (int it = threadIdx.x; it < kOcc * NP2; it += NT) {
+                    const int oc = it / NP2, c = 2 * (it - oc * NP2);
+                    const double sc = s_scale[oc];
+                    int8_t* d = o.i8 + base0 + unsigned(oc * plane + c);
+                    const int* ys = s_y + oc * YS + c;
+                    if (fabs(sc * rq) < 1.0) {
+#pragma unroll
+                        for (int t1 = 0; t1 < M; ++t1) {
+                            const int2 v = *reinterpret_cast<const int2*>(ys + t1 * (kOcc * YS));
+                            const int qa = requant_i8_small(v.x, sc, rq), qb = requant_i8_small(v.y, sc, rq);
+                            *reinterpret_cast<uint16_t*>(d + t1 * WO) = uint16_t(__byte_perm(uint32_t(qa), uint32_t(qb), 0x0040));
+                        }
+                    } else {
+#pragma unroll
+                        for (int t1 = 0; t1 < M; ++t1) {
+                            const int2 v = *reinterpret_cast<const int2*>(ys + t1 * (kOcc * YS));
+                            const int qa = requant_i8(double(v.x) * sc * rq), qb = requant_i8(double(v.y) * sc * rq);
+                            *reinterpret_cast<uint16_t*>(d + t1 * WO) = uint16_t((qa & 0xff) | ((qb & 0xff) << 8));
+                        }
+                    }
+                }
+                continue;
+            }
             emit_rows_i8<M>(s_y, YS, NT, noc, hrows, base0, plane, WO, ncol, s_scale, rq, o.i8);
             continue;
         }
